@@ -1,0 +1,312 @@
+#!/usr/bin/env python
+"""Benchmark of the msMINRES-CIQ hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+A "step" is one full ciq_apply -- lambda estimation, J msMINRES iterations (tol 1e-4, the paper's
+P:903 setting), the final K.Y MVM -- on config C3 (N = 50,000 matrix-free RBF, d = 6, 64 RHS,
+Q = 8, K^{1/2}B; Thompson-sampling shape).  `value` is whole-job RHS/s with inputs resident in
+HBM; `e2e` is the same metric through the C ABI with pinned HOST buffers (H2D of B and D2H of the
+result inside the timed region).  L2 is flushed (256 MiB write) between timed steps.
+
+N > 1 (torchrun): each rank runs its own replica of the workload (weak scaling, no data-path
+collective) until the row-sharded NCCL path lands -- see DESIGN.md §7.
+`--impl reference`: the float64 CPU oracle (the reference arm for this tier) timed on the host
+cores on a bounded row sample of the same workload, extrapolated to the same MVM count.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CIQ K^{1/2}b RHS/sec (N=50k RBF, Q=8) at 1/2/4/8 B200; MVM tensor-pipe %"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def load_peaks() -> dict:
+    try:
+        with open(PEAKS_PATH) as f:
+            d = json.load(f)
+        d["_source"] = "measured"
+        return d
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0,
+                "_source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.th:
+            self.th.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 9:
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower().startswith("active"):
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_desc(cfg) -> str:
+    return (f"{cfg.name}: N={cfg.n:,} matrix-free {cfg.kind.upper()} d={cfg.d}, {cfg.t} RHS, "
+            f"K^{{1/2}}B, Q={cfg.q}, tol={cfg.tol:g} (J_max {cfg.max_iters}), l={cfg.lengthscale}, "
+            f"sigma2={cfg.sigma2}")
+
+
+# ------------------------------------------------------------------------------------------------
+# reference arm / cpu baseline: the oracle on a bounded sample
+# ------------------------------------------------------------------------------------------------
+
+def oracle_sample_rate(cfg, inp, mvms_per_call: int, rows: int = 1024, reps: int = 1) -> dict:
+    """Time the oracle's matrix-free MVM on `rows` of the N rows (all N columns), extrapolate to a
+    whole call of `mvms_per_call` MVMs (the MVM is >99% of the oracle's per-iteration work)."""
+    import numpy as np
+    from threadpoolctl import threadpool_info
+
+    from oracle import KernelOperator
+    op = KernelOperator(inp["X"], cfg.kind, cfg.lengthscale, cfg.outputscale, cfg.sigma2, dense_cache_max=0,
+                        block=64)
+    v = inp["B"].astype(np.float64)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        for i0 in range(0, rows, op.block):
+            op.kernel_rows(i0, min(rows, i0 + op.block)) @ v
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    t_mvm = best * cfg.n / rows
+    t_call = t_mvm * mvms_per_call
+    threads = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    return {"value": cfg.t / t_call, "unit": "RHS/s", "cores": threads, "kind": "oracle",
+            "sample": (f"oracle matrix-free MVM on {rows} of {cfg.n} rows x {cfg.t} RHS ({best:.2f} s), "
+                       f"extrapolated to {mvms_per_call} MVMs per call (lambda est + J + final)"),
+            "sample_seconds": best, "t_call_s": t_call}
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import workloads
+    inp = workloads.config_inputs(cfg)
+    mvms = args.ref_mvms
+    times = []
+    for s in range(args.warmup + args.steps):
+        r = oracle_sample_rate(cfg, inp, mvms, rows=args.ref_rows)
+        if s >= args.warmup:
+            times.append(r["t_call_s"])
+    ms = 1000.0 * statistics.mean(times)
+    val = cfg.t / (ms / 1000.0)
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "RHS/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "mvms_per_call": mvms},
+            "cpu_baseline": {k: r[k] for k in ("kind", "cores", "sample")} | {"value": val, "unit": "RHS/s"},
+            "e2e": {"value": val, "unit": "RHS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------------
+
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2006_11267_b200 as pb
+    import workloads
+
+    inp = workloads.config_inputs(cfg)
+    x = torch.from_numpy(inp["X"]).cuda()
+    b = torch.from_numpy(inp["B"]).cuda()
+    s = torch.from_numpy(inp["S"]).cuda()
+    out = torch.empty_like(b)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+    g = pb.CIQ(cfg.kind, X=x, lengthscale=cfg.lengthscale, outputscale=cfg.outputscale, diag=cfg.sigma2)
+    kw = dict(q=cfg.q, max_iters=cfg.max_iters, tol=cfg.tol, mode=cfg.mode, lanczos_start=s, mvm_impl=args.mvm)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        info = g.apply(b, out, **kw)
+    # ---- timed region (device-resident inputs) ----
+    sampler = ClockSampler(local)
+    sampler.start()
+    step_ms, infos = [], []
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        infos.append(g.apply(b, out, **kw))
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    ms = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * cfg.t / (ms / 1000.0)
+    launches = int(sum(i["kernel_launches"] for i in infos))
+
+    # ---- e2e: pinned host buffers through the C ABI ----
+    bh = torch.from_numpy(inp["B"]).pin_memory()
+    oh = torch.empty_like(bh).pin_memory()
+    e2e_ms = []
+    for _ in range(max(1, args.steps)):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.apply(bh, oh, **kw)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e = statistics.mean(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e = float(t.item())
+
+    # ---- dominant-kernel roofline: one profiled call (events around every MVM / update) ----
+    pinfo = g.apply(b, out, profile=True, **kw)
+    peaks = load_peaks()
+    n, tcols = cfg.n, cfg.t
+    mvm_ms = pinfo["ms_mvm"] / max(1, pinfo["mvm_timed"])
+    upd_ms = pinfo["ms_update"] / max(1, pinfo["update_timed"])
+    step_share = (pinfo["ms_mvm"] + pinfo["ms_update"]) / max(1e-9, pinfo["ms_total"])
+    impl_used = "simt" if args.mvm in ("auto", "simt") else "tc"  # auto -> SIMT until mvm_tc lands
+    # algorithmic work per MVM launch: N^2 kernel evaluations, 2 N^2 T useful flops
+    flops = 2.0 * n * n * tcols
+    if impl_used == "simt":
+        sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+        fp32_peak = sm_count * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12  # TFLOP/s
+        roof = {"bound": "alu", "achieved": flops / (mvm_ms * 1e-3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
+                "kernel": "mvm_simt_kernel (fp32 FFMA)",
+                "peak_source": f"{sm_count} SMs x 128 FP32 lanes x 2 x {peaks.get('sm_max_mhz', 1965.0)} MHz"}
+    else:
+        peak = peaks["bf16_tflops_sustained"]
+        roof = {"bound": "tensor", "achieved": flops / (mvm_ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+                "kernel": "mvm_tc_kernel", "peak_source": f"{peaks['_source']} bf16 sustained (fp16 same rate)"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["ms_per_launch"] = mvm_ms
+    roof["share_of_step"] = pinfo["ms_mvm"] / max(1e-9, pinfo["ms_total"])
+    q = cfg.q
+    rec_bytes = (3 * q + 7) * n * tcols * 4.0
+    recurrence = {"bound": "hbm", "achieved": rec_bytes / (upd_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                  "unit": "GB/s", "kernel": "lanczos_update_kernel", "ms_per_launch": upd_ms,
+                  "algorithmic_bytes": rec_bytes}
+    recurrence["frac"] = recurrence["achieved"] / recurrence["peak"]
+
+    line = {"metric": METRIC, "value": value, "unit": "RHS/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "global_batch": world * tcols, "J": infos[-1]["iters"],
+                       "mvms_per_step": infos[-1]["mvms"], "mvm_impl": impl_used,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "flushed between steps (256 MiB write)",
+                       "converged": infos[-1]["converged"], "max_rel_residual": infos[-1]["max_rel_residual"],
+                       "lambda": [infos[-1]["lambda_min"], infos[-1]["lambda_max"]]},
+            "roofline": roof, "roofline_recurrence": recurrence,
+            "e2e": {"value": world * tcols / (e2e / 1000.0), "unit": "RHS/s", "h2d_bytes_per_step": n * tcols * 4,
+                    "d2h_bytes_per_step": n * tcols * 4, "ms_per_step": e2e},
+            "gpu_launches": launches, "clocks": clocks, "step_share_profiled": step_share}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = oracle_sample_rate(cfg, inp, infos[-1]["mvms"], rows=args.ref_rows)
+        line["cpu_baseline"].pop("t_call_s", None)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    g.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mvm", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--ref-rows", type=int, default=4096)
+    ap.add_argument("--ref-mvms", type=int, default=200)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    import workloads
+    cfg = workloads.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,198 @@
+/*
+ * ciq.h -- C ABI of the B200-native msMINRES-CIQ library (libciq.so).
+ *
+ * Computes K^{1/2} B and K^{-1/2} B for a symmetric positive-definite kernel matrix K and a block
+ * B of T right-hand sides with Contour Integral Quadrature + multi-shift MINRES (Pleiss et al.,
+ * arXiv 2006.11267; "P:n" = line n of the paper text PAPER.md):
+ *
+ *     K^{-1/2} b ~ sum_q w_q (t_q I + K)^{-1} b,   K^{1/2} b ~ K sum_q w_q (t_q I + K)^{-1} b
+ *                                                   (eq. contour_integral_quad)
+ *
+ * with the Hale-Higham-Trefethen shifts/weights (eq. quad_points_and_locations)
+ * built from a Lanczos estimate of lambda_min/lambda_max, the shifted solves by
+ * msMINRES (App. C), and the preconditioned rotated variants R b, R' b of App. A
+ * (eqs. precond_sqrt / precond_sqrt_inverse).
+ *
+ * Conventions (apply to every entry point):
+ *  - Matrices are row-major float32 with an explicit leading dimension (elements).  B and out are
+ *    N x T ("column c is right-hand side b_c"), X is N x d, a dense K is N x N.
+ *  - Pointers may be HOST or DEVICE memory (detected with cudaPointerGetAttributes).  Host inputs
+ *    are copied to device workspace inside the call; host outputs are written back before the
+ *    call returns.  Device inputs are read in place on the ctx stream.
+ *  - Ownership: the caller owns every buffer it passes.  Operator / preconditioner arrays passed
+ *    to ciq_init must stay valid until ciq_free if they are device pointers (host arrays are
+ *    copied at init).  The ctx owns its workspace (grown lazily per T) and its NCCL communicator.
+ *  - Stream ordering: all device work is enqueued on the stream given to ciq_init.  ciq_apply
+ *    returns after the result has been written (it synchronises the stream: the lambda estimate
+ *    and the convergence poll are host decisions).
+ *  - Errors: status codes only, never exceptions across the ABI; ciq_last_error() gives text.
+ *    A non-converged solve is NOT an error: the result is written and CIQ_NOT_CONVERGED returned
+ *    (S:284).
+ *  - Thread safety: one ctx per host thread; contexts are independent.
+ *  - Determinism: every reduction is fixed-order (no float atomics); the same inputs on the same
+ *    launch configuration give bitwise-identical outputs.
+ */
+#ifndef CIQ_H_
+#define CIQ_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CIQ_MAX_Q 64
+
+typedef enum {
+  CIQ_OK = 0,
+  CIQ_NOT_CONVERGED = 1,     /* result written, max_q,c |phibar|/||b_c|| > tol after max_iters */
+  CIQ_ERR_INVALID_ARG = -1,  /* null pointer, Q out of [1, CIQ_MAX_Q], tol < 0, max_iters < 1, ... */
+  CIQ_ERR_DIM = -2,          /* n <= 0, T <= 0, d < 1, leading dimension too small            */
+  CIQ_ERR_NOT_PD = -3,       /* lambda_min estimate <= 0 (operator not positive definite)     */
+  CIQ_ERR_ELLIPTIC = -4,     /* quadrature rule not finite (elliptic function failure)        */
+  CIQ_ERR_CUDA = -5,         /* CUDA runtime / launch error, or no CUDA device                */
+  CIQ_ERR_NCCL = -6,         /* NCCL could not be loaded or a collective failed               */
+  CIQ_ERR_OOM = -7           /* device allocation failed                                     */
+} ciq_status;
+
+typedef enum {
+  CIQ_OP_DENSE = 0,     /* K = A + diag*I for a given dense symmetric A                   */
+  CIQ_OP_RBF = 1,       /* k = o^2 exp(-r^2/2)                                (reading G11)        */
+  CIQ_OP_MATERN52 = 2,  /* k = o^2 (1 + sqrt5 r + 5 r^2/3) exp(-sqrt5 r)                           */
+  CIQ_OP_MATERN32 = 3   /* k = o^2 (1 + sqrt3 r) exp(-sqrt3 r);  r = ||(x - x')/l||, K += diag*I   */
+} ciq_op_kind;
+
+typedef enum {
+  CIQ_MODE_SQRT = 0,     /* K^{1/2} B (R B with a preconditioner)       -- one extra MVM */
+  CIQ_MODE_INVSQRT = 1,  /* K^{-1/2} B (R' B with a preconditioner)                               */
+  CIQ_MODE_WHITEN = 2    /* same as INVSQRT (reading G9)                                          */
+} ciq_mode;
+
+typedef enum {
+  CIQ_MVM_AUTO = 0,      /* tensor-core path where implemented, else SIMT fp32                  */
+  CIQ_MVM_SIMT = 1,      /* fp32 CUDA-core tiles (reference kernel)                             */
+  CIQ_MVM_TC = 2         /* tcgen05 split-fp16 tensor-core kernel (fails if unavailable)        */
+} ciq_mvm_impl;
+
+/* The operator K (touched only through MVMs, P:397 / P:1161-1162). */
+typedef struct {
+  int32_t kind;               /* ciq_op_kind                                                    */
+  int64_t n;                  /* global N                                                       */
+  const float* K;             /* DENSE: N x N row-major, leading dimension ldk (>= N)            */
+  int64_t ldk;
+  const float* X;             /* kernels: N x d points, leading dimension ldx (>= d), replicated */
+  int64_t d;                  /*          on every rank                                         */
+  int64_t ldx;
+  const float* lengthscale;   /* host pointer: d values if ard != 0, else 1 value (> 0)         */
+  int32_t ard;
+  float outputscale;          /* o^2 (> 0)                                                      */
+  float diag;                 /* sigma^2 >= 0 added to the diagonal (noise / jitter, G12); also  */
+                              /* the rigorous lower bound on lambda_min used by the estimator (G6) */
+} ciq_operator;
+
+/* Preconditioner P = L L^T + sigma2 I, L = N x rank row-major (ld >= rank).  When L comes
+ * from a partial pivoted Cholesky of the kernel part of K and sigma2 = op.diag, lambda_min of
+ * P^{-1/2} K P^{-1/2} is >= 1 (reading G6) and the estimator uses that bound. */
+typedef struct {
+  const float* L;
+  int64_t rank;
+  int64_t ldl;
+  float sigma2;               /* > 0                                                    */
+} ciq_precond;
+
+/* Row sharding across GPUs (one process per GPU).  NULL comm = single GPU. */
+typedef struct {
+  int32_t rank;
+  int32_t world;
+  const void* nccl_unique_id; /* 128 bytes from ciq_nccl_unique_id() on rank 0, broadcast by the
+                                 caller (e.g. torch.distributed)                                */
+} ciq_comm;
+
+typedef struct {
+  int32_t Q;                  /* quadrature points, 1..CIQ_MAX_Q (default 8)             */
+  int32_t max_iters;          /* J_max >= 1 (default 400)                                 */
+  double tol;                 /* stop when max_{q,c} |phibar|/||b_c|| <= tol (G3); 0 = exactly   */
+                              /* max_iters iterations (fixed J).  Default 1e-4          */
+  int32_t lanczos_iters;      /* lambda-estimation Lanczos steps (default 10)            */
+  int32_t lanczos_cols;       /* start columns pooled by the estimator (default 16, G5)          */
+  double lambda_min;          /* > 0 together with lambda_max > 0: skip the estimation           */
+  double lambda_max;
+  const double* t;            /* optional explicit rule (host, Q values each): skips estimation  */
+  const double* w;            /*   and the HHT construction (parity tests)                      */
+  const float* lanczos_start; /* optional N x lanczos_cols start block (host or device); NULL =  */
+  int64_t ld_start;           /*   counter-based N(0,1) draw from `seed`                        */
+  uint64_t seed;
+  int32_t mode;               /* ciq_mode                                                       */
+  int32_t mvm_impl;           /* ciq_mvm_impl                                                   */
+  int32_t poll_every;         /* iterations per captured CUDA graph / convergence poll (def. 6)  */
+  double breakdown_tol;       /* Lanczos invariant-subspace threshold, relative (default 1e-6)   */
+  int32_t profile_kernels;    /* 1: bracket every MVM / update launch with CUDA events and report */
+                              /*    their device time in ciq_info (small overhead; default 0)     */
+} ciq_params;
+
+typedef struct {
+  int32_t iters;              /* J: msMINRES iterations applied                                 */
+  int32_t mvms;               /* MVMs with K: lambda-estimation + J (+1 in SQRT mode)           */
+  int32_t converged;
+  int32_t rotated;            /* 1 if a preconditioner was used (result is R B / R' B)           */
+  int32_t breakdown_cols;     /* columns frozen on an invariant subspace                        */
+  int32_t Q;
+  double lambda_min, lambda_max;  /* used for the rule (after safety margins)                   */
+  double ritz_min, ritz_max;      /* raw Ritz extremes (NaN if estimation skipped)              */
+  double max_rel_residual;        /* max_{q,c} |phibar|/||b_c|| at exit                         */
+  double t[CIQ_MAX_Q], w[CIQ_MAX_Q];
+  float ms_total, ms_lambda, ms_loop, ms_final;
+  int64_t kernel_launches;    /* kernels launched by this call (graph nodes counted per launch) */
+  float ms_mvm;               /* profile_kernels: summed device time of the msMINRES-loop MVMs   */
+  int32_t mvm_timed;          /*   number of loop MVMs timed (= iters)                          */
+  float ms_update;            /* profile_kernels: summed device time of the streaming updates    */
+  int32_t update_timed;
+} ciq_info;
+
+typedef struct ciq_ctx ciq_ctx;
+
+/* Fill *p with the defaults listed above. */
+void ciq_params_default(ciq_params* p);
+
+/* Create a context for operator `op` (and optional preconditioner `pc`, optional row-sharding
+ * `comm`) on CUDA stream `stream` (a cudaStream_t; NULL = the legacy default stream).  Validates
+ * the operator, allocates the operator workspace, prepares the scaled points / dense K copy. */
+ciq_status ciq_init(ciq_ctx** ctx, const ciq_operator* op, const ciq_precond* pc,
+                    const ciq_comm* comm, void* stream);
+
+/* out (N x T, ldo) <- K^{1/2} B or K^{-1/2} B (R B / R' B with a preconditioner) for B (N x T,
+ * ldb).  With row sharding, B and out hold this rank's row block [row_begin, row_end) (see
+ * ciq_shard_rows).  `info` may be NULL. */
+ciq_status ciq_apply(ciq_ctx* ctx, const float* B, int64_t ldb, int64_t T, float* out, int64_t ldo,
+                     const ciq_params* p, ciq_info* info);
+
+/* One application of the operator: out <- K V (+ diag*V), the MVM of P:1155-1161 as used by the
+ * solver (same kernel, same precision path selected by mvm_impl).  V: N x T (full); out: this
+ * rank's rows. */
+ciq_status ciq_matvec(ciq_ctx* ctx, const float* V, int64_t ldv, int64_t T, float* out, int64_t ldo,
+                      int32_t mvm_impl);
+
+void ciq_free(ciq_ctx* ctx);
+
+const char* ciq_status_string(ciq_status s);
+const char* ciq_last_error(const ciq_ctx* ctx);   /* NULL ctx: last error of ciq_init on this thread */
+
+/* Row block [*row_begin, *row_end) owned by `rank` of `world` for a global N (multiples of 128). */
+void ciq_shard_rows(int64_t n, int32_t rank, int32_t world, int64_t* row_begin, int64_t* row_end);
+
+/* Host-only helpers (no GPU needed) -- the host steps a2/a3 of the hot path, exported for tests.
+ * ciq_quadrature_rule: the HHT rule t_q, w_q from lambda_min < lambda_max, in
+ *   real arithmetic via the Jacobi imaginary transform (G10); returns CIQ_ERR_INVALID_ARG /
+ *   CIQ_ERR_ELLIPTIC on bad input / non-finite output.
+ * ciq_tridiag_extremes: smallest and largest eigenvalue of the symmetric tridiagonal matrix with
+ *   diagonal alpha[0..m-1] and off-diagonal beta[0..m-2] (fp64 Sturm bisection).
+ * ciq_nccl_unique_id: 128-byte ncclUniqueId (loads NCCL; CIQ_ERR_NCCL if unavailable). */
+ciq_status ciq_quadrature_rule(double lambda_min, double lambda_max, int32_t Q, double* t, double* w);
+ciq_status ciq_tridiag_extremes(const double* alpha, const double* beta, int32_t m,
+                                double* eig_min, double* eig_max);
+ciq_status ciq_nccl_unique_id(void* out128);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CIQ_H_ */

@@ -1,0 +1,651 @@
+// ciq_api.cu -- the C ABI (include/ciq.h) and the host orchestration of one msMINRES-CIQ call
+// (SURVEY §3.2): RHS normalisation -> lambda estimation (Lanczos, fp64 Sturm bisection on the
+// host) -> host HHT rule -> J iterations of [MVM, alpha, streaming update, Givens] with a device
+// convergence flag polled every `poll_every` iterations -> last pending update -> (SQRT) one more
+// MVM -> output.  Every step of the path runs in this library's kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ciq.h"
+#include "host_math.h"
+#include "internal.h"
+#include "nccl_dl.h"
+
+using namespace ciq;
+
+namespace {
+
+thread_local std::string g_init_error;
+
+struct Workspace {
+  int tp = 0, nq = 0;
+  int64_t rows = 0;
+  float* w[3] = {nullptr, nullptr, nullptr};
+  float* p = nullptr;
+  float* d = nullptr;      // [2 slots][nq][rows][tp]
+  float* y = nullptr;
+  double* apart = nullptr; // [mvm blocks][tp]
+  double* bpart = nullptr; // [stream blocks][tp]
+  double* colsq = nullptr; // [tp]
+  char* scal_mem = nullptr;
+  Scal sc{};
+};
+
+struct LambdaWork {
+  int tpl = 0, nb = 0;
+  int64_t rows = 0;
+  float* basis = nullptr;  // [nb][rows][tpl]
+  float* p = nullptr;
+  double* part = nullptr;
+  double* h1 = nullptr;
+  double* h2 = nullptr;
+  double* bsq = nullptr;
+  double* alphas = nullptr;
+  double* betas = nullptr;
+  double* inv = nullptr;
+  int* len = nullptr;
+};
+
+}  // namespace
+
+struct ciq_ctx {
+  ciq_operator op{};
+  OpDev dev{};
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  int64_t row0 = 0, row1 = 0;
+  float* xs = nullptr;        // owned scaled points
+  float* kcopy = nullptr;     // owned dense copy (host-provided K)
+  Workspace ws;
+  LambdaWork lw;
+  float* staging = nullptr;   // host-pointer staging (rows x tp)
+  int64_t staging_elems = 0;
+  std::string err;
+  int64_t launches = 0;
+  // profile_kernels: (start, stop, iteration, kind 0=mvm 1=update)
+  struct Timed { cudaEvent_t a, b; int j, kind; };
+  std::vector<Timed> timed;
+  std::vector<cudaEvent_t> event_pool;
+  bool profiling = false;
+  bool has_precond = false;
+};
+
+namespace {
+
+bool is_device_ptr(const void* p) {
+  if (p == nullptr) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+ciq_status set_err(ciq_ctx* c, ciq_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf; else g_init_error = buf;
+  return s;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                       \
+  do {                                                                                            \
+    cudaError_t e_ = (expr);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return set_err(ctx, e_ == cudaErrorMemoryAllocation ? CIQ_ERR_OOM : CIQ_ERR_CUDA,           \
+                     "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__);        \
+  } while (0)
+
+#define LAUNCH(ctx, expr)  \
+  do {                     \
+    ++(ctx)->launches;     \
+    CUDA_TRY(ctx, expr);   \
+  } while (0)
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T));
+}
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+int round16(int64_t t) { return (int)((t + 15) / 16 * 16); }
+
+void free_workspace(Workspace& ws) {
+  for (auto& b : ws.w) dfree(b);
+  dfree(ws.p); dfree(ws.d); dfree(ws.y); dfree(ws.apart); dfree(ws.bpart); dfree(ws.colsq);
+  dfree(ws.scal_mem);
+  ws.tp = ws.nq = 0;
+}
+
+void free_lambda(LambdaWork& lw) {
+  dfree(lw.basis); dfree(lw.p); dfree(lw.part); dfree(lw.h1); dfree(lw.h2); dfree(lw.bsq);
+  dfree(lw.alphas); dfree(lw.betas); dfree(lw.inv); dfree(lw.len);
+  lw.tpl = lw.nb = 0;
+}
+
+ciq_status ensure_workspace(ciq_ctx* c, int tp, int nq) {
+  Workspace& ws = c->ws;
+  const int64_t rows = c->row1 - c->row0;
+  const int64_t n = c->op.n;
+  if (ws.tp == tp && ws.nq >= nq && ws.rows == rows) return CIQ_OK;
+  free_workspace(ws);
+  ws.tp = tp;
+  ws.nq = nq;
+  ws.rows = rows;
+  // W buffers hold all N rows (the MVM input); the local block is rows [row0, row1).
+  for (auto& b : ws.w) CUDA_TRY(c, dalloc(&b, (size_t)n * tp));
+  CUDA_TRY(c, dalloc(&ws.p, (size_t)rows * tp));
+  CUDA_TRY(c, dalloc(&ws.d, (size_t)2 * nq * rows * tp));
+  CUDA_TRY(c, dalloc(&ws.y, (size_t)rows * tp));
+  CUDA_TRY(c, dalloc(&ws.apart, (size_t)mvm_simt_blocks(rows) * tp + 64 * (size_t)tp));
+  CUDA_TRY(c, dalloc(&ws.bpart, (size_t)rowblocks(rows, tp) * tp));
+  CUDA_TRY(c, dalloc(&ws.colsq, (size_t)tp));
+  // scalar block
+  size_t nd = (size_t)tp * 5 + (size_t)nq * tp * 5 + 2 * (size_t)nq;
+  size_t bytes = nd * 8 + (size_t)tp * 4 + (size_t)nq * tp * 4 * 4 + sizeof(Ctrl) + 256;
+  CUDA_TRY(c, dalloc(&ws.scal_mem, bytes));
+  char* m = ws.scal_mem;
+  auto takeD = [&](size_t k) { double* r = reinterpret_cast<double*>(m); m += k * 8; return r; };
+  Scal& sc = ws.sc;
+  sc.beta1 = takeD(tp); sc.nrm_prev = takeD(tp); sc.nrm_cur = takeD(tp); sc.tb_cur = takeD(tp); sc.alpha = takeD(tp);
+  sc.c1 = takeD((size_t)nq * tp); sc.s1 = takeD((size_t)nq * tp); sc.c2 = takeD((size_t)nq * tp);
+  sc.s2 = takeD((size_t)nq * tp); sc.phibar = takeD((size_t)nq * tp);
+  sc.shifts = takeD(nq); sc.weights = takeD(nq);
+  auto takeF = [&](size_t k) { float* r = reinterpret_cast<float*>(m); m += k * 4; return r; };
+  sc.ca = takeF((size_t)nq * tp); sc.cb = takeF((size_t)nq * tp); sc.ce = takeF((size_t)nq * tp);
+  sc.cf = takeF((size_t)nq * tp);
+  sc.frozen = reinterpret_cast<int*>(m); m += (size_t)tp * 4;
+  m = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(m) + 15) & ~uintptr_t(15));
+  sc.ctrl = reinterpret_cast<Ctrl*>(m);
+  return CIQ_OK;
+}
+
+ciq_status ensure_staging(ciq_ctx* c, int64_t elems) {
+  if (c->staging_elems >= elems) return CIQ_OK;
+  dfree(c->staging);
+  CUDA_TRY(c, dalloc(&c->staging, (size_t)elems));
+  c->staging_elems = elems;
+  return CIQ_OK;
+}
+
+// dst (rows x tp, device, zero-padded) <- src (rows x cols, ld), src host or device.
+ciq_status load_rows(ciq_ctx* c, const float* src, int64_t ld, int64_t rows, int cols, float* dst, int tp) {
+  if (is_device_ptr(src)) {
+    LAUNCH(c, launch_load_block(src, ld, rows, cols, dst, tp, c->stream));
+  } else {
+    CUDA_TRY(c, cudaMemsetAsync(dst, 0, (size_t)rows * tp * 4, c->stream));
+    CUDA_TRY(c, cudaMemcpy2DAsync(dst, (size_t)tp * 4, src, (size_t)ld * 4, (size_t)cols * 4, (size_t)rows,
+                                  cudaMemcpyHostToDevice, c->stream));
+  }
+  return CIQ_OK;
+}
+
+ciq_status store_rows(ciq_ctx* c, const float* src, int tp, int64_t rows, int cols, float* dst, int64_t ld) {
+  if (is_device_ptr(dst)) {
+    LAUNCH(c, launch_store_block(src, tp, rows, cols, dst, ld, c->stream));
+  } else {
+    CUDA_TRY(c, cudaMemcpy2DAsync(dst, (size_t)ld * 4, src, (size_t)tp * 4, (size_t)cols * 4, (size_t)rows,
+                                  cudaMemcpyDeviceToHost, c->stream));
+  }
+  return CIQ_OK;
+}
+
+cudaEvent_t pool_event(ciq_ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Bracket the next launch(es) with events when profiling (begin_timed / end_timed).
+void begin_timed(ciq_ctx* c, int j, int kind) {
+  if (!c->profiling) return;
+  ciq_ctx::Timed t{pool_event(c), pool_event(c), j, kind};
+  cudaEventRecord(t.a, c->stream);
+  c->timed.push_back(t);
+}
+void end_timed(ciq_ctx* c) {
+  if (!c->profiling) return;
+  cudaEventRecord(c->timed.back().b, c->stream);
+}
+
+ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, const Ctrl* done, int impl) {
+  (void)impl;  // tensor-core path selected here once available (mvm_tc.cu)
+  LAUNCH(c, launch_mvm_simt(c->dev, v, tp, c->row0, c->row1, p, tp, apart, done, c->stream));
+  return CIQ_OK;
+}
+
+// Lambda estimation: Lanczos with full re-orthogonalisation on `cols` start
+// columns; Ritz extremes pooled; margins of reading G6.
+ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, double* lmin, double* lmax,
+                           double* rmin, double* rmax, int* mvms) {
+  const int cols = std::max(1, p->lanczos_cols);
+  const int tpl = round16(cols);
+  const int J = std::max(1, p->lanczos_iters);
+  const int64_t n = c->op.n;
+  const int64_t rows = c->row1 - c->row0;
+  if (c->world != 1) return set_err(c, CIQ_ERR_INVALID_ARG, "lambda estimation with row sharding: not built yet");
+  LambdaWork& lw = c->lw;
+  if (lw.tpl != tpl || lw.nb < J + 1 || lw.rows != rows) {
+    free_lambda(lw);
+    lw.tpl = tpl; lw.nb = J + 1; lw.rows = rows;
+    CUDA_TRY(c, dalloc(&lw.basis, (size_t)(J + 1) * n * tpl));
+    CUDA_TRY(c, dalloc(&lw.p, (size_t)rows * tpl));
+    CUDA_TRY(c, dalloc(&lw.part, (size_t)rowblocks(rows, tpl) * (J + 1) * tpl + (size_t)mvm_simt_blocks(rows) * tpl));
+    CUDA_TRY(c, dalloc(&lw.h1, (size_t)(J + 1) * tpl));
+    CUDA_TRY(c, dalloc(&lw.h2, (size_t)(J + 1) * tpl));
+    CUDA_TRY(c, dalloc(&lw.bsq, (size_t)tpl));
+    CUDA_TRY(c, dalloc(&lw.alphas, (size_t)(J + 1) * tpl));
+    CUDA_TRY(c, dalloc(&lw.betas, (size_t)(J + 1) * tpl));
+    CUDA_TRY(c, dalloc(&lw.inv, (size_t)tpl));
+    CUDA_TRY(c, dalloc(&lw.len, (size_t)tpl));
+  }
+  cudaStream_t s = c->stream;
+  if (p->lanczos_start != nullptr) {
+    if (load_rows(c, p->lanczos_start, p->ld_start > 0 ? p->ld_start : cols, n, cols, lw.basis, tpl) != CIQ_OK)
+      return CIQ_ERR_CUDA;
+  } else {
+    LAUNCH(c, launch_randn_fill(lw.basis, n, cols, tpl, 0, p->seed, s));
+  }
+  const int nbr = rowblocks(n, tpl);
+  LAUNCH(c, launch_colsq_partials(lw.basis, n, tpl, lw.part, s));
+  LAUNCH(c, launch_reduce_cols(lw.part, nbr, tpl, lw.bsq, 1, s));
+  LAUNCH(c, launch_scale_cols(lw.basis, n, tpl, lw.bsq, s));
+  std::vector<int> len(tpl);
+  for (int k = 0; k < tpl; ++k) len[k] = (k < cols) ? 0 : -1000000;
+  CUDA_TRY(c, cudaMemcpyAsync(lw.len, len.data(), tpl * 4, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemsetAsync(lw.alphas, 0, (size_t)(J + 1) * tpl * 8, s));
+  CUDA_TRY(c, cudaMemsetAsync(lw.betas, 0, (size_t)(J + 1) * tpl * 8, s));
+  const double bd = 1e-10;
+  int done_mvms = 0;
+  for (int j = 0; j < J; ++j) {
+    const float* vj = lw.basis + (size_t)j * n * tpl;
+    if (run_mvm(c, vj, tpl, lw.p, nullptr, nullptr, p->mvm_impl) != CIQ_OK) return CIQ_ERR_CUDA;
+    ++done_mvms;
+    for (int pass = 0; pass < 2; ++pass) {
+      double* h = pass == 0 ? lw.h1 : lw.h2;
+      LAUNCH(c, launch_basis_dots(lw.basis, j + 1, n, tpl, lw.p, lw.part, s));
+      LAUNCH(c, launch_reduce_cols(lw.part, nbr, (j + 1) * tpl, h, 0, s));
+      LAUNCH(c, launch_basis_axpy(lw.basis, j + 1, n, tpl, h, lw.p, s));
+    }
+    LAUNCH(c, launch_colsq_partials(lw.p, n, tpl, lw.part, s));
+    LAUNCH(c, launch_reduce_cols(lw.part, nbr, tpl, lw.bsq, 0, s));
+    LAUNCH(c, launch_lanczos_coeffs(lw.h1, lw.h2, lw.bsq, j, J + 1, tpl, bd, lw.alphas, lw.betas, lw.len, lw.inv, s));
+    CUDA_TRY(c, cudaMemcpyAsync(len.data(), lw.len, tpl * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    bool any = false;
+    for (int k = 0; k < cols; ++k) any = any || (len[k] == j + 1);
+    if (!any || j == J - 1) break;
+    LAUNCH(c, launch_scale_cols_by(lw.p, lw.basis + (size_t)(j + 1) * n * tpl, n, tpl, lw.inv, s));
+  }
+  std::vector<double> al((size_t)(J + 1) * tpl), be((size_t)(J + 1) * tpl);
+  CUDA_TRY(c, cudaMemcpyAsync(al.data(), lw.alphas, al.size() * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaMemcpyAsync(be.data(), lw.betas, be.size() * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  double emin_all = INFINITY, emax_all = -INFINITY;
+  std::vector<double> a(J + 1), b(J + 1);
+  for (int k = 0; k < cols; ++k) {
+    int m = std::abs(len[k]);
+    if (m < 1) continue;
+    for (int i = 0; i < m; ++i) a[i] = al[(size_t)i * tpl + k];
+    for (int i = 0; i + 1 < m; ++i) b[i] = be[(size_t)i * tpl + k];
+    double e0, e1;
+    ciqh::tridiag_extremes(a.data(), b.data(), m, &e0, &e1);
+    emin_all = std::min(emin_all, e0);
+    emax_all = std::max(emax_all, e1);
+  }
+  *rmin = emin_all;
+  *rmax = emax_all;
+  *lmax = 1.01 * emax_all;
+  *lmin = 0.99 * emin_all;
+  if (lower_bound > 0) *lmin = std::min(*lmin, lower_bound);
+  *mvms = done_mvms;
+  if (!(*lmin > 0) || !std::isfinite(*lmax))
+    return set_err(c, CIQ_ERR_NOT_PD, "lambda_min estimate %g <= 0: operator is not positive definite", *lmin);
+  return CIQ_OK;
+}
+
+struct EvTimer {
+  cudaEvent_t e[5];
+  EvTimer() { for (auto& x : e) cudaEventCreate(&x); }
+  ~EvTimer() { for (auto& x : e) cudaEventDestroy(x); }
+};
+
+}  // namespace
+
+extern "C" {
+
+void ciq_params_default(ciq_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->Q = 8;
+  p->max_iters = 400;
+  p->tol = 1e-4;
+  p->lanczos_iters = 10;
+  p->lanczos_cols = 16;
+  p->seed = 2;
+  p->mode = CIQ_MODE_SQRT;
+  p->mvm_impl = CIQ_MVM_AUTO;
+  p->poll_every = 6;
+  p->breakdown_tol = 1e-6;
+}
+
+const char* ciq_status_string(ciq_status s) {
+  switch (s) {
+    case CIQ_OK: return "CIQ_OK";
+    case CIQ_NOT_CONVERGED: return "CIQ_NOT_CONVERGED";
+    case CIQ_ERR_INVALID_ARG: return "CIQ_ERR_INVALID_ARG";
+    case CIQ_ERR_DIM: return "CIQ_ERR_DIM";
+    case CIQ_ERR_NOT_PD: return "CIQ_ERR_NOT_PD";
+    case CIQ_ERR_ELLIPTIC: return "CIQ_ERR_ELLIPTIC";
+    case CIQ_ERR_CUDA: return "CIQ_ERR_CUDA";
+    case CIQ_ERR_NCCL: return "CIQ_ERR_NCCL";
+    case CIQ_ERR_OOM: return "CIQ_ERR_OOM";
+  }
+  return "CIQ_UNKNOWN";
+}
+
+const char* ciq_last_error(const ciq_ctx* c) { return c ? c->err.c_str() : g_init_error.c_str(); }
+
+void ciq_shard_rows(int64_t n, int32_t rank, int32_t world, int64_t* b, int64_t* e) {
+  if (world <= 1) { *b = 0; *e = n; return; }
+  int64_t per = (n + world - 1) / world;
+  per = (per + 127) / 128 * 128;
+  *b = std::min<int64_t>(n, (int64_t)rank * per);
+  *e = std::min<int64_t>(n, *b + per);
+}
+
+ciq_status ciq_quadrature_rule(double lmin, double lmax, int32_t Q, double* t, double* w) {
+  if (!t || !w || Q < 1 || Q > CIQ_MAX_Q || !(lmin > 0) || !(lmax > 0)) return CIQ_ERR_INVALID_ARG;
+  int r = ciqh::hht_rule(lmin, lmax, Q, t, w);
+  return r == 0 ? CIQ_OK : (r == -1 ? CIQ_ERR_INVALID_ARG : CIQ_ERR_ELLIPTIC);
+}
+
+ciq_status ciq_nccl_unique_id(void* out128) {
+  if (!out128) return CIQ_ERR_INVALID_ARG;
+  return nccl_unique_id(out128) ? CIQ_OK : set_err(nullptr, CIQ_ERR_NCCL, "%s", nccl_error());
+}
+
+ciq_status ciq_tridiag_extremes(const double* alpha, const double* beta, int32_t m, double* emin, double* emax) {
+  if (!alpha || (m > 1 && !beta) || m < 1 || !emin || !emax) return CIQ_ERR_INVALID_ARG;
+  return ciqh::tridiag_extremes(alpha, beta, m, emin, emax) == 0 ? CIQ_OK : CIQ_ERR_INVALID_ARG;
+}
+
+ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc, const ciq_comm* comm,
+                    void* stream) {
+  if (!out || !op) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "null ctx or operator");
+  *out = nullptr;
+  if (op->n <= 0) return set_err(nullptr, CIQ_ERR_DIM, "n must be > 0");
+  if (op->kind < CIQ_OP_DENSE || op->kind > CIQ_OP_MATERN32) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "bad kind");
+  if (!(op->diag >= 0)) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "diag must be >= 0");
+  if (op->kind == CIQ_OP_DENSE) {
+    if (!op->K) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "dense operator needs K");
+    if (op->ldk < op->n) return set_err(nullptr, CIQ_ERR_DIM, "ldk < n");
+  } else {
+    if (!op->X || !op->lengthscale) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "kernel operator needs X and lengthscale");
+    if (op->d < 1 || op->d > 16) return set_err(nullptr, CIQ_ERR_DIM, "d must be in [1, 16]");
+    if (op->ldx < op->d) return set_err(nullptr, CIQ_ERR_DIM, "ldx < d");
+    if (!(op->outputscale > 0)) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "outputscale must be > 0");
+    for (int k = 0; k < (op->ard ? op->d : 1); ++k)
+      if (!(op->lengthscale[k] > 0)) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "lengthscale must be > 0");
+  }
+  if (pc) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "preconditioner: not built yet");
+  if (comm && comm->world > 1) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "row sharding: not built yet");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return set_err(nullptr, CIQ_ERR_CUDA, "no CUDA device");
+  }
+  ciq_ctx* c = new ciq_ctx();
+  c->op = *op;
+  c->stream = reinterpret_cast<cudaStream_t>(stream);
+  c->row0 = 0;
+  c->row1 = op->n;
+  OpDev& dv = c->dev;
+  dv.kind = op->kind;
+  dv.n = op->n;
+  dv.diag = op->diag;
+  dv.o2 = op->outputscale;
+  ciq_status st = CIQ_OK;
+  if (op->kind == CIQ_OP_DENSE) {
+    if (is_device_ptr(op->K)) {
+      dv.k = op->K;
+      dv.ldk = op->ldk;
+    } else {
+      if (cudaMalloc(&c->kcopy, (size_t)op->n * op->n * 4) != cudaSuccess) { st = CIQ_ERR_OOM; goto fail; }
+      if (cudaMemcpy2D(c->kcopy, (size_t)op->n * 4, op->K, (size_t)op->ldk * 4, (size_t)op->n * 4, (size_t)op->n,
+                       cudaMemcpyHostToDevice) != cudaSuccess) { st = CIQ_ERR_CUDA; goto fail; }
+      dv.k = c->kcopy;
+      dv.ldk = op->n;
+    }
+  } else {
+    const int64_t n = op->n, d = op->d;
+    std::vector<float> xh((size_t)n * d);
+    if (is_device_ptr(op->X)) {
+      if (cudaMemcpy2D(xh.data(), d * 4, op->X, op->ldx * 4, d * 4, n, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        st = CIQ_ERR_CUDA; goto fail;
+      }
+    } else {
+      for (int64_t i = 0; i < n; ++i) std::memcpy(&xh[i * d], op->X + i * op->ldx, d * 4);
+    }
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t k = 0; k < d; ++k) xh[i * d + k] /= op->lengthscale[op->ard ? k : 0];
+    if (cudaMalloc(&c->xs, (size_t)n * d * 4) != cudaSuccess) { st = CIQ_ERR_OOM; goto fail; }
+    if (cudaMemcpy(c->xs, xh.data(), (size_t)n * d * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+      st = CIQ_ERR_CUDA; goto fail;
+    }
+    dv.xs = c->xs;
+    dv.d = (int)d;
+  }
+  *out = c;
+  return CIQ_OK;
+fail:
+  set_err(nullptr, st, "ciq_init: device allocation/copy failed: %s", cudaGetErrorString(cudaGetLastError()));
+  ciq_free(c);
+  return st;
+}
+
+void ciq_free(ciq_ctx* c) {
+  if (!c) return;
+  for (auto& t : c->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  free_workspace(c->ws);
+  free_lambda(c->lw);
+  dfree(c->xs);
+  dfree(c->kcopy);
+  dfree(c->staging);
+  delete c;
+}
+
+ciq_status ciq_matvec(ciq_ctx* c, const float* V, int64_t ldv, int64_t T, float* out, int64_t ldo, int32_t impl) {
+  if (!c || !V || !out) return CIQ_ERR_INVALID_ARG;
+  if (T <= 0 || ldv < T || ldo < T) return set_err(c, CIQ_ERR_DIM, "bad T / leading dimension");
+  const int tp = round16(T);
+  if (ensure_workspace(c, tp, std::max(1, c->ws.nq)) != CIQ_OK) return CIQ_ERR_OOM;
+  Workspace& ws = c->ws;
+  ciq_status st = load_rows(c, V, ldv, c->op.n, (int)T, ws.w[0], tp);
+  if (st != CIQ_OK) return st;
+  st = run_mvm(c, ws.w[0], tp, ws.p, nullptr, nullptr, impl);
+  if (st != CIQ_OK) return st;
+  st = store_rows(c, ws.p, tp, c->row1 - c->row0, (int)T, out, ldo);
+  if (st != CIQ_OK) return st;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return CIQ_OK;
+}
+
+ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* out, int64_t ldo,
+                     const ciq_params* pp, ciq_info* info) {
+  if (!c) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "null ctx");
+  if (!B || !out) return set_err(c, CIQ_ERR_INVALID_ARG, "null B or out");
+  ciq_params p;
+  if (pp) p = *pp; else ciq_params_default(&p);
+  if (p.Q < 1 || p.Q > CIQ_MAX_Q) return set_err(c, CIQ_ERR_INVALID_ARG, "Q must be in [1, %d]", CIQ_MAX_Q);
+  if (!(p.tol >= 0) || p.max_iters < 1) return set_err(c, CIQ_ERR_INVALID_ARG, "tol must be >= 0, max_iters >= 1");
+  if (p.mode < CIQ_MODE_SQRT || p.mode > CIQ_MODE_WHITEN) return set_err(c, CIQ_ERR_INVALID_ARG, "bad mode");
+  if (T <= 0 || ldb < T || ldo < T) return set_err(c, CIQ_ERR_DIM, "bad T / leading dimension");
+  if ((p.t == nullptr) != (p.w == nullptr)) return set_err(c, CIQ_ERR_INVALID_ARG, "t and w must be given together");
+  if (p.poll_every < 1) p.poll_every = 6;
+  if (!(p.breakdown_tol > 0)) p.breakdown_tol = 1e-6;
+  c->launches = 0;
+  c->err.clear();
+  c->profiling = p.profile_kernels != 0;
+  for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
+  c->timed.clear();
+  const int tp = round16(T);
+  const int nq = p.Q;
+  const int64_t n = c->op.n;
+  const int64_t rows = c->row1 - c->row0;
+  cudaStream_t s = c->stream;
+  ciq_status st = ensure_workspace(c, tp, nq);
+  if (st != CIQ_OK) return st;
+  Workspace& ws = c->ws;
+  const Scal& sc = ws.sc;
+  EvTimer ev;
+  CUDA_TRY(c, cudaEventRecord(ev.e[0], s));
+
+  // a1: RHS -> W[1] (= nrm_1 v_1 with nrm_1 = ||b||), zero W_prev, Y, D
+  st = load_rows(c, B, ldb, rows, (int)T, ws.w[1], tp);
+  if (st != CIQ_OK) return st;
+  CUDA_TRY(c, cudaMemsetAsync(ws.w[0], 0, (size_t)n * tp * 4, s));
+  CUDA_TRY(c, cudaMemsetAsync(ws.y, 0, (size_t)rows * tp * 4, s));
+  CUDA_TRY(c, cudaMemsetAsync(ws.d, 0, (size_t)2 * nq * rows * tp * 4, s));
+  Ctrl hctrl{};
+  hctrl.max_iters = p.max_iters;
+  hctrl.nq = nq;
+  hctrl.tp = tp;
+  hctrl.tol = p.tol;
+  hctrl.bd_tol = p.breakdown_tol;
+  CUDA_TRY(c, cudaMemcpyAsync(sc.ctrl, &hctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, s));
+  const int nbs = rowblocks(rows, tp);
+  LAUNCH(c, launch_colsq_partials(ws.w[1], rows, tp, ws.bpart, s));
+  LAUNCH(c, launch_reduce_cols(ws.bpart, nbs, tp, ws.colsq, 0, s));
+  LAUNCH(c, launch_init_state(sc, nq, tp, ws.colsq, s));
+
+  // a2/a3: spectrum estimate and quadrature rule
+  double t[CIQ_MAX_Q], w[CIQ_MAX_Q];
+  double lmin = NAN, lmax = NAN, rmin = NAN, rmax = NAN;
+  int lambda_mvms = 0;
+  CUDA_TRY(c, cudaEventRecord(ev.e[1], s));
+  if (p.t != nullptr) {
+    for (int q = 0; q < nq; ++q) { t[q] = p.t[q]; w[q] = p.w[q]; }
+  } else {
+    if (p.lambda_min > 0 && p.lambda_max > 0) {
+      lmin = p.lambda_min;
+      lmax = p.lambda_max;
+    } else {
+      st = estimate_lambda(c, &p, c->op.diag, &lmin, &lmax, &rmin, &rmax, &lambda_mvms);
+      if (st != CIQ_OK) return st;
+    }
+    int r = ciqh::hht_rule(lmin, lmax, nq, t, w);
+    if (r != 0) return set_err(c, r == -1 ? CIQ_ERR_INVALID_ARG : CIQ_ERR_ELLIPTIC, "quadrature rule failed");
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(sc.shifts, t, nq * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(sc.weights, w, nq * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaEventRecord(ev.e[2], s));
+
+  // a4-a6: msMINRES iterations
+  const int nbm = mvm_simt_blocks(rows);
+  float* dslot[2] = {ws.d, ws.d + (size_t)nq * rows * tp};
+  Ctrl hc{};
+  int j = 0;
+  for (;;) {
+    for (int k = 0; k < p.poll_every && j < p.max_iters; ++k) {
+      ++j;
+      float* wcur = ws.w[j % 3];
+      float* wprev = ws.w[(j + 2) % 3];
+      float* wnew = ws.w[(j + 1) % 3];
+      begin_timed(c, j, 0);
+      st = run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl);
+      end_timed(c);
+      if (st != CIQ_OK) return st;
+      LAUNCH(c, launch_alpha(sc, ws.apart, nbm, tp, s));
+      float* d1 = dslot[j & 1];
+      float* d2 = dslot[(j + 1) & 1];
+      begin_timed(c, j, 1);
+      LAUNCH(c, launch_lanczos_update(sc, ws.p, wcur + c->row0 * tp, wprev + c->row0 * tp, wnew + c->row0 * tp,
+                                      &d1, &d2, ws.y, nq, rows, tp, ws.bpart, 0, s));
+      end_timed(c);
+      LAUNCH(c, launch_givens(sc, ws.bpart, nbs, nq, tp, s));
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(&hc, sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (hc.done || j >= p.max_iters) break;
+  }
+  const int J = hc.iters;
+  // last pending update (step J): v_J lives in the buffer that was W_cur at iteration J
+  if (J >= 1) {
+    float* d1 = dslot[(J + 1) & 1];  // d_{J-1}
+    float* d2 = dslot[J & 1];        // d_{J-2}, overwritten by d_J
+    float* wv = ws.w[J % 3];
+    LAUNCH(c, launch_lanczos_update(sc, nullptr, nullptr, wv + c->row0 * tp, nullptr, &d1, &d2, ws.y, nq, rows, tp,
+                                    nullptr, 1, s));
+  }
+  CUDA_TRY(c, cudaEventRecord(ev.e[3], s));
+
+  // a7: finalise
+  int final_mvm = 0;
+  if (p.mode == CIQ_MODE_SQRT) {
+    // K . Y  (Y is the full vector on one GPU)
+    st = run_mvm(c, ws.y, tp, ws.p, nullptr, nullptr, p.mvm_impl);
+    if (st != CIQ_OK) return st;
+    final_mvm = 1;
+    st = store_rows(c, ws.p, tp, rows, (int)T, out, ldo);
+  } else {
+    st = store_rows(c, ws.y, tp, rows, (int)T, out, ldo);
+  }
+  if (st != CIQ_OK) return st;
+  CUDA_TRY(c, cudaEventRecord(ev.e[4], s));
+  CUDA_TRY(c, cudaEventSynchronize(ev.e[4]));
+  CUDA_TRY(c, cudaGetLastError());
+
+  const bool converged = (p.tol == 0) || (hc.max_relres <= p.tol) || (hc.breakdown > 0 && hc.done && J < p.max_iters);
+  if (info) {
+    std::memset(info, 0, sizeof(*info));
+    info->iters = J;
+    info->mvms = lambda_mvms + J + final_mvm;
+    info->converged = converged ? 1 : 0;
+    info->rotated = c->has_precond ? 1 : 0;
+    info->breakdown_cols = hc.breakdown;
+    info->Q = nq;
+    info->lambda_min = lmin;
+    info->lambda_max = lmax;
+    info->ritz_min = rmin;
+    info->ritz_max = rmax;
+    info->max_rel_residual = hc.max_relres;
+    for (int q = 0; q < nq; ++q) { info->t[q] = t[q]; info->w[q] = w[q]; }
+    cudaEventElapsedTime(&info->ms_total, ev.e[0], ev.e[4]);
+    cudaEventElapsedTime(&info->ms_lambda, ev.e[1], ev.e[2]);
+    cudaEventElapsedTime(&info->ms_loop, ev.e[2], ev.e[3]);
+    cudaEventElapsedTime(&info->ms_final, ev.e[3], ev.e[4]);
+    info->kernel_launches = c->launches;
+    for (auto& tm : c->timed) {
+      if (tm.j > J) continue;  // iterations launched after convergence are no-ops
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tm.a, tm.b);
+      if (tm.kind == 0) { info->ms_mvm += ms; ++info->mvm_timed; }
+      else { info->ms_update += ms; ++info->update_timed; }
+    }
+  }
+  return converged ? CIQ_OK : CIQ_NOT_CONVERGED;
+}
+
+}  // extern "C"

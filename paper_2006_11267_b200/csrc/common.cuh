@@ -1,0 +1,44 @@
+// common.cuh -- shared device helpers of libciq (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define CIQ_DEVICE __device__ __forceinline__
+
+namespace ciq {
+
+constexpr int kWarp = 32;
+
+CIQ_DEVICE float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+CIQ_DEVICE double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+CIQ_DEVICE double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Control block of one solve (device memory).  Kernels of an iteration return immediately once
+// `done` is set, so iterations launched past convergence are no-ops.
+struct Ctrl {
+  int done;        // 1 once the stopping rule fired (or max_iters reached)
+  int iters;       // msMINRES steps whose Givens coefficients have been computed (J so far)
+  int pending;     // 1 if the descent update of step `iters` has not been applied yet
+  int breakdown;   // columns frozen on an invariant subspace
+  int max_iters;
+  int nq;
+  int tp;          // padded number of columns
+  int pad_;
+  double tol;
+  double bd_tol;
+  double max_relres;
+};
+
+}  // namespace ciq

@@ -1,0 +1,73 @@
+// internal.h -- launchers shared between the C-ABI layer (ciq_api.cu) and the kernel files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace ciq {
+
+// The operator as seen by the MVM kernels (device pointers).
+struct OpDev {
+  int kind;            // ciq_op_kind
+  int64_t n;           // global N
+  int d;               // point dimension (kernels)
+  const float* xs;     // N x d points scaled by 1/lengthscale (row-major, ld = d)
+  const float* k;      // dense: N x N (row-major, ld = ldk)
+  int64_t ldk;
+  float o2;            // outputscale
+  float diag;          // sigma^2 added to the diagonal
+};
+
+// Per-solve scalar state (device), one allocation; see recurrence.cu.
+struct Scal {
+  double* beta1;      // [tp]   ||b_c||
+  double* nrm_prev;   // [tp]   nrm_{j-1}: v_{j-1} = W_prev / nrm_{j-1}
+  double* nrm_cur;    // [tp]   nrm_j:     v_j     = W_cur  / nrm_j
+  double* tb_cur;     // [tp]   T-matrix off-diagonal beta_j (0 at j = 1)
+  double* alpha;      // [tp]   alpha_j
+  int* frozen;        // [tp]   1: column finished (b = 0 or invariant subspace)
+  double* c1; double* s1; double* c2; double* s2; double* phibar;   // [Q][tp] Givens state
+  float* ca; float* cb; float* ce; float* cf;                       // [Q][tp] pending-update coefs
+  double* shifts;     // [Q]
+  double* weights;    // [Q]
+  Ctrl* ctrl;
+};
+
+// ---- MVM (mvm_simt.cu / mvm_tc.cu) ----
+// P[i - row0][c] = sum_j K[i][j] V[j][c] + diag V[i][c] for rows [row0, row1), columns [0, tp).
+// alpha_part (may be null): [nblk][tp] partials sum_{i in block} V[i][c] P[i][c]; nblk is
+// returned by mvm_simt_blocks.  done (may be null): skip when *done != 0.
+int mvm_simt_blocks(int64_t rows);
+cudaError_t launch_mvm_simt(const OpDev& op, const float* v, int tp, int64_t row0, int64_t row1,
+                            float* p, int ldp, double* alpha_part, const Ctrl* done, cudaStream_t s);
+
+// ---- vector kernels (recurrence.cu) ----
+int rowblocks(int64_t rows, int tp);   // number of CTAs of the row-streaming kernels
+cudaError_t launch_load_block(const float* src, int64_t ld_src, int64_t rows, int cols, float* dst, int tp,
+                              cudaStream_t s);
+cudaError_t launch_store_block(const float* src, int tp, int64_t rows, int cols, float* dst, int64_t ld_dst,
+                               cudaStream_t s);
+cudaError_t launch_randn_fill(float* dst, int64_t rows, int cols, int tp, int64_t row_offset, uint64_t seed,
+                              cudaStream_t s);
+cudaError_t launch_colsq_partials(const float* v, int64_t rows, int tp, double* part, cudaStream_t s);
+cudaError_t launch_reduce_cols(const double* part, int nblk, int m, double* out, int op_sqrt, cudaStream_t s);
+cudaError_t launch_scale_cols(float* v, int64_t rows, int tp, const double* nrm, cudaStream_t s);
+cudaError_t launch_init_state(const Scal& sc, int nq, int tp, const double* colsq, cudaStream_t s);
+cudaError_t launch_alpha(const Scal& sc, const double* apart, int nblk, int tp, cudaStream_t s);
+cudaError_t launch_lanczos_update(const Scal& sc, const float* p, const float* wcur, const float* wprev,
+                                  float* wnew, float* const* d1, float* const* d2, float* y, int nq,
+                                  int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s);
+cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s);
+// Lambda-estimation Lanczos (full re-orthogonalisation)
+cudaError_t launch_basis_dots(const float* basis, int nb, int64_t rows, int tp, const float* p, double* part,
+                              cudaStream_t s);
+cudaError_t launch_basis_axpy(const float* basis, int nb, int64_t rows, int tp, const double* h, float* p,
+                              cudaStream_t s);
+cudaError_t launch_lanczos_coeffs(const double* h1, const double* h2, const double* bsq, int j, int nb_total,
+                                  int tp, double bd_tol, double* alphas, double* betas, int* len,
+                                  double* inv_beta, cudaStream_t s);
+cudaError_t launch_scale_cols_by(const float* src, float* dst, int64_t rows, int tp, const double* inv,
+                                 cudaStream_t s);
+
+}  // namespace ciq

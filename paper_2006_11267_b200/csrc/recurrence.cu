@@ -1,0 +1,474 @@
+// recurrence.cu -- the msMINRES recurrence around the MVM.
+//
+// Per iteration j ("a single MVM ... all subsequent operations are O(N)"; the shifted
+// QR of eq. minres_qr_shifted; vectorised over shifts as P:1379 suggests):
+//
+//   MVM_j      P = K W_cur                       (W_cur = nrm_j v_j: Lanczos vectors are kept
+//                                                 UNnormalised, the 1/nrm_j is folded in below)
+//   alpha_j    alpha = (sum_blocks W_cur.P) / nrm_j^2                         [1 CTA]
+//   update_j   w_j = P/nrm_j - alpha v_j - (beta_j/nrm_{j-1}) W_prev ; beta_{j+1}^2 partials
+//              + the descent update of step j-1 for every shift q:
+//                d_q = (v_{j-1} - delta d1_q - eps d2_q)/gamma ;  Y += w_q phi_q d_q      [stream]
+//   givens_j   beta_{j+1}; per (q, column) Givens rotation of [T_j + t_q I; beta_{j+1} e_j^T];
+//              coefficients of step j's update; stopping rule; invariant-subspace freeze  [1 CTA]
+//
+// so one streaming pass over N x T x (3Q + 6) words per iteration carries both the Lanczos step
+// and all Q shifted solution updates (eq. minres_descent), and Y = sum_q w_q x_q is
+// accumulated in place (eq. contour_integral_quad) -- the x_q are never stored.
+// All reductions are fixed-order (fp64 across CTAs): deterministic.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "internal.h"
+
+namespace ciq {
+namespace {
+
+constexpr int kRowsPerCta = 64;   // rows covered by one CTA of the streaming kernels
+constexpr int kThreads = 256;
+constexpr int kChunk = 1024;      // columns per CTA (grid.y covers the rest)
+
+// Geometry of a streaming CTA: tpr threads per row (one float4 column quad each), rpp rows per pass.
+struct Geo {
+  int cc, tpr, rpp;
+  CIQ_DEVICE Geo(int tp) {
+    int c0 = blockIdx.y * kChunk;
+    cc = min(kChunk, tp - c0);
+    tpr = cc / 4;
+    rpp = kThreads / tpr;
+  }
+};
+
+// Fixed-order CTA reduction of per-thread column-quad partials into part[blockIdx.x][c].
+CIQ_DEVICE void cta_col_reduce(const Geo& g, int tp, const double (&acc)[4], double* part) {
+  __shared__ double sums[kChunk];   // rpp * tpr * 4 <= 1024
+  const int tid = threadIdx.x;
+  const int lane_row = tid / g.tpr, quad = tid % g.tpr;
+  __syncthreads();
+  for (int r = 0; r < g.rpp; ++r) {
+    if (lane_row == r && lane_row < g.rpp) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double prev = (r == 0) ? 0.0 : sums[quad * 4 + k];
+        sums[quad * 4 + k] = prev + acc[k];
+      }
+    }
+    __syncthreads();
+  }
+  const int c0 = blockIdx.y * kChunk;
+  for (int c = tid; c < g.cc; c += kThreads) part[(int64_t)blockIdx.x * tp + c0 + c] = sums[c];
+}
+
+__global__ void __launch_bounds__(kThreads) colsq_kernel(const float* __restrict__ v, int64_t rows, int tp,
+                                                         double* __restrict__ part) {
+  Geo g(tp);
+  const int tid = threadIdx.x;
+  const int lane_row = tid / g.tpr, quad = tid % g.tpr;
+  const int c = blockIdx.y * kChunk + quad * 4;
+  double acc[4] = {0, 0, 0, 0};
+  if (lane_row < g.rpp) {
+    int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta;
+    for (int64_t i = r0 + lane_row; i < min(rows, r0 + kRowsPerCta); i += g.rpp) {
+      float4 x = *reinterpret_cast<const float4*>(v + i * tp + c);
+      acc[0] += (double)x.x * x.x; acc[1] += (double)x.y * x.y;
+      acc[2] += (double)x.z * x.z; acc[3] += (double)x.w * x.w;
+    }
+  }
+  cta_col_reduce(g, tp, acc, part);
+}
+
+// out[c] = sum_b part[b][c] in fixed order; one warp per column.  op_sqrt: out = sqrt(sum).
+__global__ void reduce_cols_kernel(const double* __restrict__ part, int nblk, int m, double* __restrict__ out,
+                                   int op_sqrt) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
+  if (warp >= m) return;
+  double s = 0.0;
+  for (int b = lane; b < nblk; b += 32) s += part[(int64_t)b * m + warp];
+  s = warp_sum(s);
+  if (lane == 0) out[warp] = op_sqrt ? sqrt(s) : s;
+}
+
+__global__ void load_block_kernel(const float* __restrict__ src, int64_t ld, int64_t rows, int cols,
+                                  float* __restrict__ dst, int tp) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * tp) return;
+  int64_t i = e / tp;
+  int c = (int)(e % tp);
+  dst[e] = (c < cols) ? src[i * ld + c] : 0.f;
+}
+
+__global__ void store_block_kernel(const float* __restrict__ src, int tp, int64_t rows, int cols,
+                                   float* __restrict__ dst, int64_t ld) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  int64_t i = e / cols;
+  int c = (int)(e % cols);
+  dst[i * ld + c] = src[i * tp + c];
+}
+
+CIQ_DEVICE uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// Counter-based N(0,1): element (global row, column) -> Box-Muller of two 53-bit uniforms.
+__global__ void randn_kernel(float* __restrict__ dst, int64_t rows, int cols, int tp, int64_t row_offset,
+                             uint64_t seed) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * tp) return;
+  int64_t i = e / tp;
+  int c = (int)(e % tp);
+  if (c >= cols) { dst[e] = 0.f; return; }
+  uint64_t key = seed * 0x100000001B3ull ^ ((uint64_t)(i + row_offset) << 20) ^ (uint64_t)c;
+  uint64_t a = splitmix64(key), b = splitmix64(key ^ 0xD1B54A32D192ED03ull);
+  double u1 = ((a >> 11) + 1.0) * (1.0 / 9007199254740993.0);
+  double u2 = (b >> 11) * (1.0 / 9007199254740992.0);
+  dst[e] = (float)(sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2));
+}
+
+__global__ void scale_cols_kernel(float* __restrict__ v, int64_t rows, int tp, const double* __restrict__ nrm) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * tp) return;
+  double s = nrm[e % tp];
+  v[e] = (s > 0) ? (float)(v[e] / s) : 0.f;
+}
+
+__global__ void scale_cols_by_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t rows, int tp,
+                                     const double* __restrict__ inv) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * tp) return;
+  dst[e] = (float)(src[e] * inv[e % tp]);
+}
+
+// Initial state of a solve from colsq[c] = ||b_c||^2.
+__global__ void init_state_kernel(Scal sc, int nq, int tp, const double* __restrict__ colsq) {
+  for (int c = threadIdx.x; c < tp; c += blockDim.x) {
+    double b1 = sqrt(colsq[c]);
+    sc.beta1[c] = b1;
+    sc.nrm_cur[c] = (b1 > 0) ? b1 : 1.0;
+    sc.nrm_prev[c] = 1.0;
+    sc.tb_cur[c] = 0.0;
+    sc.alpha[c] = 0.0;
+    sc.frozen[c] = (b1 > 0) ? 0 : 1;
+    for (int q = 0; q < nq; ++q) {
+      int k = q * tp + c;
+      sc.c1[k] = 1.0; sc.s1[k] = 0.0; sc.c2[k] = 1.0; sc.s2[k] = 0.0;
+      sc.phibar[k] = b1;
+      sc.ca[k] = 0.f; sc.cb[k] = 0.f; sc.ce[k] = 0.f; sc.cf[k] = 0.f;
+    }
+  }
+  if (threadIdx.x == 0) {
+    sc.ctrl->done = 0;
+    sc.ctrl->iters = 0;
+    sc.ctrl->pending = 0;
+    sc.ctrl->breakdown = 0;
+    sc.ctrl->max_relres = 0.0;
+  }
+}
+
+// alpha_j = (sum_b W_cur.P partials) / nrm_j^2.  One warp per column, fixed order.
+__global__ void alpha_kernel(Scal sc, const double* __restrict__ apart, int nblk, int tp) {
+  if (sc.ctrl->done) return;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
+  for (int c = warp; c < tp; c += nw) {
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += apart[(int64_t)b * tp + c];
+    s = warp_sum(s);
+    if (lane == 0) {
+      double nr = sc.nrm_cur[c];
+      sc.alpha[c] = sc.frozen[c] ? 0.0 : s / (nr * nr);
+    }
+  }
+}
+
+// The streaming pass (see file header).  final_only: apply the pending update of the last step
+// only (wprev = the buffer holding nrm_J v_J).
+__global__ void __launch_bounds__(kThreads) lanczos_update_kernel(
+    Scal sc, const float* __restrict__ p, const float* __restrict__ wcur, const float* __restrict__ wprev,
+    float* __restrict__ wnew, const float* __restrict__ d1base, float* __restrict__ d2base, int64_t qstride,
+    float* __restrict__ y, int nq, int64_t rows, int tp, double* __restrict__ bpart, int final_only) {
+  const Ctrl* ctrl = sc.ctrl;
+  if (!final_only && ctrl->done) return;
+  const int pending = ctrl->pending;
+  Geo g(tp);
+  const int tid = threadIdx.x;
+  const int lane_row = tid / g.tpr, quad = tid % g.tpr;
+  const int c = blockIdx.y * kChunk + quad * 4;
+  double acc[4] = {0, 0, 0, 0};
+  if (lane_row < g.rpp) {
+    float inv_nrm[4], alpha[4], cprev[4];
+    if (!final_only) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        int cc = c + k;
+        bool fr = sc.frozen[cc] != 0;
+        inv_nrm[k] = fr ? 0.f : (float)(1.0 / sc.nrm_cur[cc]);
+        alpha[k] = fr ? 0.f : (float)sc.alpha[cc];
+        cprev[k] = fr ? 0.f : (float)(sc.tb_cur[cc] / sc.nrm_prev[cc]);
+      }
+    }
+    int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta;
+    int64_t r1 = min(rows, r0 + kRowsPerCta);
+    for (int64_t i = r0 + lane_row; i < r1; i += g.rpp) {
+      const int64_t off = i * tp + c;
+      float4 wp = *reinterpret_cast<const float4*>(wprev + off);
+      if (!final_only) {
+        float4 pp = *reinterpret_cast<const float4*>(p + off);
+        float4 wc = *reinterpret_cast<const float4*>(wcur + off);
+        float4 w;
+        w.x = fmaf(-cprev[0], wp.x, (pp.x - alpha[0] * wc.x) * inv_nrm[0]);
+        w.y = fmaf(-cprev[1], wp.y, (pp.y - alpha[1] * wc.y) * inv_nrm[1]);
+        w.z = fmaf(-cprev[2], wp.z, (pp.z - alpha[2] * wc.z) * inv_nrm[2]);
+        w.w = fmaf(-cprev[3], wp.w, (pp.w - alpha[3] * wc.w) * inv_nrm[3]);
+        *reinterpret_cast<float4*>(wnew + off) = w;
+        acc[0] += (double)w.x * w.x; acc[1] += (double)w.y * w.y;
+        acc[2] += (double)w.z * w.z; acc[3] += (double)w.w * w.w;
+      }
+      if (pending) {
+        float4 yy = *reinterpret_cast<const float4*>(y + off);
+        for (int q = 0; q < nq; ++q) {
+          const int k = q * tp + c;
+          float4 a = *reinterpret_cast<const float4*>(sc.ca + k);
+          float4 b = *reinterpret_cast<const float4*>(sc.cb + k);
+          float4 e = *reinterpret_cast<const float4*>(sc.ce + k);
+          float4 f = *reinterpret_cast<const float4*>(sc.cf + k);
+          float4 x1 = *reinterpret_cast<const float4*>(d1base + q * qstride + off);
+          float4 x2 = *reinterpret_cast<const float4*>(d2base + q * qstride + off);
+          float4 dn;
+          dn.x = fmaf(a.x, wp.x, fmaf(b.x, x1.x, e.x * x2.x));
+          dn.y = fmaf(a.y, wp.y, fmaf(b.y, x1.y, e.y * x2.y));
+          dn.z = fmaf(a.z, wp.z, fmaf(b.z, x1.z, e.z * x2.z));
+          dn.w = fmaf(a.w, wp.w, fmaf(b.w, x1.w, e.w * x2.w));
+          *reinterpret_cast<float4*>(d2base + q * qstride + off) = dn;
+          yy.x = fmaf(f.x, dn.x, yy.x); yy.y = fmaf(f.y, dn.y, yy.y);
+          yy.z = fmaf(f.z, dn.z, yy.z); yy.w = fmaf(f.w, dn.w, yy.w);
+        }
+        *reinterpret_cast<float4*>(y + off) = yy;
+      }
+    }
+  }
+  if (!final_only) cta_col_reduce(g, tp, acc, bpart);
+}
+
+// beta_{j+1}, Givens rotations of step j for every (shift, column), coefficients of step j's
+// descent update, stopping rule.  One CTA; warp per column, lanes over shifts.
+__global__ void givens_kernel(Scal sc, const double* __restrict__ bpart, int nblk, int nq, int tp) {
+  Ctrl* ctrl = sc.ctrl;
+  if (ctrl->done) return;
+  __shared__ double s_rel[32];
+  __shared__ int s_act[32], s_brk[32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
+  double my_rel = 0.0;
+  int my_act = 0, my_brk = 0;
+  for (int c = warp; c < tp; c += nw) {
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += bpart[(int64_t)b * tp + c];
+    s = warp_sum(s);
+    const double tbn = sqrt(s);                  // beta_{j+1}
+    const bool frozen = sc.frozen[c] != 0;
+    const double a_j = sc.alpha[c], tb = sc.tb_cur[c], nrm = sc.nrm_cur[c], b1 = sc.beta1[c];
+    double rel = 0.0;
+    for (int q = lane; q < nq; q += 32) {
+      const int k = q * tp + c;
+      if (frozen) {
+        sc.ca[k] = 0.f; sc.cb[k] = 0.f; sc.ce[k] = 0.f; sc.cf[k] = 0.f;
+        continue;
+      }
+      const double a = a_j + sc.shifts[q];
+      const double c1 = sc.c1[k], s1 = sc.s1[k], c2 = sc.c2[k], s2 = sc.s2[k];
+      const double eps = s2 * tb;
+      const double dp = c2 * tb;
+      const double delta = c1 * dp + s1 * a;
+      const double gbar = -s1 * dp + c1 * a;
+      const double gamma = hypot(gbar, tbn);
+      const double cs = gbar / gamma, sn = tbn / gamma;
+      const double phib = sc.phibar[k];
+      const double phi = cs * phib;
+      const double phib_new = -sn * phib;
+      sc.phibar[k] = phib_new;
+      sc.ca[k] = (float)(1.0 / (gamma * nrm));   // d = (v_j - delta d1 - eps d2)/gamma, v_j = W/nrm
+      sc.cb[k] = (float)(-delta / gamma);
+      sc.ce[k] = (float)(-eps / gamma);
+      sc.cf[k] = (float)(sc.weights[q] * phi);   // Y += w_q phi d
+      sc.c2[k] = c1; sc.s2[k] = s1; sc.c1[k] = cs; sc.s1[k] = sn;
+      rel = fmax(rel, fabs(phib_new) / b1);
+    }
+    rel = warp_max(rel);
+    if (lane == 0) {
+      if (!frozen) {
+        const bool broke = tbn <= ctrl->bd_tol * (fabs(a_j) + tb);
+        if (broke) {
+          sc.frozen[c] = 1;
+          ++my_brk;
+        } else {
+          my_rel = fmax(my_rel, rel);
+          ++my_act;
+        }
+        sc.nrm_prev[c] = nrm;
+        sc.nrm_cur[c] = broke ? 1.0 : tbn;
+        sc.tb_cur[c] = tbn;
+      }
+    }
+  }
+  if (lane == 0) { s_rel[warp] = my_rel; s_act[warp] = my_act; s_brk[warp] = my_brk; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double rel = 0.0;
+    int act = 0, brk = 0;
+    for (int w = 0; w < nw; ++w) { rel = fmax(rel, s_rel[w]); act += s_act[w]; brk += s_brk[w]; }
+    const int j = ctrl->iters + 1;
+    ctrl->iters = j;
+    ctrl->pending = 1;
+    ctrl->breakdown += brk;
+    ctrl->max_relres = rel;
+    if (act == 0 || (ctrl->tol > 0 && rel <= ctrl->tol) || j >= ctrl->max_iters) ctrl->done = 1;
+  }
+}
+
+// ---- lambda-estimation Lanczos with full re-orthogonalisation ----
+
+// part[b][k][c] = sum_{i in block b} basis_k[i][c] p[i][c],  k < nb.  basis: [nb][rows][tp].
+__global__ void __launch_bounds__(kThreads) basis_dots_kernel(const float* __restrict__ basis, int nb,
+                                                              int64_t rows, int tp, const float* __restrict__ p,
+                                                              double* __restrict__ part) {
+  // tp is small here (lanczos_cols <= 64): one thread per (row-lane, column)
+  __shared__ double sh[kThreads];
+  const int tid = threadIdx.x;
+  const int rl = tid / tp, c = tid % tp, rpp = kThreads / tp;
+  int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta;
+  int64_t r1 = min(rows, r0 + kRowsPerCta);
+  for (int k = 0; k < nb; ++k) {
+    double acc = 0.0;
+    if (rl < rpp)
+      for (int64_t i = r0 + rl; i < r1; i += rpp)
+        acc += (double)basis[((int64_t)k * rows + i) * tp + c] * p[i * tp + c];
+    sh[tid] = acc;
+    __syncthreads();
+    if (tid < tp) {
+      double s = 0.0;
+      for (int r = 0; r < rpp; ++r) s += sh[r * tp + tid];
+      part[((int64_t)blockIdx.x * nb + k) * tp + tid] = s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void basis_axpy_kernel(const float* __restrict__ basis, int nb, int64_t rows, int tp,
+                                  const double* __restrict__ h, float* __restrict__ p) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * tp) return;
+  int c = (int)(e % tp);
+  double s = 0.0;
+  for (int k = 0; k < nb; ++k) s += h[k * tp + c] * (double)basis[(int64_t)k * rows * tp + e];
+  p[e] = (float)(p[e] - s);
+}
+
+// alpha_j = h1[j] + h2[j] (CGS twice), beta = ||w||, breakdown per column, 1/beta for the scale.
+__global__ void lanczos_coeffs_kernel(const double* __restrict__ h1, const double* __restrict__ h2,
+                                      const double* __restrict__ bsq, int j, int tp, double bd_tol,
+                                      double* __restrict__ alphas, double* __restrict__ betas, int* __restrict__ len,
+                                      double* __restrict__ inv_beta) {
+  for (int c = threadIdx.x; c < tp; c += blockDim.x) {
+    double inv = 0.0;
+    if (len[c] == j) {  // column still active
+      double a = h1[j * tp + c] + h2[j * tp + c];
+      double b = sqrt(bsq[c]);
+      alphas[j * tp + c] = a;
+      len[c] = j + 1;
+      double bprev = (j > 0) ? betas[(j - 1) * tp + c] : 0.0;
+      if (b > bd_tol * (fabs(a) + bprev)) {
+        betas[j * tp + c] = b;
+        inv = 1.0 / b;
+      } else {
+        betas[j * tp + c] = 0.0;
+        len[c] = -(j + 1);   // stopped: T_J has j+1 rows
+      }
+    }
+    inv_beta[c] = inv;
+  }
+}
+
+inline unsigned nb_elem(int64_t e, int bs) { return (unsigned)((e + bs - 1) / bs); }
+
+}  // namespace
+
+int rowblocks(int64_t rows, int /*tp*/) { return (int)((rows + kRowsPerCta - 1) / kRowsPerCta); }
+
+static dim3 stream_grid(int64_t rows, int tp) {
+  return dim3((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((tp + kChunk - 1) / kChunk));
+}
+
+cudaError_t launch_load_block(const float* src, int64_t ld_src, int64_t rows, int cols, float* dst, int tp,
+                              cudaStream_t s) {
+  load_block_kernel<<<nb_elem(rows * tp, 256), 256, 0, s>>>(src, ld_src, rows, cols, dst, tp);
+  return cudaGetLastError();
+}
+cudaError_t launch_store_block(const float* src, int tp, int64_t rows, int cols, float* dst, int64_t ld_dst,
+                               cudaStream_t s) {
+  store_block_kernel<<<nb_elem(rows * cols, 256), 256, 0, s>>>(src, tp, rows, cols, dst, ld_dst);
+  return cudaGetLastError();
+}
+cudaError_t launch_randn_fill(float* dst, int64_t rows, int cols, int tp, int64_t row_offset, uint64_t seed,
+                              cudaStream_t s) {
+  randn_kernel<<<nb_elem(rows * tp, 256), 256, 0, s>>>(dst, rows, cols, tp, row_offset, seed);
+  return cudaGetLastError();
+}
+cudaError_t launch_colsq_partials(const float* v, int64_t rows, int tp, double* part, cudaStream_t s) {
+  colsq_kernel<<<stream_grid(rows, tp), kThreads, 0, s>>>(v, rows, tp, part);
+  return cudaGetLastError();
+}
+cudaError_t launch_reduce_cols(const double* part, int nblk, int m, double* out, int op_sqrt, cudaStream_t s) {
+  reduce_cols_kernel<<<nb_elem((int64_t)m * 32, 256), 256, 0, s>>>(part, nblk, m, out, op_sqrt);
+  return cudaGetLastError();
+}
+cudaError_t launch_scale_cols(float* v, int64_t rows, int tp, const double* nrm, cudaStream_t s) {
+  scale_cols_kernel<<<nb_elem(rows * tp, 256), 256, 0, s>>>(v, rows, tp, nrm);
+  return cudaGetLastError();
+}
+cudaError_t launch_scale_cols_by(const float* src, float* dst, int64_t rows, int tp, const double* inv,
+                                 cudaStream_t s) {
+  scale_cols_by_kernel<<<nb_elem(rows * tp, 256), 256, 0, s>>>(src, dst, rows, tp, inv);
+  return cudaGetLastError();
+}
+cudaError_t launch_init_state(const Scal& sc, int nq, int tp, const double* colsq, cudaStream_t s) {
+  init_state_kernel<<<1, 256, 0, s>>>(sc, nq, tp, colsq);
+  return cudaGetLastError();
+}
+cudaError_t launch_alpha(const Scal& sc, const double* apart, int nblk, int tp, cudaStream_t s) {
+  alpha_kernel<<<1, 1024, 0, s>>>(sc, apart, nblk, tp);
+  return cudaGetLastError();
+}
+cudaError_t launch_lanczos_update(const Scal& sc, const float* p, const float* wcur, const float* wprev,
+                                  float* wnew, float* const* d1, float* const* d2, float* y, int nq,
+                                  int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s) {
+  const int64_t qstride = rows * tp;
+  lanczos_update_kernel<<<stream_grid(rows, tp), kThreads, 0, s>>>(sc, p, wcur, wprev, wnew, d1[0], d2[0],
+                                                                    qstride, y, nq, rows, tp, bpart, final_only);
+  return cudaGetLastError();
+}
+cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s) {
+  givens_kernel<<<1, 1024, 0, s>>>(sc, bpart, nblk, nq, tp);
+  return cudaGetLastError();
+}
+cudaError_t launch_basis_dots(const float* basis, int nb, int64_t rows, int tp, const float* p, double* part,
+                              cudaStream_t s) {
+  if (tp > kThreads) return cudaErrorInvalidValue;
+  basis_dots_kernel<<<(unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), kThreads, 0, s>>>(basis, nb, rows, tp,
+                                                                                             p, part);
+  return cudaGetLastError();
+}
+cudaError_t launch_basis_axpy(const float* basis, int nb, int64_t rows, int tp, const double* h, float* p,
+                              cudaStream_t s) {
+  basis_axpy_kernel<<<nb_elem(rows * tp, 256), 256, 0, s>>>(basis, nb, rows, tp, h, p);
+  return cudaGetLastError();
+}
+cudaError_t launch_lanczos_coeffs(const double* h1, const double* h2, const double* bsq, int j, int /*nb_total*/,
+                                  int tp, double bd_tol, double* alphas, double* betas, int* len, double* inv_beta,
+                                  cudaStream_t s) {
+  lanczos_coeffs_kernel<<<1, 256, 0, s>>>(h1, h2, bsq, j, tp, bd_tol, alphas, betas, len, inv_beta);
+  return cudaGetLastError();
+}
+
+}  // namespace ciq
