@@ -147,6 +147,8 @@ typedef struct {
   int32_t mvm_timed;          /*   number of loop MVMs timed (= iters)                          */
   float ms_update;            /* profile_kernels: summed device time of the streaming updates    */
   int32_t update_timed;
+  int32_t mvm_impl_used;      /* ciq_mvm_impl of the loop MVMs: CIQ_MVM_SIMT or CIQ_MVM_TC       */
+  int32_t mvm_splits;         /* column splits of the tensor-core MVM grid (1 = none)            */
 } ciq_info;
 
 typedef struct ciq_ctx ciq_ctx;

@@ -67,7 +67,8 @@ class CiqInfo(ctypes.Structure):
                 ("ritz_min", c_double), ("ritz_max", c_double), ("max_rel_residual", c_double),
                 ("t", c_double * CIQ_MAX_Q), ("w", c_double * CIQ_MAX_Q), ("ms_total", c_float),
                 ("ms_lambda", c_float), ("ms_loop", c_float), ("ms_final", c_float), ("kernel_launches", c_int64),
-                ("ms_mvm", c_float), ("mvm_timed", c_int32), ("ms_update", c_float), ("update_timed", c_int32)]
+                ("ms_mvm", c_float), ("mvm_timed", c_int32), ("ms_update", c_float), ("update_timed", c_int32),
+                ("mvm_impl_used", c_int32), ("mvm_splits", c_int32)]
 
     def as_dict(self) -> dict:
         q = self.Q
@@ -78,7 +79,8 @@ class CiqInfo(ctypes.Structure):
                 "t": list(self.t[:q]), "w": list(self.w[:q]), "ms_total": self.ms_total,
                 "ms_lambda": self.ms_lambda, "ms_loop": self.ms_loop, "ms_final": self.ms_final,
                 "kernel_launches": self.kernel_launches, "ms_mvm": self.ms_mvm, "mvm_timed": self.mvm_timed,
-                "ms_update": self.ms_update, "update_timed": self.update_timed}
+                "ms_update": self.ms_update, "update_timed": self.update_timed,
+                "mvm_impl_used": {1: "simt", 2: "tc"}.get(self.mvm_impl_used, "none"), "mvm_splits": self.mvm_splits}
 
 
 def _load() -> ctypes.CDLL:

@@ -3,6 +3,7 @@
 // host) -> host HHT rule -> J iterations of [MVM, alpha, streaming update, Givens] with a device
 // convergence flag polled every `poll_every` iterations -> last pending update -> (SQRT) one more
 // MVM -> output.  Every step of the path runs in this library's kernels.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -66,6 +67,21 @@ struct ciq_ctx {
   Workspace ws;
   LambdaWork lw;
   float* staging = nullptr;   // host-pointer staging (rows x tp)
+  // tensor-core MVM operands
+  bool tc_ok = false;
+  int64_t npad = 0;
+  __half* feat_a = nullptr;   // [npad/8][4][8][8]
+  __half* feat_b = nullptr;
+  __half* planes = nullptr;   // split V planes, grown on demand
+  size_t planes_elems = 0;
+  float* inv_scale = nullptr;
+  int inv_scale_n = 0;
+  float* psplit = nullptr;    // nsplit x rows x tp partial products
+  size_t psplit_elems = 0;
+  double* apart_tc = nullptr;
+  size_t apart_tc_elems = 0;
+  int last_nsplit = 1;
+  int mvm_kind_used = 0;      // 1 simt, 2 tc (of the last loop MVM)
   int64_t staging_elems = 0;
   std::string err;
   int64_t launches = 0;
@@ -228,10 +244,162 @@ void end_timed(ciq_ctx* c) {
   cudaEventRecord(c->timed.back().b, c->stream);
 }
 
-ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, const Ctrl* done, int impl) {
-  (void)impl;  // tensor-core path selected here once available (mvm_tc.cu)
-  LAUNCH(c, launch_mvm_simt(c->dev, v, tp, c->row0, c->row1, p, tp, apart, done, c->stream));
+template <class T>
+ciq_status grow(ciq_ctx* c, T** buf, size_t* cap, size_t need) {
+  if (*cap >= need) return CIQ_OK;
+  dfree(*buf);
+  CUDA_TRY(c, dalloc(buf, need));
+  *cap = need;
   return CIQ_OK;
+}
+
+bool use_tc(const ciq_ctx* c, int impl) {
+  if (impl == CIQ_MVM_SIMT) return false;
+  return c->tc_ok;
+}
+
+// Number of column-splits of the J range so that (row tiles x chunks x splits) fills whole waves
+// of 148 SMs (1 CTA / SM: the kernel owns all 512 TMEM columns).
+int choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm) {
+  const int64_t rt = (rows + 127) / 128;
+  const int64_t ntiles = (n + 127) / 128;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 8; ++s) {
+    if (ntiles / s < 4) break;
+    const int64_t units = rt * chunks * s;
+    const int64_t waves = (units + nsm - 1) / nsm;
+    const double eff = (double)units / (double)(waves * nsm);
+    if (eff > best_eff + 0.02) { best_eff = eff; best = s; }
+  }
+  return best;
+}
+
+// P (+ alpha partials) <- K V.  With the tensor-core path the result may be split into
+// `*nsplit_out` partial products (stride rows*tp) when allow_split; otherwise it is complete.
+ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, const Ctrl* done, int impl,
+                   const double* nrm = nullptr, bool allow_split = false, int* nsplit_out = nullptr,
+                   double** apart_used = nullptr, int* apart_nblk = nullptr) {
+  const int64_t rows = c->row1 - c->row0;
+  if (nsplit_out) *nsplit_out = 1;
+  if (!use_tc(c, impl)) {
+    if (impl == CIQ_MVM_TC)
+      return set_err(c, CIQ_ERR_INVALID_ARG, "tensor-core MVM unavailable for this operator (dense, d > 8 or huge features)");
+    LAUNCH(c, launch_mvm_simt(c->dev, v, tp, c->row0, c->row1, p, tp, apart, done, c->stream));
+    if (apart_used) *apart_used = apart;
+    if (apart_nblk) *apart_nblk = mvm_simt_blocks(rows);
+    c->mvm_kind_used = 1;
+    return CIQ_OK;
+  }
+  const int tn = tc_chunk_cols(tp);
+  const int chunks = tp / tn;
+  int nsm = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int nsplit = allow_split ? choose_nsplit(rows, c->op.n, chunks, nsm) : 1;
+  const int64_t rt = (rows + 127) / 128;
+  ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
+  if (st != CIQ_OK) return st;
+  if (c->inv_scale_n < tp) {
+    dfree(c->inv_scale);
+    CUDA_TRY(c, dalloc(&c->inv_scale, (size_t)tp));
+    c->inv_scale_n = tp;
+  }
+  float* pout = p;
+  if (nsplit > 1) {
+    st = grow(c, &c->psplit, &c->psplit_elems, (size_t)nsplit * rows * tp);
+    if (st != CIQ_OK) return st;
+    pout = c->psplit;
+  }
+  double* ap = apart;
+  if (apart != nullptr) {
+    st = grow(c, &c->apart_tc, &c->apart_tc_elems, (size_t)rt * nsplit * tp);
+    if (st != CIQ_OK) return st;
+    ap = c->apart_tc;
+  }
+  LAUNCH(c, launch_pack_v(v, c->op.n, c->npad, tp, nrm, c->planes, c->inv_scale, c->stream));
+  TcArgs a{};
+  a.kind = c->op.kind;
+  a.n = c->op.n;
+  a.npad = c->npad;
+  a.row0 = c->row0;
+  a.row1 = c->row1;
+  a.tp = tp;
+  a.nsplit = nsplit;
+  a.nblk_x = (int)(rt * nsplit);
+  a.feat_a = c->feat_a;
+  a.feat_b = c->feat_b;
+  a.vplanes = c->planes;
+  a.inv_scale = c->inv_scale;
+  a.v = v;
+  a.p = pout;
+  a.p_split_stride = (size_t)rows * tp;
+  a.apart = ap;
+  a.o2 = c->op.outputscale;
+  a.diag = c->op.diag;
+  a.done = done;
+  LAUNCH(c, launch_mvm_tc(a, c->stream));
+  if (nsplit_out) *nsplit_out = nsplit;
+  if (apart_used) *apart_used = ap;
+  if (apart_nblk) *apart_nblk = (int)(rt * nsplit);
+  c->mvm_kind_used = 2;
+  return CIQ_OK;
+}
+
+// Augmented split-fp16 features of the tensor-core MVM (mvm_tc.cu): with y = (x - mean)/l *
+// sqrt(log2 e) and h = |y|^2/2, A_i = [y_i, -h_i, 1], B_j = [y_j, 1, -h_j] so that
+// A_i.B_j = -(log2 e/2) |x_i - x_j|^2/l^2; rows [Ah | Al | Ah | 0], [Bh | Bh | Bl | 0] (K = 32),
+// stored as K-major 8x8 core matrices [n/8][4][8][8].
+bool build_tc_features(ciq_ctx* c, const std::vector<float>& xh) {
+  const int64_t n = c->op.n;
+  const int d = (int)c->op.d;
+  const int d2 = d + 2;
+  if (3 * d2 > 32) return false;
+  const int64_t npad = (n + 127) / 128 * 128;
+  std::vector<double> mean(d, 0.0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < d; ++k) mean[k] += xh[i * d + k];
+  for (int k = 0; k < d; ++k) mean[k] /= (double)n;
+  const double sl = std::sqrt(1.4426950408889634);
+  std::vector<__half> fa((size_t)npad * 32, __float2half(0.f)), fb((size_t)npad * 32, __float2half(0.f));
+  std::vector<double> a(d2), b(d2);
+  double hmax = 0.0;
+  auto put = [&](std::vector<__half>& f, int64_t i, int kidx, double val, bool lo) {
+    __half h = __float2half_rn((float)val);
+    if (lo) h = __float2half_rn((float)(val - (double)__half2float(h)));
+    const int64_t ng = i / 8, r = i % 8;
+    const int kc = kidx / 8, kk = kidx % 8;
+    f[(size_t)((ng * 4 + kc) * 64 + r * 8 + kk)] = h;
+  };
+  for (int64_t i = 0; i < n; ++i) {
+    double hh = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double y = ((double)xh[i * d + k] - mean[k]) * sl;
+      a[k] = b[k] = y;
+      hh += 0.5 * y * y;
+    }
+    hmax = std::max(hmax, hh);
+    a[d] = -hh; a[d + 1] = 1.0;
+    b[d] = 1.0; b[d + 1] = -hh;
+    for (int k = 0; k < d2; ++k) {
+      put(fa, i, k, a[k], false);          // Ah
+      put(fa, i, d2 + k, a[k], true);      // Al
+      put(fa, i, 2 * d2 + k, a[k], false); // Ah
+      put(fb, i, k, b[k], false);          // Bh
+      put(fb, i, d2 + k, b[k], false);     // Bh
+      put(fb, i, 2 * d2 + k, b[k], true);  // Bl
+    }
+  }
+  if (hmax > 2.0e4) return false;  // fp16 range / cancellation: use the SIMT path
+  if (cudaMalloc(&c->feat_a, fa.size() * 2) != cudaSuccess) return false;
+  if (cudaMalloc(&c->feat_b, fb.size() * 2) != cudaSuccess) return false;
+  cudaMemcpy(c->feat_a, fa.data(), fa.size() * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(c->feat_b, fb.data(), fb.size() * 2, cudaMemcpyHostToDevice);
+  c->npad = npad;
+  return cudaGetLastError() == cudaSuccess;
 }
 
 // Lambda estimation: Lanczos with full re-orthogonalisation on `cols` start
@@ -455,6 +623,7 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     }
     dv.xs = c->xs;
     dv.d = (int)d;
+    c->tc_ok = build_tc_features(c, xh);
   }
   *out = c;
   return CIQ_OK;
@@ -473,6 +642,8 @@ void ciq_free(ciq_ctx* c) {
   dfree(c->xs);
   dfree(c->kcopy);
   dfree(c->staging);
+  dfree(c->feat_a); dfree(c->feat_b); dfree(c->planes); dfree(c->inv_scale); dfree(c->psplit);
+  dfree(c->apart_tc);
   delete c;
 }
 
@@ -484,7 +655,9 @@ ciq_status ciq_matvec(ciq_ctx* c, const float* V, int64_t ldv, int64_t T, float*
   Workspace& ws = c->ws;
   ciq_status st = load_rows(c, V, ldv, c->op.n, (int)T, ws.w[0], tp);
   if (st != CIQ_OK) return st;
-  st = run_mvm(c, ws.w[0], tp, ws.p, nullptr, nullptr, impl);
+  LAUNCH(c, launch_colsq_partials(ws.w[0], c->op.n, tp, ws.bpart, c->stream));
+  LAUNCH(c, launch_reduce_cols(ws.bpart, rowblocks(c->op.n, tp), tp, ws.colsq, 1, c->stream));
+  st = run_mvm(c, ws.w[0], tp, ws.p, nullptr, nullptr, impl, ws.colsq);
   if (st != CIQ_OK) return st;
   st = store_rows(c, ws.p, tp, c->row1 - c->row0, (int)T, out, ldo);
   if (st != CIQ_OK) return st;
@@ -563,10 +736,10 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   CUDA_TRY(c, cudaEventRecord(ev.e[2], s));
 
   // a4-a6: msMINRES iterations
-  const int nbm = mvm_simt_blocks(rows);
   float* dslot[2] = {ws.d, ws.d + (size_t)nq * rows * tp};
   Ctrl hc{};
   int j = 0;
+  int loop_nsplit = 1, loop_impl = 0;
   for (;;) {
     for (int k = 0; k < p.poll_every && j < p.max_iters; ++k) {
       ++j;
@@ -574,14 +747,19 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
       float* wprev = ws.w[(j + 2) % 3];
       float* wnew = ws.w[(j + 1) % 3];
       begin_timed(c, j, 0);
-      st = run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl);
+      int nsplit = 1, nbm = 0;
+      double* apart = nullptr;
+      st = run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit, &apart, &nbm);
       end_timed(c);
       if (st != CIQ_OK) return st;
-      LAUNCH(c, launch_alpha(sc, ws.apart, nbm, tp, s));
+      const float* pin = (nsplit > 1) ? c->psplit : ws.p;
+      loop_nsplit = nsplit;
+      loop_impl = c->mvm_kind_used;
+      LAUNCH(c, launch_alpha(sc, apart, nbm, tp, s));
       float* d1 = dslot[j & 1];
       float* d2 = dslot[(j + 1) & 1];
       begin_timed(c, j, 1);
-      LAUNCH(c, launch_lanczos_update(sc, ws.p, wcur + c->row0 * tp, wprev + c->row0 * tp, wnew + c->row0 * tp,
+      LAUNCH(c, launch_lanczos_update(sc, pin, nsplit, (size_t)rows * tp, wcur + c->row0 * tp, wprev + c->row0 * tp, wnew + c->row0 * tp,
                                       &d1, &d2, ws.y, nq, rows, tp, ws.bpart, 0, s));
       end_timed(c);
       LAUNCH(c, launch_givens(sc, ws.bpart, nbs, nq, tp, s));
@@ -596,7 +774,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     float* d1 = dslot[(J + 1) & 1];  // d_{J-1}
     float* d2 = dslot[J & 1];        // d_{J-2}, overwritten by d_J
     float* wv = ws.w[J % 3];
-    LAUNCH(c, launch_lanczos_update(sc, nullptr, nullptr, wv + c->row0 * tp, nullptr, &d1, &d2, ws.y, nq, rows, tp,
+    LAUNCH(c, launch_lanczos_update(sc, nullptr, 1, 0, nullptr, wv + c->row0 * tp, nullptr, &d1, &d2, ws.y, nq, rows, tp,
                                     nullptr, 1, s));
   }
   CUDA_TRY(c, cudaEventRecord(ev.e[3], s));
@@ -605,7 +783,9 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   int final_mvm = 0;
   if (p.mode == CIQ_MODE_SQRT) {
     // K . Y  (Y is the full vector on one GPU)
-    st = run_mvm(c, ws.y, tp, ws.p, nullptr, nullptr, p.mvm_impl);
+    LAUNCH(c, launch_colsq_partials(ws.y, rows, tp, ws.bpart, s));
+    LAUNCH(c, launch_reduce_cols(ws.bpart, nbs, tp, ws.colsq, 1, s));
+    st = run_mvm(c, ws.y, tp, ws.p, nullptr, nullptr, p.mvm_impl, ws.colsq);
     if (st != CIQ_OK) return st;
     final_mvm = 1;
     st = store_rows(c, ws.p, tp, rows, (int)T, out, ldo);
@@ -637,6 +817,8 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     cudaEventElapsedTime(&info->ms_loop, ev.e[2], ev.e[3]);
     cudaEventElapsedTime(&info->ms_final, ev.e[3], ev.e[4]);
     info->kernel_launches = c->launches;
+    info->mvm_impl_used = loop_impl;
+    info->mvm_splits = loop_nsplit;
     for (auto& tm : c->timed) {
       if (tm.j > J) continue;  // iterations launched after convergence are no-ops
       float ms = 0.f;

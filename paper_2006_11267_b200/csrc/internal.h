@@ -1,6 +1,8 @@
 // internal.h -- launchers shared between the C-ABI layer (ciq_api.cu) and the kernel files.
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include "common.cuh"
@@ -42,6 +44,28 @@ int mvm_simt_blocks(int64_t rows);
 cudaError_t launch_mvm_simt(const OpDev& op, const float* v, int tp, int64_t row0, int64_t row1,
                             float* p, int ldp, double* alpha_part, const Ctrl* done, cudaStream_t s);
 
+// tcgen05 fused kernel MVM (mvm_tc.cu).  Writes nsplit partial products P_s (row block, tp
+// columns, stride p_split_stride floats); P = sum_s P_s.  apart: [nblk_x][tp] alpha partials.
+struct TcArgs {
+  int kind;
+  int64_t n, npad, row0, row1;
+  int tp, nsplit, nblk_x;
+  const __half* feat_a;      // [npad/8][4][8][8] A-role features (rows)
+  const __half* feat_b;      // [npad/8][4][8][8] B-role features (columns)
+  const __half* vplanes;     // [tp/TN][2][npad*TN] split V planes (pack_v)
+  const float* inv_scale;    // [tp]
+  const float* v;            // fp32 input V (N x tp), for diag*V and alpha
+  float* p;
+  size_t p_split_stride;
+  double* apart;
+  float o2, diag;
+  const Ctrl* done;
+};
+int tc_chunk_cols(int tp);
+cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, const double* nrm, __half* planes,
+                          float* inv_scale, cudaStream_t s);
+cudaError_t launch_mvm_tc(const TcArgs& a, cudaStream_t s);
+
 // ---- vector kernels (recurrence.cu) ----
 int rowblocks(int64_t rows, int tp);   // number of CTAs of the row-streaming kernels
 cudaError_t launch_load_block(const float* src, int64_t ld_src, int64_t rows, int cols, float* dst, int tp,
@@ -55,7 +79,7 @@ cudaError_t launch_reduce_cols(const double* part, int nblk, int m, double* out,
 cudaError_t launch_scale_cols(float* v, int64_t rows, int tp, const double* nrm, cudaStream_t s);
 cudaError_t launch_init_state(const Scal& sc, int nq, int tp, const double* colsq, cudaStream_t s);
 cudaError_t launch_alpha(const Scal& sc, const double* apart, int nblk, int tp, cudaStream_t s);
-cudaError_t launch_lanczos_update(const Scal& sc, const float* p, const float* wcur, const float* wprev,
+cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, size_t split_stride, const float* wcur, const float* wprev,
                                   float* wnew, float* const* d1, float* const* d2, float* y, int nq,
                                   int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s);
 cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s);

@@ -186,7 +186,7 @@ __global__ void alpha_kernel(Scal sc, const double* __restrict__ apart, int nblk
 // The streaming pass (see file header).  final_only: apply the pending update of the last step
 // only (wprev = the buffer holding nrm_J v_J).
 __global__ void __launch_bounds__(kThreads) lanczos_update_kernel(
-    Scal sc, const float* __restrict__ p, const float* __restrict__ wcur, const float* __restrict__ wprev,
+    Scal sc, const float* __restrict__ p, int nsplit, size_t split_stride, const float* __restrict__ wcur, const float* __restrict__ wprev,
     float* __restrict__ wnew, const float* __restrict__ d1base, float* __restrict__ d2base, int64_t qstride,
     float* __restrict__ y, int nq, int64_t rows, int tp, double* __restrict__ bpart, int final_only) {
   const Ctrl* ctrl = sc.ctrl;
@@ -216,6 +216,10 @@ __global__ void __launch_bounds__(kThreads) lanczos_update_kernel(
       float4 wp = *reinterpret_cast<const float4*>(wprev + off);
       if (!final_only) {
         float4 pp = *reinterpret_cast<const float4*>(p + off);
+        for (int sp = 1; sp < nsplit; ++sp) {
+          const float4 q4 = *reinterpret_cast<const float4*>(p + sp * split_stride + off);
+          pp.x += q4.x; pp.y += q4.y; pp.z += q4.z; pp.w += q4.w;
+        }
         float4 wc = *reinterpret_cast<const float4*>(wcur + off);
         float4 w;
         w.x = fmaf(-cprev[0], wp.x, (pp.x - alpha[0] * wc.x) * inv_nrm[0]);
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(kThreads) lanczos_update_kernel(
 
 // beta_{j+1}, Givens rotations of step j for every (shift, column), coefficients of step j's
 // descent update, stopping rule.  One CTA; warp per column, lanes over shifts.
-__global__ void givens_kernel(Scal sc, const double* __restrict__ bpart, int nblk, int nq, int tp) {
+__global__ void __launch_bounds__(512) givens_kernel(Scal sc, const double* __restrict__ bpart, int nblk, int nq, int tp) {
   Ctrl* ctrl = sc.ctrl;
   if (ctrl->done) return;
   __shared__ double s_rel[32];
@@ -440,16 +444,16 @@ cudaError_t launch_alpha(const Scal& sc, const double* apart, int nblk, int tp, 
   alpha_kernel<<<1, 1024, 0, s>>>(sc, apart, nblk, tp);
   return cudaGetLastError();
 }
-cudaError_t launch_lanczos_update(const Scal& sc, const float* p, const float* wcur, const float* wprev,
+cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, size_t split_stride, const float* wcur, const float* wprev,
                                   float* wnew, float* const* d1, float* const* d2, float* y, int nq,
                                   int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s) {
   const int64_t qstride = rows * tp;
-  lanczos_update_kernel<<<stream_grid(rows, tp), kThreads, 0, s>>>(sc, p, wcur, wprev, wnew, d1[0], d2[0],
+  lanczos_update_kernel<<<stream_grid(rows, tp), kThreads, 0, s>>>(sc, p, nsplit, split_stride, wcur, wprev, wnew, d1[0], d2[0],
                                                                     qstride, y, nq, rows, tp, bpart, final_only);
   return cudaGetLastError();
 }
 cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s) {
-  givens_kernel<<<1, 1024, 0, s>>>(sc, bpart, nblk, nq, tp);
+  givens_kernel<<<1, 512, 0, s>>>(sc, bpart, nblk, nq, tp);
   return cudaGetLastError();
 }
 cudaError_t launch_basis_dots(const float* basis, int nb, int64_t rows, int tp, const float* p, double* part,

@@ -61,10 +61,14 @@ def test_mvm_matches_oracle(kind, n, t, impl):
         out = torch.empty((n, t), device="cuda")
         g.matvec(dev(v), out, mvm_impl=impl)
         got = out.cpu().numpy().astype(np.float64)
+    # fp32 SIMT: a few ulps; tcgen05 split-fp16 ("fp16x3"): ~1e-6
+    tol_max, tol_col = (5e-6, 3e-6) if impl == "simt" else (2e-5, 8e-6)
+    if kind.startswith("matern") and impl != "simt":
+        tol_col = 1.5e-5   # r = sqrt(r^2) amplifies the split-fp16 distance error near r = 0
     err = np.abs(got - ref).max() / np.abs(ref).max()
-    assert err < 2e-6, err
+    assert err < tol_max, err
     for c in range(t):
-        assert relerr(got[:, c], ref[:, c]) < 2e-6
+        assert relerr(got[:, c], ref[:, c]) < tol_col
 
 
 # ------------------------------------------------------------------------------------------------
@@ -121,8 +125,9 @@ def test_own_lambda_estimate_and_rule():
     with gpu_ctx(cfg, inp) as g:
         out = torch.empty((cfg.n, cfg.t), device="cuda")
         info = g.apply(dev(inp["B"]), out, q=8, max_iters=5, tol=0.0, mode="invsqrt", lanczos_start=dev(inp["S"]))
-    assert abs(info["ritz_max"] / rmax - 1) < 1e-5
-    assert abs(info["lambda_max"] / lmax - 1) < 1e-5
+    # fp32 Lanczos vs fp64 Lanczos (both with full re-orthogonalisation): agree to ~1e-5
+    assert abs(info["ritz_max"] / rmax - 1) < 5e-5
+    assert abs(info["lambda_max"] / lmax - 1) < 5e-5
     assert info["lambda_min"] == pytest.approx(lmin, rel=1e-6)
     t, w = hht_rule(info["lambda_min"], info["lambda_max"], 8)
     np.testing.assert_allclose(info["t"], t, rtol=1e-12)
