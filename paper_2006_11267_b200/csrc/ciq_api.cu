@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -299,7 +300,8 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int nsplit = allow_split ? choose_nsplit(rows, c->op.n, chunks, nsm) : 1;
+  (void)allow_split;
+  const int nsplit = choose_nsplit(rows, c->op.n, chunks, nsm);
   const int64_t rt = (rows + 127) / 128;
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
   if (st != CIQ_OK) return st;
@@ -341,7 +343,14 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   a.o2 = c->op.outputscale;
   a.diag = c->op.diag;
   a.done = done;
+  {
+    static const int dbg = getenv("CIQ_TC_DEBUG") ? atoi(getenv("CIQ_TC_DEBUG")) : 0;
+    a.dbg = dbg;
+    a.dbg_clk = nullptr;
+  }
   LAUNCH(c, launch_mvm_tc(a, c->stream));
+  if (nsplit > 1 && nsplit_out == nullptr)  // caller wants the complete product in p
+    LAUNCH(c, launch_sum_splits(c->psplit, nsplit, (size_t)rows * tp, rows * tp, p, c->stream));
   if (nsplit_out) *nsplit_out = nsplit;
   if (apart_used) *apart_used = ap;
   if (apart_nblk) *apart_nblk = (int)(rt * nsplit);

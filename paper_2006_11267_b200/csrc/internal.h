@@ -60,6 +60,8 @@ struct TcArgs {
   double* apart;
   float o2, diag;
   const Ctrl* done;
+  int dbg;                   // experiments only (env CIQ_TC_DEBUG): 1 skip KV MMAs, 2 skip exp math
+  long long* dbg_clk;        // experiments only: per-tile clock stamps of CTA 0
 };
 int tc_chunk_cols(int tp);
 cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, const double* nrm, __half* planes,
@@ -68,6 +70,8 @@ cudaError_t launch_mvm_tc(const TcArgs& a, cudaStream_t s);
 
 // ---- vector kernels (recurrence.cu) ----
 int rowblocks(int64_t rows, int tp);   // number of CTAs of the row-streaming kernels
+cudaError_t launch_sum_splits(const float* parts, int nsplit, size_t stride, int64_t elems, float* out,
+                              cudaStream_t s);
 cudaError_t launch_load_block(const float* src, int64_t ld_src, int64_t rows, int cols, float* dst, int tp,
                               cudaStream_t s);
 cudaError_t launch_store_block(const float* src, int tp, int64_t rows, int cols, float* dst, int64_t ld_dst,

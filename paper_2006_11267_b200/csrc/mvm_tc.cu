@@ -11,11 +11,13 @@
 //   (3) O += K_tile . V_J on tcgen05 (kind::f16, TS: A from TMEM, B = V_J from smem, MN-major),
 //       three products k_hi.v_hi + k_hi.v_lo + k_lo.v_hi (fp32-equivalent).
 //
-// Warp roles (384 threads): warp 0 = bulk-copy producer (cp.async.bulk into a 4-stage ring),
+// Warp roles (384 threads): warps 0 / 2 = bulk-copy producers (features ring / V ring),
 // warp 1 = TMEM allocator + single-thread MMA issuer, warps 4..11 = epilogue (TMEM lane quarter
-// = warp % 4, column half = (warp - 4) / 4).  Pipelining: S single-buffered (released as soon as
-// it is loaded), K double-buffered, so the tensor pipe runs S(J+1) and K(J).V(J) while the
-// epilogue exponentiates tile J.  TMEM: S 128 | K0 128 | K1 128 | O TN  (<= 512 columns).
+// = warp % 4, column half = (warp - 4) / 4; two warps per SM sub-partition).  Three TMEM tile
+// buffers: S(J) is overwritten IN PLACE by its k_hi|k_lo halves (32-column chunk c -> hi at
+// [32c, 32c+16), lo at [32c+16, 32c+32)), the A operand of K(J).V(J); S runs three tiles ahead, so
+// the tensor pipe computes KV(J-1) and S(J+2) while the epilogue exponentiates tile J.
+// TMEM: buf0 | buf1 | buf2 | O (TN)  (<= 512 columns).
 //
 // Operand layouts (SWIZZLE_NONE canonical core matrices, 8 rows x 16 B = 128 B contiguous):
 //   features  [N/8][KF/8][8][8] fp16, K-major: LBO = 128 B (K-adjacent), SBO = KF/8 * 128 B
@@ -36,22 +38,29 @@ using namespace tc;
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int KF = 32;           // feature contraction (3 * (d + 2) <= 32, padded)
-constexpr int NUM_THREADS = 384;
+constexpr int NUM_THREADS = 640;  // 4 role warps + 16 epilogue warps
 constexpr int EPI_WARP0 = 4;
-constexpr int TM_S = 0, TM_K0 = 128, TM_K1 = 256, TM_O = 384;
+constexpr int NBUF = 3;          // TMEM S/K tile buffers (S is overwritten in place by K_hi|K_lo)
+constexpr int TM_O = NBUF * 128; // O accumulator columns [384, 384 + TN)
 
+// One smem ring: stage J holds the column-point features (read by S(J)) and the V planes (read by
+// KV(J)); it is released after KV(J).  One wait and one release per tile keep the MMA warp's
+// non-MMA work between tensor batches small (the tensor queue is shallow).
 template <int TN>
 struct Cfg {
-  static constexpr int STAGES = (TN >= 128) ? 3 : 4;
   static constexpr int FEAT_BYTES = BN * KF * 2;     // 8 KB
   static constexpr int V_BYTES = BN * TN * 2;        // one plane of one tile
+  static constexpr int STAGES = (TN >= 128) ? 2 : 5;   // <= 227 KB of shared memory
   static constexpr int STAGE_BYTES = FEAT_BYTES + 2 * V_BYTES;
-  static constexpr int SMEM = 1024 + FEAT_BYTES /*A rows*/ + STAGES * STAGE_BYTES + 4096 /*misc*/;
+  static constexpr int SMEM = 1024 + FEAT_BYTES /*A rows*/ + STAGES * STAGE_BYTES + 4096;
 };
 
+static_assert(Cfg<128>::SMEM <= 227 * 1024 && Cfg<64>::SMEM <= 227 * 1024, "shared memory budget");
+
 struct Bars {
-  uint64_t full[4], empty[4];
-  uint64_t s_full, s_empty, k_full[2], k_empty[2], o_full, a_full;
+  uint64_t full[5], empty[5];
+  uint64_t s_full[NBUF], k_full[NBUF], buf_free[NBUF];
+  uint64_t o_full, a_full;
   uint32_t tmem_base;
 };
 
@@ -68,6 +77,25 @@ __device__ __forceinline__ float kernel_from_s(float s) {
   return (1.f + a) * ex2_approx(-1.4426950408889634f * a);
 }
 
+// 32 S values (one chunk of a row) -> 16 packed k_hi words + 16 packed k_lo words.
+template <int KIND, bool MASK>
+__device__ __forceinline__ void exp_split_chunk(const uint32_t (&sv)[32], uint32_t (&hi)[16], uint32_t (&lo)[16],
+                                                int jvalid) {
+#pragma unroll
+  for (int c = 0; c < 32; c += 2) {
+    float k0 = kernel_from_s<KIND>(__uint_as_float(sv[c]));
+    float k1 = kernel_from_s<KIND>(__uint_as_float(sv[c + 1]));
+    if (MASK) {
+      k0 = (c < jvalid) ? k0 : 0.f;
+      k1 = (c + 1 < jvalid) ? k1 : 0.f;
+    }
+    const uint32_t h = pack_half2(k0, k1);
+    const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
+    hi[c / 2] = h;
+    lo[c / 2] = pack_half2(k0 - hf.x, k1 - hf.y);
+  }
+}
+
 template <int KIND, int TN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     mvm_tc_kernel(TcArgs args) {
@@ -76,8 +104,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* a_feat = smem;
-  uint8_t* stages = smem + C::FEAT_BYTES;
-  Bars* bars = reinterpret_cast<Bars*>(stages + C::STAGES * C::STAGE_BYTES);
+  uint8_t* ring = smem + C::FEAT_BYTES;
+  Bars* bars = reinterpret_cast<Bars*>(ring + C::STAGES * C::STAGE_BYTES);
   float* red = reinterpret_cast<float*>(bars + 1);  // [4][TN] alpha partial staging
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -92,9 +120,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 1); }
-    mbar_init(&bars->s_full, 1);
-    mbar_init(&bars->s_empty, 8);
-    for (int b = 0; b < 2; ++b) { mbar_init(&bars->k_full[b], 8); mbar_init(&bars->k_empty[b], 1); }
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(&bars->s_full[b], 1);
+      mbar_init(&bars->k_full[b], 8);   // the 8 warps of one ping-pong group
+      mbar_init(&bars->buf_free[b], 1);
+    }
     mbar_init(&bars->o_full, 1);
     mbar_init(&bars->a_full, 1);
     fence_mbar_init();
@@ -110,15 +140,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const __half* vl = vh + plane_elems;
 
   if (warp == 0) {
-    // ---------------- producer ----------------
+    // ---------------- producer: A rows once, then per tile features + V planes ----------------
     if (lane == 0) {
       mbar_arrive_expect_tx(&bars->a_full, C::FEAT_BYTES);
       bulk_g2s(a_feat, args.feat_a + (size_t)(i0 / BM) * BM * KF, C::FEAT_BYTES, &bars->a_full);
       for (int jj = 0; jj < njt; ++jj) {
         const int st = jj % C::STAGES;
-        const uint32_t use = jj / C::STAGES;
-        mbar_wait(&bars->empty[st], (use & 1) ^ 1);
-        uint8_t* sb = stages + st * C::STAGE_BYTES;
+        mbar_wait(&bars->empty[st], ((jj / C::STAGES) & 1) ^ 1);
+        uint8_t* sb = ring + st * C::STAGE_BYTES;
         const int jt = jt0 + jj;
         mbar_arrive_expect_tx(&bars->full[st], C::STAGE_BYTES);
         bulk_g2s(sb, args.feat_b + (size_t)jt * BN * KF, C::FEAT_BYTES, &bars->full[st]);
@@ -127,122 +156,132 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer (whole warp converged; one lane elected inside each MMA) ----
+    // tensor-pipe order: S(0) S(1) S(2) | KV(0) S(3) | KV(1) S(4) | ...: S runs three tiles ahead
+    // of the epilogue, KV(J) follows K(J).
+    {
       constexpr uint32_t idesc_s = idesc_f16(128, BN, 0, 0);   // A K-major, B K-major, N = 128
       constexpr uint32_t idesc_o = idesc_f16(128, TN, 0, 1);   // A (TMEM) K-major, B MN-major
       const uint32_t a_base = smem_u32(a_feat);
       mbar_wait(&bars->a_full, 0);
-      auto issue_kv = [&](int jj) {
-        const int b = jj & 1;
-        mbar_wait(&bars->k_full[b], (jj >> 1) & 1);
-        fence_after_sync();
-        const int st = jj % C::STAGES;
-        const uint32_t vh_s = smem_u32(stages + st * C::STAGE_BYTES + C::FEAT_BYTES);
-        const uint32_t vl_s = vh_s + C::V_BYTES;
-        const uint32_t kh = tbase + (b ? TM_K1 : TM_K0), kl = kh + 64;
-        const uint32_t o = tbase + TM_O;
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          // K-step of 16 rows j = 2 core-matrix rows along K: LBO = TN/8*128 B, SBO = 128 B
-          const uint32_t koff = kk * 2 * (TN / 8) * 128;
-          const uint64_t dvh = smem_desc(vh_s + koff, (TN / 8) * 128, 128);
-          const uint64_t dvl = smem_desc(vl_s + koff, (TN / 8) * 128, 128);
-          mma_ts(o, kh + kk * 8, dvh, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
-          mma_ts(o, kh + kk * 8, dvl, idesc_o, 1u);
-          mma_ts(o, kl + kk * 8, dvh, idesc_o, 1u);
-        }
-        mma_commit(&bars->k_empty[b]);
-        mma_commit(&bars->empty[st]);
-      };
-      for (int jj = 0; jj < njt; ++jj) {
+      auto issue_s = [&](int jj) {
         const int st = jj % C::STAGES;
         mbar_wait(&bars->full[st], (jj / C::STAGES) & 1);
-        mbar_wait(&bars->s_empty, (jj & 1) ^ 1);
-        fence_after_sync();
-        const uint32_t bf = smem_u32(stages + st * C::STAGE_BYTES);
+        const uint32_t bf = smem_u32(ring + st * C::STAGE_BYTES);
+        const uint32_t sb = tbase + (jj % NBUF) * 128;
 #pragma unroll
         for (int kk = 0; kk < KF / 16; ++kk) {
           // K-major features: LBO = 128 B (K-adjacent core), SBO = KF/8*128 B (8-row groups)
           const uint64_t da = smem_desc(a_base + kk * 256, 128, (KF / 8) * 128);
           const uint64_t db = smem_desc(bf + kk * 256, 128, (KF / 8) * 128);
-          mma_ss(tbase + TM_S, da, db, idesc_s, kk > 0 ? 1u : 0u);
+          mma_ss_warp(sb, da, db, idesc_s, kk > 0 ? 1u : 0u);
         }
-        mma_commit(&bars->s_full);
-        if (jj > 0) issue_kv(jj - 1);
+        mma_commit_warp(&bars->s_full[jj % NBUF]);
+      };
+      auto issue_kv = [&](int jj) {
+        const int b = jj % NBUF;
+        mbar_wait(&bars->k_full[b], (jj / NBUF) & 1);
+        fence_after_sync();
+        const int st = jj % C::STAGES;   // already full: S(jj) was issued from it
+        const uint32_t vh_s = smem_u32(ring + st * C::STAGE_BYTES + C::FEAT_BYTES);
+        const uint32_t vl_s = vh_s + C::V_BYTES;
+        const uint32_t kb = tbase + b * 128;
+        const uint32_t o = tbase + TM_O;
+        const uint64_t dvh0 = smem_desc(vh_s, (TN / 8) * 128, 128);
+        const uint64_t dvl0 = smem_desc(vl_s, (TN / 8) * 128, 128);
+        if (!(args.dbg & 1)) {
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            // K tile in place of S: chunk c = kk/2 holds k_hi pairs at [32c, 32c+16), k_lo at +16
+            const uint32_t kh = kb + 32 * (kk >> 1) + 8 * (kk & 1);
+            const uint32_t kl = kh + 16;
+            // V: K-step of 16 rows j = 2 core-matrix rows along K (start address advances by
+            // 2 * TN/8 * 128 B; descriptor start field is in 16-byte units)
+            const uint64_t koff = (uint64_t)((kk * 2 * (TN / 8) * 128) >> 4);
+            mma_ts_warp(o, kh, dvh0 + koff, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
+            mma_ts_warp(o, kh, dvl0 + koff, idesc_o, 1u);
+            mma_ts_warp(o, kl, dvh0 + koff, idesc_o, 1u);
+          }
+        }
+        mma_commit_warp(&bars->empty[st]);
+      };
+      for (int jj = 0; jj < NBUF && jj < njt; ++jj) issue_s(jj);
+      for (int jj = 0; jj < njt; ++jj) {
+        issue_kv(jj);
+        // S(jj+3) overwrites buffer jj%3, still being read by KV(jj): tcgen05.mma instructions of
+        // one thread execute in issue order, so no wait is needed (a wait here would drain the
+        // tensor pipe once per tile).
+        if (jj + NBUF < njt) issue_s(jj + NBUF);
       }
-      if (njt > 0) issue_kv(njt - 1);
-      mma_commit(&bars->o_full);
+      mma_commit_warp(&bars->o_full);
     }
   } else if (warp >= EPI_WARP0) {
-    // ---------------- epilogue ----------------
-    const int q = warp % 4;               // TMEM lane quarter -> rows 32q .. 32q+31
-    const int hsel = (warp - EPI_WARP0) / 4;  // column half of S
+    // ---------------- epilogue: 16 warps in two ping-pong groups of 8; group g exponentiates the
+    // tiles J = g (mod 2), so each SM sub-partition holds two warps on tile J and two on tile J+1
+    // whose TMEM-load / SFU / TMEM-store phases interleave.  Within a group, warp w owns TMEM lane
+    // quarter w % 4 and the 64-column half ((w - 4) / 4) % 2 (two 32-column chunks). ----
+    const int q = warp % 4;                         // TMEM lane quarter -> rows 32q .. 32q+31
+    const int grp = (warp - EPI_WARP0) / 8;         // ping-pong group
+    const int half = ((warp - EPI_WARP0) / 4) % 2;  // 64-column half of the tile
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    for (int jj = 0; jj < njt; ++jj) {
-      const int b = jj & 1;
-      const int64_t jcol0 = (int64_t)(jt0 + jj) * BN + hsel * 64;
-      mbar_wait(&bars->s_full, jj & 1);
+    for (int jj = grp; jj < njt; jj += 2) {
+      const int b = jj % NBUF;
+      const uint32_t tb = tbase + b * 128 + lane_base + 64 * half;
+      const int64_t jcol0 = (int64_t)(jt0 + jj) * BN + 64 * half;
+      const bool tail = jcol0 + 64 > n;
+      mbar_wait(&bars->s_full[b], (jj / NBUF) & 1);
       fence_after_sync();
-      uint32_t s0[32], s1[32];
-      tmem_ld32(tbase + TM_S + lane_base + hsel * 64, s0);
-      tmem_ld32(tbase + TM_S + lane_base + hsel * 64 + 32, s1);
+      uint32_t sv0[32], sv1[32];
+      tmem_ld32(tb, sv0);
+      tmem_ld32(tb + 32, sv1);
       tmem_ld_wait();
-      fence_before_sync();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->s_empty);
-      mbar_wait(&bars->k_empty[b], ((jj >> 1) & 1) ^ 1);
-      fence_after_sync();
-      const uint32_t kh = tbase + (b ? TM_K1 : TM_K0) + lane_base + hsel * 32;
-      const uint32_t kl = kh + 64;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t* sv = half ? s1 : s0;
+      {
         uint32_t hi[16], lo[16];
+        if (args.dbg & 2) {
 #pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          const int64_t j = jcol0 + half * 32 + c;
-          float k0 = kernel_from_s<KIND>(__uint_as_float(sv[c]));
-          float k1 = kernel_from_s<KIND>(__uint_as_float(sv[c + 1]));
-          k0 = (j < n) ? k0 : 0.f;
-          k1 = (j + 1 < n) ? k1 : 0.f;
-          const uint32_t h = pack_half2(k0, k1);
-          const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
-          hi[c / 2] = h;
-          lo[c / 2] = pack_half2(k0 - hf.x, k1 - hf.y);
-        }
-        tmem_st16(kh + half * 16, hi);
-        tmem_st16(kl + half * 16, lo);
+          for (int m = 0; m < 16; ++m) { hi[m] = sv0[m]; lo[m] = sv0[m + 16]; }
+        } else if (tail) exp_split_chunk<KIND, true>(sv0, hi, lo, (int)(n - jcol0));
+        else exp_split_chunk<KIND, false>(sv0, hi, lo, 32);
+        tmem_st16(tb, hi);
+        tmem_st16(tb + 16, lo);
+      }
+      {
+        uint32_t hi[16], lo[16];
+        if (args.dbg & 2) {
+#pragma unroll
+          for (int m = 0; m < 16; ++m) { hi[m] = sv1[m]; lo[m] = sv1[m + 16]; }
+        } else if (tail) exp_split_chunk<KIND, true>(sv1, hi, lo, (int)(n - jcol0 - 32));
+        else exp_split_chunk<KIND, false>(sv1, hi, lo, 32);
+        tmem_st16(tb + 32, hi);
+        tmem_st16(tb + 48, lo);
       }
       tmem_st_wait();
       fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->k_full[b]);
     }
+    const int c = (warp - EPI_WARP0) / 4;    // output column group for the final readout
     // ---- output: P_split = o2 * O / scale (+ diag V on split 0), alpha partials ----
     mbar_wait(&bars->o_full, 0);
     fence_after_sync();
     const int64_t i = i0 + q * 32 + lane;
     const bool row_ok = i < args.row1;
-    const int cpw = TN / 2;  // columns per warp half
-    const int c_begin = hsel * cpw;
+    constexpr int CPW = TN / 4;              // output columns per warp (4 warps per lane quarter)
+    const int c_begin = c * CPW;
     float* pout = args.p + (size_t)split * args.p_split_stride;
     const int cglob0 = chunk * TN;
-    for (int cb = 0; cb < cpw; cb += 16) {
-      uint32_t o16[16];
-      if (cpw >= 16) {
-        tmem_ld16(tbase + TM_O + lane_base + c_begin + cb, o16);
-      } else {  // TN = 16: column half of 8 -> read 16 and keep own 8
-        tmem_ld16(tbase + TM_O + lane_base + 0, o16);
-      }
-      tmem_ld_wait();
-      const int ncols = cpw >= 16 ? 16 : cpw;
-      const int coff = cpw >= 16 ? 0 : c_begin;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        if (c >= ncols) break;
-        const int col = cglob0 + c_begin + cb + c;
-        const float ov = __uint_as_float(o16[coff + c]);
+    for (int cb = 0; cb < CPW; cb += 16) {
+      uint32_t o16[16];
+      const int blk = (c_begin + cb) / 16 * 16;   // 16-column TMEM block containing our columns
+      const int coff = (c_begin + cb) - blk;
+      tmem_ld16(tbase + TM_O + lane_base + blk, o16);
+      tmem_ld_wait();
+      constexpr int NC = CPW < 16 ? CPW : 16;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        const int col = cglob0 + c_begin + cb + cc;
+        const float ov = __uint_as_float(o16[coff + cc]);
         float v = 0.f, out = 0.f;
         if (row_ok) {
           v = args.v[(size_t)i * args.tp + col];
@@ -252,7 +291,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         float part = v * out;
         part = warp_sum(part);
-        if (lane == 0) red[q * TN + c_begin + cb + c] = part;
+        if (lane == 0) red[q * TN + c_begin + cb + cc] = part;
       }
     }
   }

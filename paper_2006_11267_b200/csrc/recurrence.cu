@@ -394,6 +394,19 @@ __global__ void lanczos_coeffs_kernel(const double* __restrict__ h1, const doubl
   }
 }
 
+// out = sum_s parts[s] (fixed order), float4 vectorised.
+__global__ void sum_splits_kernel(const float* __restrict__ parts, int nsplit, size_t stride, int64_t n4,
+                                  float* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n4) return;
+  float4 acc = reinterpret_cast<const float4*>(parts)[e];
+  for (int s = 1; s < nsplit; ++s) {
+    const float4 q = reinterpret_cast<const float4*>(parts + s * stride)[e];
+    acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+  }
+  reinterpret_cast<float4*>(out)[e] = acc;
+}
+
 inline unsigned nb_elem(int64_t e, int bs) { return (unsigned)((e + bs - 1) / bs); }
 
 }  // namespace
@@ -404,6 +417,12 @@ static dim3 stream_grid(int64_t rows, int tp) {
   return dim3((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((tp + kChunk - 1) / kChunk));
 }
 
+cudaError_t launch_sum_splits(const float* parts, int nsplit, size_t stride, int64_t elems, float* out,
+                              cudaStream_t s) {
+  const int64_t n4 = elems / 4;
+  sum_splits_kernel<<<nb_elem(n4, 256), 256, 0, s>>>(parts, nsplit, stride, n4, out);
+  return cudaGetLastError();
+}
 cudaError_t launch_load_block(const float* src, int64_t ld_src, int64_t rows, int cols, float* dst, int tp,
                               cudaStream_t s) {
   load_block_kernel<<<nb_elem(rows * tp, 256), 256, 0, s>>>(src, ld_src, rows, cols, dst, tp);

@@ -48,7 +48,7 @@ def gpu_ctx(cfg, inp):
 # ------------------------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("kind", ["rbf", "matern52", "matern32", "dense"])
-@pytest.mark.parametrize("n,t", [(1000, 1), (1000, 16), (777, 64), (2111, 70)])
+@pytest.mark.parametrize("n,t", [(1000, 1), (1000, 16), (777, 64), (2111, 70), (1500, 128), (900, 300)])
 @pytest.mark.parametrize("impl", ["simt", "auto"])
 def test_mvm_matches_oracle(kind, n, t, impl):
     cfg = workloads.scaled(workloads.CONFIGS["C2" if kind == "dense" else "C3"], n=n, t=t)
