@@ -22,9 +22,10 @@
  *  - Ownership: the caller owns every buffer it passes.  Operator / preconditioner arrays passed
  *    to ciq_init must stay valid until ciq_free if they are device pointers (host arrays are
  *    copied at init).  The ctx owns its workspace (grown lazily per T) and its NCCL communicator.
- *  - Stream ordering: all device work is enqueued on the stream given to ciq_init.  ciq_apply
- *    returns after the result has been written (it synchronises the stream: the lambda estimate
- *    and the convergence poll are host decisions).
+ *  - Stream ordering: device work runs on a private non-blocking stream of the ctx, ordered after
+ *    everything already enqueued on the stream given to ciq_init (event join).  ciq_apply /
+ *    ciq_matvec return after the result has been written (the lambda estimate and the
+ *    convergence poll are host decisions), so the caller may use the output immediately.
  *  - Errors: status codes only, never exceptions across the ABI; ciq_last_error() gives text.
  *    A non-converged solve is NOT an error: the result is written and CIQ_NOT_CONVERGED returned
  *    (S:284).

@@ -60,7 +60,9 @@ struct LambdaWork {
 struct ciq_ctx {
   ciq_operator op{};
   OpDev dev{};
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;       // private non-blocking work stream (graph-capturable)
+  cudaStream_t user_stream = nullptr;  // the caller's stream given to ciq_init
+  cudaEvent_t join_ev = nullptr;
   int rank = 0, world = 1;
   int64_t row0 = 0, row1 = 0;
   float* xs = nullptr;        // owned scaled points
@@ -83,6 +85,12 @@ struct ciq_ctx {
   size_t apart_tc_elems = 0;
   int last_nsplit = 1;
   int mvm_kind_used = 0;      // 1 simt, 2 tc (of the last loop MVM)
+  // CUDA graph of `poll_every` msMINRES iterations (period-6 buffer rotation => replayable)
+  uint64_t buf_gen = 0;       // bumped on every device re-allocation (invalidates the graph)
+  cudaGraphExec_t gexec = nullptr;
+  uint64_t gkey[6] = {0, 0, 0, 0, 0, 0};
+  int64_t graph_nodes = 0;
+  Ctrl* ctrl_host = nullptr;  // pinned poll slots [2]
   int64_t staging_elems = 0;
   std::string err;
   int64_t launches = 0;
@@ -160,6 +168,7 @@ ciq_status ensure_workspace(ciq_ctx* c, int tp, int nq) {
   const int64_t rows = c->row1 - c->row0;
   const int64_t n = c->op.n;
   if (ws.tp == tp && ws.nq >= nq && ws.rows == rows) return CIQ_OK;
+  ++c->buf_gen;
   free_workspace(ws);
   ws.tp = tp;
   ws.nq = nq;
@@ -248,6 +257,7 @@ void end_timed(ciq_ctx* c) {
 template <class T>
 ciq_status grow(ciq_ctx* c, T** buf, size_t* cap, size_t need) {
   if (*cap >= need) return CIQ_OK;
+  ++c->buf_gen;
   dfree(*buf);
   CUDA_TRY(c, dalloc(buf, need));
   *cap = need;
@@ -274,6 +284,32 @@ int choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm) {
     if (eff > best_eff + 0.02) { best_eff = eff; best = s; }
   }
   return best;
+}
+
+// Allocate every buffer run_mvm(tp, allow_split) may need (so a CUDA-graph capture never
+// allocates).
+ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
+  if (!use_tc(c, impl)) return CIQ_OK;
+  const int64_t rows = c->row1 - c->row0;
+  const int tn = tc_chunk_cols(tp);
+  int nsm = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsplit = choose_nsplit(rows, c->op.n, tp / tn, nsm);
+  const int64_t rt = (rows + 127) / 128;
+  ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
+  if (st != CIQ_OK) return st;
+  if (c->inv_scale_n < tp) {
+    ++c->buf_gen;
+    dfree(c->inv_scale);
+    CUDA_TRY(c, dalloc(&c->inv_scale, (size_t)tp));
+    c->inv_scale_n = tp;
+  }
+  if (nsplit > 1) {
+    st = grow(c, &c->psplit, &c->psplit_elems, (size_t)nsplit * rows * tp);
+    if (st != CIQ_OK) return st;
+  }
+  return grow(c, &c->apart_tc, &c->apart_tc_elems, (size_t)rt * nsplit * tp);
 }
 
 // P (+ alpha partials) <- K V.  With the tensor-core path the result may be split into
@@ -306,6 +342,7 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
   if (st != CIQ_OK) return st;
   if (c->inv_scale_n < tp) {
+    ++c->buf_gen;
     dfree(c->inv_scale);
     CUDA_TRY(c, dalloc(&c->inv_scale, (size_t)tp));
     c->inv_scale_n = tp;
@@ -501,6 +538,13 @@ ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, 
   return CIQ_OK;
 }
 
+// Order the private work stream after everything already enqueued on the caller's stream.
+ciq_status join_user_stream(ciq_ctx* c) {
+  CUDA_TRY(c, cudaEventRecord(c->join_ev, c->user_stream));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->join_ev, 0));
+  return CIQ_OK;
+}
+
 struct EvTimer {
   cudaEvent_t e[5];
   EvTimer() { for (auto& x : e) cudaEventCreate(&x); }
@@ -594,7 +638,12 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
   }
   ciq_ctx* c = new ciq_ctx();
   c->op = *op;
-  c->stream = reinterpret_cast<cudaStream_t>(stream);
+  c->user_stream = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming) != cudaSuccess) {
+    delete c;
+    return set_err(nullptr, CIQ_ERR_CUDA, "stream creation failed");
+  }
   c->row0 = 0;
   c->row1 = op->n;
   OpDev& dv = c->dev;
@@ -644,6 +693,10 @@ fail:
 
 void ciq_free(ciq_ctx* c) {
   if (!c) return;
+  if (c->stream) { cudaStreamSynchronize(c->stream); cudaStreamDestroy(c->stream); }
+  if (c->join_ev) cudaEventDestroy(c->join_ev);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->ctrl_host) cudaFreeHost(c->ctrl_host);
   for (auto& t : c->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
   for (auto e : c->event_pool) cudaEventDestroy(e);
   free_workspace(c->ws);
@@ -661,6 +714,7 @@ ciq_status ciq_matvec(ciq_ctx* c, const float* V, int64_t ldv, int64_t T, float*
   if (T <= 0 || ldv < T || ldo < T) return set_err(c, CIQ_ERR_DIM, "bad T / leading dimension");
   const int tp = round16(T);
   if (ensure_workspace(c, tp, std::max(1, c->ws.nq)) != CIQ_OK) return CIQ_ERR_OOM;
+  if (join_user_stream(c) != CIQ_OK) return CIQ_ERR_CUDA;
   Workspace& ws = c->ws;
   ciq_status st = load_rows(c, V, ldv, c->op.n, (int)T, ws.w[0], tp);
   if (st != CIQ_OK) return st;
@@ -701,6 +755,8 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   if (st != CIQ_OK) return st;
   Workspace& ws = c->ws;
   const Scal& sc = ws.sc;
+  st = join_user_stream(c);
+  if (st != CIQ_OK) return st;
   EvTimer ev;
   CUDA_TRY(c, cudaEventRecord(ev.e[0], s));
 
@@ -744,38 +800,106 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   CUDA_TRY(c, cudaMemcpyAsync(sc.weights, w, nq * 8, cudaMemcpyHostToDevice, s));
   CUDA_TRY(c, cudaEventRecord(ev.e[2], s));
 
-  // a4-a6: msMINRES iterations
+  // a4-a6: msMINRES iterations.  Buffers rotate with period 6 in j (W: j mod 3, D: j mod 2) and
+  // every kernel reads the iteration state from device memory, so a block of `poll_every`
+  // (a multiple of 6) iterations is captured once as a CUDA graph and replayed; iterations past
+  // the device-side stopping rule are no-ops.
   float* dslot[2] = {ws.d, ws.d + (size_t)nq * rows * tp};
   Ctrl hc{};
-  int j = 0;
   int loop_nsplit = 1, loop_impl = 0;
-  for (;;) {
-    for (int k = 0; k < p.poll_every && j < p.max_iters; ++k) {
-      ++j;
-      float* wcur = ws.w[j % 3];
-      float* wprev = ws.w[(j + 2) % 3];
-      float* wnew = ws.w[(j + 1) % 3];
-      begin_timed(c, j, 0);
-      int nsplit = 1, nbm = 0;
-      double* apart = nullptr;
-      st = run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit, &apart, &nbm);
-      end_timed(c);
-      if (st != CIQ_OK) return st;
-      const float* pin = (nsplit > 1) ? c->psplit : ws.p;
-      loop_nsplit = nsplit;
-      loop_impl = c->mvm_kind_used;
-      LAUNCH(c, launch_alpha(sc, apart, nbm, tp, s));
-      float* d1 = dslot[j & 1];
-      float* d2 = dslot[(j + 1) & 1];
-      begin_timed(c, j, 1);
-      LAUNCH(c, launch_lanczos_update(sc, pin, nsplit, (size_t)rows * tp, wcur + c->row0 * tp, wprev + c->row0 * tp, wnew + c->row0 * tp,
-                                      &d1, &d2, ws.y, nq, rows, tp, ws.bpart, 0, s));
-      end_timed(c);
-      LAUNCH(c, launch_givens(sc, ws.bpart, nbs, nq, tp, s));
+  auto enqueue_iter = [&](int j) -> ciq_status {
+    float* wcur = ws.w[j % 3];
+    float* wprev = ws.w[(j + 2) % 3];
+    float* wnew = ws.w[(j + 1) % 3];
+    begin_timed(c, j, 0);
+    int nsplit = 1, nbm = 0;
+    double* apart = nullptr;
+    ciq_status st2 = run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit, &apart, &nbm);
+    end_timed(c);
+    if (st2 != CIQ_OK) return st2;
+    const float* pin = (nsplit > 1) ? c->psplit : ws.p;
+    loop_nsplit = nsplit;
+    loop_impl = c->mvm_kind_used;
+    LAUNCH(c, launch_alpha(sc, apart, nbm, tp, s));
+    float* d1 = dslot[j & 1];
+    float* d2 = dslot[(j + 1) & 1];
+    begin_timed(c, j, 1);
+    LAUNCH(c, launch_lanczos_update(sc, pin, nsplit, (size_t)rows * tp, wcur + c->row0 * tp, wprev + c->row0 * tp,
+                                    wnew + c->row0 * tp, &d1, &d2, ws.y, nq, rows, tp, ws.bpart, 0, s));
+    end_timed(c);
+    LAUNCH(c, launch_givens(sc, ws.bpart, nbs, nq, tp, s));
+    return CIQ_OK;
+  };
+  const bool use_graph = !c->profiling && getenv("CIQ_NO_GRAPH") == nullptr;
+  int block = p.poll_every;
+  if (use_graph) block = std::max(6, (p.poll_every + 5) / 6 * 6);
+  if (use_graph) {
+    // size every buffer the MVM may (re)allocate before capturing
+    st = prepare_mvm_buffers(c, tp, p.mvm_impl);
+    if (st != CIQ_OK) return st;
+    const uint64_t key[6] = {c->buf_gen, (uint64_t)tp, (uint64_t)nq, (uint64_t)p.mvm_impl, (uint64_t)block,
+                             (uint64_t)(uintptr_t)ws.d};
+    if (c->gexec == nullptr || std::memcmp(key, c->gkey, sizeof(key)) != 0) {
+      if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+      const int64_t l0 = c->launches;
+      CUDA_TRY(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      ciq_status cst = CIQ_OK;
+      for (int k = 1; k <= block && cst == CIQ_OK; ++k) cst = enqueue_iter(k);
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(s, &g);
+      if (cst != CIQ_OK) { if (g) cudaGraphDestroy(g); return cst; }
+      CUDA_TRY(c, e);
+      e = cudaGraphInstantiate(&c->gexec, g, 0);
+      cudaGraphDestroy(g);
+      CUDA_TRY(c, e);
+      std::memcpy(c->gkey, key, sizeof(key));
+      c->graph_nodes = c->launches - l0;
+      c->launches = l0;
+    } else {
+      loop_impl = c->tc_ok && p.mvm_impl != CIQ_MVM_SIMT ? 2 : 1;
+      loop_nsplit = c->last_nsplit;
     }
-    CUDA_TRY(c, cudaMemcpyAsync(&hc, sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    if (c->ctrl_host == nullptr) CUDA_TRY(c, cudaMallocHost(&c->ctrl_host, 2 * sizeof(Ctrl)));
+    // keep up to two graphs in flight: the host checks block k while block k+1 runs
+    int launched = 0, checked = 0;
+    cudaEvent_t evp[2];
+    cudaEventCreateWithFlags(&evp[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&evp[1], cudaEventDisableTiming);
+    auto launch_one = [&]() -> ciq_status {
+      const int sl = launched & 1;
+      CUDA_TRY(c, cudaGraphLaunch(c->gexec, s));
+      c->launches += c->graph_nodes;
+      CUDA_TRY(c, cudaMemcpyAsync(&c->ctrl_host[sl], sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(c, cudaEventRecord(evp[sl], s));
+      ++launched;
+      return CIQ_OK;
+    };
+    for (;;) {
+      while ((int64_t)launched * block < p.max_iters && launched - checked < 2) {
+        st = launch_one();
+        if (st != CIQ_OK) return st;
+      }
+      CUDA_TRY(c, cudaEventSynchronize(evp[checked & 1]));
+      hc = c->ctrl_host[checked & 1];
+      ++checked;
+      if (hc.done || checked == launched) break;
+    }
     CUDA_TRY(c, cudaStreamSynchronize(s));
-    if (hc.done || j >= p.max_iters) break;
+    cudaEventDestroy(evp[0]);
+    cudaEventDestroy(evp[1]);
+    c->last_nsplit = loop_nsplit;
+  } else {
+    int j = 0;
+    for (;;) {
+      for (int k = 0; k < p.poll_every && j < p.max_iters; ++k) {
+        ++j;
+        st = enqueue_iter(j);
+        if (st != CIQ_OK) return st;
+      }
+      CUDA_TRY(c, cudaMemcpyAsync(&hc, sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(c, cudaStreamSynchronize(s));
+      if (hc.done || j >= p.max_iters) break;
+    }
   }
   const int J = hc.iters;
   // last pending update (step J): v_J lives in the buffer that was W_cur at iteration J

@@ -50,12 +50,12 @@ template <int TN>
 struct Cfg {
   static constexpr int FEAT_BYTES = BN * KF * 2;     // 8 KB
   static constexpr int V_BYTES = BN * TN * 2;        // one plane of one tile
-  static constexpr int STAGES = (TN >= 128) ? 2 : 5;   // <= 227 KB of shared memory
+  static constexpr int STAGES = 5;   // >= NBUF + 1 (S(J+3) is issued before KV(J+1) frees a stage)
   static constexpr int STAGE_BYTES = FEAT_BYTES + 2 * V_BYTES;
   static constexpr int SMEM = 1024 + FEAT_BYTES /*A rows*/ + STAGES * STAGE_BYTES + 4096;
 };
 
-static_assert(Cfg<128>::SMEM <= 227 * 1024 && Cfg<64>::SMEM <= 227 * 1024, "shared memory budget");
+static_assert(Cfg<64>::SMEM <= 227 * 1024, "shared memory budget");
 
 struct Bars {
   uint64_t full[5], empty[5];
@@ -366,7 +366,6 @@ cudaError_t launch_kind(const TcArgs& a, int tn, cudaStream_t s) {
     CIQ_TC_CASE(16)
     CIQ_TC_CASE(32)
     CIQ_TC_CASE(64)
-    CIQ_TC_CASE(128)
 #undef CIQ_TC_CASE
   }
   return cudaErrorInvalidValue;
@@ -374,8 +373,10 @@ cudaError_t launch_kind(const TcArgs& a, int tn, cudaStream_t s) {
 
 }  // namespace
 
+// Column chunk TN per CTA.  Capped at 64: the single smem ring needs >= NBUF + 1 = 4 stages
+// (S runs three tiles ahead of KV), which at TN = 128 would exceed shared memory; wider T is
+// handled by more chunks (the K tile is recomputed per chunk -- cheap next to the 3 GEMMs).
 int tc_chunk_cols(int tp) {
-  if (tp % 128 == 0) return 128;
   if (tp % 64 == 0) return 64;
   if (tp % 32 == 0) return 32;
   return 16;

@@ -211,3 +211,23 @@ def test_invalid_arguments_are_reported():
             g.apply(dev(inp["B"]), out, q=8, tol=-1.0)
     with pytest.raises(pb.CiqError):
         pb.CIQ("rbf", X=dev(inp["X"]), lengthscale=-1.0)
+
+
+def test_cuda_graph_replay_equals_direct_launches():
+    import os
+    cfg = workloads.scaled(workloads.CONFIGS["C3"], n=1300, t=6)
+    inp = workloads.make_inputs(cfg)
+    outs = []
+    for no_graph in (False, True, False):
+        if no_graph:
+            os.environ["CIQ_NO_GRAPH"] = "1"
+        else:
+            os.environ.pop("CIQ_NO_GRAPH", None)
+        with gpu_ctx(cfg, inp) as g:
+            out = torch.empty((cfg.n, cfg.t), device="cuda")
+            info = g.apply(dev(inp["B"]), out, q=8, max_iters=400, tol=1e-5, mode="sqrt", lanczos_start=dev(inp["S"]))
+            outs.append((out.cpu().numpy(), info["iters"]))
+    os.environ.pop("CIQ_NO_GRAPH", None)
+    assert outs[0][1] == outs[1][1] == outs[2][1]
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][0], outs[2][0])
