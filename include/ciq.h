@@ -175,6 +175,12 @@ ciq_status ciq_apply(ciq_ctx* ctx, const float* B, int64_t ldb, int64_t T, float
 ciq_status ciq_matvec(ciq_ctx* ctx, const float* V, int64_t ldv, int64_t T, float* out, int64_t ldo,
                       int32_t mvm_impl);
 
+/* Partial pivoted Cholesky of the kernel part of K (Harbrecht et al.): rank
+ * greedy steps, each picking the largest remaining diagonal residual (lowest index on ties),
+ * appending the normalised residual column.  L (N x rank, ldl >= rank, host or device) receives
+ * the factor; use it as ciq_precond.L with sigma2 = op.diag for the App. A preconditioner. */
+ciq_status ciq_pivoted_cholesky(ciq_ctx* ctx, int32_t rank, float* L, int64_t ldl);
+
 void ciq_free(ciq_ctx* ctx);
 
 const char* ciq_status_string(ciq_status s);

@@ -1,7 +1,8 @@
 """Build libciq.so in-tree for sm_100a (nvcc; no JIT cache, the .so travels with the repo copy).
 
-    python -m paper_2006_11267_b200.build            # incremental
-    python -m paper_2006_11267_b200.build --force    # rebuild everything
+    python paper_2006_11267_b200/build.py            # incremental
+    python paper_2006_11267_b200/build.py --force    # rebuild everything
+(run as a script: importing the package would load the library being built)
 """
 from __future__ import annotations
 
@@ -17,7 +18,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libciq.so")
 
-SOURCES = ["host_math.cpp", "nccl_dl.cpp", "mvm_simt.cu", "mvm_tc.cu", "recurrence.cu", "ciq_api.cu"]
+SOURCES = ["host_math.cpp", "nccl_dl.cpp", "mvm_simt.cu", "mvm_tc.cu", "recurrence.cu", "precond.cu", "ciq_api.cu"]
 HEADERS = ["common.cuh", "nccl_dl.h", "internal.h", "host_math.h", "tc_util.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"] + ARCH

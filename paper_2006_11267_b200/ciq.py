@@ -85,7 +85,7 @@ class CiqInfo(ctypes.Structure):
 
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2006_11267_b200.build` "
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2006_11267_b200/build.py` "
                           "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
     ctx_p = c_void_p
@@ -98,6 +98,8 @@ def _load() -> ctypes.CDLL:
     lib.ciq_apply.restype = c_int32
     lib.ciq_matvec.argtypes = [ctx_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int32]
     lib.ciq_matvec.restype = c_int32
+    lib.ciq_pivoted_cholesky.argtypes = [ctx_p, c_int32, c_void_p, c_int64]
+    lib.ciq_pivoted_cholesky.restype = c_int32
     lib.ciq_free.argtypes = [ctx_p]
     lib.ciq_free.restype = None
     lib.ciq_status_string.argtypes = [c_int32]
@@ -118,7 +120,8 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 
-EXPORTED = ["ciq_params_default", "ciq_init", "ciq_apply", "ciq_matvec", "ciq_free", "ciq_status_string",
+EXPORTED = ["ciq_params_default", "ciq_init", "ciq_apply", "ciq_matvec", "ciq_pivoted_cholesky", "ciq_free",
+            "ciq_status_string",
             "ciq_last_error", "ciq_shard_rows", "ciq_quadrature_rule", "ciq_tridiag_extremes",
             "ciq_nccl_unique_id"]
 
@@ -272,6 +275,14 @@ def ciq_matvec(ctx, V, out, mvm_impl: str = "auto") -> None:
         raise CiqError(st, LIB.ciq_last_error(ctx).decode())
 
 
+def ciq_pivoted_cholesky(ctx, rank: int, out) -> None:
+    keep: list = []
+    po, ldo, no, ro = _ptr_ld(out, "L", keep)
+    st = LIB.ciq_pivoted_cholesky(ctx, int(rank), po, ldo)
+    if st != CIQ_OK:
+        raise CiqError(st, LIB.ciq_last_error(ctx).decode())
+
+
 def ciq_free(ctx) -> None:
     LIB.ciq_free(ctx)
 
@@ -325,6 +336,9 @@ class CIQ:
         d = info.as_dict()
         d["status"] = st
         return d
+
+    def pivoted_cholesky(self, rank: int, out) -> None:
+        ciq_pivoted_cholesky(self.ctx, rank, out)
 
     def matvec(self, V, out, mvm_impl: str = "auto") -> None:
         ciq_matvec(self.ctx, V, out, mvm_impl)

@@ -57,8 +57,28 @@ struct LambdaWork {
 
 }  // namespace
 
+// Low-rank-plus-diagonal preconditioner on the device (precond.cu): U (n x r2, orthonormal),
+// per-power gains g_p = (s^2 + sigma2)^p - sigma2^p and scalars a_p = sigma2^p for p = -1, 1/2, -1/2.
+struct PrecondDev {
+  bool on = false;
+  int rank = 0, r2 = 0;
+  double sigma2 = 0.0;
+  float* l = nullptr;       // n x rank (owned copy)
+  float* u = nullptr;       // n x r2
+  double* g[3] = {nullptr, nullptr, nullptr};
+  float a[3] = {0.f, 0.f, 0.f};
+  // work
+  double* part = nullptr;   size_t part_cap = 0;   // utv partials  [splits][r2][tp]
+  double* h = nullptr;      size_t h_cap = 0;      // U^T v         [r2][tp]
+  double* bpart = nullptr;  size_t bpart_cap = 0;  // dot partials  [blocks][tp]
+  float* z[2] = {nullptr, nullptr}; size_t z_cap = 0;
+  float* t1 = nullptr; float* t2 = nullptr; size_t t_cap = 0;  // lambda estimate on P^-1/2 K P^-1/2
+};
+enum { PW_INV = 0, PW_HALF = 1, PW_MHALF = 2 };
+
 struct ciq_ctx {
   ciq_operator op{};
+  PrecondDev pc;
   OpDev dev{};
   cudaStream_t stream = nullptr;       // private non-blocking work stream (graph-capturable)
   cudaStream_t user_stream = nullptr;  // the caller's stream given to ciq_init
@@ -448,6 +468,9 @@ bool build_tc_features(ciq_ctx* c, const std::vector<float>& xh) {
   return cudaGetLastError() == cudaSuccess;
 }
 
+ciq_status precond_power(ciq_ctx* c, int which, const float* v, int tp, int64_t rows, float* out,
+                         const float* dotv);
+
 // Lambda estimation: Lanczos with full re-orthogonalisation on `cols` start
 // columns; Ritz extremes pooled; margins of reading G6.
 ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, double* lmin, double* lmax,
@@ -493,7 +516,18 @@ ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, 
   int done_mvms = 0;
   for (int j = 0; j < J; ++j) {
     const float* vj = lw.basis + (size_t)j * n * tpl;
-    if (run_mvm(c, vj, tpl, lw.p, nullptr, nullptr, p->mvm_impl) != CIQ_OK) return CIQ_ERR_CUDA;
+    if (c->pc.on) {
+      // Lanczos on M = P^{-1/2} K P^{-1/2} (App. A: the rule must cover the spectrum of M)
+      PrecondDev& P = c->pc;
+      ciq_status gs = grow(c, &P.t1, &P.t_cap, (size_t)2 * n * tpl);
+      if (gs != CIQ_OK) return gs;
+      P.t2 = P.t1 + (size_t)n * tpl;
+      if (precond_power(c, PW_MHALF, vj, tpl, n, P.t1, nullptr) != CIQ_OK) return CIQ_ERR_CUDA;
+      if (run_mvm(c, P.t1, tpl, P.t2, nullptr, nullptr, p->mvm_impl) != CIQ_OK) return CIQ_ERR_CUDA;
+      if (precond_power(c, PW_MHALF, P.t2, tpl, n, lw.p, nullptr) != CIQ_OK) return CIQ_ERR_CUDA;
+    } else if (run_mvm(c, vj, tpl, lw.p, nullptr, nullptr, p->mvm_impl) != CIQ_OK) {
+      return CIQ_ERR_CUDA;
+    }
     ++done_mvms;
     for (int pass = 0; pass < 2; ++pass) {
       double* h = pass == 0 ? lw.h1 : lw.h2;
@@ -543,6 +577,75 @@ ciq_status join_user_stream(ciq_ctx* c) {
   CUDA_TRY(c, cudaEventRecord(c->join_ev, c->user_stream));
   CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->join_ev, 0));
   return CIQ_OK;
+}
+
+// out = P^p v (p by index: PW_INV -1, PW_HALF 1/2, PW_MHALF -1/2) on rows x tp (device), optionally
+// with fixed-order fp64 partials of sum_i out[i][c] dotv[i][c] into c->pc.bpart.
+ciq_status precond_power(ciq_ctx* c, int which, const float* v, int tp, int64_t rows, float* out,
+                         const float* dotv) {
+  PrecondDev& P = c->pc;
+  const int ns = utv_splits(rows);
+  ciq_status st = grow(c, &P.part, &P.part_cap, (size_t)ns * P.r2 * tp);
+  if (st != CIQ_OK) return st;
+  st = grow(c, &P.h, &P.h_cap, (size_t)P.r2 * tp);
+  if (st != CIQ_OK) return st;
+  st = grow(c, &P.bpart, &P.bpart_cap, (size_t)uapply_blocks(rows) * tp);
+  if (st != CIQ_OK) return st;
+  LAUNCH(c, launch_utv(P.u, P.r2, P.r2, v, tp, rows, ns, P.part, c->stream));
+  LAUNCH(c, launch_reduce_cols(P.part, ns, P.r2 * tp, P.h, 0, c->stream));
+  LAUNCH(c, launch_uapply(P.u, P.r2, P.r2, P.g[which], P.h, v, P.a[which], tp, rows, out, dotv,
+                          dotv ? P.bpart : nullptr, c->stream));
+  return CIQ_OK;
+}
+
+// Build U, the gains and scalars from L (device, n x rank) and sigma2 (App. A).
+ciq_status build_precond(ciq_ctx* c) {
+  PrecondDev& P = c->pc;
+  const int64_t n = c->op.n;
+  const int r = P.rank;
+  double* gram_d = nullptr;
+  CUDA_TRY(c, dalloc(&gram_d, (size_t)r * r));
+  LAUNCH(c, launch_gram(P.l, r, r, n, gram_d, c->stream));
+  std::vector<double> gram((size_t)r * r), w(r), vec((size_t)r * r);
+  CUDA_TRY(c, cudaMemcpyAsync(gram.data(), gram_d, gram.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  dfree(gram_d);
+  ciqh::sym_eig_jacobi(gram.data(), r, w.data(), vec.data());   // L^T L = W diag(s^2) W^T
+  const double smax2 = std::max(w[0], 0.0);
+  int r2 = 0;
+  while (r2 < r && w[r2] > 1e-12 * smax2 && w[r2] > 0) ++r2;
+  P.r2 = std::max(r2, 1);
+  std::vector<float> wsi((size_t)r * P.r2, 0.f);
+  for (int k = 0; k < r; ++k)
+    for (int j = 0; j < r2; ++j) wsi[(size_t)k * P.r2 + j] = (float)(vec[(size_t)k * r + j] / std::sqrt(w[j]));
+  float* wsi_d = nullptr;
+  CUDA_TRY(c, dalloc(&wsi_d, wsi.size()));
+  CUDA_TRY(c, cudaMemcpyAsync(wsi_d, wsi.data(), wsi.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, dalloc(&P.u, (size_t)n * P.r2));
+  LAUNCH(c, launch_small_right_mul(P.l, r, r, wsi_d, P.r2, n, P.u, P.r2, c->stream));
+  const double s2 = P.sigma2;
+  const double pw[3] = {-1.0, 0.5, -0.5};
+  for (int k = 0; k < 3; ++k) {
+    std::vector<double> g(P.r2, 0.0);
+    const double ap = std::pow(s2, pw[k]);
+    for (int j = 0; j < r2; ++j) g[j] = std::pow(w[j] + s2, pw[k]) - ap;
+    P.a[k] = (float)ap;
+    CUDA_TRY(c, dalloc(&P.g[k], (size_t)P.r2));
+    CUDA_TRY(c, cudaMemcpyAsync(P.g[k], g.data(), g.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  dfree(wsi_d);
+  P.on = true;
+  return CIQ_OK;
+}
+
+void free_precond(PrecondDev& P) {
+  dfree(P.l); dfree(P.u);
+  for (auto& g : P.g) dfree(g);
+  dfree(P.part); dfree(P.h); dfree(P.bpart);
+  for (auto& z : P.z) dfree(z);
+  dfree(P.t1);
+  P.t2 = nullptr;
 }
 
 struct EvTimer {
@@ -629,7 +732,11 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     for (int k = 0; k < (op->ard ? op->d : 1); ++k)
       if (!(op->lengthscale[k] > 0)) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "lengthscale must be > 0");
   }
-  if (pc) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "preconditioner: not built yet");
+  if (pc) {
+    if (!pc->L || pc->rank < 1 || pc->ldl < pc->rank) return set_err(nullptr, CIQ_ERR_DIM, "bad preconditioner L / rank / ldl");
+    if (!(pc->sigma2 > 0)) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "preconditioner sigma2 must be > 0 (S:425)");
+    if (pc->rank > 2048) return set_err(nullptr, CIQ_ERR_DIM, "preconditioner rank > 2048");
+  }
   if (comm && comm->world > 1) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "row sharding: not built yet");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -683,6 +790,22 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     dv.d = (int)d;
     c->tc_ok = build_tc_features(c, xh);
   }
+  if (pc) {
+    PrecondDev& P = c->pc;
+    P.rank = (int)pc->rank;
+    P.sigma2 = pc->sigma2;
+    if (cudaMalloc(&P.l, (size_t)op->n * P.rank * 4) != cudaSuccess) { st = CIQ_ERR_OOM; goto fail; }
+    const cudaMemcpyKind kind = is_device_ptr(pc->L) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (cudaMemcpy2D(P.l, (size_t)P.rank * 4, pc->L, (size_t)pc->ldl * 4, (size_t)P.rank * 4, (size_t)op->n, kind) !=
+        cudaSuccess) { st = CIQ_ERR_CUDA; goto fail; }
+    st = build_precond(c);
+    if (st != CIQ_OK) {
+      g_init_error = c->err;
+      ciq_free(c);
+      return st;
+    }
+    c->has_precond = true;
+  }
   *out = c;
   return CIQ_OK;
 fail:
@@ -706,7 +829,29 @@ void ciq_free(ciq_ctx* c) {
   dfree(c->staging);
   dfree(c->feat_a); dfree(c->feat_b); dfree(c->planes); dfree(c->inv_scale); dfree(c->psplit);
   dfree(c->apart_tc);
+  free_precond(c->pc);
   delete c;
+}
+
+ciq_status ciq_pivoted_cholesky(ciq_ctx* c, int32_t rank, float* L, int64_t ldl) {
+  if (!c || !L) return CIQ_ERR_INVALID_ARG;
+  const int64_t n = c->op.n;
+  if (rank < 1 || rank > n || ldl < rank) return set_err(c, CIQ_ERR_DIM, "bad rank / ldl");
+  if (join_user_stream(c) != CIQ_OK) return CIQ_ERR_CUDA;
+  float* ld = nullptr;
+  double *diag = nullptr, *lcol = nullptr, *pivval = nullptr;
+  int* piv = nullptr;
+  CUDA_TRY(c, dalloc(&ld, (size_t)n * rank));
+  CUDA_TRY(c, dalloc(&diag, (size_t)n));
+  CUDA_TRY(c, dalloc(&lcol, (size_t)n * rank));
+  CUDA_TRY(c, dalloc(&pivval, (size_t)rank));
+  CUDA_TRY(c, dalloc(&piv, (size_t)rank));
+  CUDA_TRY(c, cudaMemsetAsync(ld, 0, (size_t)n * rank * 4, c->stream));
+  LAUNCH(c, launch_pivchol(c->dev, rank, ld, rank, diag, lcol, piv, pivval, c->stream));
+  ciq_status st = store_rows(c, ld, rank, n, rank, L, ldl);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  dfree(ld); dfree(diag); dfree(lcol); dfree(pivval); dfree(piv);
+  return st;
 }
 
 ciq_status ciq_matvec(ciq_ctx* c, const float* V, int64_t ldv, int64_t T, float* out, int64_t ldo, int32_t impl) {
@@ -774,8 +919,29 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   hctrl.bd_tol = p.breakdown_tol;
   CUDA_TRY(c, cudaMemcpyAsync(sc.ctrl, &hctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, s));
   const int nbs = rowblocks(rows, tp);
-  LAUNCH(c, launch_colsq_partials(ws.w[1], rows, tp, ws.bpart, s));
-  LAUNCH(c, launch_reduce_cols(ws.bpart, nbs, tp, ws.colsq, 0, s));
+  PrecondDev& P = c->pc;
+  if (P.on) {
+    // App. A: preconditioned msMINRES started from c = P^{1/2} b (eqs. precond_sqrt /
+    // precond_sqrt_inverse); r-space R_1 = c, Z_1 = P^{-1} c, beta_1^2 = c^T P^{-1} c.
+    if (P.z_cap < (size_t)n * tp) {
+      ++c->buf_gen;
+      dfree(P.z[0]);
+      dfree(P.z[1]);
+      CUDA_TRY(c, dalloc(&P.z[0], (size_t)n * tp));
+      CUDA_TRY(c, dalloc(&P.z[1], (size_t)n * tp));
+      P.z_cap = (size_t)n * tp;
+    }
+    st = precond_power(c, PW_HALF, ws.w[1], tp, rows, P.z[0], nullptr);
+    if (st != CIQ_OK) return st;
+    CUDA_TRY(c, cudaMemcpyAsync(ws.w[1], P.z[0], (size_t)rows * tp * 4, cudaMemcpyDeviceToDevice, s));
+    st = precond_power(c, PW_INV, ws.w[1], tp, rows, P.z[1], ws.w[1]);
+    if (st != CIQ_OK) return st;
+    CUDA_TRY(c, cudaMemsetAsync(P.z[0], 0, (size_t)n * tp * 4, s));
+    LAUNCH(c, launch_reduce_cols(P.bpart, uapply_blocks(rows), tp, ws.colsq, 0, s));
+  } else {
+    LAUNCH(c, launch_colsq_partials(ws.w[1], rows, tp, ws.bpart, s));
+    LAUNCH(c, launch_reduce_cols(ws.bpart, nbs, tp, ws.colsq, 0, s));
+  }
   LAUNCH(c, launch_init_state(sc, nq, tp, ws.colsq, s));
 
   // a2/a3: spectrum estimate and quadrature rule
@@ -790,7 +956,8 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
       lmin = p.lambda_min;
       lmax = p.lambda_max;
     } else {
-      st = estimate_lambda(c, &p, c->op.diag, &lmin, &lmax, &rmin, &rmax, &lambda_mvms);
+      // rigorous lower bound on lambda_min (reading G6): sigma2 for K, 1 for P^{-1/2} K P^{-1/2}
+      st = estimate_lambda(c, &p, P.on ? 1.0 : (double)c->op.diag, &lmin, &lmax, &rmin, &rmax, &lambda_mvms);
       if (st != CIQ_OK) return st;
     }
     int r = ciqh::hht_rule(lmin, lmax, nq, t, w);
@@ -807,7 +974,35 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   float* dslot[2] = {ws.d, ws.d + (size_t)nq * rows * tp};
   Ctrl hc{};
   int loop_nsplit = 1, loop_impl = 0;
+  auto enqueue_iter_pc = [&](int j) -> ciq_status {
+    // preconditioned step j: MVM on Z_j, r-space recurrence + update of step j-1 with Z_{j-1},
+    // Z_{j+1} = P^{-1} R_{j+1} (into Z_{j-1}'s slot) with the beta^2 partials R.Z, Givens.
+    float* rcur = ws.w[j % 3];
+    float* rprev = ws.w[(j + 2) % 3];
+    float* rnew = ws.w[(j + 1) % 3];
+    float* zcur = P.z[j & 1];
+    float* zprev = P.z[(j + 1) & 1];
+    begin_timed(c, j, 0);
+    int nsplit = 1, nbm = 0;
+    double* apart = nullptr;
+    ciq_status st2 = run_mvm(c, zcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit, &apart, &nbm);
+    end_timed(c);
+    if (st2 != CIQ_OK) return st2;
+    const float* pin = (nsplit > 1) ? c->psplit : ws.p;
+    loop_nsplit = nsplit;
+    loop_impl = c->mvm_kind_used;
+    LAUNCH(c, launch_alpha(sc, apart, nbm, tp, s));
+    begin_timed(c, j, 1);
+    LAUNCH(c, launch_precond_update(sc, pin, nsplit, (size_t)rows * tp, rcur, rprev, rnew, zprev, dslot[j & 1],
+                                    dslot[(j + 1) & 1], ws.y, nq, rows, tp, 0, s));
+    end_timed(c);
+    st2 = precond_power(c, PW_INV, rnew, tp, rows, zprev, rnew);
+    if (st2 != CIQ_OK) return st2;
+    LAUNCH(c, launch_givens(sc, P.bpart, uapply_blocks(rows), nq, tp, s));
+    return CIQ_OK;
+  };
   auto enqueue_iter = [&](int j) -> ciq_status {
+    if (P.on) return enqueue_iter_pc(j);
     float* wcur = ws.w[j % 3];
     float* wprev = ws.w[(j + 2) % 3];
     float* wnew = ws.w[(j + 1) % 3];
@@ -837,6 +1032,10 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     // size every buffer the MVM may (re)allocate before capturing
     st = prepare_mvm_buffers(c, tp, p.mvm_impl);
     if (st != CIQ_OK) return st;
+    if (P.on) {  // precond_power's work buffers at this tp (already grown by the start vector)
+      st = grow(c, &P.part, &P.part_cap, (size_t)utv_splits(rows) * P.r2 * tp);
+      if (st != CIQ_OK) return st;
+    }
     const uint64_t key[6] = {c->buf_gen, (uint64_t)tp, (uint64_t)nq, (uint64_t)p.mvm_impl, (uint64_t)block,
                              (uint64_t)(uintptr_t)ws.d};
     if (c->gexec == nullptr || std::memcmp(key, c->gkey, sizeof(key)) != 0) {
@@ -902,8 +1101,11 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     }
   }
   const int J = hc.iters;
-  // last pending update (step J): v_J lives in the buffer that was W_cur at iteration J
-  if (J >= 1) {
+  // last pending update (step J): v_J lives in the buffer that was W_cur (Z_cur) at iteration J
+  if (J >= 1 && P.on) {
+    LAUNCH(c, launch_precond_update(sc, nullptr, 1, 0, nullptr, nullptr, nullptr, P.z[J & 1], dslot[(J + 1) & 1],
+                                    dslot[J & 1], ws.y, nq, rows, tp, 1, s));
+  } else if (J >= 1) {
     float* d1 = dslot[(J + 1) & 1];  // d_{J-1}
     float* d2 = dslot[J & 1];        // d_{J-2}, overwritten by d_J
     float* wv = ws.w[J % 3];

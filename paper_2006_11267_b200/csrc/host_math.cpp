@@ -9,7 +9,9 @@
 // Independent of oracle/ (which evaluates the complex formula with mpmath).
 #include <cmath>
 #include <cstdint>
+#include <algorithm>
 #include <limits>
+#include <vector>
 
 #include "host_math.h"
 
@@ -123,6 +125,57 @@ int tridiag_extremes(const double* alpha, const double* beta, int m, double* emi
     if (sturm_count(alpha, beta, m, mid) >= m) b = mid; else a = mid;
   }
   *emax = 0.5 * (a + b);
+  return 0;
+}
+
+// Cyclic Jacobi eigendecomposition of a symmetric n x n matrix a (row-major, destroyed):
+// eigenvalues -> w (descending), eigenvectors -> columns of v (row-major n x n).
+int sym_eig_jacobi(double* a, int n, double* w, double* v) {
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) v[i * n + j] = (i == j) ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        tot += a[i * n + j] * a[i * n + j];
+        if (i != j) off += a[i * n + j] * a[i * n + j];
+      }
+    if (off <= 1e-30 * tot || off == 0.0) break;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = a[p * n + q];
+        if (std::fabs(apq) < 1e-300) continue;
+        const double app = a[p * n + p], aqq = a[q * n + q];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < n; ++k) {  // rotate columns p, q
+          const double akp = a[k * n + p], akq = a[k * n + q];
+          a[k * n + p] = c * akp - s * akq;
+          a[k * n + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {  // rotate rows p, q
+          const double apk = a[p * n + k], aqk = a[q * n + k];
+          a[p * n + k] = c * apk - s * aqk;
+          a[q * n + k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double vkp = v[k * n + p], vkq = v[k * n + q];
+          v[k * n + p] = c * vkp - s * vkq;
+          v[k * n + q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  // sort descending
+  std::vector<int> idx(n);
+  for (int i = 0; i < n; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int x, int y) { return a[x * n + x] > a[y * n + y]; });
+  std::vector<double> vs((size_t)n * n);
+  for (int j = 0; j < n; ++j) {
+    w[j] = a[idx[j] * n + idx[j]];
+    for (int i = 0; i < n; ++i) vs[(size_t)i * n + j] = v[i * n + idx[j]];
+  }
+  std::copy(vs.begin(), vs.end(), v);
   return 0;
 }
 

@@ -10,4 +10,6 @@ void ellipj_comp(double u, double m, double m1, double* sn, double* cn, double* 
 int hht_rule(double lambda_min, double lambda_max, int Q, double* t, double* w);
 // Extreme eigenvalues of a symmetric tridiagonal matrix (Sturm bisection). 0 ok.
 int tridiag_extremes(const double* alpha, const double* beta, int m, double* emin, double* emax);
+// Symmetric eigendecomposition (cyclic Jacobi, fp64): w descending, eigenvectors in columns of v.
+int sym_eig_jacobi(double* a, int n, double* w, double* v);
 }  // namespace ciqh

@@ -1,0 +1,122 @@
+"""GPU parity of the preconditioned variant (App. A).
+
+The GPU runs the P^{-1}-only preconditioned msMINRES (r-space recurrence, reading G13) from
+c = P^{1/2} b; the oracle runs the explicit symmetric route M = P^{-1/2} K P^{-1/2}
+(oracle.precond_ciq).  Both produce R' b (whiten) and R b (sqrt) for the same P, so they agree to
+the solver tolerance.  The preconditioner factor L is an INPUT of the library (ciq_precond.L);
+the tests take it from the oracle's pivoted Cholesky, like the explicit quadrature rule."""
+import numpy as np
+import pytest
+import torch
+
+import workloads
+from oracle import KernelOperator, LowRankPlusDiag, estimate_spectrum, hht_rule, pivoted_cholesky, precond_ciq
+
+pytestmark = pytest.mark.gpu
+
+import paper_2006_11267_b200 as pb  # noqa: E402
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def relerr(x, y):
+    return float(np.linalg.norm(np.asarray(x, np.float64) - y) / np.linalg.norm(y))
+
+
+def c4_like(n, t, rank):
+    cfg = workloads.scaled(workloads.CONFIGS["C4"], n=n, t=t)
+    inp = workloads.config_inputs(cfg)
+    op = KernelOperator(inp["X"], cfg.kind, cfg.lengthscale, cfg.outputscale, cfg.sigma2)
+    lfac = pivoted_cholesky(op, rank)
+    return cfg, inp, op, lfac
+
+
+@pytest.mark.parametrize("mode", ["whiten", "sqrt"])
+def test_precond_parity_explicit_rule(mode):
+    cfg, inp, op, lfac = c4_like(1500, 16, 64)
+    pre = LowRankPlusDiag(lfac, cfg.sigma2)
+
+    class _M:
+        def mvm(self, v):
+            return pre.power(op.mvm(pre.power(v, -0.5)), -0.5)
+
+    lmin, lmax, _, _ = estimate_spectrum(_M().mvm, inp["S"], 10, lower_bound=1.0)
+    t, w = hht_rule(lmin, lmax, cfg.q)
+    j = 120
+    ref = precond_ciq(op, pre, inp["B"].astype(np.float64), q=cfg.q, max_iters=j, tol=0.0, mode=mode, rule=(t, w))
+    assert np.max(np.abs(ref.solve.phibar) / ref.solve.beta1) < 1e-5
+    with pb.CIQ(cfg.kind, X=dev(inp["X"]), lengthscale=cfg.lengthscale, outputscale=cfg.outputscale,
+                diag=cfg.sigma2, precond_L=dev(lfac), precond_sigma2=cfg.sigma2) as g:
+        out = torch.empty((cfg.n, cfg.t), device="cuda")
+        info = g.apply(dev(inp["B"]), out, q=cfg.q, max_iters=j, tol=0.0, mode=mode, rule=(t, w))
+    assert info["rotated"]
+    assert relerr(out.cpu().numpy(), ref.out) < 1e-4
+
+
+def test_precond_own_estimate_end_to_end():
+    cfg, inp, op, lfac = c4_like(1200, 8, 48)
+    pre = LowRankPlusDiag(lfac, cfg.sigma2)
+    ref = precond_ciq(op, pre, inp["B"].astype(np.float64), q=cfg.q, max_iters=150, tol=0.0, mode="whiten",
+                      lanczos_start=inp["S"])
+    with pb.CIQ(cfg.kind, X=dev(inp["X"]), lengthscale=cfg.lengthscale, outputscale=cfg.outputscale,
+                diag=cfg.sigma2, precond_L=dev(lfac), precond_sigma2=cfg.sigma2) as g:
+        out = torch.empty((cfg.n, cfg.t), device="cuda")
+        info = g.apply(dev(inp["B"]), out, q=cfg.q, max_iters=150, tol=0.0, mode="whiten",
+                       lanczos_start=dev(inp["S"]))
+    assert abs(info["lambda_max"] / ref.lambda_max - 1) < 1e-4
+    assert info["lambda_min"] == pytest.approx(ref.lambda_min, rel=1e-5)
+    assert relerr(out.cpu().numpy(), ref.out) < 1e-4
+
+
+def test_identity_preconditioner_reproduces_plain_path():
+    cfg = workloads.scaled(workloads.CONFIGS["C3"], n=1000, t=4)
+    inp = workloads.make_inputs(cfg)
+    x = dev(inp["X"])
+    op = KernelOperator(inp["X"], cfg.kind, cfg.lengthscale, cfg.outputscale, cfg.sigma2)
+    lmin, lmax, _, _ = estimate_spectrum(op.mvm, inp["S"], 10, lower_bound=cfg.sigma2)
+    rule = hht_rule(lmin, lmax, 8)
+    outs = []
+    for pc in (None, np.zeros((1000, 1), np.float32)):
+        kw = {} if pc is None else dict(precond_L=dev(pc), precond_sigma2=1.0)
+        with pb.CIQ(cfg.kind, X=x, lengthscale=cfg.lengthscale, outputscale=cfg.outputscale, diag=cfg.sigma2, **kw) as g:
+            out = torch.empty((cfg.n, cfg.t), device="cuda")
+            g.apply(dev(inp["B"]), out, q=8, max_iters=60, tol=0.0, mode="invsqrt", rule=rule)
+            outs.append(out.cpu().numpy().astype(np.float64))
+    assert relerr(outs[1], outs[0]) < 2e-6
+
+
+def test_gram_identities_on_gpu():
+    n = 64
+    cfg = workloads.scaled(workloads.CONFIGS["C4"], n=n, t=n)
+    inp = workloads.make_inputs(cfg)
+    op = KernelOperator(inp["X"], cfg.kind, 0.4, 1.0, 1e-2)
+    lfac = pivoted_cholesky(op, 8)
+    k = op.dense()
+    eye = np.eye(n, dtype=np.float32)
+    with pb.CIQ(cfg.kind, X=dev(inp["X"]), lengthscale=0.4, outputscale=1.0, diag=1e-2, precond_L=dev(lfac),
+                precond_sigma2=1e-2) as g:
+        rp = torch.empty((n, n), device="cuda")
+        g.apply(dev(eye), rp, q=16, max_iters=200, tol=1e-7, mode="whiten", lanczos_start=dev(workloads.lanczos_start(n, 4)))
+        r = torch.empty((n, n), device="cuda")
+        g.apply(dev(eye), r, q=16, max_iters=200, tol=1e-7, mode="sqrt", lanczos_start=dev(workloads.lanczos_start(n, 4)))
+    rp = rp.cpu().numpy().astype(np.float64)
+    r = r.cpu().numpy().astype(np.float64)
+    kinv = np.linalg.inv(k)
+    assert np.linalg.norm(rp @ rp.T - kinv) / np.linalg.norm(kinv) < 1e-3   # R' R'^T = K^{-1}
+    assert np.linalg.norm(r @ r.T - k) / np.linalg.norm(k) < 1e-3            # R R^T = K
+
+
+def test_gpu_pivoted_cholesky_matches_oracle():
+    cfg = workloads.scaled(workloads.CONFIGS["C4"], n=2000, t=1)
+    inp = workloads.make_inputs(cfg)
+    op = KernelOperator(inp["X"], cfg.kind, cfg.lengthscale, cfg.outputscale, cfg.sigma2)
+    ref = pivoted_cholesky(op, 40)
+    with pb.CIQ(cfg.kind, X=dev(inp["X"]), lengthscale=cfg.lengthscale, outputscale=cfg.outputscale,
+                diag=cfg.sigma2) as g:
+        lout = torch.zeros((cfg.n, 40), device="cuda")
+        g.pivoted_cholesky(40, lout)
+    got = lout.cpu().numpy().astype(np.float64)
+    # the factor is unique given the pivot sequence; pivots are decided in fp64 on both sides
+    np.testing.assert_allclose(got, ref, rtol=0, atol=2e-6)
