@@ -64,15 +64,14 @@ struct PrecondDev {
   int rank = 0, r2 = 0;
   double sigma2 = 0.0;
   float* l = nullptr;       // n x rank (owned copy)
-  float* u = nullptr;       // n x r2
+  double* u = nullptr;      // n x r2 (fp64: see precond.cu)
   double* g[3] = {nullptr, nullptr, nullptr};
   float a[3] = {0.f, 0.f, 0.f};
   // work
   double* part = nullptr;   size_t part_cap = 0;   // utv partials  [splits][r2][tp]
   double* h = nullptr;      size_t h_cap = 0;      // U^T v         [r2][tp]
   double* bpart = nullptr;  size_t bpart_cap = 0;  // dot partials  [blocks][tp]
-  float* z[2] = {nullptr, nullptr}; size_t z_cap = 0;
-  float* t1 = nullptr; float* t2 = nullptr; size_t t_cap = 0;  // lambda estimate on P^-1/2 K P^-1/2
+  float* t1 = nullptr; size_t t_cap = 0;  // [2][n][tp] scratch of M v = P^-1/2 K P^-1/2 v
 };
 enum { PW_INV = 0, PW_HALF = 1, PW_MHALF = 2 };
 
@@ -521,10 +520,10 @@ ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, 
       PrecondDev& P = c->pc;
       ciq_status gs = grow(c, &P.t1, &P.t_cap, (size_t)2 * n * tpl);
       if (gs != CIQ_OK) return gs;
-      P.t2 = P.t1 + (size_t)n * tpl;
+      float* t2 = P.t1 + (size_t)n * tpl;
       if (precond_power(c, PW_MHALF, vj, tpl, n, P.t1, nullptr) != CIQ_OK) return CIQ_ERR_CUDA;
-      if (run_mvm(c, P.t1, tpl, P.t2, nullptr, nullptr, p->mvm_impl) != CIQ_OK) return CIQ_ERR_CUDA;
-      if (precond_power(c, PW_MHALF, P.t2, tpl, n, lw.p, nullptr) != CIQ_OK) return CIQ_ERR_CUDA;
+      if (run_mvm(c, P.t1, tpl, t2, nullptr, nullptr, p->mvm_impl) != CIQ_OK) return CIQ_ERR_CUDA;
+      if (precond_power(c, PW_MHALF, t2, tpl, n, lw.p, nullptr) != CIQ_OK) return CIQ_ERR_CUDA;
     } else if (run_mvm(c, vj, tpl, lw.p, nullptr, nullptr, p->mvm_impl) != CIQ_OK) {
       return CIQ_ERR_CUDA;
     }
@@ -615,12 +614,12 @@ ciq_status build_precond(ciq_ctx* c) {
   int r2 = 0;
   while (r2 < r && w[r2] > 1e-12 * smax2 && w[r2] > 0) ++r2;
   P.r2 = std::max(r2, 1);
-  std::vector<float> wsi((size_t)r * P.r2, 0.f);
+  std::vector<double> wsi((size_t)r * P.r2, 0.0);
   for (int k = 0; k < r; ++k)
-    for (int j = 0; j < r2; ++j) wsi[(size_t)k * P.r2 + j] = (float)(vec[(size_t)k * r + j] / std::sqrt(w[j]));
-  float* wsi_d = nullptr;
+    for (int j = 0; j < r2; ++j) wsi[(size_t)k * P.r2 + j] = vec[(size_t)k * r + j] / std::sqrt(w[j]);
+  double* wsi_d = nullptr;
   CUDA_TRY(c, dalloc(&wsi_d, wsi.size()));
-  CUDA_TRY(c, cudaMemcpyAsync(wsi_d, wsi.data(), wsi.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(wsi_d, wsi.data(), wsi.size() * 8, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, dalloc(&P.u, (size_t)n * P.r2));
   LAUNCH(c, launch_small_right_mul(P.l, r, r, wsi_d, P.r2, n, P.u, P.r2, c->stream));
   const double s2 = P.sigma2;
@@ -643,9 +642,7 @@ void free_precond(PrecondDev& P) {
   dfree(P.l); dfree(P.u);
   for (auto& g : P.g) dfree(g);
   dfree(P.part); dfree(P.h); dfree(P.bpart);
-  for (auto& z : P.z) dfree(z);
   dfree(P.t1);
-  P.t2 = nullptr;
 }
 
 struct EvTimer {
@@ -920,29 +917,16 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   CUDA_TRY(c, cudaMemcpyAsync(sc.ctrl, &hctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, s));
   const int nbs = rowblocks(rows, tp);
   PrecondDev& P = c->pc;
-  if (P.on) {
-    // App. A: preconditioned msMINRES started from c = P^{1/2} b (eqs. precond_sqrt /
-    // precond_sqrt_inverse); r-space R_1 = c, Z_1 = P^{-1} c, beta_1^2 = c^T P^{-1} c.
-    if (P.z_cap < (size_t)n * tp) {
-      ++c->buf_gen;
-      dfree(P.z[0]);
-      dfree(P.z[1]);
-      CUDA_TRY(c, dalloc(&P.z[0], (size_t)n * tp));
-      CUDA_TRY(c, dalloc(&P.z[1], (size_t)n * tp));
-      P.z_cap = (size_t)n * tp;
-    }
-    st = precond_power(c, PW_HALF, ws.w[1], tp, rows, P.z[0], nullptr);
-    if (st != CIQ_OK) return st;
-    CUDA_TRY(c, cudaMemcpyAsync(ws.w[1], P.z[0], (size_t)rows * tp * 4, cudaMemcpyDeviceToDevice, s));
-    st = precond_power(c, PW_INV, ws.w[1], tp, rows, P.z[1], ws.w[1]);
-    if (st != CIQ_OK) return st;
-    CUDA_TRY(c, cudaMemsetAsync(P.z[0], 0, (size_t)n * tp * 4, s));
-    LAUNCH(c, launch_reduce_cols(P.bpart, uapply_blocks(rows), tp, ws.colsq, 0, s));
-  } else {
-    LAUNCH(c, launch_colsq_partials(ws.w[1], rows, tp, ws.bpart, s));
-    LAUNCH(c, launch_reduce_cols(ws.bpart, nbs, tp, ws.colsq, 0, s));
-  }
+  LAUNCH(c, launch_colsq_partials(ws.w[1], rows, tp, ws.bpart, s));
+  LAUNCH(c, launch_reduce_cols(ws.bpart, nbs, tp, ws.colsq, 0, s));
   LAUNCH(c, launch_init_state(sc, nq, tp, ws.colsq, s));
+  if (P.on) {  // work buffers of precond_power / apply_m at this tp (before any graph capture)
+    st = grow(c, &P.part, &P.part_cap, (size_t)utv_splits(rows) * P.r2 * tp);
+    if (st == CIQ_OK) st = grow(c, &P.h, &P.h_cap, (size_t)P.r2 * tp);
+    if (st == CIQ_OK) st = grow(c, &P.bpart, &P.bpart_cap, (size_t)uapply_blocks(rows) * tp);
+    if (st == CIQ_OK) st = grow(c, &P.t1, &P.t_cap, (size_t)2 * n * tp);
+    if (st != CIQ_OK) return st;
+  }
 
   // a2/a3: spectrum estimate and quadrature rule
   double t[CIQ_MAX_Q], w[CIQ_MAX_Q];
@@ -974,42 +958,32 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   float* dslot[2] = {ws.d, ws.d + (size_t)nq * rows * tp};
   Ctrl hc{};
   int loop_nsplit = 1, loop_impl = 0;
-  auto enqueue_iter_pc = [&](int j) -> ciq_status {
-    // preconditioned step j: MVM on Z_j, r-space recurrence + update of step j-1 with Z_{j-1},
-    // Z_{j+1} = P^{-1} R_{j+1} (into Z_{j-1}'s slot) with the beta^2 partials R.Z, Givens.
-    float* rcur = ws.w[j % 3];
-    float* rprev = ws.w[(j + 2) % 3];
-    float* rnew = ws.w[(j + 1) % 3];
-    float* zcur = P.z[j & 1];
-    float* zprev = P.z[(j + 1) & 1];
-    begin_timed(c, j, 0);
-    int nsplit = 1, nbm = 0;
-    double* apart = nullptr;
-    ciq_status st2 = run_mvm(c, zcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit, &apart, &nbm);
-    end_timed(c);
+  // Preconditioned operator M = P^{-1/2} K P^{-1/2} (App. A): out = M v with the fixed-order
+  // partials of v.out (the alpha partials); the column norms of P^{-1/2} v (needed by the split-
+  // fp16 packing) come from the same streaming pass.
+  auto apply_m = [&](const float* v, float* out, double** apart, int* nbm) -> ciq_status {
+    ciq_status st2 = precond_power(c, PW_MHALF, v, tp, rows, P.t1, P.t1);
     if (st2 != CIQ_OK) return st2;
-    const float* pin = (nsplit > 1) ? c->psplit : ws.p;
-    loop_nsplit = nsplit;
-    loop_impl = c->mvm_kind_used;
-    LAUNCH(c, launch_alpha(sc, apart, nbm, tp, s));
-    begin_timed(c, j, 1);
-    LAUNCH(c, launch_precond_update(sc, pin, nsplit, (size_t)rows * tp, rcur, rprev, rnew, zprev, dslot[j & 1],
-                                    dslot[(j + 1) & 1], ws.y, nq, rows, tp, 0, s));
-    end_timed(c);
-    st2 = precond_power(c, PW_INV, rnew, tp, rows, zprev, rnew);
+    LAUNCH(c, launch_reduce_cols(P.bpart, uapply_blocks(rows), tp, ws.colsq, 1, s));
+    float* t2 = P.t1 + (size_t)n * tp;   // second half of the t1 allocation (2 n tp)
+    st2 = run_mvm(c, P.t1, tp, t2, nullptr, nullptr, p.mvm_impl, ws.colsq);
     if (st2 != CIQ_OK) return st2;
-    LAUNCH(c, launch_givens(sc, P.bpart, uapply_blocks(rows), nq, tp, s));
+    st2 = precond_power(c, PW_MHALF, t2, tp, rows, out, v);
+    if (st2 != CIQ_OK) return st2;
+    *apart = P.bpart;
+    *nbm = uapply_blocks(rows);
     return CIQ_OK;
   };
   auto enqueue_iter = [&](int j) -> ciq_status {
-    if (P.on) return enqueue_iter_pc(j);
     float* wcur = ws.w[j % 3];
     float* wprev = ws.w[(j + 2) % 3];
     float* wnew = ws.w[(j + 1) % 3];
     begin_timed(c, j, 0);
     int nsplit = 1, nbm = 0;
     double* apart = nullptr;
-    ciq_status st2 = run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit, &apart, &nbm);
+    ciq_status st2 = P.on ? apply_m(wcur, ws.p, &apart, &nbm)
+                          : run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit,
+                                    &apart, &nbm);
     end_timed(c);
     if (st2 != CIQ_OK) return st2;
     const float* pin = (nsplit > 1) ? c->psplit : ws.p;
@@ -1032,10 +1006,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     // size every buffer the MVM may (re)allocate before capturing
     st = prepare_mvm_buffers(c, tp, p.mvm_impl);
     if (st != CIQ_OK) return st;
-    if (P.on) {  // precond_power's work buffers at this tp (already grown by the start vector)
-      st = grow(c, &P.part, &P.part_cap, (size_t)utv_splits(rows) * P.r2 * tp);
-      if (st != CIQ_OK) return st;
-    }
+
     const uint64_t key[6] = {c->buf_gen, (uint64_t)tp, (uint64_t)nq, (uint64_t)p.mvm_impl, (uint64_t)block,
                              (uint64_t)(uintptr_t)ws.d};
     if (c->gexec == nullptr || std::memcmp(key, c->gkey, sizeof(key)) != 0) {
@@ -1101,11 +1072,8 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     }
   }
   const int J = hc.iters;
-  // last pending update (step J): v_J lives in the buffer that was W_cur (Z_cur) at iteration J
-  if (J >= 1 && P.on) {
-    LAUNCH(c, launch_precond_update(sc, nullptr, 1, 0, nullptr, nullptr, nullptr, P.z[J & 1], dslot[(J + 1) & 1],
-                                    dslot[J & 1], ws.y, nq, rows, tp, 1, s));
-  } else if (J >= 1) {
+  // last pending update (step J): v_J lives in the buffer that was W_cur at iteration J
+  if (J >= 1) {
     float* d1 = dslot[(J + 1) & 1];  // d_{J-1}
     float* d2 = dslot[J & 1];        // d_{J-2}, overwritten by d_J
     float* wv = ws.w[J % 3];
@@ -1114,18 +1082,25 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   }
   CUDA_TRY(c, cudaEventRecord(ev.e[3], s));
 
-  // a7: finalise
+  // a7: finalise.  With P: Y = M^{-1/2} b in M-space, R' b = P^{-1/2} Y (eq. precond_sqrt_inverse,
+  // P:55-64) and R b = K R' b (eq. precond_sqrt).
+  float* yout = ws.y;
+  if (P.on) {
+    st = precond_power(c, PW_MHALF, ws.y, tp, rows, P.t1, nullptr);
+    if (st != CIQ_OK) return st;
+    yout = P.t1;
+  }
   int final_mvm = 0;
   if (p.mode == CIQ_MODE_SQRT) {
     // K . Y  (Y is the full vector on one GPU)
-    LAUNCH(c, launch_colsq_partials(ws.y, rows, tp, ws.bpart, s));
+    LAUNCH(c, launch_colsq_partials(yout, rows, tp, ws.bpart, s));
     LAUNCH(c, launch_reduce_cols(ws.bpart, nbs, tp, ws.colsq, 1, s));
-    st = run_mvm(c, ws.y, tp, ws.p, nullptr, nullptr, p.mvm_impl, ws.colsq);
+    st = run_mvm(c, yout, tp, ws.p, nullptr, nullptr, p.mvm_impl, ws.colsq);
     if (st != CIQ_OK) return st;
     final_mvm = 1;
     st = store_rows(c, ws.p, tp, rows, (int)T, out, ldo);
   } else {
-    st = store_rows(c, ws.y, tp, rows, (int)T, out, ldo);
+    st = store_rows(c, yout, tp, rows, (int)T, out, ldo);
   }
   if (st != CIQ_OK) return st;
   CUDA_TRY(c, cudaEventRecord(ev.e[4], s));

@@ -101,16 +101,13 @@ cudaError_t launch_scale_cols_by(const float* src, float* dst, int64_t rows, int
 // ---- preconditioner P = L L^T + sigma2 I (precond.cu) ----
 int utv_splits(int64_t rows);
 int uapply_blocks(int64_t rows);
-cudaError_t launch_utv(const float* u, int ldu, int r, const float* v, int tp, int64_t rows, int nsplit, double* part,
+cudaError_t launch_utv(const double* u, int ldu, int r, const float* v, int tp, int64_t rows, int nsplit, double* part,
                        cudaStream_t s);
-cudaError_t launch_uapply(const float* u, int ldu, int r, const double* g, const double* h, const float* v, float a,
+cudaError_t launch_uapply(const double* u, int ldu, int r, const double* g, const double* h, const float* v, float a,
                           int tp, int64_t rows, float* out, const float* dotv, double* bpart, cudaStream_t s);
 cudaError_t launch_gram(const float* l, int ldl, int r, int64_t n, double* gram, cudaStream_t s);
-cudaError_t launch_small_right_mul(const float* l, int ldl, int r, const float* wsi, int r2, int64_t n, float* u,
+cudaError_t launch_small_right_mul(const float* l, int ldl, int r, const double* wsi, int r2, int64_t n, double* u,
                                    int ldu, cudaStream_t s);
-cudaError_t launch_precond_update(const Scal& sc, const float* p, int nsplit, size_t split_stride, const float* rcur,
-                                  const float* rprev, float* rnew, const float* zprev, float* d1, float* d2,
-                                  float* y, int nq, int64_t rows, int tp, int final_only, cudaStream_t s);
 cudaError_t launch_pivchol(const OpDev& op, int rank, float* l, int ldl, double* diag, double* lcol, int* piv,
                            double* pivval, cudaStream_t s);
 

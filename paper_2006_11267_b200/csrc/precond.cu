@@ -5,12 +5,14 @@
 // With the eigendecomposition L^T L = W diag(s^2) W^T (fp64 on the host) and U = L W diag(1/s)
 // (orthonormal N x r), every power of P is
 //     P^p v = sigma2^p v + U diag((s^2 + sigma2)^p - sigma2^p) U^T v,
-// so P^{-1} ("matrix inversion lemma"), P^{1/2} (start vector) and P^{-1/2} (the
-// lambda estimate on P^{-1/2} K P^{-1/2}) are all the same two skinny GEMMs with U:
+// so P^{-1} ("matrix inversion lemma") and P^{+-1/2} are all the same two skinny GEMMs with U.
+// The solver runs on M = P^{-1/2} K P^{-1/2} (reading G13): per iteration
+// M v = P^{-1/2} (K (P^{-1/2} v)), and R' b = P^{-1/2} M^{-1/2} b at the end:
 //     H = U^T V  (r x T, split-K over row blocks, fixed-order fp64 reduction)
 //     out = a V + U (g o H)       (optionally with the fp64 partials of sum_i out_ic x_ic)
-// U is orthonormal, so the fp32 application is well conditioned even when C = sigma2 I + L^T L
-// is not (the explicit Woodbury inverse would lose ~kappa(C) in fp32).
+// U is orthonormal and kept in fp64 with fp64 accumulation: P^{-1/2} amplifies by 1/sigma, and fp32
+// storage of U alone costs ~1e-4 relative error at kappa(K) ~ 3e4 (numpy emulation);
+// inputs/outputs stay fp32.
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -23,33 +25,33 @@ constexpr int TB = 64;   // tile of the skinny GEMMs (rows x columns)
 constexpr int KB = 16;   // contraction step
 
 // part[split][k][c] = sum_{i in split rows} U[i][k] V[i][c]   (k < r, c < tp)
-__global__ void __launch_bounds__(256) utv_kernel(const float* __restrict__ u, int ldu, int r,
+__global__ void __launch_bounds__(256) utv_kernel(const double* __restrict__ u, int ldu, int r,
                                                   const float* __restrict__ v, int tp, int64_t rows, int nsplit,
                                                   double* __restrict__ part) {
-  __shared__ float us[KB][TB + 1];
+  __shared__ double us[KB][TB + 1];
   __shared__ float vs[KB][TB + 1];
   const int k0 = blockIdx.x * TB, c0 = blockIdx.y * TB, sp = blockIdx.z;
   const int64_t i_begin = rows * sp / nsplit, i_end = rows * (sp + 1) / nsplit;
   const int tid = threadIdx.x, tk = tid / 16, tc = tid % 16;  // 4x4 outputs per thread
-  float acc[4][4] = {};
+  double acc[4][4] = {};
   for (int64_t i0 = i_begin; i0 < i_end; i0 += KB) {
     __syncthreads();
     for (int e = tid; e < KB * TB; e += 256) {
       const int ii = e / TB, cc = e % TB;
       const int64_t i = i0 + ii;
-      us[ii][cc] = (i < i_end && k0 + cc < r) ? u[i * ldu + k0 + cc] : 0.f;
+      us[ii][cc] = (i < i_end && k0 + cc < r) ? u[i * ldu + k0 + cc] : 0.0;
       vs[ii][cc] = (i < i_end && c0 + cc < tp) ? v[i * tp + c0 + cc] : 0.f;
     }
     __syncthreads();
 #pragma unroll
     for (int ii = 0; ii < KB; ++ii) {
-      float a[4], b[4];
+      double a[4], b[4];
 #pragma unroll
-      for (int x = 0; x < 4; ++x) { a[x] = us[ii][tk * 4 + x]; b[x] = vs[ii][tc * 4 + x]; }
+      for (int x = 0; x < 4; ++x) { a[x] = us[ii][tk * 4 + x]; b[x] = (double)vs[ii][tc * 4 + x]; }
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(a[x], b[y], acc[x][y]);
+        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
     }
   }
 #pragma unroll
@@ -57,43 +59,43 @@ __global__ void __launch_bounds__(256) utv_kernel(const float* __restrict__ u, i
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
       const int k = k0 + tk * 4 + x, c = c0 + tc * 4 + y;
-      if (k < r && c < tp) part[((size_t)sp * r + k) * tp + c] = (double)acc[x][y];
+      if (k < r && c < tp) part[((size_t)sp * r + k) * tp + c] = acc[x][y];
     }
 }
 
 // out[i][c] = a * V[i][c] + sum_k U[i][k] g[k] H[k][c];  bpart (optional): partial sums over the
 // CTA's rows of out[i][c] * dotv[i][c] (fp64, fixed order).
-__global__ void __launch_bounds__(256) uapply_kernel(const float* __restrict__ u, int ldu, int r,
+__global__ void __launch_bounds__(256) uapply_kernel(const double* __restrict__ u, int ldu, int r,
                                                      const double* __restrict__ g, const double* __restrict__ h,
                                                      const float* __restrict__ v, float a, int tp, int64_t rows,
                                                      float* __restrict__ out, const float* __restrict__ dotv,
                                                      double* __restrict__ bpart) {
-  __shared__ float us[TB][KB + 1];
-  __shared__ float hs[KB][TB + 1];
+  __shared__ double us[TB][KB + 1];
+  __shared__ double hs[KB][TB + 1];
   __shared__ double red[16][TB];
   const int64_t i0 = (int64_t)blockIdx.x * TB;
   const int c0 = blockIdx.y * TB;
   const int tid = threadIdx.x, ti = tid / 16, tc = tid % 16;
-  float acc[4][4] = {};
+  double acc[4][4] = {};
   for (int k0 = 0; k0 < r; k0 += KB) {
     __syncthreads();
     for (int e = tid; e < TB * KB; e += 256) {
       const int ii = e / KB, kk = e % KB;
       const int64_t i = i0 + ii;
-      us[ii][kk] = (i < rows && k0 + kk < r) ? u[i * ldu + k0 + kk] : 0.f;
+      us[ii][kk] = (i < rows && k0 + kk < r) ? u[i * ldu + k0 + kk] : 0.0;
       const int kk2 = e / TB, cc = e % TB;
-      hs[kk2][cc] = (k0 + kk2 < r && c0 + cc < tp) ? (float)(g[k0 + kk2] * h[(size_t)(k0 + kk2) * tp + c0 + cc]) : 0.f;
+      hs[kk2][cc] = (k0 + kk2 < r && c0 + cc < tp) ? g[k0 + kk2] * h[(size_t)(k0 + kk2) * tp + c0 + cc] : 0.0;
     }
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < KB; ++kk) {
-      float x[4], y[4];
+      double x[4], y[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) { x[q] = us[ti * 4 + q][kk]; y[q] = hs[kk][tc * 4 + q]; }
 #pragma unroll
       for (int p = 0; p < 4; ++p)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[p][q] = fmaf(x[p], y[q], acc[p][q]);
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(x[p], y[q], acc[p][q]);
     }
   }
   double part[4] = {0, 0, 0, 0};
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(256) uapply_kernel(const float* __restrict__ u
     for (int q = 0; q < 4; ++q) {
       const int c = c0 + tc * 4 + q;
       if (c >= tp) continue;
-      const float o = fmaf(a, v[i * tp + c], acc[p][q]);
+      const float o = (float)fma((double)a, (double)v[i * tp + c], acc[p][q]);
       out[i * tp + c] = o;
       if (dotv) part[q] += (double)o * (double)dotv[i * tp + c];
     }
@@ -132,80 +134,17 @@ __global__ void gram_kernel(const float* __restrict__ l, int ldl, int r, int64_t
   gram[(size_t)m * r + k] = s;
 }
 
-// U[i][c] = sum_k L[i][k] Wsi[k][c]   (Wsi = W diag(1/s), r x r2, fp32)
-__global__ void small_right_mul_kernel(const float* __restrict__ l, int ldl, int r, const float* __restrict__ wsi,
-                                       int r2, int64_t n, float* __restrict__ u, int ldu) {
+// U[i][c] = sum_k L[i][k] Wsi[k][c]   (Wsi = W diag(1/s), r x r2, fp64)
+__global__ void small_right_mul_kernel(const float* __restrict__ l, int ldl, int r, const double* __restrict__ wsi,
+                                       int r2, int64_t n, double* __restrict__ u, int ldu) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n * ldu) return;
   const int64_t i = e / ldu;
   const int c = (int)(e % ldu);
-  if (c >= r2) { u[e] = 0.f; return; }
+  if (c >= r2) { u[e] = 0.0; return; }
   double s = 0.0;
-  for (int k = 0; k < r; ++k) s += (double)l[i * ldl + k] * (double)wsi[(size_t)k * r2 + c];
-  u[e] = (float)s;
-}
-
-// R_new = P / nrm_j - alpha R_cur / nrm_j - (beta_j / nrm_{j-1}) R_prev   and the descent update
-// of step j-1 with v_{j-1} = Z_prev / nrm_{j-1}  (preconditioned three-term recurrence in
-// r-space: Paige-Saunders / Choi form, reading G13).  Mirrors lanczos_update_kernel without the
-// beta partials (beta needs Z_new = P^{-1} R_new).
-__global__ void __launch_bounds__(256) precond_update_kernel(
-    Scal sc, const float* __restrict__ p, int nsplit, size_t split_stride, const float* __restrict__ rcur,
-    const float* __restrict__ rprev, float* __restrict__ rnew, const float* __restrict__ zprev,
-    const float* __restrict__ d1base, float* __restrict__ d2base, int64_t qstride, float* __restrict__ y, int nq,
-    int64_t rows, int tp, int final_only) {
-  const Ctrl* ctrl = sc.ctrl;
-  if (!final_only && ctrl->done) return;
-  const int pending = ctrl->pending;
-  const int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one float4 per thread
-  if (e4 * 4 >= rows * tp) return;
-  const int64_t off = e4 * 4;
-  const int c = (int)(off % tp);
-  if (!final_only) {
-    float4 pp = *reinterpret_cast<const float4*>(p + off);
-    for (int s = 1; s < nsplit; ++s) {
-      const float4 q4 = *reinterpret_cast<const float4*>(p + s * split_stride + off);
-      pp.x += q4.x; pp.y += q4.y; pp.z += q4.z; pp.w += q4.w;
-    }
-    const float4 rc = *reinterpret_cast<const float4*>(rcur + off);
-    const float4 rp = *reinterpret_cast<const float4*>(rprev + off);
-    float in[4], al[4], cp[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool fr = sc.frozen[c + k] != 0;
-      in[k] = fr ? 0.f : (float)(1.0 / sc.nrm_cur[c + k]);
-      al[k] = fr ? 0.f : (float)sc.alpha[c + k];
-      cp[k] = fr ? 0.f : (float)(sc.tb_cur[c + k] / sc.nrm_prev[c + k]);
-    }
-    float4 w;
-    w.x = fmaf(-cp[0], rp.x, (pp.x - al[0] * rc.x) * in[0]);
-    w.y = fmaf(-cp[1], rp.y, (pp.y - al[1] * rc.y) * in[1]);
-    w.z = fmaf(-cp[2], rp.z, (pp.z - al[2] * rc.z) * in[2]);
-    w.w = fmaf(-cp[3], rp.w, (pp.w - al[3] * rc.w) * in[3]);
-    *reinterpret_cast<float4*>(rnew + off) = w;
-  }
-  if (pending) {
-    const float4 zp = *reinterpret_cast<const float4*>(zprev + off);
-    float4 yy = *reinterpret_cast<const float4*>(y + off);
-    for (int q = 0; q < nq; ++q) {
-      const int k = q * tp + c;
-      const float4 a = *reinterpret_cast<const float4*>(sc.ca + k);
-      const float4 b = *reinterpret_cast<const float4*>(sc.cb + k);
-      const float4 e = *reinterpret_cast<const float4*>(sc.ce + k);
-      const float4 f = *reinterpret_cast<const float4*>(sc.cf + k);
-      const float4 x1 = *reinterpret_cast<const float4*>(d1base + q * qstride + off);
-      const float4 x2 = *reinterpret_cast<const float4*>(d2base + q * qstride + off);
-      float4 dn;
-      dn.x = fmaf(a.x, zp.x, fmaf(b.x, x1.x, e.x * x2.x));
-      dn.y = fmaf(a.y, zp.y, fmaf(b.y, x1.y, e.y * x2.y));
-      dn.z = fmaf(a.z, zp.z, fmaf(b.z, x1.z, e.z * x2.z));
-      dn.w = fmaf(a.w, zp.w, fmaf(b.w, x1.w, e.w * x2.w));
-      *reinterpret_cast<float4*>(d2base + q * qstride + off) = dn;
-      yy.x = fmaf(f.x, dn.x, yy.x); yy.y = fmaf(f.y, dn.y, yy.y);
-      yy.z = fmaf(f.z, dn.z, yy.z); yy.w = fmaf(f.w, dn.w, yy.w);
-    }
-    *reinterpret_cast<float4*>(y + off) = yy;
-  }
+  for (int k = 0; k < r; ++k) s += (double)l[i * ldl + k] * wsi[(size_t)k * r2 + c];
+  u[e] = s;
 }
 
 // ---- partial pivoted Cholesky of the kernel part k(X, X) (rows a9) ----
@@ -281,14 +220,14 @@ inline unsigned nbk(int64_t e, int bs) { return (unsigned)((e + bs - 1) / bs); }
 
 int utv_splits(int64_t rows) { return (int)std::min<int64_t>(32, std::max<int64_t>(1, rows / 256)); }
 
-cudaError_t launch_utv(const float* u, int ldu, int r, const float* v, int tp, int64_t rows, int nsplit, double* part,
+cudaError_t launch_utv(const double* u, int ldu, int r, const float* v, int tp, int64_t rows, int nsplit, double* part,
                        cudaStream_t s) {
   dim3 grid((r + TB - 1) / TB, (tp + TB - 1) / TB, nsplit);
   utv_kernel<<<grid, 256, 0, s>>>(u, ldu, r, v, tp, rows, nsplit, part);
   return cudaGetLastError();
 }
 
-cudaError_t launch_uapply(const float* u, int ldu, int r, const double* g, const double* h, const float* v, float a,
+cudaError_t launch_uapply(const double* u, int ldu, int r, const double* g, const double* h, const float* v, float a,
                           int tp, int64_t rows, float* out, const float* dotv, double* bpart, cudaStream_t s) {
   dim3 grid((unsigned)((rows + TB - 1) / TB), (tp + TB - 1) / TB);
   uapply_kernel<<<grid, 256, 0, s>>>(u, ldu, r, g, h, v, a, tp, rows, out, dotv, bpart);
@@ -302,18 +241,9 @@ cudaError_t launch_gram(const float* l, int ldl, int r, int64_t n, double* gram,
   return cudaGetLastError();
 }
 
-cudaError_t launch_small_right_mul(const float* l, int ldl, int r, const float* wsi, int r2, int64_t n, float* u,
+cudaError_t launch_small_right_mul(const float* l, int ldl, int r, const double* wsi, int r2, int64_t n, double* u,
                                    int ldu, cudaStream_t s) {
   small_right_mul_kernel<<<nbk(n * ldu, 256), 256, 0, s>>>(l, ldl, r, wsi, r2, n, u, ldu);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_precond_update(const Scal& sc, const float* p, int nsplit, size_t split_stride, const float* rcur,
-                                  const float* rprev, float* rnew, const float* zprev, float* d1, float* d2,
-                                  float* y, int nq, int64_t rows, int tp, int final_only, cudaStream_t s) {
-  const int64_t n4 = rows * tp / 4;
-  precond_update_kernel<<<nbk(n4, 256), 256, 0, s>>>(sc, p, nsplit, split_stride, rcur, rprev, rnew, zprev, d1, d2,
-                                                      rows * tp, y, nq, rows, tp, final_only);
   return cudaGetLastError();
 }
 

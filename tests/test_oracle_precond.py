@@ -94,3 +94,59 @@ def test_preconditioning_reduces_iterations():
     pre = LowRankPlusDiag(pivoted_cholesky(op, 64), sigma2)
     pc = precond_ciq(op, pre, b, q=12, max_iters=3000, tol=1e-4, mode="whiten", lanczos_start=s)
     assert pc.converged and pc.iters < plain.iters
+
+
+def test_pinv_only_recurrence_equals_symmetric_route():
+    """App. A: preconditioned msMINRES needs only P^{-1}.  An independent fp64
+    emulation of that r-space (Paige-Saunders/Choi) recurrence for (K + t_q P) x = P^{1/2} b must
+    reproduce the oracle's explicit M = P^{-1/2} K P^{-1/2} route (reading G13)."""
+    import math as _m
+    x = workloads.points(300, 3)
+    sigma2 = 1e-3
+    op = KernelOperator(x, "matern52", 0.3, 1.0, sigma2=sigma2)
+    pre = LowRankPlusDiag(pivoted_cholesky(op, 24), sigma2)
+    b = workloads.rhs(300, 3).astype(np.float64)
+    ref = precond_ciq(op, pre, b, q=8, max_iters=400, tol=0.0, mode="whiten", spectrum=(1.0, 2000.0))
+    assert np.max(np.abs(ref.solve.phibar) / ref.solve.beta1) < 1e-9
+    k = op.dense()
+    t, w = ref.t, ref.w
+    cvec = pre.power(b, 0.5)
+    y_acc = np.zeros_like(b)
+    for col in range(3):
+        for q in range(len(t)):
+            # scipy-style preconditioned MINRES on (K + t_q P) with preconditioner P (M^{-1} = P^{-1})
+            r1 = cvec[:, col].copy()
+            y = pre.power(r1, -1.0)
+            beta1 = _m.sqrt(r1 @ y)
+            beta, oldb = beta1, 0.0
+            r2 = r1.copy()
+            dbar = epsln = 0.0
+            phibar = beta1
+            cs, sn = -1.0, 0.0
+            wv = np.zeros(300); w2 = np.zeros(300); xq = np.zeros(300)
+            for itn in range(1, 401):
+                v = y / beta
+                y = k @ v + t[q] * pre.apply(v)
+                if itn >= 2:
+                    y = y - (beta / oldb) * r1
+                alfa = v @ y
+                y = y - (alfa / beta) * r2
+                r1, r2 = r2, y
+                y = pre.power(r2, -1.0)
+                oldb, beta = beta, _m.sqrt(max(r2 @ y, 0.0))
+                oldeps = epsln
+                delta = cs * dbar + sn * alfa
+                gbar = sn * dbar - cs * alfa
+                epsln = sn * beta
+                dbar = -cs * beta
+                gamma = max(_m.hypot(gbar, beta), 1e-300)
+                cs, sn = gbar / gamma, beta / gamma
+                phi = cs * phibar
+                phibar = sn * phibar
+                w1, w2 = w2, wv
+                wv = (v - oldeps * w1 - delta * w2) / gamma
+                xq = xq + phi * wv
+                if beta == 0.0:
+                    break
+            y_acc[:, col] += w[q] * xq
+    np.testing.assert_allclose(y_acc, ref.out, rtol=1e-6, atol=1e-9)
