@@ -101,12 +101,17 @@ typedef struct {
   float sigma2;               /* > 0                                                    */
 } ciq_precond;
 
-/* Row sharding across GPUs (one process per GPU).  NULL comm = single GPU. */
+/* Row sharding across GPUs (one process per GPU).  NULL comm = single GPU.  Rank r
+ * owns rows ciq_shard_rows(n, r, world); per iteration the ranks all-gather the next Lanczos
+ * block and the T-sized alpha / beta^2 partial sums (summed in rank order: bit-identical scalar
+ * state on every rank). */
 typedef struct {
   int32_t rank;
   int32_t world;
   const void* nccl_unique_id; /* 128 bytes from ciq_nccl_unique_id() on rank 0, broadcast by the
                                  caller (e.g. torch.distributed)                                */
+  void* loopback_group;       /* non-NULL: in-process loopback transport instead of NCCL (ranks are
+                                 threads sharing one GPU; from ciq_loopback_group_create)      */
 } ciq_comm;
 
 typedef struct {
@@ -200,6 +205,11 @@ ciq_status ciq_quadrature_rule(double lambda_min, double lambda_max, int32_t Q, 
 ciq_status ciq_tridiag_extremes(const double* alpha, const double* beta, int32_t m,
                                 double* eig_min, double* eig_max);
 ciq_status ciq_nccl_unique_id(void* out128);
+
+/* In-process loopback transport for `world` ranks (threads of one process, any device): used to
+ * exercise the row-sharded path without NCCL.  Destroy after every ctx using it is freed. */
+void* ciq_loopback_group_create(int32_t world);
+void ciq_loopback_group_destroy(void* group);
 
 #ifdef __cplusplus
 }

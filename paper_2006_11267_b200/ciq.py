@@ -50,7 +50,7 @@ class CiqPrecond(ctypes.Structure):
 
 
 class CiqComm(ctypes.Structure):
-    _fields_ = [("rank", c_int32), ("world", c_int32), ("nccl_unique_id", c_void_p)]
+    _fields_ = [("rank", c_int32), ("world", c_int32), ("nccl_unique_id", c_void_p), ("loopback_group", c_void_p)]
 
 
 class CiqParams(ctypes.Structure):
@@ -115,6 +115,10 @@ def _load() -> ctypes.CDLL:
     lib.ciq_tridiag_extremes.restype = c_int32
     lib.ciq_nccl_unique_id.argtypes = [c_void_p]
     lib.ciq_nccl_unique_id.restype = c_int32
+    lib.ciq_loopback_group_create.argtypes = [c_int32]
+    lib.ciq_loopback_group_create.restype = c_void_p
+    lib.ciq_loopback_group_destroy.argtypes = [c_void_p]
+    lib.ciq_loopback_group_destroy.restype = None
     return lib
 
 
@@ -123,7 +127,7 @@ LIB = _load()
 EXPORTED = ["ciq_params_default", "ciq_init", "ciq_apply", "ciq_matvec", "ciq_pivoted_cholesky", "ciq_free",
             "ciq_status_string",
             "ciq_last_error", "ciq_shard_rows", "ciq_quadrature_rule", "ciq_tridiag_extremes",
-            "ciq_nccl_unique_id"]
+            "ciq_nccl_unique_id", "ciq_loopback_group_create", "ciq_loopback_group_destroy"]
 
 
 class CiqError(RuntimeError):
@@ -202,6 +206,19 @@ def ciq_nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class LoopbackGroup:
+    """In-process loopback transport for `world` ranks (threads) -- exercises row sharding on one GPU."""
+
+    def __init__(self, world: int):
+        self.handle = LIB.ciq_loopback_group_create(int(world))
+        self.world = int(world)
+
+    def close(self):
+        if self.handle:
+            LIB.ciq_loopback_group_destroy(self.handle)
+            self.handle = None
+
+
 def _stream_handle(stream):
     if stream is None:
         try:
@@ -218,7 +235,8 @@ def _stream_handle(stream):
 
 def ciq_init(kind: str, n: int, *, X=None, K=None, lengthscale=1.0, outputscale: float = 1.0, diag: float = 0.0,
              precond_L=None, precond_sigma2: float = 0.0, comm: tuple | None = None, stream=None):
-    """Returns (ctx handle, keepalive list).  comm = (rank, world, unique_id_bytes) or None."""
+    """Returns (ctx handle, keepalive list).  comm = (rank, world, unique_id_bytes) for NCCL,
+    (rank, world, LoopbackGroup) for the in-process loopback transport, or None."""
     keep: list = []
     op = CiqOperator()
     op.kind = OP_KINDS[kind]
@@ -244,9 +262,12 @@ def ciq_init(kind: str, n: int, *, X=None, K=None, lengthscale=1.0, outputscale:
     if comm is not None:
         cm = CiqComm()
         cm.rank, cm.world = int(comm[0]), int(comm[1])
-        idbuf = ctypes.create_string_buffer(comm[2], 128)
-        keep.append(idbuf)
-        cm.nccl_unique_id = ctypes.cast(idbuf, c_void_p)
+        if isinstance(comm[2], LoopbackGroup):
+            cm.loopback_group = comm[2].handle
+        else:
+            idbuf = ctypes.create_string_buffer(comm[2], 128)
+            keep.append(idbuf)
+            cm.nccl_unique_id = ctypes.cast(idbuf, c_void_p)
     ctx = c_void_p()
     st = LIB.ciq_init(ctypes.byref(ctx), ctypes.byref(op), ctypes.byref(pc) if pc else None,
                       ctypes.byref(cm) if cm else None, _stream_handle(stream))

@@ -18,6 +18,7 @@
 #include "../../include/ciq.h"
 #include "host_math.h"
 #include "internal.h"
+#include "comm.h"
 #include "nccl_dl.h"
 
 using namespace ciq;
@@ -84,6 +85,13 @@ struct ciq_ctx {
   cudaEvent_t join_ev = nullptr;
   int rank = 0, world = 1;
   int64_t row0 = 0, row1 = 0;
+  int64_t per = 0;            // rows per shard (multiple of 128; last shard may be shorter)
+  int64_t nfull = 0;          // rows of the replicated (all-gathered) vectors = world * per >= n
+  Comm* comm = nullptr;
+  double* gsum = nullptr;     // [world][m] allgather buffer of cross-rank partial sums
+  size_t gsum_cap = 0;
+  double* tsum = nullptr;     // [tp] local sums
+  size_t tsum_cap = 0;
   float* xs = nullptr;        // owned scaled points
   float* kcopy = nullptr;     // owned dense copy (host-provided K)
   Workspace ws;
@@ -192,13 +200,15 @@ ciq_status ensure_workspace(ciq_ctx* c, int tp, int nq) {
   ws.tp = tp;
   ws.nq = nq;
   ws.rows = rows;
-  // W buffers hold all N rows (the MVM input); the local block is rows [row0, row1).
-  for (auto& b : ws.w) CUDA_TRY(c, dalloc(&b, (size_t)n * tp));
+  // W buffers hold all N rows (the MVM input; world * per >= N with zero padding); the local
+  // block is rows [row0, row1).
+  (void)n;
+  for (auto& b : ws.w) CUDA_TRY(c, dalloc(&b, (size_t)c->nfull * tp));
   CUDA_TRY(c, dalloc(&ws.p, (size_t)rows * tp));
   CUDA_TRY(c, dalloc(&ws.d, (size_t)2 * nq * rows * tp));
   CUDA_TRY(c, dalloc(&ws.y, (size_t)rows * tp));
   CUDA_TRY(c, dalloc(&ws.apart, (size_t)mvm_simt_blocks(rows) * tp + 64 * (size_t)tp));
-  CUDA_TRY(c, dalloc(&ws.bpart, (size_t)rowblocks(rows, tp) * tp));
+  CUDA_TRY(c, dalloc(&ws.bpart, (size_t)rowblocks(std::max(rows, c->nfull), tp) * tp));
   CUDA_TRY(c, dalloc(&ws.colsq, (size_t)tp));
   // scalar block
   size_t nd = (size_t)tp * 5 + (size_t)nq * tp * 5 + 2 * (size_t)nq;
@@ -470,6 +480,26 @@ bool build_tc_features(ciq_ctx* c, const std::vector<float>& xh) {
 ciq_status precond_power(ciq_ctx* c, int which, const float* v, int tp, int64_t rows, float* out,
                          const float* dotv);
 
+// vals[0..m) <- sum over ranks of vals (allgather + rank-order sum): identical on every rank.
+ciq_status global_sum(ciq_ctx* c, double* vals, int m) {
+  if (c->world == 1) return CIQ_OK;
+  ciq_status st = grow(c, &c->gsum, &c->gsum_cap, (size_t)c->world * m);
+  if (st != CIQ_OK) return st;
+  if (!c->comm->allgather(vals, c->gsum, (size_t)m * 8, c->stream))
+    return set_err(c, CIQ_ERR_NCCL, "allgather: %s", c->comm->error());
+  LAUNCH(c, launch_sum_ranks(c->gsum, c->world, m, vals, c->stream));
+  return CIQ_OK;
+}
+
+// Every rank's row block [row0, row1) of a full-height (nfull x tp) vector -> all ranks.
+ciq_status allgather_rows(ciq_ctx* c, float* full, int tp) {
+  if (c->world == 1) return CIQ_OK;
+  const size_t bytes = (size_t)c->per * tp * 4;
+  if (!c->comm->allgather(full + (size_t)c->rank * c->per * tp, full, bytes, c->stream))
+    return set_err(c, CIQ_ERR_NCCL, "allgather: %s", c->comm->error());
+  return CIQ_OK;
+}
+
 // Lambda estimation: Lanczos with full re-orthogonalisation on `cols` start
 // columns; Ritz extremes pooled; margins of reading G6.
 ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, double* lmin, double* lmax,
@@ -478,13 +508,16 @@ ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, 
   const int tpl = round16(cols);
   const int J = std::max(1, p->lanczos_iters);
   const int64_t n = c->op.n;
+  const int64_t nf = c->nfull;                 // basis vectors are full height (row-sharded work)
   const int64_t rows = c->row1 - c->row0;
-  if (c->world != 1) return set_err(c, CIQ_ERR_INVALID_ARG, "lambda estimation with row sharding: not built yet");
+  const int64_t r0 = c->row0;
+  if (c->world != 1 && c->pc.on)
+    return set_err(c, CIQ_ERR_INVALID_ARG, "preconditioner with row sharding: not supported");
   LambdaWork& lw = c->lw;
   if (lw.tpl != tpl || lw.nb < J + 1 || lw.rows != rows) {
     free_lambda(lw);
     lw.tpl = tpl; lw.nb = J + 1; lw.rows = rows;
-    CUDA_TRY(c, dalloc(&lw.basis, (size_t)(J + 1) * n * tpl));
+    CUDA_TRY(c, dalloc(&lw.basis, (size_t)(J + 1) * nf * tpl));
     CUDA_TRY(c, dalloc(&lw.p, (size_t)rows * tpl));
     CUDA_TRY(c, dalloc(&lw.part, (size_t)rowblocks(rows, tpl) * (J + 1) * tpl + (size_t)mvm_simt_blocks(rows) * tpl));
     CUDA_TRY(c, dalloc(&lw.h1, (size_t)(J + 1) * tpl));
@@ -496,16 +529,25 @@ ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, 
     CUDA_TRY(c, dalloc(&lw.len, (size_t)tpl));
   }
   cudaStream_t s = c->stream;
-  if (p->lanczos_start != nullptr) {
-    if (load_rows(c, p->lanczos_start, p->ld_start > 0 ? p->ld_start : cols, n, cols, lw.basis, tpl) != CIQ_OK)
+  const int64_t bstride = nf * tpl;
+  auto vec = [&](int k) { return lw.basis + (size_t)k * bstride; };
+  CUDA_TRY(c, cudaMemsetAsync(lw.basis, 0, (size_t)bstride * 4, s));
+  if (p->lanczos_start != nullptr) {  // this rank's rows of the start block
+    if (load_rows(c, p->lanczos_start, p->ld_start > 0 ? p->ld_start : cols, rows, cols, vec(0) + r0 * tpl, tpl) !=
+        CIQ_OK)
       return CIQ_ERR_CUDA;
   } else {
-    LAUNCH(c, launch_randn_fill(lw.basis, n, cols, tpl, 0, p->seed, s));
+    LAUNCH(c, launch_randn_fill(vec(0) + r0 * tpl, rows, cols, tpl, r0, p->seed, s));
   }
-  const int nbr = rowblocks(n, tpl);
-  LAUNCH(c, launch_colsq_partials(lw.basis, n, tpl, lw.part, s));
-  LAUNCH(c, launch_reduce_cols(lw.part, nbr, tpl, lw.bsq, 1, s));
-  LAUNCH(c, launch_scale_cols(lw.basis, n, tpl, lw.bsq, s));
+  const int nbr = rowblocks(rows, tpl);
+  LAUNCH(c, launch_colsq_partials(vec(0) + r0 * tpl, rows, tpl, lw.part, s));
+  LAUNCH(c, launch_reduce_cols(lw.part, nbr, tpl, lw.bsq, 0, s));
+  ciq_status gst = global_sum(c, lw.bsq, tpl);
+  if (gst != CIQ_OK) return gst;
+  LAUNCH(c, launch_sqrt_inplace(lw.bsq, tpl, s));
+  LAUNCH(c, launch_scale_cols(vec(0) + r0 * tpl, rows, tpl, lw.bsq, s));
+  gst = allgather_rows(c, vec(0), tpl);
+  if (gst != CIQ_OK) return gst;
   std::vector<int> len(tpl);
   for (int k = 0; k < tpl; ++k) len[k] = (k < cols) ? 0 : -1000000;
   CUDA_TRY(c, cudaMemcpyAsync(lw.len, len.data(), tpl * 4, cudaMemcpyHostToDevice, s));
@@ -514,7 +556,7 @@ ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, 
   const double bd = 1e-10;
   int done_mvms = 0;
   for (int j = 0; j < J; ++j) {
-    const float* vj = lw.basis + (size_t)j * n * tpl;
+    const float* vj = vec(j);
     if (c->pc.on) {
       // Lanczos on M = P^{-1/2} K P^{-1/2} (App. A: the rule must cover the spectrum of M)
       PrecondDev& P = c->pc;
@@ -530,19 +572,25 @@ ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, 
     ++done_mvms;
     for (int pass = 0; pass < 2; ++pass) {
       double* h = pass == 0 ? lw.h1 : lw.h2;
-      LAUNCH(c, launch_basis_dots(lw.basis, j + 1, n, tpl, lw.p, lw.part, s));
+      LAUNCH(c, launch_basis_dots(vec(0) + r0 * tpl, bstride, j + 1, rows, tpl, lw.p, lw.part, s));
       LAUNCH(c, launch_reduce_cols(lw.part, nbr, (j + 1) * tpl, h, 0, s));
-      LAUNCH(c, launch_basis_axpy(lw.basis, j + 1, n, tpl, h, lw.p, s));
+      gst = global_sum(c, h, (j + 1) * tpl);
+      if (gst != CIQ_OK) return gst;
+      LAUNCH(c, launch_basis_axpy(vec(0) + r0 * tpl, bstride, j + 1, rows, tpl, h, lw.p, s));
     }
-    LAUNCH(c, launch_colsq_partials(lw.p, n, tpl, lw.part, s));
+    LAUNCH(c, launch_colsq_partials(lw.p, rows, tpl, lw.part, s));
     LAUNCH(c, launch_reduce_cols(lw.part, nbr, tpl, lw.bsq, 0, s));
+    gst = global_sum(c, lw.bsq, tpl);
+    if (gst != CIQ_OK) return gst;
     LAUNCH(c, launch_lanczos_coeffs(lw.h1, lw.h2, lw.bsq, j, J + 1, tpl, bd, lw.alphas, lw.betas, lw.len, lw.inv, s));
     CUDA_TRY(c, cudaMemcpyAsync(len.data(), lw.len, tpl * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(c, cudaStreamSynchronize(s));
     bool any = false;
     for (int k = 0; k < cols; ++k) any = any || (len[k] == j + 1);
     if (!any || j == J - 1) break;
-    LAUNCH(c, launch_scale_cols_by(lw.p, lw.basis + (size_t)(j + 1) * n * tpl, n, tpl, lw.inv, s));
+    LAUNCH(c, launch_scale_cols_by(lw.p, vec(j + 1) + r0 * tpl, rows, tpl, lw.inv, s));
+    gst = allgather_rows(c, vec(j + 1), tpl);
+    if (gst != CIQ_OK) return gst;
   }
   std::vector<double> al((size_t)(J + 1) * tpl), be((size_t)(J + 1) * tpl);
   CUDA_TRY(c, cudaMemcpyAsync(al.data(), lw.alphas, al.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -706,6 +754,9 @@ ciq_status ciq_nccl_unique_id(void* out128) {
   return nccl_unique_id(out128) ? CIQ_OK : set_err(nullptr, CIQ_ERR_NCCL, "%s", nccl_error());
 }
 
+void* ciq_loopback_group_create(int32_t world) { return world >= 1 ? new LoopbackGroup(world) : nullptr; }
+void ciq_loopback_group_destroy(void* g) { delete static_cast<LoopbackGroup*>(g); }
+
 ciq_status ciq_tridiag_extremes(const double* alpha, const double* beta, int32_t m, double* emin, double* emax) {
   if (!alpha || (m > 1 && !beta) || m < 1 || !emin || !emax) return CIQ_ERR_INVALID_ARG;
   return ciqh::tridiag_extremes(alpha, beta, m, emin, emax) == 0 ? CIQ_OK : CIQ_ERR_INVALID_ARG;
@@ -734,7 +785,12 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     if (!(pc->sigma2 > 0)) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "preconditioner sigma2 must be > 0 (S:425)");
     if (pc->rank > 2048) return set_err(nullptr, CIQ_ERR_DIM, "preconditioner rank > 2048");
   }
-  if (comm && comm->world > 1) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "row sharding: not built yet");
+  if (comm && comm->world > 1) {
+    if (comm->rank < 0 || comm->rank >= comm->world) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "bad rank");
+    if (!comm->loopback_group && !comm->nccl_unique_id)
+      return set_err(nullptr, CIQ_ERR_INVALID_ARG, "row sharding needs an NCCL unique id or a loopback group");
+    if (pc) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "preconditioner with row sharding: not supported yet");
+  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -748,8 +804,26 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     delete c;
     return set_err(nullptr, CIQ_ERR_CUDA, "stream creation failed");
   }
-  c->row0 = 0;
-  c->row1 = op->n;
+  if (comm && comm->world > 1) {
+    c->rank = comm->rank;
+    c->world = comm->world;
+    ciq_shard_rows(op->n, c->rank, c->world, &c->row0, &c->row1);
+    c->per = (op->n + c->world - 1) / c->world;
+    c->per = (c->per + 127) / 128 * 128;
+    c->nfull = c->per * c->world;
+    c->comm = comm->loopback_group
+                  ? make_loopback_comm(static_cast<LoopbackGroup*>(comm->loopback_group), c->rank)
+                  : make_nccl_comm(c->rank, c->world, comm->nccl_unique_id);
+    if (c->comm == nullptr) {
+      delete c;
+      return set_err(nullptr, CIQ_ERR_NCCL, "communicator creation failed: %s", nccl_error());
+    }
+  } else {
+    c->row0 = 0;
+    c->row1 = op->n;
+    c->per = op->n;
+    c->nfull = op->n;
+  }
   OpDev& dv = c->dev;
   dv.kind = op->kind;
   dv.n = op->n;
@@ -757,14 +831,17 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
   dv.o2 = op->outputscale;
   ciq_status st = CIQ_OK;
   if (op->kind == CIQ_OP_DENSE) {
+    // K holds this rank's row block [row0, row1) (all rows on one GPU); the MVM kernels index it
+    // by the global row, hence the pointer shift by -row0 rows.
+    const int64_t lrows = c->row1 - c->row0;
     if (is_device_ptr(op->K)) {
-      dv.k = op->K;
+      dv.k = op->K - c->row0 * op->ldk;
       dv.ldk = op->ldk;
     } else {
-      if (cudaMalloc(&c->kcopy, (size_t)op->n * op->n * 4) != cudaSuccess) { st = CIQ_ERR_OOM; goto fail; }
-      if (cudaMemcpy2D(c->kcopy, (size_t)op->n * 4, op->K, (size_t)op->ldk * 4, (size_t)op->n * 4, (size_t)op->n,
+      if (cudaMalloc(&c->kcopy, (size_t)lrows * op->n * 4) != cudaSuccess) { st = CIQ_ERR_OOM; goto fail; }
+      if (cudaMemcpy2D(c->kcopy, (size_t)op->n * 4, op->K, (size_t)op->ldk * 4, (size_t)op->n * 4, (size_t)lrows,
                        cudaMemcpyHostToDevice) != cudaSuccess) { st = CIQ_ERR_CUDA; goto fail; }
-      dv.k = c->kcopy;
+      dv.k = c->kcopy - c->row0 * op->n;
       dv.ldk = op->n;
     }
   } else {
@@ -827,6 +904,9 @@ void ciq_free(ciq_ctx* c) {
   dfree(c->feat_a); dfree(c->feat_b); dfree(c->planes); dfree(c->inv_scale); dfree(c->psplit);
   dfree(c->apart_tc);
   free_precond(c->pc);
+  dfree(c->gsum);
+  dfree(c->tsum);
+  delete c->comm;
   delete c;
 }
 
@@ -902,10 +982,17 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   EvTimer ev;
   CUDA_TRY(c, cudaEventRecord(ev.e[0], s));
 
-  // a1: RHS -> W[1] (= nrm_1 v_1 with nrm_1 = ||b||), zero W_prev, Y, D
-  st = load_rows(c, B, ldb, rows, (int)T, ws.w[1], tp);
+  // a1: RHS -> W[1] (= nrm_1 v_1 with nrm_1 = ||b||), zero W_prev, Y, D.  With row sharding B is
+  // this rank's row block; the full first Lanczos block is all-gathered.
+  for (auto& wb : ws.w) CUDA_TRY(c, cudaMemsetAsync(wb, 0, (size_t)c->nfull * tp * 4, s));
+  st = load_rows(c, B, ldb, rows, (int)T, ws.w[1] + c->row0 * tp, tp);
   if (st != CIQ_OK) return st;
-  CUDA_TRY(c, cudaMemsetAsync(ws.w[0], 0, (size_t)n * tp * 4, s));
+  st = allgather_rows(c, ws.w[1], tp);
+  if (st != CIQ_OK) return st;
+  st = grow(c, &c->tsum, &c->tsum_cap, (size_t)2 * tp);
+  if (st != CIQ_OK) return st;
+  double* tsum_a = c->tsum;        // world > 1: globally summed alpha partials
+  double* tsum_b = c->tsum + tp;   // world > 1: globally summed beta^2 partials
   CUDA_TRY(c, cudaMemsetAsync(ws.y, 0, (size_t)rows * tp * 4, s));
   CUDA_TRY(c, cudaMemsetAsync(ws.d, 0, (size_t)2 * nq * rows * tp * 4, s));
   Ctrl hctrl{};
@@ -917,8 +1004,10 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   CUDA_TRY(c, cudaMemcpyAsync(sc.ctrl, &hctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, s));
   const int nbs = rowblocks(rows, tp);
   PrecondDev& P = c->pc;
-  LAUNCH(c, launch_colsq_partials(ws.w[1], rows, tp, ws.bpart, s));
+  LAUNCH(c, launch_colsq_partials(ws.w[1] + c->row0 * tp, rows, tp, ws.bpart, s));
   LAUNCH(c, launch_reduce_cols(ws.bpart, nbs, tp, ws.colsq, 0, s));
+  st = global_sum(c, ws.colsq, tp);
+  if (st != CIQ_OK) return st;
   LAUNCH(c, launch_init_state(sc, nq, tp, ws.colsq, s));
   if (P.on) {  // work buffers of precond_power / apply_m at this tp (before any graph capture)
     st = grow(c, &P.part, &P.part_cap, (size_t)utv_splits(rows) * P.r2 * tp);
@@ -989,17 +1078,34 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     const float* pin = (nsplit > 1) ? c->psplit : ws.p;
     loop_nsplit = nsplit;
     loop_impl = c->mvm_kind_used;
-    LAUNCH(c, launch_alpha(sc, apart, nbm, tp, s));
+    if (c->world == 1) {
+      LAUNCH(c, launch_alpha(sc, apart, nbm, tp, s));
+    } else {
+      LAUNCH(c, launch_reduce_cols(apart, nbm, tp, tsum_a, 0, s));
+      st2 = global_sum(c, tsum_a, tp);
+      if (st2 != CIQ_OK) return st2;
+      LAUNCH(c, launch_alpha_from_sum(sc, tsum_a, tp, s));
+    }
     float* d1 = dslot[j & 1];
     float* d2 = dslot[(j + 1) & 1];
     begin_timed(c, j, 1);
     LAUNCH(c, launch_lanczos_update(sc, pin, nsplit, (size_t)rows * tp, wcur + c->row0 * tp, wprev + c->row0 * tp,
                                     wnew + c->row0 * tp, &d1, &d2, ws.y, nq, rows, tp, ws.bpart, 0, s));
     end_timed(c);
-    LAUNCH(c, launch_givens(sc, ws.bpart, nbs, nq, tp, s));
+    if (c->world == 1) {
+      LAUNCH(c, launch_givens(sc, ws.bpart, nbs, nq, tp, s));
+    } else {
+      LAUNCH(c, launch_reduce_cols(ws.bpart, nbs, tp, tsum_b, 0, s));
+      st2 = global_sum(c, tsum_b, tp);
+      if (st2 != CIQ_OK) return st2;
+      LAUNCH(c, launch_givens(sc, tsum_b, 1, nq, tp, s));
+      st2 = allgather_rows(c, wnew, tp);   // next Lanczos block to every rank
+      if (st2 != CIQ_OK) return st2;
+    }
     return CIQ_OK;
   };
-  const bool use_graph = !c->profiling && getenv("CIQ_NO_GRAPH") == nullptr;
+  const bool use_graph = !c->profiling && getenv("CIQ_NO_GRAPH") == nullptr &&
+                         (c->world == 1 || c->comm->capturable());
   int block = p.poll_every;
   if (use_graph) block = std::max(6, (p.poll_every + 5) / 6 * 6);
   if (use_graph) {
@@ -1092,10 +1198,17 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   }
   int final_mvm = 0;
   if (p.mode == CIQ_MODE_SQRT) {
-    // K . Y  (Y is the full vector on one GPU)
-    LAUNCH(c, launch_colsq_partials(yout, rows, tp, ws.bpart, s));
-    LAUNCH(c, launch_reduce_cols(ws.bpart, nbs, tp, ws.colsq, 1, s));
-    st = run_mvm(c, yout, tp, ws.p, nullptr, nullptr, p.mvm_impl, ws.colsq);
+    // K . Y: Y is this rank's row block -> all-gather it into a free full-height W buffer
+    float* yfull = yout;
+    if (c->world > 1) {
+      yfull = ws.w[(J + 1) % 3];
+      CUDA_TRY(c, cudaMemcpyAsync(yfull + c->row0 * tp, yout, (size_t)rows * tp * 4, cudaMemcpyDeviceToDevice, s));
+      st = allgather_rows(c, yfull, tp);
+      if (st != CIQ_OK) return st;
+    }
+    LAUNCH(c, launch_colsq_partials(yfull, c->op.n, tp, ws.bpart, s));
+    LAUNCH(c, launch_reduce_cols(ws.bpart, rowblocks(c->op.n, tp), tp, ws.colsq, 1, s));
+    st = run_mvm(c, yfull, tp, ws.p, nullptr, nullptr, p.mvm_impl, ws.colsq);
     if (st != CIQ_OK) return st;
     final_mvm = 1;
     st = store_rows(c, ws.p, tp, rows, (int)T, out, ldo);

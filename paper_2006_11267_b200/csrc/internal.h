@@ -86,12 +86,15 @@ cudaError_t launch_alpha(const Scal& sc, const double* apart, int nblk, int tp, 
 cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, size_t split_stride, const float* wcur, const float* wprev,
                                   float* wnew, float* const* d1, float* const* d2, float* y, int nq,
                                   int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s);
+cudaError_t launch_alpha_from_sum(const Scal& sc, const double* sums, int tp, cudaStream_t s);
+cudaError_t launch_sum_ranks(const double* g, int world, int m, double* out, cudaStream_t s);
 cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s);
 // Lambda-estimation Lanczos (full re-orthogonalisation)
-cudaError_t launch_basis_dots(const float* basis, int nb, int64_t rows, int tp, const float* p, double* part,
-                              cudaStream_t s);
-cudaError_t launch_basis_axpy(const float* basis, int nb, int64_t rows, int tp, const double* h, float* p,
-                              cudaStream_t s);
+cudaError_t launch_basis_dots(const float* basis, int64_t bstride, int nb, int64_t rows, int tp, const float* p,
+                              double* part, cudaStream_t s);
+cudaError_t launch_basis_axpy(const float* basis, int64_t bstride, int nb, int64_t rows, int tp, const double* h,
+                              float* p, cudaStream_t s);
+cudaError_t launch_sqrt_inplace(double* v, int m, cudaStream_t s);
 cudaError_t launch_lanczos_coeffs(const double* h1, const double* h2, const double* bsq, int j, int nb_total,
                                   int tp, double bd_tol, double* alphas, double* betas, int* len,
                                   double* inv_beta, cudaStream_t s);

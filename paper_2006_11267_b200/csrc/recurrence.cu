@@ -128,6 +128,11 @@ __global__ void randn_kernel(float* __restrict__ dst, int64_t rows, int cols, in
   dst[e] = (float)(sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2));
 }
 
+__global__ void sqrt_inplace_kernel(double* __restrict__ v, int m) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < m) v[k] = sqrt(v[k]);
+}
+
 __global__ void scale_cols_kernel(float* __restrict__ v, int64_t rows, int tp, const double* __restrict__ nrm) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * tp) return;
@@ -181,6 +186,24 @@ __global__ void alpha_kernel(Scal sc, const double* __restrict__ apart, int nblk
       sc.alpha[c] = sc.frozen[c] ? 0.0 : s / (nr * nr);
     }
   }
+}
+
+// Row-sharded variant: alpha_j from the already globally summed W_cur.P (one value per column).
+__global__ void alpha_from_sum_kernel(Scal sc, const double* __restrict__ sums, int tp) {
+  if (sc.ctrl->done) return;
+  for (int c = threadIdx.x; c < tp; c += blockDim.x) {
+    const double nr = sc.nrm_cur[c];
+    sc.alpha[c] = sc.frozen[c] ? 0.0 : sums[c] / (nr * nr);
+  }
+}
+
+// out[k] = sum_r g[r][k] in rank order (cross-rank fixed-order sum after an allgather).
+__global__ void sum_ranks_kernel(const double* __restrict__ g, int world, int m, double* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  double s = 0.0;
+  for (int r = 0; r < world; ++r) s += g[(size_t)r * m + k];
+  out[k] = s;
 }
 
 // The streaming pass (see file header).  final_only: apply the pending update of the last step
@@ -333,10 +356,10 @@ __global__ void __launch_bounds__(512) givens_kernel(Scal sc, const double* __re
 
 // ---- lambda-estimation Lanczos with full re-orthogonalisation ----
 
-// part[b][k][c] = sum_{i in block b} basis_k[i][c] p[i][c],  k < nb.  basis: [nb][rows][tp].
-__global__ void __launch_bounds__(kThreads) basis_dots_kernel(const float* __restrict__ basis, int nb,
-                                                              int64_t rows, int tp, const float* __restrict__ p,
-                                                              double* __restrict__ part) {
+// part[b][k][c] = sum_{i in block b} basis_k[i][c] p[i][c],  k < nb.  basis_k = basis + k bstride.
+__global__ void __launch_bounds__(kThreads) basis_dots_kernel(const float* __restrict__ basis, int64_t bstride,
+                                                              int nb, int64_t rows, int tp,
+                                                              const float* __restrict__ p, double* __restrict__ part) {
   // tp is small here (lanczos_cols <= 64): one thread per (row-lane, column)
   __shared__ double sh[kThreads];
   const int tid = threadIdx.x;
@@ -347,7 +370,7 @@ __global__ void __launch_bounds__(kThreads) basis_dots_kernel(const float* __res
     double acc = 0.0;
     if (rl < rpp)
       for (int64_t i = r0 + rl; i < r1; i += rpp)
-        acc += (double)basis[((int64_t)k * rows + i) * tp + c] * p[i * tp + c];
+        acc += (double)basis[(int64_t)k * bstride + i * tp + c] * p[i * tp + c];
     sh[tid] = acc;
     __syncthreads();
     if (tid < tp) {
@@ -359,13 +382,13 @@ __global__ void __launch_bounds__(kThreads) basis_dots_kernel(const float* __res
   }
 }
 
-__global__ void basis_axpy_kernel(const float* __restrict__ basis, int nb, int64_t rows, int tp,
+__global__ void basis_axpy_kernel(const float* __restrict__ basis, int64_t bstride, int nb, int64_t rows, int tp,
                                   const double* __restrict__ h, float* __restrict__ p) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * tp) return;
   int c = (int)(e % tp);
   double s = 0.0;
-  for (int k = 0; k < nb; ++k) s += h[k * tp + c] * (double)basis[(int64_t)k * rows * tp + e];
+  for (int k = 0; k < nb; ++k) s += h[k * tp + c] * (double)basis[(int64_t)k * bstride + e];
   p[e] = (float)(p[e] - s);
 }
 
@@ -446,6 +469,10 @@ cudaError_t launch_reduce_cols(const double* part, int nblk, int m, double* out,
   reduce_cols_kernel<<<nb_elem((int64_t)m * 32, 256), 256, 0, s>>>(part, nblk, m, out, op_sqrt);
   return cudaGetLastError();
 }
+cudaError_t launch_sqrt_inplace(double* v, int m, cudaStream_t s) {
+  sqrt_inplace_kernel<<<nb_elem(m, 256), 256, 0, s>>>(v, m);
+  return cudaGetLastError();
+}
 cudaError_t launch_scale_cols(float* v, int64_t rows, int tp, const double* nrm, cudaStream_t s) {
   scale_cols_kernel<<<nb_elem(rows * tp, 256), 256, 0, s>>>(v, rows, tp, nrm);
   return cudaGetLastError();
@@ -471,20 +498,28 @@ cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, si
                                                                     qstride, y, nq, rows, tp, bpart, final_only);
   return cudaGetLastError();
 }
+cudaError_t launch_alpha_from_sum(const Scal& sc, const double* sums, int tp, cudaStream_t s) {
+  alpha_from_sum_kernel<<<1, 256, 0, s>>>(sc, sums, tp);
+  return cudaGetLastError();
+}
+cudaError_t launch_sum_ranks(const double* g, int world, int m, double* out, cudaStream_t s) {
+  sum_ranks_kernel<<<nb_elem(m, 256), 256, 0, s>>>(g, world, m, out);
+  return cudaGetLastError();
+}
 cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s) {
   givens_kernel<<<1, 512, 0, s>>>(sc, bpart, nblk, nq, tp);
   return cudaGetLastError();
 }
-cudaError_t launch_basis_dots(const float* basis, int nb, int64_t rows, int tp, const float* p, double* part,
-                              cudaStream_t s) {
+cudaError_t launch_basis_dots(const float* basis, int64_t bstride, int nb, int64_t rows, int tp, const float* p,
+                              double* part, cudaStream_t s) {
   if (tp > kThreads) return cudaErrorInvalidValue;
-  basis_dots_kernel<<<(unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), kThreads, 0, s>>>(basis, nb, rows, tp,
-                                                                                             p, part);
+  basis_dots_kernel<<<(unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), kThreads, 0, s>>>(basis, bstride, nb,
+                                                                                             rows, tp, p, part);
   return cudaGetLastError();
 }
-cudaError_t launch_basis_axpy(const float* basis, int nb, int64_t rows, int tp, const double* h, float* p,
-                              cudaStream_t s) {
-  basis_axpy_kernel<<<nb_elem(rows * tp, 256), 256, 0, s>>>(basis, nb, rows, tp, h, p);
+cudaError_t launch_basis_axpy(const float* basis, int64_t bstride, int nb, int64_t rows, int tp, const double* h,
+                              float* p, cudaStream_t s) {
+  basis_axpy_kernel<<<nb_elem(rows * tp, 256), 256, 0, s>>>(basis, bstride, nb, rows, tp, h, p);
   return cudaGetLastError();
 }
 cudaError_t launch_lanczos_coeffs(const double* h1, const double* h2, const double* bsq, int j, int /*nb_total*/,
