@@ -9,8 +9,10 @@ Q = 8, K^{1/2}B; Thompson-sampling shape).  `value` is whole-job RHS/s with inpu
 HBM; `e2e` is the same metric through the C ABI with pinned HOST buffers (H2D of B and D2H of the
 result inside the timed region).  L2 is flushed (256 MiB write) between timed steps.
 
-N > 1 (torchrun): each rank runs its own replica of the workload (weak scaling, no data-path
-collective) until the row-sharded NCCL path lands -- see DESIGN.md §7.
+N > 1 (torchrun): K is row-sharded across the ranks: each GPU owns a 128-aligned row
+block of K, B and the output; per iteration NCCL all-gathers the next Lanczos block and the
+alpha / beta^2 partial sums (strong scaling: the job is the same 64-RHS solve at every N).
+`--parallelism replicas` instead runs one independent replica per GPU (weak scaling).
 `--impl reference`: the float64 CPU oracle (the reference arm for this tier) timed on the host
 cores on a bounded row sample of the same workload, extrapolated to the same MVM count.
 """
@@ -164,6 +166,13 @@ def run_reference(args, cfg):
 # our arm
 # ------------------------------------------------------------------------------------------------
 
+def broadcast_uid(dist, rank: int, make_uid) -> bytes:
+    """NCCL unique id created on rank 0 and broadcast over the torch process group."""
+    obj = [make_uid() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
 def run_ours(args, cfg):
     import numpy as np
     import torch
@@ -176,13 +185,20 @@ def run_ours(args, cfg):
     import paper_2006_11267_b200 as pb
     import workloads
 
+    sharded = world > 1 and args.parallelism == "rows"
     inp = workloads.config_inputs(cfg)
+    r0, r1 = pb.ciq_shard_rows(cfg.n, rank, world) if sharded else (0, cfg.n)
     x = torch.from_numpy(inp["X"]).cuda()
-    b = torch.from_numpy(inp["B"]).cuda()
-    s = torch.from_numpy(inp["S"]).cuda()
+    b = torch.from_numpy(np.ascontiguousarray(inp["B"][r0:r1])).cuda()
+    s = torch.from_numpy(np.ascontiguousarray(inp["S"][r0:r1])).cuda()
     out = torch.empty_like(b)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
-    g = pb.CIQ(cfg.kind, X=x, lengthscale=cfg.lengthscale, outputscale=cfg.outputscale, diag=cfg.sigma2)
+    comm = None
+    if sharded:
+        uid = broadcast_uid(torch.distributed, rank, pb.ciq_nccl_unique_id)
+        comm = (rank, world, uid)
+    g = pb.CIQ(cfg.kind, n=cfg.n, X=x, lengthscale=cfg.lengthscale, outputscale=cfg.outputscale, diag=cfg.sigma2,
+               comm=comm)
     kw = dict(q=cfg.q, max_iters=cfg.max_iters, tol=cfg.tol, mode=cfg.mode, lanczos_start=s, mvm_impl=args.mvm)
     stream = torch.cuda.current_stream()
 
@@ -212,11 +228,11 @@ def run_ours(args, cfg):
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * cfg.t / (ms / 1000.0)
+    value = (1 if sharded else world) * cfg.t / (ms / 1000.0)
     launches = int(sum(i["kernel_launches"] for i in infos))
 
     # ---- e2e: pinned host buffers through the C ABI ----
-    bh = torch.from_numpy(inp["B"]).pin_memory()
+    bh = torch.from_numpy(np.ascontiguousarray(inp["B"][r0:r1])).pin_memory()
     oh = torch.empty_like(bh).pin_memory()
     e2e_ms = []
     for _ in range(max(1, args.steps)):
@@ -238,12 +254,13 @@ def run_ours(args, cfg):
     pinfo = g.apply(b, out, profile=True, **kw)
     peaks = load_peaks()
     n, tcols = cfg.n, cfg.t
+    rows_local = r1 - r0
     mvm_ms = pinfo["ms_mvm"] / max(1, pinfo["mvm_timed"])
     upd_ms = pinfo["ms_update"] / max(1, pinfo["update_timed"])
     step_share = (pinfo["ms_mvm"] + pinfo["ms_update"]) / max(1e-9, pinfo["ms_total"])
     impl_used = pinfo["mvm_impl_used"]
     # algorithmic work per MVM launch: N^2 kernel evaluations, 2 N^2 T useful flops
-    flops = 2.0 * n * n * tcols
+    flops = 2.0 * rows_local * n * tcols        # this rank's rows of K . V
     if impl_used == "simt":
         sm_count = torch.cuda.get_device_properties(local).multi_processor_count
         fp32_peak = sm_count * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12  # TFLOP/s
@@ -258,32 +275,35 @@ def run_ours(args, cfg):
                 "note": "achieved counts only the algorithmic 2*N^2*T flops; the kernel issues ~3.5x that"}
         sm_count = torch.cuda.get_device_properties(local).multi_processor_count
         sfu_peak = sm_count * 16 * peaks.get("sm_max_mhz", 1965.0) * 1e6  # MUFU.EX2 per second
-        roof["sfu"] = {"achieved_evals_per_s": n * n / (mvm_ms * 1e-3), "peak_evals_per_s": sfu_peak,
-                       "frac": n * n / (mvm_ms * 1e-3) / sfu_peak,
+        roof["sfu"] = {"achieved_evals_per_s": rows_local * n / (mvm_ms * 1e-3), "peak_evals_per_s": sfu_peak,
+                       "frac": rows_local * n / (mvm_ms * 1e-3) / sfu_peak,
                        "peak_source": f"{sm_count} SMs x 16 MUFU.EX2/clk x sm_max_mhz (1 ex2 per kernel entry)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = None
     roof["ms_per_launch"] = mvm_ms
     roof["share_of_step"] = pinfo["ms_mvm"] / max(1e-9, pinfo["ms_total"])
     q = cfg.q
-    rec_bytes = (3 * q + 7) * n * tcols * 4.0
+    rec_bytes = (3 * q + 7) * rows_local * tcols * 4.0
     recurrence = {"bound": "hbm", "achieved": rec_bytes / (upd_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
                   "unit": "GB/s", "kernel": "lanczos_update_kernel", "ms_per_launch": upd_ms,
                   "algorithmic_bytes": rec_bytes}
     recurrence["frac"] = recurrence["achieved"] / recurrence["peak"]
 
     line = {"metric": METRIC, "value": value, "unit": "RHS/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload_desc(cfg), "global_batch": world * tcols, "J": infos[-1]["iters"],
+            "config": {"workload": workload_desc(cfg), "global_batch": (1 if sharded else world) * tcols,
+                       "J": infos[-1]["iters"],
                        "mvms_per_step": infos[-1]["mvms"], "mvm_impl": impl_used,
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": (f"rows{world}" if sharded else f"replicas{world}") if world > 1 else "single",
                        "l2": "flushed between steps (256 MiB write)",
                        "converged": infos[-1]["converged"], "max_rel_residual": infos[-1]["max_rel_residual"],
                        "lambda": [infos[-1]["lambda_min"], infos[-1]["lambda_max"]]},
             "roofline": roof, "roofline_recurrence": recurrence,
-            "e2e": {"value": world * tcols / (e2e / 1000.0), "unit": "RHS/s", "h2d_bytes_per_step": n * tcols * 4,
-                    "d2h_bytes_per_step": n * tcols * 4, "ms_per_step": e2e},
+            "e2e": {"value": (1 if sharded else world) * tcols / (e2e / 1000.0), "unit": "RHS/s",
+                    "h2d_bytes_per_step": rows_local * tcols * 4, "d2h_bytes_per_step": rows_local * tcols * 4,
+                    "ms_per_step": e2e},
             "gpu_launches": launches, "clocks": clocks, "step_share_profiled": step_share}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = oracle_sample_rate(cfg, inp, infos[-1]["mvms"], rows=args.ref_rows)
@@ -306,6 +326,7 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=4096)
     ap.add_argument("--ref-mvms", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parallelism", default="rows", choices=["rows", "replicas"])
     args = ap.parse_args()
     import workloads
     cfg = workloads.CONFIGS[args.config]
