@@ -324,7 +324,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mvm", default="auto", choices=["auto", "simt", "tc"])
     ap.add_argument("--ref-rows", type=int, default=4096)
-    ap.add_argument("--ref-mvms", type=int, default=200)
+    ap.add_argument("--ref-mvms", type=int, default=176)  # C3: 10 (lambda) + J=165 + 1 (final K.Y)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--parallelism", default="rows", choices=["rows", "replicas"])
     args = ap.parse_args()
