@@ -211,8 +211,8 @@ ciq_status ensure_workspace(ciq_ctx* c, int tp, int nq) {
   CUDA_TRY(c, dalloc(&ws.bpart, (size_t)rowblocks(std::max(rows, c->nfull), tp) * tp));
   CUDA_TRY(c, dalloc(&ws.colsq, (size_t)tp));
   // scalar block
-  size_t nd = (size_t)tp * 5 + (size_t)nq * tp * 5 + 2 * (size_t)nq;
-  size_t bytes = nd * 8 + (size_t)tp * 4 + (size_t)nq * tp * 4 * 4 + sizeof(Ctrl) + 256;
+  size_t nd = (size_t)tp * 6 + (size_t)nq * tp * 5 + 2 * (size_t)nq;
+  size_t bytes = nd * 8 + (size_t)tp * 8 + (size_t)nq * tp * 4 * 4 + sizeof(Ctrl) + 256;
   CUDA_TRY(c, dalloc(&ws.scal_mem, bytes));
   char* m = ws.scal_mem;
   auto takeD = [&](size_t k) { double* r = reinterpret_cast<double*>(m); m += k * 8; return r; };
@@ -220,11 +220,12 @@ ciq_status ensure_workspace(ciq_ctx* c, int tp, int nq) {
   sc.beta1 = takeD(tp); sc.nrm_prev = takeD(tp); sc.nrm_cur = takeD(tp); sc.tb_cur = takeD(tp); sc.alpha = takeD(tp);
   sc.c1 = takeD((size_t)nq * tp); sc.s1 = takeD((size_t)nq * tp); sc.c2 = takeD((size_t)nq * tp);
   sc.s2 = takeD((size_t)nq * tp); sc.phibar = takeD((size_t)nq * tp);
-  sc.shifts = takeD(nq); sc.weights = takeD(nq);
+  sc.shifts = takeD(nq); sc.weights = takeD(nq); sc.col_rel = takeD(tp);
   auto takeF = [&](size_t k) { float* r = reinterpret_cast<float*>(m); m += k * 4; return r; };
   sc.ca = takeF((size_t)nq * tp); sc.cb = takeF((size_t)nq * tp); sc.ce = takeF((size_t)nq * tp);
   sc.cf = takeF((size_t)nq * tp);
   sc.frozen = reinterpret_cast<int*>(m); m += (size_t)tp * 4;
+  sc.col_state = reinterpret_cast<int*>(m); m += (size_t)tp * 4;
   m = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(m) + 15) & ~uintptr_t(15));
   sc.ctrl = reinterpret_cast<Ctrl*>(m);
   return CIQ_OK;

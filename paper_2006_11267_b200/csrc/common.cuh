@@ -35,7 +35,7 @@ struct Ctrl {
   int max_iters;
   int nq;
   int tp;          // padded number of columns
-  int pad_;
+  unsigned int arrive;  // column-CTAs of the current givens launch that have finished (last one decides)
   double tol;
   double bd_tol;
   double max_relres;

@@ -33,6 +33,8 @@ struct Scal {
   float* ca; float* cb; float* ce; float* cf;                       // [Q][tp] pending-update coefs
   double* shifts;     // [Q]
   double* weights;    // [Q]
+  double* col_rel;    // [tp]   per-column max relative residual of the last Givens step
+  int* col_state;     // [tp]   0 frozen before, 1 active, 2 broke in the last step
   Ctrl* ctrl;
 };
 

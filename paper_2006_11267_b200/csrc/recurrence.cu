@@ -39,6 +39,18 @@ struct Geo {
   }
 };
 
+// Fixed-order sum over a 256-thread CTA (warp shuffles, then warp 0 over the 8 warp sums).
+CIQ_DEVICE double block_sum256(double v) {
+  __shared__ double ws[8];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = (threadIdx.x < 8) ? ws[threadIdx.x] : 0.0;
+  if (threadIdx.x < 32) t = warp_sum(t);
+  __syncthreads();
+  return t;  // valid in thread 0
+}
+
 // Fixed-order CTA reduction of per-thread column-quad partials into part[blockIdx.x][c].
 CIQ_DEVICE void cta_col_reduce(const Geo& g, int tp, const double (&acc)[4], double* part) {
   __shared__ double sums[kChunk];   // rpp * tpr * 4 <= 1024
@@ -170,21 +182,21 @@ __global__ void init_state_kernel(Scal sc, int nq, int tp, const double* __restr
     sc.ctrl->pending = 0;
     sc.ctrl->breakdown = 0;
     sc.ctrl->max_relres = 0.0;
+    sc.ctrl->arrive = 0;
   }
 }
 
 // alpha_j = (sum_b W_cur.P partials) / nrm_j^2.  One warp per column, fixed order.
-__global__ void alpha_kernel(Scal sc, const double* __restrict__ apart, int nblk, int tp) {
+// One CTA per column c (256 threads): fixed-order reduction of the nblk partials.
+__global__ void __launch_bounds__(256) alpha_kernel(Scal sc, const double* __restrict__ apart, int nblk, int tp) {
   if (sc.ctrl->done) return;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
-  for (int c = warp; c < tp; c += nw) {
-    double s = 0.0;
-    for (int b = lane; b < nblk; b += 32) s += apart[(int64_t)b * tp + c];
-    s = warp_sum(s);
-    if (lane == 0) {
-      double nr = sc.nrm_cur[c];
-      sc.alpha[c] = sc.frozen[c] ? 0.0 : s / (nr * nr);
-    }
+  const int c = blockIdx.x;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += 256) s += apart[(int64_t)b * tp + c];
+  s = block_sum256(s);
+  if (threadIdx.x == 0) {
+    const double nr = sc.nrm_cur[c];
+    sc.alpha[c] = sc.frozen[c] ? 0.0 : s / (nr * nr);
   }
 }
 
@@ -208,7 +220,7 @@ __global__ void sum_ranks_kernel(const double* __restrict__ g, int world, int m,
 
 // The streaming pass (see file header).  final_only: apply the pending update of the last step
 // only (wprev = the buffer holding nrm_J v_J).
-__global__ void __launch_bounds__(kThreads) lanczos_update_kernel(
+__global__ void __launch_bounds__(kThreads, 3) lanczos_update_kernel(
     Scal sc, const float* __restrict__ p, int nsplit, size_t split_stride, const float* __restrict__ wcur, const float* __restrict__ wprev,
     float* __restrict__ wnew, const float* __restrict__ d1base, float* __restrict__ d2base, int64_t qstride,
     float* __restrict__ y, int nq, int64_t rows, int tp, double* __restrict__ bpart, int final_only) {
@@ -280,77 +292,85 @@ __global__ void __launch_bounds__(kThreads) lanczos_update_kernel(
 }
 
 // beta_{j+1}, Givens rotations of step j for every (shift, column), coefficients of step j's
-// descent update, stopping rule.  One CTA; warp per column, lanes over shifts.
-__global__ void __launch_bounds__(512) givens_kernel(Scal sc, const double* __restrict__ bpart, int nblk, int nq, int tp) {
+// descent update, stopping rule.  One CTA per column (threads over shifts); per-column results
+// go to col_rel / col_state and the last CTA to finish (atomic arrival count) takes the global
+// decision -- max and counts are order-independent, so the outcome is deterministic.
+__global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __restrict__ bpart, int nblk, int nq,
+                                                     int tp, double* __restrict__ col_rel, int* __restrict__ col_state) {
   Ctrl* ctrl = sc.ctrl;
   if (ctrl->done) return;
-  __shared__ double s_rel[32];
-  __shared__ int s_act[32], s_brk[32];
-  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
-  double my_rel = 0.0;
-  int my_act = 0, my_brk = 0;
-  for (int c = warp; c < tp; c += nw) {
-    double s = 0.0;
-    for (int b = lane; b < nblk; b += 32) s += bpart[(int64_t)b * tp + c];
-    s = warp_sum(s);
-    const double tbn = sqrt(s);                  // beta_{j+1}
-    const bool frozen = sc.frozen[c] != 0;
-    const double a_j = sc.alpha[c], tb = sc.tb_cur[c], nrm = sc.nrm_cur[c], b1 = sc.beta1[c];
-    double rel = 0.0;
-    for (int q = lane; q < nq; q += 32) {
-      const int k = q * tp + c;
-      if (frozen) {
-        sc.ca[k] = 0.f; sc.cb[k] = 0.f; sc.ce[k] = 0.f; sc.cf[k] = 0.f;
-        continue;
-      }
-      const double a = a_j + sc.shifts[q];
-      const double c1 = sc.c1[k], s1 = sc.s1[k], c2 = sc.c2[k], s2 = sc.s2[k];
-      const double eps = s2 * tb;
-      const double dp = c2 * tb;
-      const double delta = c1 * dp + s1 * a;
-      const double gbar = -s1 * dp + c1 * a;
-      const double gamma = hypot(gbar, tbn);
-      const double cs = gbar / gamma, sn = tbn / gamma;
-      const double phib = sc.phibar[k];
-      const double phi = cs * phib;
-      const double phib_new = -sn * phib;
-      sc.phibar[k] = phib_new;
-      sc.ca[k] = (float)(1.0 / (gamma * nrm));   // d = (v_j - delta d1 - eps d2)/gamma, v_j = W/nrm
-      sc.cb[k] = (float)(-delta / gamma);
-      sc.ce[k] = (float)(-eps / gamma);
-      sc.cf[k] = (float)(sc.weights[q] * phi);   // Y += w_q phi d
-      sc.c2[k] = c1; sc.s2[k] = s1; sc.c1[k] = cs; sc.s1[k] = sn;
-      rel = fmax(rel, fabs(phib_new) / b1);
+  const int c = blockIdx.x;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += 256) s += bpart[(int64_t)b * tp + c];
+  s = block_sum256(s);
+  __shared__ double s_tbn;
+  __shared__ double s_rel[8];
+  if (threadIdx.x == 0) s_tbn = sqrt(s);
+  __syncthreads();
+  const double tbn = s_tbn;                      // beta_{j+1}
+  const bool frozen = sc.frozen[c] != 0;
+  const double a_j = sc.alpha[c], tb = sc.tb_cur[c], nrm = sc.nrm_cur[c], b1 = sc.beta1[c];
+  double rel = 0.0;
+  for (int q = threadIdx.x; q < nq; q += 256) {
+    const int k = q * tp + c;
+    if (frozen) {
+      sc.ca[k] = 0.f; sc.cb[k] = 0.f; sc.ce[k] = 0.f; sc.cf[k] = 0.f;
+      continue;
     }
-    rel = warp_max(rel);
-    if (lane == 0) {
-      if (!frozen) {
-        const bool broke = tbn <= ctrl->bd_tol * (fabs(a_j) + tb);
-        if (broke) {
-          sc.frozen[c] = 1;
-          ++my_brk;
-        } else {
-          my_rel = fmax(my_rel, rel);
-          ++my_act;
-        }
-        sc.nrm_prev[c] = nrm;
-        sc.nrm_cur[c] = broke ? 1.0 : tbn;
-        sc.tb_cur[c] = tbn;
-      }
-    }
+    const double a = a_j + sc.shifts[q];
+    const double c1 = sc.c1[k], s1 = sc.s1[k], c2 = sc.c2[k], s2 = sc.s2[k];
+    const double eps = s2 * tb;
+    const double dp = c2 * tb;
+    const double delta = c1 * dp + s1 * a;
+    const double gbar = -s1 * dp + c1 * a;
+    const double gamma = hypot(gbar, tbn);
+    const double cs = gbar / gamma, sn = tbn / gamma;
+    const double phib = sc.phibar[k];
+    const double phi = cs * phib;
+    const double phib_new = -sn * phib;
+    sc.phibar[k] = phib_new;
+    sc.ca[k] = (float)(1.0 / (gamma * nrm));   // d = (v_j - delta d1 - eps d2)/gamma, v_j = W/nrm
+    sc.cb[k] = (float)(-delta / gamma);
+    sc.ce[k] = (float)(-eps / gamma);
+    sc.cf[k] = (float)(sc.weights[q] * phi);   // Y += w_q phi d
+    sc.c2[k] = c1; sc.s2[k] = s1; sc.c1[k] = cs; sc.s1[k] = sn;
+    rel = fmax(rel, fabs(phib_new) / b1);
   }
-  if (lane == 0) { s_rel[warp] = my_rel; s_act[warp] = my_act; s_brk[warp] = my_brk; }
+  rel = warp_max(rel);
+  if ((threadIdx.x & 31) == 0) s_rel[threadIdx.x >> 5] = rel;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double rel = 0.0;
-    int act = 0, brk = 0;
-    for (int w = 0; w < nw; ++w) { rel = fmax(rel, s_rel[w]); act += s_act[w]; brk += s_brk[w]; }
-    const int j = ctrl->iters + 1;
-    ctrl->iters = j;
-    ctrl->pending = 1;
-    ctrl->breakdown += brk;
-    ctrl->max_relres = rel;
-    if (act == 0 || (ctrl->tol > 0 && rel <= ctrl->tol) || j >= ctrl->max_iters) ctrl->done = 1;
+    for (int w = 1; w < 8; ++w) rel = fmax(rel, s_rel[w]);
+    int state = 0;  // 0 frozen before, 1 active, 2 broke now
+    if (!frozen) {
+      const bool broke = tbn <= ctrl->bd_tol * (fabs(a_j) + tb);
+      if (broke) sc.frozen[c] = 1;
+      state = broke ? 2 : 1;
+      sc.nrm_prev[c] = nrm;
+      sc.nrm_cur[c] = broke ? 1.0 : tbn;
+      sc.tb_cur[c] = tbn;
+    }
+    col_rel[c] = (state == 1) ? rel : 0.0;
+    col_state[c] = state;
+    __threadfence();
+    const unsigned int prev = atomicAdd(&ctrl->arrive, 1u);
+    if (prev == (unsigned)tp - 1) {   // last column CTA: global decision
+      __threadfence();
+      double mx = 0.0;
+      int act = 0, brk = 0;
+      for (int cc = 0; cc < tp; ++cc) {
+        const int st = ((volatile int*)col_state)[cc];
+        if (st == 1) { ++act; mx = fmax(mx, ((volatile double*)col_rel)[cc]); }
+        if (st == 2) ++brk;
+      }
+      const int j = ctrl->iters + 1;
+      ctrl->iters = j;
+      ctrl->pending = 1;
+      ctrl->breakdown += brk;
+      ctrl->max_relres = mx;
+      ctrl->arrive = 0;
+      if (act == 0 || (ctrl->tol > 0 && mx <= ctrl->tol) || j >= ctrl->max_iters) ctrl->done = 1;
+    }
   }
 }
 
@@ -487,7 +507,7 @@ cudaError_t launch_init_state(const Scal& sc, int nq, int tp, const double* cols
   return cudaGetLastError();
 }
 cudaError_t launch_alpha(const Scal& sc, const double* apart, int nblk, int tp, cudaStream_t s) {
-  alpha_kernel<<<1, 1024, 0, s>>>(sc, apart, nblk, tp);
+  alpha_kernel<<<tp, 256, 0, s>>>(sc, apart, nblk, tp);
   return cudaGetLastError();
 }
 cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, size_t split_stride, const float* wcur, const float* wprev,
@@ -507,7 +527,7 @@ cudaError_t launch_sum_ranks(const double* g, int world, int m, double* out, cud
   return cudaGetLastError();
 }
 cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s) {
-  givens_kernel<<<1, 512, 0, s>>>(sc, bpart, nblk, nq, tp);
+  givens_kernel<<<tp, 256, 0, s>>>(sc, bpart, nblk, nq, tp, sc.col_rel, sc.col_state);
   return cudaGetLastError();
 }
 cudaError_t launch_basis_dots(const float* basis, int64_t bstride, int nb, int64_t rows, int tp, const float* p,
