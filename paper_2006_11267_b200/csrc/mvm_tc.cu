@@ -78,9 +78,13 @@ __device__ __forceinline__ float kernel_from_s(float s) {
 }
 
 // 32 S values (one chunk of a row) -> 16 packed k_hi words + 16 packed k_lo words.
-template <int KIND, bool MASK>
-__device__ __forceinline__ void exp_split_chunk(const uint32_t (&sv)[32], uint32_t (&hi)[16], uint32_t (&lo)[16],
-                                                int jvalid) {
+// Split by mantissa truncation: k_hi = k with the low 13 mantissa bits cleared is exactly an fp16
+// value for k in the fp16 normal range (k <= 1 here: o^2 is applied after the GEMM), so
+// k_lo = k - k_hi is exact and both conversions are exact up to fp16 rounding of k_lo
+// (3 issue slots per entry: LOP3 + FADD + 1/2 F2FP x 2, instead of a round-trip conversion).
+template <int KIND, bool MASK, bool TRUNC>
+__device__ __forceinline__ void exp_split_chunk_impl(const uint32_t (&sv)[32], uint32_t (&hi)[16], uint32_t (&lo)[16],
+                                                     int jvalid) {
 #pragma unroll
   for (int c = 0; c < 32; c += 2) {
     float k0 = kernel_from_s<KIND>(__uint_as_float(sv[c]));
@@ -89,11 +93,24 @@ __device__ __forceinline__ void exp_split_chunk(const uint32_t (&sv)[32], uint32
       k0 = (c < jvalid) ? k0 : 0.f;
       k1 = (c + 1 < jvalid) ? k1 : 0.f;
     }
-    const uint32_t h = pack_half2(k0, k1);
-    const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
-    hi[c / 2] = h;
-    lo[c / 2] = pack_half2(k0 - hf.x, k1 - hf.y);
+    if (TRUNC) {
+      const float h0 = __uint_as_float(__float_as_uint(k0) & 0xFFFFE000u);
+      const float h1 = __uint_as_float(__float_as_uint(k1) & 0xFFFFE000u);
+      hi[c / 2] = pack_half2(h0, h1);
+      lo[c / 2] = pack_half2(k0 - h0, k1 - h1);
+    } else {
+      const uint32_t h = pack_half2(k0, k1);
+      const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
+      hi[c / 2] = h;
+      lo[c / 2] = pack_half2(k0 - hf.x, k1 - hf.y);
+    }
   }
+}
+template <int KIND, bool MASK>
+__device__ __forceinline__ void exp_split_chunk(const uint32_t (&sv)[32], uint32_t (&hi)[16], uint32_t (&lo)[16],
+                                                int jvalid, bool trunc) {
+  if (trunc) exp_split_chunk_impl<KIND, MASK, true>(sv, hi, lo, jvalid);
+  else exp_split_chunk_impl<KIND, MASK, false>(sv, hi, lo, jvalid);
 }
 
 template <int KIND, int TN>
@@ -224,6 +241,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int grp = (warp - EPI_WARP0) / 8;         // ping-pong group
     const int half = ((warp - EPI_WARP0) / 4) % 2;  // 64-column half of the tile
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const bool trunc = (args.dbg & 1024) != 0;
     for (int jj = grp; jj < njt; jj += 2) {
       const int b = jj % NBUF;
       const uint32_t tb = tbase + b * 128 + lane_base + 64 * half;
@@ -240,8 +258,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (args.dbg & 2) {
 #pragma unroll
           for (int m = 0; m < 16; ++m) { hi[m] = sv0[m]; lo[m] = sv0[m + 16]; }
-        } else if (tail) exp_split_chunk<KIND, true>(sv0, hi, lo, (int)(n - jcol0));
-        else exp_split_chunk<KIND, false>(sv0, hi, lo, 32);
+        } else if (tail) exp_split_chunk<KIND, true>(sv0, hi, lo, (int)(n - jcol0), trunc);
+        else exp_split_chunk<KIND, false>(sv0, hi, lo, 32, trunc);
         tmem_st16(tb, hi);
         tmem_st16(tb + 16, lo);
       }
@@ -250,8 +268,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (args.dbg & 2) {
 #pragma unroll
           for (int m = 0; m < 16; ++m) { hi[m] = sv1[m]; lo[m] = sv1[m + 16]; }
-        } else if (tail) exp_split_chunk<KIND, true>(sv1, hi, lo, (int)(n - jcol0 - 32));
-        else exp_split_chunk<KIND, false>(sv1, hi, lo, 32);
+        } else if (tail) exp_split_chunk<KIND, true>(sv1, hi, lo, (int)(n - jcol0 - 32), trunc);
+        else exp_split_chunk<KIND, false>(sv1, hi, lo, 32, trunc);
         tmem_st16(tb + 32, hi);
         tmem_st16(tb + 48, lo);
       }
