@@ -104,9 +104,10 @@ def dist_env():
 
 
 def workload_desc(cfg) -> str:
-    return (f"{cfg.name}: N={cfg.n:,} matrix-free {cfg.kind.upper()} d={cfg.d}, {cfg.t} RHS, "
-            f"K^{{1/2}}B, Q={cfg.q}, tol={cfg.tol:g} (J_max {cfg.max_iters}), l={cfg.lengthscale}, "
-            f"sigma2={cfg.sigma2}")
+    op = ("dense RBF (precomputed K, d=%d)" % cfg.d) if cfg.kind == "dense" else f"matrix-free {cfg.kind.upper()} d={cfg.d}"
+    what = {"sqrt": "K^{1/2}B", "invsqrt": "K^{-1/2}B", "whiten": "K^{-1/2}B"}[cfg.mode]
+    return (f"{cfg.name}: N={cfg.n:,} {op}, {cfg.t} RHS, {what}, Q={cfg.q}, tol={cfg.tol:g} "
+            f"(J_max {cfg.max_iters}), l={cfg.lengthscale}, sigma2={cfg.sigma2}")
 
 
 # ------------------------------------------------------------------------------------------------
@@ -197,8 +198,12 @@ def run_ours(args, cfg):
     if sharded:
         uid = broadcast_uid(torch.distributed, rank, pb.ciq_nccl_unique_id)
         comm = (rank, world, uid)
-    g = pb.CIQ(cfg.kind, n=cfg.n, X=x, lengthscale=cfg.lengthscale, outputscale=cfg.outputscale, diag=cfg.sigma2,
-               comm=comm)
+    if cfg.kind == "dense":
+        kloc = torch.from_numpy(np.ascontiguousarray(inp["K"][r0:r1])).cuda()
+        g = pb.CIQ("dense", n=cfg.n, K=kloc, diag=cfg.sigma2, comm=comm)
+    else:
+        g = pb.CIQ(cfg.kind, n=cfg.n, X=x, lengthscale=cfg.lengthscale, outputscale=cfg.outputscale,
+                   diag=cfg.sigma2, comm=comm)
     kw = dict(q=cfg.q, max_iters=cfg.max_iters, tol=cfg.tol, mode=cfg.mode, lanczos_start=s, mvm_impl=args.mvm)
     stream = torch.cuda.current_stream()
 
@@ -261,7 +266,12 @@ def run_ours(args, cfg):
     impl_used = pinfo["mvm_impl_used"]
     # algorithmic work per MVM launch: N^2 kernel evaluations, 2 N^2 T useful flops
     flops = 2.0 * rows_local * n * tcols        # this rank's rows of K . V
-    if impl_used == "simt":
+    if cfg.kind == "dense" and impl_used == "tc":
+        kbytes = 4.0 * rows_local * n                # split fp16 planes: 4 B per entry of K, read once
+        roof = {"bound": "hbm", "achieved": kbytes / (mvm_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "kernel": "mvm_dense_tc_kernel (K streamed once per MVM, tcgen05 split products)",
+                "peak_source": f"{peaks['_source']} HBM copy bandwidth"}
+    elif impl_used == "simt":
         sm_count = torch.cuda.get_device_properties(local).multi_processor_count
         fp32_peak = sm_count * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12  # TFLOP/s
         roof = {"bound": "alu", "achieved": flops / (mvm_ms * 1e-3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",

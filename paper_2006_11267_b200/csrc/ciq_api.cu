@@ -100,6 +100,9 @@ struct ciq_ctx {
   // tensor-core MVM operands
   bool tc_ok = false;
   int64_t npad = 0;
+  __half* kplanes = nullptr;  // dense path: split K planes [hi | lo]
+  int64_t kplane_elems = 0;
+  float kscale = 1.f;
   __half* feat_a = nullptr;   // [npad/8][4][8][8]
   __half* feat_b = nullptr;
   __half* planes = nullptr;   // split V planes, grown on demand
@@ -316,6 +319,23 @@ int choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm) {
   return best;
 }
 
+// Dense path: split the K stream (npad/64 tiles per row block) so that row tiles x chunks x splits
+// fill whole waves, keeping >= 6 K tiles per CTA.
+int choose_nsplit_dense(int64_t rows, int64_t npad, int chunks, int nsm) {
+  const int64_t rt = (rows + 127) / 128;
+  const int64_t nkt = npad / 64;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 64; ++s) {
+    if (nkt / s < 6) break;
+    const int64_t units = rt * chunks * s;
+    const int64_t waves = (units + nsm - 1) / nsm;
+    const double eff = (double)units / (double)(waves * nsm) - 0.002 * waves;  // favour fewer waves
+    if (eff > best_eff + 0.01) { best_eff = eff; best = s; }
+  }
+  return best;
+}
+
 // Allocate every buffer run_mvm(tp, allow_split) may need (so a CUDA-graph capture never
 // allocates).
 ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
@@ -325,7 +345,8 @@ ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
   int nsm = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int nsplit = choose_nsplit(rows, c->op.n, tp / tn, nsm);
+  const int nsplit = c->op.kind == CIQ_OP_DENSE ? choose_nsplit_dense(rows, c->npad, tp / tn, nsm)
+                                                : choose_nsplit(rows, c->op.n, tp / tn, nsm);
   const int64_t rt = (rows + 127) / 128;
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
   if (st != CIQ_OK) return st;
@@ -367,7 +388,8 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   (void)allow_split;
-  const int nsplit = choose_nsplit(rows, c->op.n, chunks, nsm);
+  const bool dense = c->op.kind == CIQ_OP_DENSE;
+  const int nsplit = dense ? choose_nsplit_dense(rows, c->npad, chunks, nsm) : choose_nsplit(rows, c->op.n, chunks, nsm);
   const int64_t rt = (rows + 127) / 128;
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
   if (st != CIQ_OK) return st;
@@ -410,12 +432,16 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   a.o2 = c->op.outputscale;
   a.diag = c->op.diag;
   a.done = done;
+  a.kplanes = c->kplanes;
+  a.kplane_elems = c->kplane_elems;
+  a.kscale_inv = 1.f / c->kscale;
   {
     static const int dbg = getenv("CIQ_TC_DEBUG") ? atoi(getenv("CIQ_TC_DEBUG")) : 0;
     a.dbg = dbg;
     a.dbg_clk = nullptr;
   }
-  LAUNCH(c, launch_mvm_tc(a, c->stream));
+  if (dense) LAUNCH(c, launch_mvm_dense_tc(a, c->stream));
+  else LAUNCH(c, launch_mvm_tc(a, c->stream));
   if (nsplit > 1 && nsplit_out == nullptr)  // caller wants the complete product in p
     LAUNCH(c, launch_sum_splits(c->psplit, nsplit, (size_t)rows * tp, rows * tp, p, c->stream));
   if (nsplit_out) *nsplit_out = nsplit;
@@ -423,6 +449,34 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   if (apart_nblk) *apart_nblk = (int)(rt * nsplit);
   c->mvm_kind_used = 2;
   return CIQ_OK;
+}
+
+// Dense path: split the (local rows of) K once into fp16 planes with a global power-of-two scale
+// 2^(14 - ceil(log2 max|K|)) so both halves stay in the fp16 normal range.
+bool build_dense_planes(ciq_ctx* c) {
+  const int64_t rows = c->row1 - c->row0, n = c->op.n;
+  const int64_t npad = (n + 127) / 128 * 128;
+  const int64_t rows_pad = (rows + 127) / 128 * 128;
+  unsigned int* mx = nullptr;
+  if (cudaMalloc(&mx, 4) != cudaSuccess) return false;
+  cudaMemset(mx, 0, 4);
+  const float* kloc = c->dev.k + c->row0 * c->dev.ldk;
+  launch_absmax(kloc, c->dev.ldk, rows, n, mx, c->stream);
+  unsigned int hbits = 0;
+  cudaMemcpy(&hbits, mx, 4, cudaMemcpyDeviceToHost);
+  cudaFree(mx);
+  float amax;
+  std::memcpy(&amax, &hbits, 4);
+  if (!(amax > 0) || !std::isfinite(amax)) amax = 1.f;
+  c->kscale = std::ldexp(1.f, 14 - (int)std::ceil(std::log2(amax)));
+  c->kplane_elems = rows_pad * npad;
+  if (cudaMalloc(&c->kplanes, (size_t)2 * c->kplane_elems * 2) != cudaSuccess) return false;
+  if (launch_split_dense(kloc, c->dev.ldk, rows, n, npad, c->kscale, c->kplanes, c->kplanes + c->kplane_elems,
+                         c->stream) != cudaSuccess)
+    return false;
+  c->npad = npad;
+  c->tc_ok = cudaStreamSynchronize(c->stream) == cudaSuccess;
+  return c->tc_ok;
 }
 
 // Augmented split-fp16 features of the tensor-core MVM (mvm_tc.cu): with y = (x - mean)/l *
@@ -845,6 +899,7 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
       dv.k = c->kcopy - c->row0 * op->n;
       dv.ldk = op->n;
     }
+    if (!build_dense_planes(c)) cudaGetLastError();  // tensor-core dense path unavailable -> SIMT
   } else {
     const int64_t n = op->n, d = op->d;
     std::vector<float> xh((size_t)n * d);
@@ -902,6 +957,7 @@ void ciq_free(ciq_ctx* c) {
   dfree(c->xs);
   dfree(c->kcopy);
   dfree(c->staging);
+  dfree(c->kplanes);
   dfree(c->feat_a); dfree(c->feat_b); dfree(c->planes); dfree(c->inv_scale); dfree(c->psplit);
   dfree(c->apart_tc);
   free_precond(c->pc);

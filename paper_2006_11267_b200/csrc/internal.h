@@ -62,6 +62,9 @@ struct TcArgs {
   double* apart;
   float o2, diag;
   const Ctrl* done;
+  const __half* kplanes;     // dense path: split K planes [hi | lo], each kplane_elems
+  int64_t kplane_elems;
+  float kscale_inv;          // dense path: 1 / global K scale
   int dbg;                   // experiments only (env CIQ_TC_DEBUG): 1 skip KV MMAs, 2 skip exp math
   long long* dbg_clk;        // experiments only: per-tile clock stamps of CTA 0
 };
@@ -69,6 +72,10 @@ int tc_chunk_cols(int tp);
 cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, const double* nrm, __half* planes,
                           float* inv_scale, cudaStream_t s);
 cudaError_t launch_mvm_tc(const TcArgs& a, cudaStream_t s);
+cudaError_t launch_mvm_dense_tc(const TcArgs& a, cudaStream_t s);
+cudaError_t launch_absmax(const float* k, int64_t ldk, int64_t rows, int64_t n, unsigned int* out, cudaStream_t s);
+cudaError_t launch_split_dense(const float* k, int64_t ldk, int64_t rows, int64_t n, int64_t npad, float scale,
+                               __half* hi, __half* lo, cudaStream_t s);
 
 // ---- vector kernels (recurrence.cu) ----
 int rowblocks(int64_t rows, int tp);   // number of CTAs of the row-streaming kernels

@@ -389,6 +389,193 @@ cudaError_t launch_kind(const TcArgs& a, int tn, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
+
+// ============================================================================================
+// Dense-K streaming MVM (SURVEY K2, §8(a) row a4 for a precomputed K): P = K V + sigma^2 V
+// with K pre-split once (ciq_init) into fp16 planes K_hi + K_lo (x global power-of-two scale),
+// i.e. the same 4 bytes per entry as fp32, laid out as K-major core matrices per 128 x 64 tile so
+// each tile is one bulk copy.  HBM-bound: every byte of K is read once per MVM; the tensor core
+// does the three split products (hi.hi + hi.lo + lo.hi) with fp32 accumulation in TMEM.
+// Warps: 0 = producer (4-stage ring of K_hi | K_lo | V_hi | V_lo), 1 = MMA issuer, 4..7 = epilogue.
+// ============================================================================================
+constexpr int DK = 64;            // K-dim (columns j of K) per stage
+constexpr int D_THREADS = 256;
+
+template <int TN>
+struct DCfg {
+  static constexpr int KT_BYTES = BM * DK * 2;        // one fp16 plane of a 128 x 64 K tile (16 KB)
+  static constexpr int VT_BYTES = DK * TN * 2;        // one plane of a 64-row V slab
+  static constexpr int STAGE_BYTES = 2 * KT_BYTES + 2 * VT_BYTES;
+  static constexpr int STAGES = 4;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 2048;
+};
+static_assert(DCfg<64>::SMEM <= 227 * 1024, "shared memory budget");
+
+struct DBars {
+  uint64_t full[4], empty[4];
+  uint64_t o_full;
+  uint32_t tmem_base;
+};
+
+template <int TN>
+__global__ void __launch_bounds__(D_THREADS, 1) mvm_dense_tc_kernel(TcArgs args) {
+  using C = DCfg<TN>;
+  if (args.done != nullptr && args.done->done) return;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;
+  DBars* bars = reinterpret_cast<DBars*>(ring + C::STAGES * C::STAGE_BYTES);
+  float* red = reinterpret_cast<float*>(bars + 1);  // [4][TN]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nsplit = args.nsplit;
+  const int rt = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
+  const int chunk = blockIdx.y;
+  const int64_t n = args.n;
+  const int64_t i0 = args.row0 + (int64_t)rt * BM;
+  const int nkt = (int)(args.npad / DK);                      // K tiles along j (npad multiple of 128)
+  const int kt0 = (int)((int64_t)nkt * split / nsplit), kt1 = (int)((int64_t)nkt * (split + 1) / nsplit);
+  const int nk = kt1 - kt0;
+  const int rt_local = (int)((i0 - args.row0) / BM);          // row tile within this rank's K planes
+  if (threadIdx.x == 0) {
+    for (int s2 = 0; s2 < C::STAGES; ++s2) { mbar_init(&bars->full[s2], 1); mbar_init(&bars->empty[s2], 1); }
+    mbar_init(&bars->o_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<64>(&bars->tmem_base);
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tbase = bars->tmem_base;
+  const size_t kplane = (size_t)args.kplane_elems;             // elements of one K plane
+  const __half* kh = args.kplanes + (size_t)rt_local * nkt * BM * DK;
+  const __half* kl = kh + kplane;
+  const size_t vplane = (size_t)args.npad * TN;
+  const __half* vh = args.vplanes + (size_t)chunk * 2 * vplane;
+  const __half* vl = vh + vplane;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kk = 0; kk < nk; ++kk) {
+        const int st = kk % C::STAGES;
+        mbar_wait(&bars->empty[st], ((kk / C::STAGES) & 1) ^ 1);
+        uint8_t* sb = ring + st * C::STAGE_BYTES;
+        const int kt = kt0 + kk;
+        mbar_arrive_expect_tx(&bars->full[st], C::STAGE_BYTES);
+        bulk_g2s(sb, kh + (size_t)kt * BM * DK, C::KT_BYTES, &bars->full[st]);
+        bulk_g2s(sb + C::KT_BYTES, kl + (size_t)kt * BM * DK, C::KT_BYTES, &bars->full[st]);
+        // V slab of rows [64 kt, 64 kt + 64): half of the 128-row V tile (kc-major => contiguous)
+        const size_t voff = (size_t)(kt / 2) * BN * TN + (size_t)(kt & 1) * DK * TN;
+        bulk_g2s(sb + 2 * C::KT_BYTES, vh + voff, C::VT_BYTES, &bars->full[st]);
+        bulk_g2s(sb + 2 * C::KT_BYTES + C::VT_BYTES, vl + voff, C::VT_BYTES, &bars->full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_o = idesc_f16(128, TN, 0, 1);   // A (smem) K-major, B MN-major
+    for (int kk = 0; kk < nk; ++kk) {
+      const int st = kk % C::STAGES;
+      mbar_wait(&bars->full[st], (kk / C::STAGES) & 1);
+      fence_after_sync();
+      const uint32_t a_h = smem_u32(ring + st * C::STAGE_BYTES);
+      const uint32_t a_l = a_h + C::KT_BYTES;
+      const uint32_t v_h = a_h + 2 * C::KT_BYTES;
+      const uint32_t v_l = v_h + C::VT_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < DK / 16; ++ks) {
+        // A: K-major core matrices [16 row groups][8 k chunks]: LBO = 128 B, SBO = 8*128 B; K step 256 B
+        const uint64_t dah = smem_desc(a_h + ks * 256, 128, (DK / 8) * 128);
+        const uint64_t dal = smem_desc(a_l + ks * 256, 128, (DK / 8) * 128);
+        // B: MN-major [k chunk][n group]: LBO = TN/8*128 B, SBO = 128 B; K step 2 k-chunks
+        const uint32_t koff = ks * 2 * (TN / 8) * 128;
+        const uint64_t dvh = smem_desc(v_h + koff, (TN / 8) * 128, 128);
+        const uint64_t dvl = smem_desc(v_l + koff, (TN / 8) * 128, 128);
+        mma_ss_warp(tbase, dah, dvh, idesc_o, (kk > 0 || ks > 0) ? 1u : 0u);
+        mma_ss_warp(tbase, dah, dvl, idesc_o, 1u);
+        mma_ss_warp(tbase, dal, dvh, idesc_o, 1u);
+      }
+      mma_commit_warp(&bars->empty[st]);
+    }
+    mma_commit_warp(&bars->o_full);
+  } else if (warp >= 4) {
+    const int q = warp % 4;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    mbar_wait(&bars->o_full, 0);
+    fence_after_sync();
+    const int64_t i = i0 + q * 32 + lane;
+    const bool row_ok = i < args.row1 && nk > 0;
+    float* pout = args.p + (size_t)split * args.p_split_stride;
+    const int cglob0 = chunk * TN;
+#pragma unroll
+    for (int cb = 0; cb < TN; cb += 16) {
+      uint32_t o16[16];
+      tmem_ld16(tbase + lane_base + cb, o16);
+      tmem_ld_wait();
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) {
+        const int col = cglob0 + cb + cc;
+        float v = 0.f, out = 0.f;
+        if (i < args.row1) {
+          v = args.v[(size_t)i * args.tp + col];
+          out = row_ok ? __uint_as_float(o16[cc]) * args.kscale_inv * args.inv_scale[col] : 0.f;
+          if (split == 0) out = fmaf(args.diag, v, out);
+          pout[(size_t)(i - args.row0) * args.tp + col] = out;
+        }
+        float part = v * out;
+        part = warp_sum(part);
+        if (lane == 0) red[q * TN + cb + cc] = part;
+      }
+    }
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (args.apart != nullptr) {
+    for (int c = threadIdx.x; c < TN; c += D_THREADS) {
+      double sum = 0.0;
+      for (int qq = 0; qq < 4; ++qq) sum += (double)red[qq * TN + c];
+      args.apart[(size_t)blockIdx.x * args.tp + chunk * TN + c] = sum;
+    }
+  }
+  if (warp == 1) {
+    fence_after_sync();
+    tmem_dealloc<64>(tbase);
+  }
+}
+
+// max |K| over the row block (non-negative floats order like their bit patterns -> atomicMax)
+__global__ void absmax_kernel(const float* __restrict__ k, int64_t ldk, int64_t rows, int64_t n,
+                              unsigned int* __restrict__ out) {
+  float m = 0.f;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * n; e += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(k[(e / n) * ldk + e % n]));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// K (rows x n fp32, ld) * scale -> K-major split planes [rows/128][npad/64][16][8][8][8] (hi, lo)
+__global__ void split_dense_kernel(const float* __restrict__ k, int64_t ldk, int64_t rows, int64_t n, int64_t npad,
+                                   float scale, __half* __restrict__ hi, __half* __restrict__ lo) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one thread per (row, 8 columns)
+  const int64_t rows_pad = (rows + BM - 1) / BM * BM;
+  const int64_t groups = npad / 8;
+  if (e >= rows_pad * groups) return;
+  const int64_t i = e / groups, g = e % groups;
+  const int64_t j0 = g * 8;
+  uint32_t hw[4], lw[4];
+#pragma unroll
+  for (int m = 0; m < 8; m += 2) {
+    float x0 = 0.f, x1 = 0.f;
+    if (i < rows && j0 + m < n) x0 = k[i * ldk + j0 + m] * scale;
+    if (i < rows && j0 + m + 1 < n) x1 = k[i * ldk + j0 + m + 1] * scale;
+    const uint32_t h = tc::pack_half2(x0, x1);
+    const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
+    hw[m / 2] = h;
+    lw[m / 2] = tc::pack_half2(x0 - hf.x, x1 - hf.y);
+  }
+  const int64_t rt = i / BM, r = i % BM, kt = j0 / DK, kc = (j0 % DK) / 8;
+  const int64_t nkt = npad / DK;
+  const size_t off = ((size_t)(rt * nkt + kt) * BM * DK) + (size_t)((r / 8) * (DK / 8) + kc) * 64 + (r % 8) * 8;
+  *reinterpret_cast<uint4*>(hi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+  *reinterpret_cast<uint4*>(lo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+}
+
 }  // namespace
 
 // Column chunk TN per CTA.  Capped at 64: the single smem ring needs >= NBUF + 1 = 4 stages
@@ -406,6 +593,39 @@ cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, const
   const int64_t total = npad * (tp / 8);
   pack_v_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(v, n, npad, tp, tn, nrm, planes, inv_scale);
   return cudaGetLastError();
+}
+
+cudaError_t launch_split_dense(const float* k, int64_t ldk, int64_t rows, int64_t n, int64_t npad, float scale,
+                               __half* hi, __half* lo, cudaStream_t s) {
+  const int64_t rows_pad = (rows + BM - 1) / BM * BM;
+  const int64_t total = rows_pad * (npad / 8);
+  split_dense_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(k, ldk, rows, n, npad, scale, hi, lo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_absmax(const float* k, int64_t ldk, int64_t rows, int64_t n, unsigned int* out, cudaStream_t s) {
+  absmax_kernel<<<1184, 256, 0, s>>>(k, ldk, rows, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mvm_dense_tc(const TcArgs& a, cudaStream_t s) {
+  const int tn = tc_chunk_cols(a.tp);
+  dim3 grid(a.nblk_x, a.tp / tn);
+  switch (tn) {
+#define CIQ_DTC_CASE(TNV)                                                                                   \
+  case TNV: {                                                                                               \
+    auto k = mvm_dense_tc_kernel<TNV>;                                                                      \
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, DCfg<TNV>::SMEM);   \
+    if (e != cudaSuccess) return e;                                                                         \
+    k<<<grid, D_THREADS, DCfg<TNV>::SMEM, s>>>(a);                                                          \
+    return cudaGetLastError();                                                                              \
+  }
+    CIQ_DTC_CASE(16)
+    CIQ_DTC_CASE(32)
+    CIQ_DTC_CASE(64)
+#undef CIQ_DTC_CASE
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_mvm_tc(const TcArgs& a, cudaStream_t s) {

@@ -23,7 +23,10 @@ inp = workloads.make_inputs(cfg)
 x = torch.from_numpy(inp["X"]).cuda()
 v = torch.from_numpy(workloads.rhs(cfg.n, cfg.t, seed=9)).cuda()
 out = torch.empty_like(v)
-g = pb.CIQ(cfg.kind, X=x, lengthscale=cfg.lengthscale, outputscale=cfg.outputscale, diag=cfg.sigma2)
+if cfg.kind == "dense":
+    g = pb.CIQ("dense", K=torch.from_numpy(inp["K"]).cuda(), diag=cfg.sigma2)
+else:
+    g = pb.CIQ(cfg.kind, X=x, lengthscale=cfg.lengthscale, outputscale=cfg.outputscale, diag=cfg.sigma2)
 st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for r in range(a.reps):
     st.record()
