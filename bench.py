@@ -201,6 +201,13 @@ def run_ours(args, cfg):
     if cfg.kind == "dense":
         kloc = torch.from_numpy(np.ascontiguousarray(inp["K"][r0:r1])).cuda()
         g = pb.CIQ("dense", n=cfg.n, K=kloc, diag=cfg.sigma2, comm=comm)
+    elif cfg.precond_rank > 0:
+        # App. A preconditioner: rank-R partial pivoted Cholesky built by the library on the GPU
+        with pb.CIQ(cfg.kind, X=x, lengthscale=cfg.lengthscale, outputscale=cfg.outputscale, diag=cfg.sigma2) as g0:
+            lfac = torch.zeros((cfg.n, cfg.precond_rank), device="cuda")
+            g0.pivoted_cholesky(cfg.precond_rank, lfac)
+        g = pb.CIQ(cfg.kind, n=cfg.n, X=x, lengthscale=cfg.lengthscale, outputscale=cfg.outputscale,
+                   diag=cfg.sigma2, precond_L=lfac, precond_sigma2=cfg.sigma2)
     else:
         g = pb.CIQ(cfg.kind, n=cfg.n, X=x, lengthscale=cfg.lengthscale, outputscale=cfg.outputscale,
                    diag=cfg.sigma2, comm=comm)
