@@ -22,6 +22,9 @@ SOURCES = ["host_math.cpp", "nccl_dl.cpp", "comm.cpp", "mvm_simt.cu", "mvm_tc.cu
 HEADERS = ["common.cuh", "nccl_dl.h", "comm.h", "internal.h", "host_math.h", "tc_util.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"] + ARCH
+# CIQ_TC_TRACE=1: compile the K1 per-tile clock stamps (experiments; see mvm_tc.cu)
+if os.environ.get("CIQ_TC_TRACE"):
+    NVCC_FLAGS.append("-DCIQ_TC_TRACE")
 
 
 def _nvcc() -> str:

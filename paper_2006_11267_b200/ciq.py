@@ -17,7 +17,8 @@ from ctypes import POINTER, c_char_p, c_double, c_float, c_int32, c_int64, c_uin
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libciq.so")
+# CIQ_LIB overrides the library path (A/B experiments between builds only)
+LIB_PATH = os.environ.get("CIQ_LIB") or os.path.join(_HERE, "libciq.so")
 
 CIQ_MAX_Q = 64
 

@@ -304,8 +304,8 @@ bool use_tc(const ciq_ctx* c, int impl) {
 
 // Number of column-splits of the J range so that (row tiles x chunks x splits) fills whole waves
 // of 148 SMs (1 CTA / SM: the kernel owns all 512 TMEM columns).
-int choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm) {
-  const int64_t rt = (rows + 127) / 128;
+int choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm, int cl) {
+  const int64_t rt = ((rows + 127) / 128 + cl - 1) / cl * cl;
   const int64_t ntiles = (n + 127) / 128;
   int best = 1;
   double best_eff = 0.0;
@@ -346,8 +346,9 @@ ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int nsplit = c->op.kind == CIQ_OP_DENSE ? choose_nsplit_dense(rows, c->npad, tp / tn, nsm)
-                                                : choose_nsplit(rows, c->op.n, tp / tn, nsm);
-  const int64_t rt = (rows + 127) / 128;
+                                                : choose_nsplit(rows, c->op.n, tp / tn, nsm, tc_cluster_size());
+  const int cl = c->op.kind == CIQ_OP_DENSE ? 1 : tc_cluster_size();
+  const int64_t rt = ((rows + 127) / 128 + cl - 1) / cl * cl;   // row tiles, padded to whole clusters
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
   if (st != CIQ_OK) return st;
   if (c->inv_scale_n < tp) {
@@ -389,8 +390,9 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   }
   (void)allow_split;
   const bool dense = c->op.kind == CIQ_OP_DENSE;
-  const int nsplit = dense ? choose_nsplit_dense(rows, c->npad, chunks, nsm) : choose_nsplit(rows, c->op.n, chunks, nsm);
-  const int64_t rt = (rows + 127) / 128;
+  const int nsplit = dense ? choose_nsplit_dense(rows, c->npad, chunks, nsm) : choose_nsplit(rows, c->op.n, chunks, nsm, tc_cluster_size());
+  const int cl = c->op.kind == CIQ_OP_DENSE ? 1 : tc_cluster_size();
+  const int64_t rt = ((rows + 127) / 128 + cl - 1) / cl * cl;   // row tiles, padded to whole clusters
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
   if (st != CIQ_OK) return st;
   if (c->inv_scale_n < tp) {
@@ -421,6 +423,7 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   a.tp = tp;
   a.nsplit = nsplit;
   a.nblk_x = (int)(rt * nsplit);
+  a.cl = cl;
   a.feat_a = c->feat_a;
   a.feat_b = c->feat_b;
   a.vplanes = c->planes;
@@ -439,9 +442,25 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     static const int dbg = getenv("CIQ_TC_DEBUG") ? atoi(getenv("CIQ_TC_DEBUG")) : 0;
     a.dbg = dbg;
     a.dbg_clk = nullptr;
+    if ((dbg & 128) && !dense) cudaMallocManaged(&a.dbg_clk, 12 * 256 * sizeof(long long));
+    if (a.dbg_clk) cudaMemset(a.dbg_clk, 0, 12 * 256 * sizeof(long long));
   }
   if (dense) LAUNCH(c, launch_mvm_dense_tc(a, c->stream));
   else LAUNCH(c, launch_mvm_tc(a, c->stream));
+  if (a.dbg_clk) {  // experiments only: dump the per-tile timeline of CTA (0, 0)
+    cudaStreamSynchronize(c->stream);
+    const long long t0 = a.dbg_clk[0 * 256];
+    fprintf(stderr, "tile  prod  it_start  k0  full_ok  epi_s  epi_done  KVdone  S+3done  s_issued  kv_iss  s_commit\n");
+    for (int j = 0; j < 48; ++j) {
+      fprintf(stderr, "%4d", j);
+      for (int sl = 0; sl < 11; ++sl) {
+        const long long v = a.dbg_clk[sl * 256 + j];
+        fprintf(stderr, " %9lld", v ? v - t0 : -1LL);
+      }
+      fprintf(stderr, "\n");
+    }
+    cudaFree(a.dbg_clk);
+  }
   if (nsplit > 1 && nsplit_out == nullptr)  // caller wants the complete product in p
     LAUNCH(c, launch_sum_splits(c->psplit, nsplit, (size_t)rows * tp, rows * tp, p, c->stream));
   if (nsplit_out) *nsplit_out = nsplit;

@@ -52,6 +52,8 @@ struct TcArgs {
   int kind;
   int64_t n, npad, row0, row1;
   int tp, nsplit, nblk_x;
+  int cl;                    // matrix-free path: CTAs per cluster along the row tiles (1, 2, 4);
+                             // nblk_x = (row tiles rounded up to cl) * nsplit
   const __half* feat_a;      // [npad/8][4][8][8] A-role features (rows)
   const __half* feat_b;      // [npad/8][4][8][8] B-role features (columns)
   const __half* vplanes;     // [tp/TN][2][npad*TN] split V planes (pack_v)
@@ -69,6 +71,7 @@ struct TcArgs {
   long long* dbg_clk;        // experiments only: per-tile clock stamps of CTA 0
 };
 int tc_chunk_cols(int tp);
+int tc_cluster_size();       // cluster size of the matrix-free kernel (env CIQ_TC_CLUSTER overrides)
 cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, const double* nrm, __half* planes,
                           float* inv_scale, cudaStream_t s);
 cudaError_t launch_mvm_tc(const TcArgs& a, cudaStream_t s);

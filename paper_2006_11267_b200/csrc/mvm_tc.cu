@@ -27,6 +27,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <stdlib.h>
+
 #include "internal.h"
 #include "tc_util.cuh"
 
@@ -43,24 +45,30 @@ constexpr int EPI_WARP0 = 4;
 constexpr int NBUF = 3;          // TMEM S/K tile buffers (S is overwritten in place by K_hi|K_lo)
 constexpr int TM_O = NBUF * 128; // O accumulator columns [384, 384 + TN)
 
-// One smem ring: stage J holds the column-point features (read by S(J)) and the V planes (read by
-// KV(J)); it is released after KV(J).  One wait and one release per tile keep the MMA warp's
-// non-MMA work between tensor batches small (the tensor queue is shallow).
+// One smem ring, skewed by the S lookahead: stage J holds the V planes of tile J (read by KV(J))
+// AND the column-point features of tile J+3 (read by S(J+3), which the MMA warp issues right after
+// KV(J)), so each tile costs the MMA warp one stage wait and one stage release, and the producer
+// runs STAGES tiles ahead of KV.  Features of tiles 0..2 come with the A rows in a prologue buffer.
+// (The MMA warp's synchronisation count per tile is what limits the tensor pipe here: every
+// mbarrier wait / tcgen05.commit on its path costs ~100 clk of issue while the tensor queue is
+// shallow.)
 template <int TN>
 struct Cfg {
   static constexpr int FEAT_BYTES = BN * KF * 2;     // 8 KB
   static constexpr int V_BYTES = BN * TN * 2;        // one plane of one tile
-  static constexpr int STAGES = 5;   // >= NBUF + 1 (S(J+3) is issued before KV(J+1) frees a stage)
-  static constexpr int STAGE_BYTES = FEAT_BYTES + 2 * V_BYTES;
-  static constexpr int SMEM = 1024 + FEAT_BYTES /*A rows*/ + STAGES * STAGE_BYTES + 4096;
+  static constexpr int STAGES = 4;
+  static constexpr int STAGE_BYTES = 2 * V_BYTES + FEAT_BYTES;
+  static constexpr int PRO_BYTES = (1 + NBUF) * FEAT_BYTES;   // A rows + features of tiles 0..2
+  static constexpr int SMEM = 1024 + PRO_BYTES + STAGES * STAGE_BYTES + 4096;
 };
 
 static_assert(Cfg<64>::SMEM <= 227 * 1024, "shared memory budget");
 
 struct Bars {
-  uint64_t full[5], empty[5];
-  uint64_t s_full[NBUF], k_full[NBUF], buf_free[NBUF];
+  uint64_t full[4], empty[4];
+  uint64_t s_full[NBUF], k_full[NBUF];
   uint64_t o_full, a_full;
+  uint64_t probe_kv[2], probe_s[2];   // experiments only (dbg & 128): tensor-pipe completion probes
   uint32_t tmem_base;
 };
 
@@ -77,13 +85,13 @@ __device__ __forceinline__ float kernel_from_s(float s) {
   return (1.f + a) * ex2_approx(-1.4426950408889634f * a);
 }
 
-// 32 S values (one chunk of a row) -> 16 packed k_hi words + 16 packed k_lo words.
-// Split by mantissa truncation: k_hi = k with the low 13 mantissa bits cleared is exactly an fp16
-// value for k in the fp16 normal range (k <= 1 here: o^2 is applied after the GEMM), so
-// k_lo = k - k_hi is exact and both conversions are exact up to fp16 rounding of k_lo
-// (3 issue slots per entry: LOP3 + FADD + 1/2 F2FP x 2, instead of a round-trip conversion).
-template <int KIND, bool MASK, bool TRUNC>
-__device__ __forceinline__ void exp_split_chunk_impl(const uint32_t (&sv)[32], uint32_t (&hi)[16], uint32_t (&lo)[16],
+// 32 S values (one chunk of a row) -> 16 packed k_hi words + 16 packed k_lo words:
+// k_hi = fp16(k) (round to nearest), k_lo = fp16(k - k_hi) -- k_hi + k_lo carries ~22 bits.
+// (Measured alternatives, both slower: a truncation split -- k_hi = k with the low 13 mantissa
+// bits cleared -- and FA4-style offload of every 4th pair to a degree-5 polynomial 2^x on the FMA
+// pipe: 1.26 vs 1.14 ms, the epilogue is issue-bound as much as SFU-bound.)
+template <int KIND, bool MASK>
+__device__ __forceinline__ void exp_split_chunk(const uint32_t (&sv)[32], uint32_t (&hi)[16], uint32_t (&lo)[16],
                                                      int jvalid) {
 #pragma unroll
   for (int c = 0; c < 32; c += 2) {
@@ -93,189 +101,241 @@ __device__ __forceinline__ void exp_split_chunk_impl(const uint32_t (&sv)[32], u
       k0 = (c < jvalid) ? k0 : 0.f;
       k1 = (c + 1 < jvalid) ? k1 : 0.f;
     }
-    if (TRUNC) {
-      const float h0 = __uint_as_float(__float_as_uint(k0) & 0xFFFFE000u);
-      const float h1 = __uint_as_float(__float_as_uint(k1) & 0xFFFFE000u);
-      hi[c / 2] = pack_half2(h0, h1);
-      lo[c / 2] = pack_half2(k0 - h0, k1 - h1);
-    } else {
-      const uint32_t h = pack_half2(k0, k1);
-      const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
-      hi[c / 2] = h;
-      lo[c / 2] = pack_half2(k0 - hf.x, k1 - hf.y);
-    }
+    const uint32_t h = pack_half2(k0, k1);
+    const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
+    hi[c / 2] = h;
+    lo[c / 2] = pack_half2(k0 - hf.x, k1 - hf.y);
   }
 }
-template <int KIND, bool MASK>
-__device__ __forceinline__ void exp_split_chunk(const uint32_t (&sv)[32], uint32_t (&hi)[16], uint32_t (&lo)[16],
-                                                int jvalid, bool trunc) {
-  if (trunc) exp_split_chunk_impl<KIND, MASK, true>(sv, hi, lo, jvalid);
-  else exp_split_chunk_impl<KIND, MASK, false>(sv, hi, lo, jvalid);
-}
 
-template <int KIND, int TN>
+// experiments only: per-tile clock64 stamps of CTA (0, 0) (build with CIQ_TC_TRACE=1 and run
+// with CIQ_TC_DEBUG=128; compiled out otherwise -- the MMA warp's issue latency is critical)
+#ifdef CIQ_TC_TRACE
+#define CIQ_STAMP(slot, idx)                                                                      \
+  do {                                                                                            \
+    if (args.dbg_clk != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && (idx) < 256) \
+      args.dbg_clk[(slot) * 256 + (idx)] = clock64();                                             \
+  } while (0)
+constexpr bool kTrace = true;
+#else
+#define CIQ_STAMP(slot, idx) \
+  do {                       \
+  } while (0)
+constexpr bool kTrace = false;
+#endif
+
+template <int KIND, int TN, int CL>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     mvm_tc_kernel(TcArgs args) {
   using C = Cfg<TN>;
   if (args.done != nullptr && args.done->done) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* a_feat = smem;
-  uint8_t* ring = smem + C::FEAT_BYTES;
+  uint8_t* a_feat = smem;                              // A rows, then features of tiles 0..2
+  uint8_t* ring = smem + C::PRO_BYTES;
   Bars* bars = reinterpret_cast<Bars*>(ring + C::STAGES * C::STAGE_BYTES);
   float* red = reinterpret_cast<float*>(bars + 1);  // [4][TN] alpha partial staging
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nsplit = args.nsplit;
-  const int rt = blockIdx.x / nsplit, split = blockIdx.x % nsplit;
+  // Cluster of CL CTAs = CL consecutive row tiles of the same (split, chunk): they stream the same
+  // column tiles J, so each producer fetches 1/CL of a stage and multicasts it to the whole cluster
+  // (L2 -> SM traffic / CL).  blockIdx.x = ((rt / CL) * nsplit + split) * CL + rt % CL.
+  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const int cgrp = blockIdx.x / CL;
+  const int split = cgrp % nsplit;
+  const int rt = (cgrp / nsplit) * CL + crank;
   const int chunk = blockIdx.y;
   const int64_t n = args.n;
-  const int64_t i0 = args.row0 + (int64_t)rt * BM;  // global row of the tile
+  const int64_t i0 = args.row0 + (int64_t)rt * BM;  // global row of the tile (>= row1: padding CTA)
   const int ntiles = (int)((n + BN - 1) / BN);
   const int jt0 = (int)((int64_t)ntiles * split / nsplit), jt1 = (int)((int64_t)ntiles * (split + 1) / nsplit);
   const int njt = jt1 - jt0;
+  const int npro = njt < NBUF ? njt : NBUF;         // tiles whose features come with the prologue
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 1); }
+    // empty[s]: one arrival per CTA of the cluster (each consumer's MMA commit is multicast)
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], CL); }
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(&bars->s_full[b], 1);
-      mbar_init(&bars->k_full[b], 8);   // the 8 warps of one ping-pong group
-      mbar_init(&bars->buf_free[b], 1);
+      mbar_init(&bars->k_full[b], 16);  // the 16 epilogue warps
     }
     mbar_init(&bars->o_full, 1);
     mbar_init(&bars->a_full, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&bars->probe_kv[i], 1); mbar_init(&bars->probe_s[i], 1); }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
   fence_before_sync();
-  __syncthreads();
+  if (CL > 1) cluster_sync();  // peers' barriers are initialised before any multicast lands
+  else __syncthreads();
   fence_after_sync();
   const uint32_t tbase = bars->tmem_base;
 
   const size_t plane_elems = (size_t)args.npad * TN;  // one plane of one chunk
   const __half* vh = args.vplanes + (size_t)chunk * 2 * plane_elems;
   const __half* vl = vh + plane_elems;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1);
 
   if (warp == 0) {
-    // ---------------- producer: A rows once, then per tile features + V planes ----------------
+    // ---------------- producer ----------------
     if (lane == 0) {
-      mbar_arrive_expect_tx(&bars->a_full, C::FEAT_BYTES);
-      bulk_g2s(a_feat, args.feat_a + (size_t)(i0 / BM) * BM * KF, C::FEAT_BYTES, &bars->a_full);
+      // prologue (not multicast: A rows differ per CTA): A rows + features of tiles 0 .. npro-1
+      mbar_arrive_expect_tx(&bars->a_full, (1 + npro) * C::FEAT_BYTES);
+      const int64_t at = min(i0 / BM, args.npad / BM - 1);  // padding CTAs read a valid tile
+      bulk_g2s(a_feat, args.feat_a + (size_t)at * BM * KF, C::FEAT_BYTES, &bars->a_full);
+      for (int jj = 0; jj < npro; ++jj)
+        bulk_g2s(a_feat + (1 + jj) * C::FEAT_BYTES, args.feat_b + (size_t)(jt0 + jj) * BN * KF, C::FEAT_BYTES,
+                 &bars->a_full);
       for (int jj = 0; jj < njt; ++jj) {
         const int st = jj % C::STAGES;
         mbar_wait(&bars->empty[st], ((jj / C::STAGES) & 1) ^ 1);
+        CIQ_STAMP(0, jj);
         uint8_t* sb = ring + st * C::STAGE_BYTES;
-        const int jt = jt0 + jj;
-        mbar_arrive_expect_tx(&bars->full[st], C::STAGE_BYTES);
-        bulk_g2s(sb, args.feat_b + (size_t)jt * BN * KF, C::FEAT_BYTES, &bars->full[st]);
-        bulk_g2s(sb + C::FEAT_BYTES, vh + (size_t)jt * BN * TN, C::V_BYTES, &bars->full[st]);
-        bulk_g2s(sb + C::FEAT_BYTES + C::V_BYTES, vl + (size_t)jt * BN * TN, C::V_BYTES, &bars->full[st]);
+        const bool feat = jj + NBUF < njt;
+        const uint8_t* gh = reinterpret_cast<const uint8_t*>(vh + (size_t)(jt0 + jj) * BN * TN);
+        const uint8_t* gl = reinterpret_cast<const uint8_t*>(vl + (size_t)(jt0 + jj) * BN * TN);
+        const uint8_t* gf = reinterpret_cast<const uint8_t*>(args.feat_b + (size_t)(jt0 + jj + NBUF) * BN * KF);
+        // the whole stage arrives here: our slice plus (CL > 1) the peers' multicast slices
+        mbar_arrive_expect_tx(&bars->full[st], 2 * C::V_BYTES + (feat ? C::FEAT_BYTES : 0));
+        if (CL == 1) {
+          bulk_g2s(sb, gh, C::V_BYTES, &bars->full[st]);
+          bulk_g2s(sb + C::V_BYTES, gl, C::V_BYTES, &bars->full[st]);
+          if (feat) bulk_g2s(sb + 2 * C::V_BYTES, gf, C::FEAT_BYTES, &bars->full[st]);
+        } else {
+          constexpr uint32_t vs = C::V_BYTES / CL, fs = C::FEAT_BYTES / CL;
+          bulk_g2s_mc(sb + crank * vs, gh + crank * vs, vs, &bars->full[st], kMask);
+          bulk_g2s_mc(sb + C::V_BYTES + crank * vs, gl + crank * vs, vs, &bars->full[st], kMask);
+          if (feat) bulk_g2s_mc(sb + 2 * C::V_BYTES + crank * fs, gf + crank * fs, fs, &bars->full[st], kMask);
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // experiments only: completion times of KV(jj) and S(jj+3) in the tensor pipe
+    if (kTrace && args.dbg_clk != nullptr && blockIdx.x == 0 && blockIdx.y == 0) {
+      for (int jj = 0; jj < njt && jj < 256; ++jj) {
+        mbar_wait(&bars->probe_kv[jj & 1], (jj >> 1) & 1);
+        CIQ_STAMP(6, jj);
+        mbar_wait(&bars->probe_s[jj & 1], (jj >> 1) & 1);
+        CIQ_STAMP(7, jj);
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (whole warp converged; one lane elected inside each MMA) ----
     // tensor-pipe order: S(0) S(1) S(2) | KV(0) S(3) | KV(1) S(4) | ...: S runs three tiles ahead
-    // of the epilogue, KV(J) follows K(J).
+    // of the epilogue, KV(J) follows K(J).  Per tile: one stage wait, one k_full wait, two commits.
     {
       constexpr uint32_t idesc_s = idesc_f16(128, BN, 0, 0);   // A K-major, B K-major, N = 128
       constexpr uint32_t idesc_o = idesc_f16(128, TN, 0, 1);   // A (TMEM) K-major, B MN-major
       const uint32_t a_base = smem_u32(a_feat);
-      mbar_wait(&bars->a_full, 0);
-      auto issue_s = [&](int jj) {
-        const int st = jj % C::STAGES;
-        mbar_wait(&bars->full[st], (jj / C::STAGES) & 1);
-        const uint32_t bf = smem_u32(ring + st * C::STAGE_BYTES);
+      // K-major features: LBO = 128 B (K-adjacent core), SBO = KF/8*128 B (8-row groups)
+      auto issue_s = [&](int jj, uint32_t bf) {
         const uint32_t sb = tbase + (jj % NBUF) * 128;
 #pragma unroll
         for (int kk = 0; kk < KF / 16; ++kk) {
-          // K-major features: LBO = 128 B (K-adjacent core), SBO = KF/8*128 B (8-row groups)
           const uint64_t da = smem_desc(a_base + kk * 256, 128, (KF / 8) * 128);
           const uint64_t db = smem_desc(bf + kk * 256, 128, (KF / 8) * 128);
           mma_ss_warp(sb, da, db, idesc_s, kk > 0 ? 1u : 0u);
         }
+        if (jj >= NBUF) CIQ_STAMP(8, jj - NBUF);
         mma_commit_warp(&bars->s_full[jj % NBUF]);
       };
-      auto issue_kv = [&](int jj) {
+      mbar_wait(&bars->a_full, 0);
+      for (int jj = 0; jj < npro; ++jj) issue_s(jj, a_base + (1 + jj) * C::FEAT_BYTES);
+      const bool probe = kTrace && args.dbg_clk != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
+      // Per tile jj: wait stage jj + K(jj); KV(jj) first half; then the previous stage's S(jj+2)
+      // (it overwrites buffer (jj-1)%3, whose KV(jj-1) is already issued) and its release; then
+      // KV(jj) second half.  The waits of tile jj+1 thus run while the tensor queue still holds
+      // the second half of KV(jj), instead of while it drains.
+      for (int jj = 0; jj < njt; ++jj) {
         const int b = jj % NBUF;
+        const int st = jj % C::STAGES;
+        const uint32_t sbase = smem_u32(ring + st * C::STAGE_BYTES);
+        CIQ_STAMP(1, jj);
+        mbar_wait(&bars->full[st], (jj / C::STAGES) & 1);
+        CIQ_STAMP(3, jj);
         mbar_wait(&bars->k_full[b], (jj / NBUF) & 1);
+        CIQ_STAMP(2, jj);
         fence_after_sync();
-        const int st = jj % C::STAGES;   // already full: S(jj) was issued from it
-        const uint32_t vh_s = smem_u32(ring + st * C::STAGE_BYTES + C::FEAT_BYTES);
-        const uint32_t vl_s = vh_s + C::V_BYTES;
         const uint32_t kb = tbase + b * 128;
         const uint32_t o = tbase + TM_O;
-        const uint64_t dvh0 = smem_desc(vh_s, (TN / 8) * 128, 128);
-        const uint64_t dvl0 = smem_desc(vl_s, (TN / 8) * 128, 128);
-        if (!(args.dbg & 1)) {
+        const uint64_t dvh0 = smem_desc(sbase, (TN / 8) * 128, 128);
+        const uint64_t dvl0 = smem_desc(sbase + C::V_BYTES, (TN / 8) * 128, 128);
+        auto kv_half = [&](int h) {
+          if (args.dbg & 1) return;
+          uint32_t kh[4], kl[4];
+          uint64_t vhd[4], vld[4];
 #pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) {
+          for (int s4 = 0; s4 < 4; ++s4) {
+            const int kk = 4 * h + s4;
             // K tile in place of S: chunk c = kk/2 holds k_hi pairs at [32c, 32c+16), k_lo at +16
-            const uint32_t kh = kb + 32 * (kk >> 1) + 8 * (kk & 1);
-            const uint32_t kl = kh + 16;
+            kh[s4] = kb + 32 * (kk >> 1) + 8 * (kk & 1);
+            kl[s4] = kh[s4] + 16;
             // V: K-step of 16 rows j = 2 core-matrix rows along K (start address advances by
             // 2 * TN/8 * 128 B; descriptor start field is in 16-byte units)
             const uint64_t koff = (uint64_t)((kk * 2 * (TN / 8) * 128) >> 4);
-            mma_ts_warp(o, kh, dvh0 + koff, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
-            mma_ts_warp(o, kh, dvl0 + koff, idesc_o, 1u);
-            mma_ts_warp(o, kl, dvh0 + koff, idesc_o, 1u);
+            vhd[s4] = dvh0 + koff;
+            vld[s4] = dvl0 + koff;
           }
+          mma_ts_split4_warp(o, kh, kl, vhd, vld, idesc_o, (jj > 0 || h > 0) ? 1u : 0u);
+        };
+        kv_half(0);
+        if (jj > 0) {
+          const int pst = (jj - 1) % C::STAGES;
+          // S(jj+2) overwrites buffer (jj-1)%3, read by KV(jj-1): tcgen05.mma instructions of one
+          // thread execute in issue order, so no wait is needed.
+          if (jj + 2 < njt) issue_s(jj + 2, smem_u32(ring + pst * C::STAGE_BYTES) + 2 * C::V_BYTES);
+          if (probe) mma_commit_warp(&bars->probe_s[(jj - 1) & 1]);
+          // the stage may be refilled once every CTA of the cluster is done with it
+          if (CL == 1) mma_commit_warp(&bars->empty[pst]);
+          else mma_commit_mc_warp(&bars->empty[pst], kMask);
         }
-        mma_commit_warp(&bars->empty[st]);
-      };
-      for (int jj = 0; jj < NBUF && jj < njt; ++jj) issue_s(jj);
-      for (int jj = 0; jj < njt; ++jj) {
-        issue_kv(jj);
-        // S(jj+3) overwrites buffer jj%3, still being read by KV(jj): tcgen05.mma instructions of
-        // one thread execute in issue order, so no wait is needed (a wait here would drain the
-        // tensor pipe once per tile).
-        if (jj + NBUF < njt) issue_s(jj + NBUF);
+        kv_half(1);
+        CIQ_STAMP(9, jj);
+        if (probe) mma_commit_warp(&bars->probe_kv[jj & 1]);
+      }
+      if (njt > 0) {
+        const int pst = (njt - 1) % C::STAGES;
+        if (probe) mma_commit_warp(&bars->probe_s[(njt - 1) & 1]);
+        if (CL == 1) mma_commit_warp(&bars->empty[pst]);
+        else mma_commit_mc_warp(&bars->empty[pst], kMask);
       }
       mma_commit_warp(&bars->o_full);
     }
   } else if (warp >= EPI_WARP0) {
-    // ---------------- epilogue: 16 warps in two ping-pong groups of 8; group g exponentiates the
-    // tiles J = g (mod 2), so each SM sub-partition holds two warps on tile J and two on tile J+1
-    // whose TMEM-load / SFU / TMEM-store phases interleave.  Within a group, warp w owns TMEM lane
-    // quarter w % 4 and the 64-column half ((w - 4) / 4) % 2 (two 32-column chunks). ----
+    // ---------------- epilogue: all 16 warps on every tile; warp w owns TMEM lane quarter w % 4
+    // (rows 32q .. 32q+31) and the 32-column chunk cw = (w - 4) / 4 of the tile, so each SM
+    // sub-partition runs four warps on the same tile (the SFU stays saturated) and a tile's K is
+    // complete as early as possible -- with S three tiles ahead, the tensor pipe's KV(J) + S(J+3)
+    // turnaround hides behind the exponentiation of tiles J+1, J+2.  (Two ping-pong groups of 8
+    // warps on alternating tiles measured strictly serialised: each group waited for its S.) ----
     const int q = warp % 4;                         // TMEM lane quarter -> rows 32q .. 32q+31
-    const int grp = (warp - EPI_WARP0) / 8;         // ping-pong group
-    const int half = ((warp - EPI_WARP0) / 4) % 2;  // 64-column half of the tile
+    const int cw = (warp - EPI_WARP0) / 4;          // 32-column chunk of the tile
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    const bool trunc = (args.dbg & 1024) != 0;
-    for (int jj = grp; jj < njt; jj += 2) {
+    for (int jj = 0; jj < njt; ++jj) {
       const int b = jj % NBUF;
-      const uint32_t tb = tbase + b * 128 + lane_base + 64 * half;
-      const int64_t jcol0 = (int64_t)(jt0 + jj) * BN + 64 * half;
-      const bool tail = jcol0 + 64 > n;
+      const uint32_t tb = tbase + b * 128 + lane_base + 32 * cw;
+      const int64_t jcol0 = (int64_t)(jt0 + jj) * BN + 32 * cw;
+      const bool tail = jcol0 + 32 > n;
       mbar_wait(&bars->s_full[b], (jj / NBUF) & 1);
+      if (warp == 4) CIQ_STAMP(4, jj);
       fence_after_sync();
-      uint32_t sv0[32], sv1[32];
-      tmem_ld32(tb, sv0);
-      tmem_ld32(tb + 32, sv1);
+      uint32_t sv[32];
+      tmem_ld32(tb, sv);
       tmem_ld_wait();
-      {
-        uint32_t hi[16], lo[16];
-        if (args.dbg & 2) {
+      uint32_t hi[16], lo[16];
+      if (args.dbg & 2) {
 #pragma unroll
-          for (int m = 0; m < 16; ++m) { hi[m] = sv0[m]; lo[m] = sv0[m + 16]; }
-        } else if (tail) exp_split_chunk<KIND, true>(sv0, hi, lo, (int)(n - jcol0), trunc);
-        else exp_split_chunk<KIND, false>(sv0, hi, lo, 32, trunc);
-        tmem_st16(tb, hi);
-        tmem_st16(tb + 16, lo);
-      }
-      {
-        uint32_t hi[16], lo[16];
-        if (args.dbg & 2) {
-#pragma unroll
-          for (int m = 0; m < 16; ++m) { hi[m] = sv1[m]; lo[m] = sv1[m + 16]; }
-        } else if (tail) exp_split_chunk<KIND, true>(sv1, hi, lo, (int)(n - jcol0 - 32), trunc);
-        else exp_split_chunk<KIND, false>(sv1, hi, lo, 32, trunc);
-        tmem_st16(tb + 32, hi);
-        tmem_st16(tb + 48, lo);
-      }
+        for (int m = 0; m < 16; ++m) { hi[m] = sv[m]; lo[m] = sv[m + 16]; }
+      } else if (tail) exp_split_chunk<KIND, true>(sv, hi, lo, (int)(n - jcol0));
+      else exp_split_chunk<KIND, false>(sv, hi, lo, 32);
+      // chunk c of S -> k_hi at [32c, 32c + 16), k_lo at [32c + 16, 32c + 32)
+      tmem_st16(tb, hi);
+      tmem_st16(tb + 16, lo);
       tmem_st_wait();
       fence_before_sync();
       __syncwarp();
+      if (warp == 4) CIQ_STAMP(5, jj);
       if (lane == 0) mbar_arrive(&bars->k_full[b]);
     }
     const int c = (warp - EPI_WARP0) / 4;    // output column group for the final readout
@@ -314,7 +374,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   fence_before_sync();
-  __syncthreads();
+  // no CTA may exit while a peer can still multicast into its smem / arrive on its barriers
+  if (CL > 1) cluster_sync();
+  else __syncthreads();
   if (args.apart != nullptr) {
     for (int c = threadIdx.x; c < TN; c += NUM_THREADS) {
       double s = 0.0;
@@ -369,22 +431,42 @@ __global__ void pack_v_kernel(const float* __restrict__ v, int64_t n, int64_t np
   *reinterpret_cast<uint4*>(planes + off + plane) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
 }
 
+template <int KIND, int TN, int CL>
+cudaError_t launch_one(const TcArgs& a, cudaStream_t s) {
+  auto k = mvm_tc_kernel<KIND, TN, CL>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<TN>::SMEM);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.nblk_x, a.tp / TN);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = Cfg<TN>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, a);
+}
+
+template <int KIND, int TN>
+cudaError_t launch_cl(const TcArgs& a, cudaStream_t s) {
+  switch (a.cl) {
+    case 1: return launch_one<KIND, TN, 1>(a, s);
+    case 2: return launch_one<KIND, TN, 2>(a, s);
+    case 4: return launch_one<KIND, TN, 4>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <int KIND>
 cudaError_t launch_kind(const TcArgs& a, int tn, cudaStream_t s) {
-  dim3 grid(a.nblk_x, a.tp / tn);
   switch (tn) {
-#define CIQ_TC_CASE(TNV)                                                                                   \
-  case TNV: {                                                                                              \
-    auto k = mvm_tc_kernel<KIND, TNV>;                                                                     \
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<TNV>::SMEM);   \
-    if (e != cudaSuccess) return e;                                                                        \
-    k<<<grid, NUM_THREADS, Cfg<TNV>::SMEM, s>>>(a);                                                         \
-    return cudaGetLastError();                                                                             \
-  }
-    CIQ_TC_CASE(16)
-    CIQ_TC_CASE(32)
-    CIQ_TC_CASE(64)
-#undef CIQ_TC_CASE
+    case 16: return launch_cl<KIND, 16>(a, s);
+    case 32: return launch_cl<KIND, 32>(a, s);
+    case 64: return launch_cl<KIND, 64>(a, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -581,6 +663,15 @@ __global__ void split_dense_kernel(const float* __restrict__ k, int64_t ldk, int
 // Column chunk TN per CTA.  Capped at 64: the single smem ring needs >= NBUF + 1 = 4 stages
 // (S runs three tiles ahead of KV), which at TN = 128 would exceed shared memory; wider T is
 // handled by more chunks (the K tile is recomputed per chunk -- cheap next to the 3 GEMMs).
+int tc_cluster_size() {
+  static const int cl = [] {
+    const char* e = getenv("CIQ_TC_CLUSTER");
+    const int v = e ? atoi(e) : 1;
+    return (v == 1 || v == 2 || v == 4) ? v : 1;
+  }();
+  return cl;
+}
+
 int tc_chunk_cols(int tp) {
   if (tp % 64 == 0) return 64;
   if (tp % 32 == 0) return 32;

@@ -52,6 +52,29 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
       : "memory");
 }
 
+// Multicast variant: the same CTA-relative smem offset (data and mbarrier) in every CTA of the
+// cluster named by cta_mask receives the bytes / the complete_tx.
+__device__ __forceinline__ void bulk_g2s_mc(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar,
+                                            uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "h"(cta_mask)
+      : "memory");
+}
+
+// ---------------- clusters ----------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// all threads of every CTA of the cluster (release / acquire: smem writes and mbarrier inits
+// become visible cluster-wide)
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // ---------------- tcgen05 ----------------
 template <uint32_t NCOLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t* smem_result) {
@@ -107,10 +130,50 @@ __device__ __forceinline__ void mma_ts_warp(uint32_t d_tmem, uint32_t a_tmem, ui
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Four K-steps of the split product O (+)= K_hi.V_hi + K_hi.V_lo + K_lo.V_hi (12 MMAs) from ONE
+// warp-collective asm block: a single elect.sync for the batch instead of an ELECT / VOTEU /
+// R2UR chain per MMA (which made the MMA warp's issue latency, not the tensor pipe, the limit).
+// kh[s] / kl[s]: TMEM addresses of the K_hi / K_lo operand of step s; vh[s] / vl[s]: smem
+// descriptors of the V_hi / V_lo slab of step s; acc0: accumulate flag of the very first MMA.
+__device__ __forceinline__ void mma_ts_split4_warp(uint32_t d_tmem, const uint32_t (&kh)[4], const uint32_t (&kl)[4],
+                                                   const uint64_t (&vh)[4], const uint64_t (&vl)[4], uint32_t idesc,
+                                                   uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %18, 0;\n\t"
+      "setp.eq.b32 t, %18, %18;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %9, %17, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %13, %17, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%5], %9, %17, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %10, %17, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %14, %17, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], %10, %17, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %11, %17, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %15, %17, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %11, %17, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %12, %17, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %16, %17, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %12, %17, t;\n\t}" ::"r"(d_tmem),
+      "r"(kh[0]), "r"(kh[1]), "r"(kh[2]), "r"(kh[3]), "r"(kl[0]), "r"(kl[1]), "r"(kl[2]), "r"(kl[3]), "l"(vh[0]),
+      "l"(vh[1]), "l"(vh[2]), "l"(vh[3]), "l"(vl[0]), "l"(vl[1]), "l"(vl[2]), "l"(vl[3]), "r"(idesc), "r"(acc0)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+// ... arriving on the mbarrier at the same smem offset in every CTA of cta_mask
+__device__ __forceinline__ void mma_commit_mc_warp(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(cta_mask)
       : "memory");
 }
 
