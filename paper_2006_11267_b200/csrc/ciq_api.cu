@@ -297,6 +297,21 @@ ciq_status grow(ciq_ctx* c, T** buf, size_t* cap, size_t need) {
   return CIQ_OK;
 }
 
+// Matrix-free tensor-core MVM: the persistent 256-row kernel (mvm_tc2.cu) unless CIQ_TC_V1=1
+// selects the 128-row one (mvm_tc.cu; A/B experiments).
+bool use_tc2(const ciq_ctx* c) {
+  static const bool v1 = getenv("CIQ_TC_V1") && atoi(getenv("CIQ_TC_V1")) != 0;
+  // (every unit of the persistent kernel needs >= 4 column tiles of 64: see tc2_choose_nsplit)
+  return c->op.kind != CIQ_OP_DENSE && !v1 && c->op.n >= 256;
+}
+
+int sm_count() {
+  int nsm = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return nsm;
+}
+
 bool use_tc(const ciq_ctx* c, int impl) {
   if (impl == CIQ_MVM_SIMT) return false;
   return c->tc_ok;
@@ -336,19 +351,32 @@ int choose_nsplit_dense(int64_t rows, int64_t npad, int chunks, int nsm) {
   return best;
 }
 
+// Column splits and number of alpha-partial rows of the tensor-core MVM for tp columns.
+void mvm_geometry(const ciq_ctx* c, int tp, int* nsplit, int64_t* nblk) {
+  const int64_t rows = c->row1 - c->row0;
+  const int chunks = tp / tc_chunk_cols(tp);
+  const int nsm = sm_count();
+  if (c->op.kind == CIQ_OP_DENSE) {
+    *nsplit = choose_nsplit_dense(rows, c->npad, chunks, nsm);
+    *nblk = (rows + 127) / 128 * *nsplit;
+  } else if (use_tc2(c)) {
+    *nsplit = tc2_choose_nsplit(rows, c->op.n, chunks, nsm);
+    *nblk = (rows + 255) / 256 * *nsplit * 8;
+  } else {
+    const int cl = tc_cluster_size();
+    *nsplit = choose_nsplit(rows, c->op.n, chunks, nsm, cl);
+    *nblk = ((rows + 127) / 128 + cl - 1) / cl * cl * *nsplit;
+  }
+}
+
 // Allocate every buffer run_mvm(tp, allow_split) may need (so a CUDA-graph capture never
 // allocates).
 ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
   if (!use_tc(c, impl)) return CIQ_OK;
   const int64_t rows = c->row1 - c->row0;
-  const int tn = tc_chunk_cols(tp);
-  int nsm = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int nsplit = c->op.kind == CIQ_OP_DENSE ? choose_nsplit_dense(rows, c->npad, tp / tn, nsm)
-                                                : choose_nsplit(rows, c->op.n, tp / tn, nsm, tc_cluster_size());
-  const int cl = c->op.kind == CIQ_OP_DENSE ? 1 : tc_cluster_size();
-  const int64_t rt = ((rows + 127) / 128 + cl - 1) / cl * cl;   // row tiles, padded to whole clusters
+  int nsplit = 1;
+  int64_t nblk = 0;
+  mvm_geometry(c, tp, &nsplit, &nblk);
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
   if (st != CIQ_OK) return st;
   if (c->inv_scale_n < tp) {
@@ -361,7 +389,7 @@ ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
     st = grow(c, &c->psplit, &c->psplit_elems, (size_t)nsplit * rows * tp);
     if (st != CIQ_OK) return st;
   }
-  return grow(c, &c->apart_tc, &c->apart_tc_elems, (size_t)rt * nsplit * tp);
+  return grow(c, &c->apart_tc, &c->apart_tc_elems, (size_t)nblk * tp);
 }
 
 // P (+ alpha partials) <- K V.  With the tensor-core path the result may be split into
@@ -382,17 +410,15 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   }
   const int tn = tc_chunk_cols(tp);
   const int chunks = tp / tn;
-  int nsm = 148;
-  {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int nsm = sm_count();
   (void)allow_split;
   const bool dense = c->op.kind == CIQ_OP_DENSE;
-  const int nsplit = dense ? choose_nsplit_dense(rows, c->npad, chunks, nsm) : choose_nsplit(rows, c->op.n, chunks, nsm, tc_cluster_size());
-  const int cl = c->op.kind == CIQ_OP_DENSE ? 1 : tc_cluster_size();
-  const int64_t rt = ((rows + 127) / 128 + cl - 1) / cl * cl;   // row tiles, padded to whole clusters
+  const bool v2 = use_tc2(c);
+  int nsplit = 1;
+  int64_t nblk = 0;
+  mvm_geometry(c, tp, &nsplit, &nblk);
+  const int cl = (dense || v2) ? 1 : tc_cluster_size();
+  const int64_t rt = ((rows + 127) / 128 + cl - 1) / cl * cl;   // 128-row tiles, padded to whole clusters
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
   if (st != CIQ_OK) return st;
   if (c->inv_scale_n < tp) {
@@ -409,7 +435,7 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   }
   double* ap = apart;
   if (apart != nullptr) {
-    st = grow(c, &c->apart_tc, &c->apart_tc_elems, (size_t)rt * nsplit * tp);
+    st = grow(c, &c->apart_tc, &c->apart_tc_elems, (size_t)nblk * tp);
     if (st != CIQ_OK) return st;
     ap = c->apart_tc;
   }
@@ -442,10 +468,13 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     static const int dbg = getenv("CIQ_TC_DEBUG") ? atoi(getenv("CIQ_TC_DEBUG")) : 0;
     a.dbg = dbg;
     a.dbg_clk = nullptr;
-    if ((dbg & 128) && !dense) cudaMallocManaged(&a.dbg_clk, 12 * 256 * sizeof(long long));
-    if (a.dbg_clk) cudaMemset(a.dbg_clk, 0, 12 * 256 * sizeof(long long));
+    if ((dbg & 128) && !dense) cudaMallocManaged(&a.dbg_clk, 32 * 256 * sizeof(long long));
+    if (a.dbg_clk) cudaMemset(a.dbg_clk, 0, 32 * 256 * sizeof(long long));
   }
+  a.chunks = chunks;
+  a.nunits = v2 ? tc2_units(rows, nsplit, chunks) : 0;
   if (dense) LAUNCH(c, launch_mvm_dense_tc(a, c->stream));
+  else if (v2) LAUNCH(c, launch_mvm_tc2(a, nsm, c->stream));
   else LAUNCH(c, launch_mvm_tc(a, c->stream));
   if (a.dbg_clk) {  // experiments only: dump the per-tile timeline of CTA (0, 0)
     cudaStreamSynchronize(c->stream);
@@ -459,13 +488,20 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
       }
       fprintf(stderr, "\n");
     }
+    fprintf(stderr, "per-warp epilogue done (warps 4..19), relative to warp 4\n");
+    for (int j = 0; j < 48; ++j) {
+      fprintf(stderr, "%4d", j);
+      const long long w4 = a.dbg_clk[16 * 256 + j];
+      for (int w = 0; w < 16; ++w) fprintf(stderr, " %6lld", a.dbg_clk[(16 + w) * 256 + j] - w4);
+      fprintf(stderr, "\n");
+    }
     cudaFree(a.dbg_clk);
   }
   if (nsplit > 1 && nsplit_out == nullptr)  // caller wants the complete product in p
     LAUNCH(c, launch_sum_splits(c->psplit, nsplit, (size_t)rows * tp, rows * tp, p, c->stream));
   if (nsplit_out) *nsplit_out = nsplit;
   if (apart_used) *apart_used = ap;
-  if (apart_nblk) *apart_nblk = (int)(rt * nsplit);
+  if (apart_nblk) *apart_nblk = (int)nblk;
   c->mvm_kind_used = 2;
   return CIQ_OK;
 }
@@ -513,7 +549,8 @@ bool build_tc_features(ciq_ctx* c, const std::vector<float>& xh) {
     for (int k = 0; k < d; ++k) mean[k] += xh[i * d + k];
   for (int k = 0; k < d; ++k) mean[k] /= (double)n;
   const double sl = std::sqrt(1.4426950408889634);
-  std::vector<__half> fa((size_t)npad * 32, __float2half(0.f)), fb((size_t)npad * 32, __float2half(0.f));
+  // (+256 zero rows: the 256-row units of mvm_tc2.cu may start at any 128-aligned row < npad)
+  std::vector<__half> fa((size_t)(npad + 256) * 32, __float2half(0.f)), fb((size_t)(npad + 256) * 32, __float2half(0.f));
   std::vector<double> a(d2), b(d2);
   double hmax = 0.0;
   auto put = [&](std::vector<__half>& f, int64_t i, int kidx, double val, bool lo) {

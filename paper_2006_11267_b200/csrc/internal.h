@@ -52,6 +52,7 @@ struct TcArgs {
   int kind;
   int64_t n, npad, row0, row1;
   int tp, nsplit, nblk_x;
+  int nunits, chunks;        // persistent matrix-free kernel (mvm_tc2.cu): units = row tiles x splits x chunks
   int cl;                    // matrix-free path: CTAs per cluster along the row tiles (1, 2, 4);
                              // nblk_x = (row tiles rounded up to cl) * nsplit
   const __half* feat_a;      // [npad/8][4][8][8] A-role features (rows)
@@ -75,6 +76,10 @@ int tc_cluster_size();       // cluster size of the matrix-free kernel (env CIQ_
 cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, const double* nrm, __half* planes,
                           float* inv_scale, cudaStream_t s);
 cudaError_t launch_mvm_tc(const TcArgs& a, cudaStream_t s);
+// persistent 256-row version (mvm_tc2.cu); alpha partials: [row tiles * nsplit * 8][tp]
+int tc2_units(int64_t rows, int nsplit, int chunks);
+int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm);
+cudaError_t launch_mvm_tc2(const TcArgs& a, int nsm, cudaStream_t s);
 cudaError_t launch_mvm_dense_tc(const TcArgs& a, cudaStream_t s);
 cudaError_t launch_absmax(const float* k, int64_t ldk, int64_t rows, int64_t n, unsigned int* out, cudaStream_t s);
 cudaError_t launch_split_dense(const float* k, int64_t ldk, int64_t rows, int64_t n, int64_t npad, float scale,

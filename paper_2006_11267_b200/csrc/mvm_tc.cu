@@ -101,10 +101,14 @@ __device__ __forceinline__ void exp_split_chunk(const uint32_t (&sv)[32], uint32
       k0 = (c < jvalid) ? k0 : 0.f;
       k1 = (c + 1 < jvalid) ? k1 : 0.f;
     }
+#ifdef CIQ_EPI_TRUNC
+    split_trunc2(k0, k1, hi[c / 2], lo[c / 2]);
+#else
     const uint32_t h = pack_half2(k0, k1);
     const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
     hi[c / 2] = h;
     lo[c / 2] = pack_half2(k0 - hf.x, k1 - hf.y);
+#endif
   }
 }
 

@@ -1,0 +1,533 @@
+// mvm_tc2.cu -- the fused matrix-free kernel MVM, persistent 256-row version (SURVEY K1, §8(a)
+// row a4):  P = K(X, X) V + sigma^2 V with K never materialised in HBM.
+//
+// Why a second design (measured on B200, profiles/ncu_k1_r01b.txt and DESIGN.md §8): the 128-row
+// kernel in mvm_tc.cu streams 40 KB of V planes + column features from L2 per 128x128 tile of
+// kernel evaluations, i.e. 6.3 GB per C3 MVM; with the B200 L2 -> SM limit (~6.3 KB/clk chip-wide)
+// that alone costs ~0.5 ms, as much as the SFU (ex2) floor, and its skeleton without any exp /
+// KV work already took 0.57 ms.  Here:
+//   * a CTA unit is 256 rows (two 128-lane halves) x a column range, streamed in 64-column tiles:
+//     per 16384 kernel evaluations the CTA loads 16 KB of V planes + 4 KB of features (half);
+//   * the grid is persistent (one CTA per SM, units round-robin), so the per-CTA ramp (TMEM
+//     alloc, barrier init, first loads) and the output read-out are paid once per SM, and the
+//     stream of tiles continues across unit boundaries (the smem ring, the S look-ahead and the
+//     TMEM buffers all run over the flattened tile sequence of the CTA).
+//
+// Per tile J of a unit (rows I = 256, columns J = 64):
+//   (1) S_h = A_{I,h} . B_J^T, h = 0, 1  (tcgen05 kind::f16 SS, M=128 N=64 K=32: augmented split-fp16
+//       features, S_ij = -(log2 e / 2) ||x_i - x_j||^2 / l^2 exactly as in mvm_tc.cu);
+//   (2) 16 epilogue warps: tcgen05.ld S -> k = kernel(S) (ex2 on the SFU), masked past N ->
+//       split k = k_hi + k_lo (fp16) -> tcgen05.st in place (chunk c -> hi at [32c, 32c+16),
+//       lo at [32c+16, 32c+32));
+//   (3) O_h += K_h . V_J (TS: A from TMEM, B = V_J MN-major): k_hi.v_hi + k_hi.v_lo + k_lo.v_hi.
+// TMEM (512 columns): S/K buffers b = 0..2 at [128 b, 128 b + 128) (half h at +64 h), O_h at
+// 384 + TN h.  S runs three tiles ahead of KV.
+// Smem: A features of the unit (256 rows, double-buffered across units), features of the first
+// three tiles, and a ring whose stage g holds V(g) and the column features of tile g+3 (skewed:
+// one stage wait / release per tile on the MMA warp).
+// The output read-out of unit k is done by the epilogue warps right after they finish the first
+// tile of unit k+1 (O is drained to registers, released, then written with plain stores).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+#include "tc_util.cuh"
+
+namespace ciq {
+namespace {
+
+using namespace tc;
+
+constexpr int BM2 = 256;            // rows per unit (two 128-lane halves)
+constexpr int BN2 = 64;             // columns per tile
+constexpr int KF2 = 32;             // feature contraction
+constexpr int NT2 = 640;            // 4 role warps + 16 epilogue warps
+constexpr int EPI0 = 4;
+constexpr int NB2 = 3;              // S/K TMEM buffers
+constexpr int TMO = NB2 * 128;      // O accumulators at [384, 384 + 2 TN)
+#ifdef CIQ_NO_PINGPONG
+constexpr bool kPingPong = false;
+#else
+constexpr bool kPingPong = true;   // measured: 0.937 vs 1.088 ms per C3 MVM (profiles/)
+#endif
+constexpr int EPI_ARRIVALS = kPingPong ? 4 : 8;    // epilogue warps per tile and half
+constexpr int RO_ARRIVALS = 8;                      // warps reading out O_h (either mode)
+
+template <int TN>
+struct Cfg2 {
+  static constexpr int A_BYTES = BM2 * KF2 * 2;      // 16 KB
+  static constexpr int F_BYTES = BN2 * KF2 * 2;      // 4 KB
+  static constexpr int V_BYTES = BN2 * TN * 2;       // one plane of one tile
+  static constexpr int STAGE = 2 * V_BYTES + F_BYTES;
+  static constexpr int STAGES = 8;
+  static constexpr int RING_OFF = 2 * A_BYTES + NB2 * F_BYTES;
+  static constexpr int SMEM = 1024 + RING_OFF + STAGES * STAGE + 1024;
+};
+static_assert(Cfg2<64>::SMEM <= 227 * 1024, "shared memory budget");
+
+struct Bars2 {
+  uint64_t full[8], empty[8];              // smem ring (empty: one commit per MMA warp)
+  uint64_t s_full[NB2][2], k_full[NB2][2];   // per TMEM buffer and 128-row half
+  uint64_t a_full[2], a_empty[2];
+  uint64_t pro_full, o_full[2], o_empty[2];
+  uint32_t tmem_base;
+};
+
+// Position in the flattened tile sequence of one CTA: unit u (local index k), tile jj of njt.
+struct Cur {
+  int k, u, jj, njt, jt0, split, chunk, rt;
+  CIQ_DEVICE void decode(const TcArgs& a, int ntiles) {
+    chunk = u % a.chunks;
+    const int t = u / a.chunks;
+    split = t % a.nsplit;
+    rt = t / a.nsplit;
+    jt0 = ntiles * split / a.nsplit;          // ntiles * nsplit < 2^31 (checked on the host)
+    njt = ntiles * (split + 1) / a.nsplit - jt0;
+  }
+  CIQ_DEVICE void start(const TcArgs& a, int ntiles) {
+    k = 0;
+    u = blockIdx.x;
+    jj = 0;
+    if (u < a.nunits) decode(a, ntiles);
+  }
+  CIQ_DEVICE bool valid(const TcArgs& a) const { return u < a.nunits; }
+  CIQ_DEVICE void advance(const TcArgs& a, int ntiles) {
+    if (++jj == njt) {
+      jj = 0;
+      ++k;
+      u += gridDim.x;
+      if (u < a.nunits) decode(a, ntiles);
+    }
+  }
+  CIQ_DEVICE int J() const { return jt0 + jj; }
+};
+
+CIQ_DEVICE bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t@p mov.u32 %0, 1;\n\t}" : "+r"(pred));
+  return pred != 0;
+}
+
+CIQ_DEVICE void commit_one(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+CIQ_DEVICE uint64_t shfl64(uint64_t v) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, 0), hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), 0);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+template <int KIND>
+CIQ_DEVICE float kern(float s) {
+  // s = -(log2 e / 2) r^2
+  if (KIND == 1) return ex2_approx(s);
+  const float r = sqrtf(fmaxf(0.f, -1.3862943611198906f * s));  // r^2 = -2 ln2 s
+  if (KIND == 2) {
+    const float a = 2.2360679774997896f * r;
+    return (1.f + a + a * a * (1.f / 3.f)) * ex2_approx(-1.4426950408889634f * a);
+  }
+  const float a = 1.7320508075688772f * r;
+  return (1.f + a) * ex2_approx(-1.4426950408889634f * a);
+}
+
+template <int KIND, bool MASK>
+CIQ_DEVICE void exp_split(const uint32_t (&sv)[32], uint32_t (&hi)[16], uint32_t (&lo)[16], int jvalid) {
+#pragma unroll
+  for (int c = 0; c < 32; c += 2) {
+    float k0 = kern<KIND>(__uint_as_float(sv[c]));
+    float k1 = kern<KIND>(__uint_as_float(sv[c + 1]));
+    if (MASK) {
+      k0 = (c < jvalid) ? k0 : 0.f;
+      k1 = (c + 1 < jvalid) ? k1 : 0.f;
+    }
+#ifdef CIQ_EPI_TRUNC
+    split_trunc2(k0, k1, hi[c / 2], lo[c / 2]);
+#else
+    const uint32_t h = pack_half2(k0, k1);
+    const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
+    hi[c / 2] = h;
+    lo[c / 2] = pack_half2(k0 - hf.x, k1 - hf.y);
+#endif
+  }
+}
+
+// S(J) of one 128-row half: two SS MMAs (K-steps of 16 over the K = 32 feature contraction),
+// issued by one elected thread.  d: TMEM columns of the half; da: A descriptor of the half's rows;
+// db: column features of the tile.  K-step: +256 B = +16 in descriptor units.
+CIQ_DEVICE void mma_s2(uint32_t d, uint64_t da, uint64_t db, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred t, f;\n\t.reg .b64 a1, b1;\n\t"
+      "setp.ne.b32 t, %3, 0;\n\t"
+      "setp.eq.b32 f, %3, 0;\n\t"
+      "add.s64 a1, %1, 16;\n\t"
+      "add.s64 b1, %2, 16;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, f;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t}" ::"r"(d),
+      "l"(da), "l"(db), "r"(idesc)
+      : "memory");
+}
+
+// KV(J) of one half: O_h (+)= K_h . V_J, 4 K-steps x (k_hi.v_hi, k_hi.v_lo, k_lo.v_hi) = 12 TS MMAs,
+// issued by one elected thread; all operands are immediates off three uniform bases, so the
+// compiler emits ~2 uniform-datapath instructions per MMA.  o: TMEM O of the half; kb: TMEM K
+// buffer of the half (K-step s -> k_hi at 32 (s/2) + 8 (s%2), k_lo at +16); dv: V_hi descriptor of
+// the stage (V_lo at +8 TN, K-step s at +2 TN s in descriptor units); acc: accumulate into O.
+template <int TN>
+CIQ_DEVICE void mma_kv12(uint32_t o, uint32_t kb, uint64_t dv, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, t;\n\t.reg .b32 h<4>, l<4>;\n\t.reg .b64 vh<4>, vl<4>;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, %4, %4;\n\t"
+      "add.u32 h0, %1, 0;\n\t add.u32 h1, %1, 8;\n\t add.u32 h2, %1, 32;\n\t add.u32 h3, %1, 40;\n\t"
+      "add.u32 l0, %1, 16;\n\t add.u32 l1, %1, 24;\n\t add.u32 l2, %1, 48;\n\t add.u32 l3, %1, 56;\n\t"
+      "add.s64 vh0, %2, 0;\n\t add.s64 vh1, %2, %5;\n\t add.s64 vh2, %2, %6;\n\t add.s64 vh3, %2, %7;\n\t"
+      "add.s64 vl0, %2, %8;\n\t add.s64 vl1, %2, %9;\n\t add.s64 vl2, %2, %10;\n\t add.s64 vl3, %2, %11;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h0], vh0, %3, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h0], vl0, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [l0], vh0, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], vh1, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], vl1, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [l1], vh1, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], vh2, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], vl2, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [l2], vh2, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], vh3, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], vl3, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [l3], vh3, %3, t;\n\t}" ::"r"(o),
+      "r"(kb), "l"(dv), "r"(idesc), "r"(acc), "n"(2 * TN), "n"(4 * TN), "n"(6 * TN), "n"(8 * TN),
+      "n"(10 * TN), "n"(12 * TN), "n"(14 * TN)
+      : "memory");
+}
+
+// experiments only: per-tile clock64 stamps of CTA 0 (build with CIQ_TC_TRACE, run with
+// CIQ_TC_DEBUG=128; same slots as mvm_tc.cu)
+#ifdef CIQ_TC_TRACE
+#define T2_STAMP(slot, idx)                                                                  \
+  do {                                                                                       \
+    if (args.dbg_clk != nullptr && blockIdx.x == 0 && lane == 0 && (idx) < 256)              \
+      args.dbg_clk[(slot) * 256 + (idx)] = clock64();                                        \
+  } while (0)
+#else
+#define T2_STAMP(slot, idx) \
+  do {                      \
+  } while (0)
+#endif
+
+template <int KIND, int TN>
+__global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
+  using C = Cfg2<TN>;
+  if (args.done != nullptr && args.done->done) return;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* abuf = smem;                                  // [2][A_BYTES]
+  uint8_t* pro = smem + 2 * C::A_BYTES;                  // [3][F_BYTES]
+  uint8_t* ring = smem + C::RING_OFF;
+  Bars2* bars = reinterpret_cast<Bars2*>(ring + C::STAGES * C::STAGE);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t n = args.n;
+  const int ntiles = (int)((n + BN2 - 1) / BN2);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 2); }
+    for (int b = 0; b < NB2; ++b)
+      for (int h = 0; h < 2; ++h) { mbar_init(&bars->s_full[b][h], 1); mbar_init(&bars->k_full[b][h], EPI_ARRIVALS); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&bars->a_full[b], 1); mbar_init(&bars->a_empty[b], 2); }
+    mbar_init(&bars->pro_full, 1);
+    for (int h = 0; h < 2; ++h) { mbar_init(&bars->o_full[h], 1); mbar_init(&bars->o_empty[h], RO_ARRIVALS); }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tbase = bars->tmem_base;
+  const size_t plane = (size_t)args.npad * TN;   // one plane of one chunk
+
+  if (warp == 0) {
+    // ---------------- producer (one thread) ----------------
+    if (lane == 0) {
+      Cur c, f;
+      c.start(args, ntiles);
+      if (c.valid(args)) {
+        // prologue: A rows of unit 0 and the column features of its first three tiles (njt >= 4)
+        const int64_t i0 = args.row0 + (int64_t)c.rt * BM2;
+        mbar_arrive_expect_tx(&bars->a_full[0], C::A_BYTES);
+        bulk_g2s(abuf, args.feat_a + (size_t)i0 * KF2, C::A_BYTES, &bars->a_full[0]);
+        const int npro = c.njt < NB2 ? c.njt : NB2;
+        mbar_arrive_expect_tx(&bars->pro_full, npro * C::F_BYTES);
+        for (int i = 0; i < npro; ++i)
+          bulk_g2s(pro + i * C::F_BYTES, args.feat_b + (size_t)(c.jt0 + i) * BN2 * KF2, C::F_BYTES, &bars->pro_full);
+        f = c;
+        for (int i = 0; i < NB2; ++i) f.advance(args, ntiles);
+      }
+      for (int g = 0; c.valid(args); ++g) {
+        const bool fv = f.valid(args);
+        if (fv && f.jj == 0 && f.k > 0) {   // S of unit f.k starts with tile g+3: its A rows
+          const int kb = f.k & 1;
+          mbar_wait_backoff(&bars->a_empty[kb], ((f.k >> 1) & 1) ^ 1);
+          const int64_t i0 = args.row0 + (int64_t)f.rt * BM2;
+          mbar_arrive_expect_tx(&bars->a_full[kb], C::A_BYTES);
+          bulk_g2s(abuf + kb * C::A_BYTES, args.feat_a + (size_t)i0 * KF2, C::A_BYTES, &bars->a_full[kb]);
+        }
+        const int st = g % C::STAGES;
+        mbar_wait_backoff(&bars->empty[st], ((g / C::STAGES) & 1) ^ 1);
+        T2_STAMP(0, g);
+        uint8_t* sb = ring + st * C::STAGE;
+        mbar_arrive_expect_tx(&bars->full[st], 2 * C::V_BYTES + (fv ? C::F_BYTES : 0));
+        const __half* vh = args.vplanes + (size_t)c.chunk * 2 * plane + (size_t)c.J() * BN2 * TN;
+        bulk_g2s(sb, vh, C::V_BYTES, &bars->full[st]);
+        bulk_g2s(sb + C::V_BYTES, vh + plane, C::V_BYTES, &bars->full[st]);
+        if (fv) bulk_g2s(sb + 2 * C::V_BYTES, args.feat_b + (size_t)f.J() * BN2 * KF2, C::F_BYTES, &bars->full[st]);
+        c.advance(args, ntiles);
+        if (fv) f.advance(args, ntiles);
+      }
+    }
+  } else if (warp == 1 || warp == 2) {
+    // ---------------- MMA issuers: warp 1 (SM sub-partition 1) owns the rows of half 0, warp 2
+    // (sub-partition 2) those of half 1 -- S_h, KV_h and O_h are independent, and each issuer shares
+    // its sub-partition with ex2-bound epilogue warps, so the issue work is split between two.
+    // Kept lean: ring / buffer indices and phase bits are counters; each MMA batch is one asm with
+    // immediates off warp-uniform bases, issued by an elected thread. ----------------
+    const int h = warp - 1;
+    constexpr uint32_t idesc_s = idesc_f16(128, BN2, 0, 0);   // A, B K-major, N = 64
+    constexpr uint32_t idesc_o = idesc_f16(128, TN, 0, 1);    // A (TMEM) K-major, B MN-major
+    Cur kv, s;
+    kv.start(args, ntiles);
+    s = kv;
+    // K-major features: LBO = 128 B (K-adjacent core), SBO = KF/8 * 128 B (8-row groups);
+    // V planes MN-major: LBO = TN/8 * 128 B, SBO = 128 B.
+    const uint64_t da0 = smem_desc(smem_u32(abuf) + h * (C::A_BYTES / 2), 128, (KF2 / 8) * 128);
+    const uint64_t dpro = smem_desc(smem_u32(pro), 128, (KF2 / 8) * 128);
+    const uint64_t dring_f = smem_desc(smem_u32(ring) + 2 * C::V_BYTES, 128, (KF2 / 8) * 128);
+    const uint64_t dring_v = smem_desc(smem_u32(ring), (TN / 8) * 128, 128);
+    const uint32_t tb_h = tbase + 64 * h;         // half h of every S / K buffer
+    const uint32_t to_h = tbase + TMO + TN * h;   // O_h
+    if (kv.valid(args)) {
+      mbar_wait(&bars->a_full[0], 0);
+      mbar_wait(&bars->pro_full, 0);
+      fence_after_sync();
+      for (int i = 0; i < NB2 && s.valid(args) && s.k == 0; ++i) {
+        const uint32_t d = __shfl_sync(0xffffffffu, tb_h + i * 128, 0);
+        const uint64_t db = shfl64(dpro + (uint64_t)((i * C::F_BYTES) >> 4));
+        const bool last = s.jj == s.njt - 1;
+        if (elect_one()) {
+          mma_s2(d, da0, db, idesc_s);
+          commit_one(&bars->s_full[i][h]);
+          if (last) commit_one(&bars->a_empty[0]);
+        }
+        __syncwarp();
+        s.advance(args, ntiles);
+      }
+    }
+    int st = 0, b = 0;
+    uint32_t ph_st = 0, ph_b = 0;
+    for (int g = 0; kv.valid(args); ++g) {
+      if (h == 0) T2_STAMP(1, g);
+      mbar_wait(&bars->full[st], ph_st);
+      if (h == 0) T2_STAMP(3, g);
+      mbar_wait(&bars->k_full[b][h], ph_b);
+      if (h == 0) T2_STAMP(2, g);
+      if (kv.jj == 0 && kv.k > 0) mbar_wait(&bars->o_empty[h], (kv.k - 1) & 1);
+      fence_after_sync();
+      const uint32_t soff16 = (uint32_t)((st * C::STAGE) >> 4);
+      // __shfl_sync(.., 0): values the compiler treats as warp-uniform (uniform registers, no
+      // per-MMA R2UR / VOTEU in the issue sequence)
+      const uint32_t kbu = __shfl_sync(0xffffffffu, tb_h + b * 128, 0);
+      const uint64_t dvu = shfl64(dring_v + soff16);
+      const uint32_t accu = __shfl_sync(0xffffffffu, kv.jj > 0 ? 1u : 0u, 0);
+      const bool olast = kv.jj == kv.njt - 1;
+      if (elect_one()) {
+        if (!(args.dbg & 1)) mma_kv12<TN>(to_h, kbu, dvu, idesc_o, accu);
+        if (olast) commit_one(&bars->o_full[h]);
+      }
+      __syncwarp();
+      if (h == 0) T2_STAMP(9, g);
+      if (s.valid(args)) {   // S(g+3): its features are in stage g (skewed ring); buffer b is free
+        const int kb = s.k & 1;
+        if (s.jj == 0) mbar_wait(&bars->a_full[kb], (s.k >> 1) & 1);
+        const uint64_t dau = shfl64(da0 + (uint64_t)(kb * (C::A_BYTES >> 4)));
+        const uint64_t dfu = shfl64(dring_f + soff16);
+        const bool last = s.jj == s.njt - 1;
+        if (elect_one()) {
+          mma_s2(kbu, dau, dfu, idesc_s);
+          commit_one(&bars->s_full[b][h]);
+          if (last) commit_one(&bars->a_empty[kb]);
+        }
+        __syncwarp();
+        if (h == 0) T2_STAMP(8, g);
+        s.advance(args, ntiles);
+      }
+      if (elect_one()) commit_one(&bars->empty[st]);
+      __syncwarp();
+      kv.advance(args, ntiles);
+      if (++st == C::STAGES) { st = 0; ph_st ^= 1; }
+      if (++b == NB2) { b = 0; ph_b ^= 1; }
+    }
+  } else if (warp >= EPI0) {
+    // ---------------- epilogue: 16 warps; warp w works on TMEM lane quarter q = w % 4.
+    // kPingPong: two groups of 8 warps take alternate tiles (group = (w - 4) / 8), warp covers half
+    // h = ((w - 4) / 4) % 2, both 32-column chunks -- while one group sits in its TMEM load / store /
+    // barrier latencies the other keeps the SFU busy.  Otherwise all 16 warps share every tile:
+    // half (w - 4) / 8, chunk ((w - 4) / 4) % 2. ----------------
+    const int q = warp % 4;
+    const int grp = kPingPong ? (warp - EPI0) >> 3 : 0;
+    const int h = kPingPong ? ((warp - EPI0) >> 2) & 1 : (warp - EPI0) >> 3;
+    const int cc0 = kPingPong ? 0 : ((warp - EPI0) >> 2) & 1;
+    constexpr int NCH = kPingPong ? 2 : 1;      // 32-column chunks per warp per tile
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    Cur c, prev;
+    c.start(args, ntiles);
+    prev = c;
+    // read-out column half of O_h: the chunk (without ping-pong) or the group (with it: both groups
+    // read out every unit, each after the first tile it takes in the next unit)
+    const int ro = kPingPong ? grp : cc0;
+    auto readout = [&](const Cur& u) {
+      // O_h columns [ro * CPW, +CPW) of rows 32 q + lane of half h
+      constexpr int CPW = TN / 2;
+      uint32_t o[CPW];
+      mbar_wait(&bars->o_full[h], u.k & 1);
+      fence_after_sync();
+      const uint32_t ta = tbase + TMO + TN * h + ro * CPW + lane_base;
+#pragma unroll
+      for (int m = 0; m < CPW; m += 8) tmem_ld8(ta + m, &o[m]);
+      tmem_ld_wait();
+      fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->o_empty[h]);
+      const int64_t i = args.row0 + (int64_t)u.rt * BM2 + 128 * h + 32 * q + lane;
+      const bool row_ok = i < args.row1;
+      const int col0 = u.chunk * TN + ro * CPW;
+      float* pout = args.p + (size_t)u.split * args.p_split_stride + (size_t)(i - args.row0) * args.tp + col0;
+      const float* vrow = args.v + (size_t)i * args.tp + col0;
+      double* ap = args.apart ? args.apart + ((size_t)(u.rt * args.nsplit + u.split) * 8 + q * 2 + h) * args.tp + col0
+                              : nullptr;
+#pragma unroll
+      for (int m = 0; m < CPW; m += 4) {
+        float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f), r4 = v4;
+        if (row_ok) {
+          v4 = *reinterpret_cast<const float4*>(vrow + m);
+          r4.x = args.o2 * __uint_as_float(o[m + 0]) * args.inv_scale[col0 + m + 0];
+          r4.y = args.o2 * __uint_as_float(o[m + 1]) * args.inv_scale[col0 + m + 1];
+          r4.z = args.o2 * __uint_as_float(o[m + 2]) * args.inv_scale[col0 + m + 2];
+          r4.w = args.o2 * __uint_as_float(o[m + 3]) * args.inv_scale[col0 + m + 3];
+          if (u.split == 0) {
+            r4.x = fmaf(args.diag, v4.x, r4.x); r4.y = fmaf(args.diag, v4.y, r4.y);
+            r4.z = fmaf(args.diag, v4.z, r4.z); r4.w = fmaf(args.diag, v4.w, r4.w);
+          }
+          *reinterpret_cast<float4*>(pout + m) = r4;
+        }
+        if (ap != nullptr) {
+          const float pv[4] = {v4.x * r4.x, v4.y * r4.y, v4.z * r4.z, v4.w * r4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float sum = warp_sum(pv[e]);
+            if (lane == 0) ap[m + e] = (double)sum;
+          }
+        }
+      }
+    };
+    int b = 0;
+    uint32_t ph_b = 0;
+    int g = 0;
+    for (; c.valid(args); ++g) {
+      if (!kPingPong || (g & 1) == grp) {
+        mbar_wait(&bars->s_full[b][h], ph_b);
+        if (warp == 4) T2_STAMP(4, g);
+        fence_after_sync();
+#pragma unroll 1
+        for (int ch = 0; ch < NCH; ++ch) {
+          const int cc = cc0 + ch;
+          const uint32_t tb = tbase + b * 128 + 64 * h + 32 * cc + lane_base;
+          const int64_t jcol0 = (int64_t)c.J() * BN2 + 32 * cc;
+          uint32_t sv[32];
+          tmem_ld32(tb, sv);
+          tmem_ld_wait();
+          uint32_t hi[16], lo[16];
+          if (args.dbg & 2) {
+#pragma unroll
+            for (int m = 0; m < 16; ++m) { hi[m] = sv[m]; lo[m] = sv[m + 16]; }
+          } else if (jcol0 + 32 > n) {
+            exp_split<KIND, true>(sv, hi, lo, (int)(n - jcol0));
+          } else {
+            exp_split<KIND, false>(sv, hi, lo, 32);
+          }
+          tmem_st16(tb, hi);
+          tmem_st16(tb + 16, lo);
+        }
+        tmem_st_wait();
+        fence_before_sync();
+        __syncwarp();
+        if (warp == 4) T2_STAMP(5, g);
+        if (warp == 19) T2_STAMP(6, g);
+        T2_STAMP(16 + warp - EPI0, g);
+        if (lane == 0) mbar_arrive(&bars->k_full[b][h]);
+        // first tile this warp takes in unit k: unit k-1 is complete (its last KV is issued)
+        if (c.k > 0 && c.k != prev.k) readout(prev);
+        prev = c;
+      }
+      c.advance(args, ntiles);
+      if (++b == NB2) { b = 0; ph_b ^= 1; }
+    }
+    if (prev.valid(args)) readout(prev);
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after_sync();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+template <int KIND, int TN>
+cudaError_t launch2(const TcArgs& a, int grid, cudaStream_t s) {
+  auto k = mvm_tc2_kernel<KIND, TN>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<TN>::SMEM);
+  if (e != cudaSuccess) return e;
+  k<<<grid, NT2, Cfg2<TN>::SMEM, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int KIND>
+cudaError_t launch2_kind(const TcArgs& a, int tn, int grid, cudaStream_t s) {
+  switch (tn) {
+    case 16: return launch2<KIND, 16>(a, grid, s);
+    case 32: return launch2<KIND, 32>(a, grid, s);
+    case 64: return launch2<KIND, 64>(a, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+int tc2_units(int64_t rows, int nsplit, int chunks) { return (int)((rows + BM2 - 1) / BM2) * nsplit * chunks; }
+
+// Column splits of the unit grid: enough units for the persistent CTAs to finish together
+// (max units per CTA x tiles per unit minimal), each split keeping >= 4 column tiles.
+int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm) {
+  const int64_t nrt = (rows + BM2 - 1) / BM2;
+  const int64_t ntiles = (n + BN2 - 1) / BN2;
+  int best = 1;
+  double best_cost = 1e300;
+  for (int s = 1; s <= 16; ++s) {
+    if (ntiles / s < 4) break;
+    const int64_t units = nrt * chunks * s;
+    const int64_t per_cta = (units + nsm - 1) / nsm;
+    const double cost = (double)per_cta * (double)((ntiles + s - 1) / s) * (1.0 + 0.002 * s);
+    if (cost < best_cost * 0.995) { best_cost = cost; best = s; }
+  }
+  return best;
+}
+
+cudaError_t launch_mvm_tc2(const TcArgs& a, int nsm, cudaStream_t s) {
+  const int tn = tc_chunk_cols(a.tp);
+  const int grid = a.nunits < nsm ? a.nunits : nsm;
+  switch (a.kind) {
+    case 1: return launch2_kind<1>(a, tn, grid, s);
+    case 2: return launch2_kind<2>(a, tn, grid, s);
+    case 3: return launch2_kind<3>(a, tn, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace ciq

@@ -39,9 +39,35 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// ... with a suspend-time hint (ns): the waiting warp sleeps until the phase completes (or the hint
+// expires) instead of re-polling, so a waiting warp issues no SYNCS/BRA traffic.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+      : "memory");
+  return ok != 0;
+}
+// Polling with a nanosleep back-off, for waiters off the critical path (the bulk-copy producer):
+// a spinning try_wait loop issues SYNCS / BRA through the MIO queue of its SM sub-partition,
+// which the ex2-bound epilogue warps of that sub-partition need (measured: profiles/).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+#ifndef CIQ_NO_BACKOFF
+    __nanosleep(64);
+#endif
+  }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef CIQ_WAIT_HINT
+  while (!mbar_try_wait_hint(bar, parity)) {
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // ---------------- bulk copy global -> shared (TMA engine, non-tensor) ----------------
@@ -201,6 +227,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
@@ -237,6 +268,21 @@ __host__ __device__ constexpr uint32_t idesc_f16(uint32_t M, uint32_t N, uint32_
 __device__ __forceinline__ uint32_t pack_half2(float lo_elem, float hi_elem) {
   __half2 h = __floats2half2_rn(lo_elem, hi_elem);  // .x = first argument (low 16 bits)
   return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// k -> (k_hi, k_lo) split of two values by truncation: k_hi = k with the low 13 mantissa bits
+// cleared (exact in fp16), k_lo = k - k_hi (exact in fp32, one packed FADD2), both packed to
+// fp16x2: 2 LOP3 + 1 FADD2 + 2 F2FP per pair.
+__device__ __forceinline__ void split_trunc2(float k0, float k1, uint32_t& hi, uint32_t& lo) {
+  const uint32_t h0 = __float_as_uint(k0) & 0xFFFFE000u, h1 = __float_as_uint(k1) & 0xFFFFE000u;
+  uint64_t ra, rb, rd;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(k0), "f"(k1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "r"(h0), "r"(h1));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+  float d0, d1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(rd));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(__uint_as_float(h1)), "f"(__uint_as_float(h0)));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(d1), "f"(d0));
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
