@@ -361,6 +361,8 @@ void mvm_geometry(const ciq_ctx* c, int tp, int* nsplit, int64_t* nblk) {
     *nblk = (rows + 127) / 128 * *nsplit;
   } else if (use_tc2(c)) {
     *nsplit = tc2_choose_nsplit(rows, c->op.n, chunks, nsm);
+    static const int force = getenv("CIQ_TC_NSPLIT") ? atoi(getenv("CIQ_TC_NSPLIT")) : 0;   // experiments
+    if (force > 0) *nsplit = force;
     *nblk = (rows + 255) / 256 * *nsplit * 8;
   } else {
     const int cl = tc_cluster_size();
@@ -485,6 +487,16 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
       for (int sl = 0; sl < 11; ++sl) {
         const long long v = a.dbg_clk[sl * 256 + j];
         fprintf(stderr, " %9lld", v ? v - t0 : -1LL);
+      }
+      fprintf(stderr, "\n");
+    }
+    fprintf(stderr, "tile  k0(MMA h0)  kv_iss  s_iss | w4: wait0 s_ok done | w12: wait0 s_ok done   (relative to t0)\n");
+    for (int j = 0; j < 64; ++j) {
+      const int sl[9] = {2, 9, 8, 10, 4, 5, 11, 12, 13};
+      fprintf(stderr, "%4d", j);
+      for (int k = 0; k < 9; ++k) {
+        const long long v = a.dbg_clk[sl[k] * 256 + j];
+        fprintf(stderr, " %8lld", v ? v - t0 : -1LL);
       }
       fprintf(stderr, "\n");
     }
