@@ -398,7 +398,7 @@ ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
 // `*nsplit_out` partial products (stride rows*tp) when allow_split; otherwise it is complete.
 ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, const Ctrl* done, int impl,
                    const double* nrm = nullptr, bool allow_split = false, int* nsplit_out = nullptr,
-                   double** apart_used = nullptr, int* apart_nblk = nullptr) {
+                   double** apart_used = nullptr, int* apart_nblk = nullptr, bool skip_pack = false) {
   const int64_t rows = c->row1 - c->row0;
   if (nsplit_out) *nsplit_out = 1;
   if (!use_tc(c, impl)) {
@@ -441,7 +441,8 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     if (st != CIQ_OK) return st;
     ap = c->apart_tc;
   }
-  LAUNCH(c, launch_pack_v(v, c->op.n, c->npad, tp, nrm, c->planes, c->inv_scale, c->stream));
+  // (skip_pack: the previous streaming pass already wrote v's split planes and inv_scale)
+  if (!skip_pack) LAUNCH(c, launch_pack_v(v, c->op.n, c->npad, tp, nrm, c->planes, c->inv_scale, c->stream));
   TcArgs a{};
   a.kind = c->op.kind;
   a.n = c->op.n;
@@ -1188,6 +1189,15 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     *nbm = uapply_blocks(rows);
     return CIQ_OK;
   };
+  // single GPU, tensor-core MVM: the streaming pass of iteration j writes W_{j+1}'s split-fp16
+  // planes (scale from nrm_j), so no iteration packs; W_1's planes are written here, outside the
+  // captured graph (graph replays and direct launches then run identical kernels)
+  const bool fuse_pack = c->world == 1 && !P.on && use_tc(c, p.mvm_impl) && getenv("CIQ_NO_FUSED_PACK") == nullptr;
+  if (fuse_pack) {
+    st = prepare_mvm_buffers(c, tp, p.mvm_impl);
+    if (st != CIQ_OK) return st;
+    LAUNCH(c, launch_pack_v(ws.w[1], c->op.n, c->npad, tp, sc.nrm_cur, c->planes, c->inv_scale, s));
+  }
   auto enqueue_iter = [&](int j) -> ciq_status {
     float* wcur = ws.w[j % 3];
     float* wprev = ws.w[(j + 2) % 3];
@@ -1195,9 +1205,11 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     begin_timed(c, j, 0);
     int nsplit = 1, nbm = 0;
     double* apart = nullptr;
+    // single GPU, tensor-core MVM: the streaming pass of iteration j writes W_{j+1}'s split-fp16
+    // planes, so iteration j+1 skips pack_v (the first iteration of a block always packs)
     ciq_status st2 = P.on ? apply_m(wcur, ws.p, &apart, &nbm)
                           : run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit,
-                                    &apart, &nbm);
+                                    &apart, &nbm, fuse_pack);
     end_timed(c);
     if (st2 != CIQ_OK) return st2;
     const float* pin = (nsplit > 1) ? c->psplit : ws.p;
@@ -1215,7 +1227,8 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     float* d2 = dslot[(j + 1) & 1];
     begin_timed(c, j, 1);
     LAUNCH(c, launch_lanczos_update(sc, pin, nsplit, (size_t)rows * tp, wcur + c->row0 * tp, wprev + c->row0 * tp,
-                                    wnew + c->row0 * tp, &d1, &d2, ws.y, nq, rows, tp, ws.bpart, 0, s));
+                                    wnew + c->row0 * tp, &d1, &d2, ws.y, nq, rows, tp, ws.bpart, 0, s,
+                                    fuse_pack ? c->planes : nullptr, c->inv_scale, c->npad, tc_chunk_cols(tp), c->op.n));
     end_timed(c);
     if (c->world == 1) {
       LAUNCH(c, launch_givens(sc, ws.bpart, nbs, nq, tp, s));

@@ -102,7 +102,9 @@ cudaError_t launch_init_state(const Scal& sc, int nq, int tp, const double* cols
 cudaError_t launch_alpha(const Scal& sc, const double* apart, int nblk, int tp, cudaStream_t s);
 cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, size_t split_stride, const float* wcur, const float* wprev,
                                   float* wnew, float* const* d1, float* const* d2, float* y, int nq,
-                                  int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s);
+                                  int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s,
+                                  __half* planes = nullptr, float* inv_scale = nullptr, int64_t npad = 0, int tn = 0,
+                                  int64_t n = 0);   // planes: also write W_{j+1}'s split-fp16 MVM operand
 cudaError_t launch_alpha_from_sum(const Scal& sc, const double* sums, int tp, cudaStream_t s);
 cudaError_t launch_sum_ranks(const double* g, int world, int m, double* out, cudaStream_t s);
 cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s);

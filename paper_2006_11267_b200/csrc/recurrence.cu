@@ -16,6 +16,7 @@
 // and all Q shifted solution updates (eq. minres_descent), and Y = sum_q w_q x_q is
 // accumulated in place (eq. contour_integral_quad) -- the x_q are never stored.
 // All reductions are fixed-order (fp64 across CTAs): deterministic.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -218,12 +219,36 @@ __global__ void sum_ranks_kernel(const double* __restrict__ g, int world, int m,
   out[k] = s;
 }
 
+// Split-fp16 operand planes of the next MVM, written by the streaming pass (world == 1): W_{j+1}
+// scaled per column by 2^e, e = round(log2(sqrt(n) / nrm_j)) -- the norm of the CURRENT block
+// stands in for beta_{j+1}, which is not known yet (any power of two that keeps both fp16 halves
+// in range gives the same product: scaling by 2^e is exact).  Layout as pack_v (mvm_tc.cu):
+// [chunk][hi|lo][npad/8][tn/8][8][8].
+struct PackOut {
+  __half* planes;      // null: no packing
+  float* inv_scale;
+  int64_t npad;
+  int tn;
+  double sqrt_n;
+};
+
+CIQ_DEVICE float pack_scale(double nrm, double sqrt_n, float* inv) {
+  int ex = 0;
+  if (nrm > 0 && isfinite(nrm)) ex = (int)lrint(log2(sqrt_n / nrm));
+  ex = max(-60, min(60, ex));
+  *inv = ldexpf(1.f, -ex);
+  return ldexpf(1.f, ex);
+}
+
 // The streaming pass (see file header).  final_only: apply the pending update of the last step
-// only (wprev = the buffer holding nrm_J v_J).
+// only (wprev = the buffer holding nrm_J v_J).  Shifts are processed in batches of QB so that the
+// 2 QB direction loads of a row are in flight together (the loop over shifts otherwise
+// serialises on the stores to d2, which the compiler cannot reorder).
 __global__ void __launch_bounds__(kThreads, 3) lanczos_update_kernel(
     Scal sc, const float* __restrict__ p, int nsplit, size_t split_stride, const float* __restrict__ wcur, const float* __restrict__ wprev,
     float* __restrict__ wnew, const float* __restrict__ d1base, float* __restrict__ d2base, int64_t qstride,
-    float* __restrict__ y, int nq, int64_t rows, int tp, double* __restrict__ bpart, int final_only) {
+    float* __restrict__ y, int nq, int64_t rows, int tp, double* __restrict__ bpart, int final_only, PackOut pk) {
+  constexpr int QB = 2;
   const Ctrl* ctrl = sc.ctrl;
   if (!final_only && ctrl->done) return;
   const int pending = ctrl->pending;
@@ -233,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 3) lanczos_update_kernel(
   const int c = blockIdx.y * kChunk + quad * 4;
   double acc[4] = {0, 0, 0, 0};
   if (lane_row < g.rpp) {
-    float inv_nrm[4], alpha[4], cprev[4];
+    float inv_nrm[4], alpha[4], cprev[4], psc[4];
     if (!final_only) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -242,6 +267,9 @@ __global__ void __launch_bounds__(kThreads, 3) lanczos_update_kernel(
         inv_nrm[k] = fr ? 0.f : (float)(1.0 / sc.nrm_cur[cc]);
         alpha[k] = fr ? 0.f : (float)sc.alpha[cc];
         cprev[k] = fr ? 0.f : (float)(sc.tb_cur[cc] / sc.nrm_prev[cc]);
+        float inv;
+        psc[k] = pack_scale(sc.nrm_cur[cc], pk.sqrt_n, &inv);
+        if (pk.planes != nullptr && blockIdx.x == 0 && lane_row == 0) pk.inv_scale[cc] = inv;
       }
     }
     int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta;
@@ -264,25 +292,53 @@ __global__ void __launch_bounds__(kThreads, 3) lanczos_update_kernel(
         *reinterpret_cast<float4*>(wnew + off) = w;
         acc[0] += (double)w.x * w.x; acc[1] += (double)w.y * w.y;
         acc[2] += (double)w.z * w.z; acc[3] += (double)w.w * w.w;
+        if (pk.planes != nullptr) {
+          const float x[4] = {w.x * psc[0], w.y * psc[1], w.z * psc[2], w.w * psc[3]};
+          uint32_t hw[2], lw[2];
+#pragma unroll
+          for (int k = 0; k < 4; k += 2) {
+            const __half2 hh = __floats2half2_rn(x[k], x[k + 1]);
+            const float2 hf = __half22float2(hh);
+            const __half2 ll = __floats2half2_rn(x[k] - hf.x, x[k + 1] - hf.y);
+            hw[k / 2] = *reinterpret_cast<const uint32_t*>(&hh);
+            lw[k / 2] = *reinterpret_cast<const uint32_t*>(&ll);
+          }
+          const int chunk = c / pk.tn, cl = c % pk.tn;
+          const size_t plane = (size_t)pk.npad * pk.tn;
+          const size_t po = (size_t)chunk * 2 * plane + ((size_t)((i / 8) * (pk.tn / 8) + cl / 8) * 64 + (i % 8) * 8 + cl % 8);
+          *reinterpret_cast<uint2*>(pk.planes + po) = make_uint2(hw[0], hw[1]);
+          *reinterpret_cast<uint2*>(pk.planes + po + plane) = make_uint2(lw[0], lw[1]);
+        }
       }
       if (pending) {
         float4 yy = *reinterpret_cast<const float4*>(y + off);
-        for (int q = 0; q < nq; ++q) {
-          const int k = q * tp + c;
-          float4 a = *reinterpret_cast<const float4*>(sc.ca + k);
-          float4 b = *reinterpret_cast<const float4*>(sc.cb + k);
-          float4 e = *reinterpret_cast<const float4*>(sc.ce + k);
-          float4 f = *reinterpret_cast<const float4*>(sc.cf + k);
-          float4 x1 = *reinterpret_cast<const float4*>(d1base + q * qstride + off);
-          float4 x2 = *reinterpret_cast<const float4*>(d2base + q * qstride + off);
-          float4 dn;
-          dn.x = fmaf(a.x, wp.x, fmaf(b.x, x1.x, e.x * x2.x));
-          dn.y = fmaf(a.y, wp.y, fmaf(b.y, x1.y, e.y * x2.y));
-          dn.z = fmaf(a.z, wp.z, fmaf(b.z, x1.z, e.z * x2.z));
-          dn.w = fmaf(a.w, wp.w, fmaf(b.w, x1.w, e.w * x2.w));
-          *reinterpret_cast<float4*>(d2base + q * qstride + off) = dn;
-          yy.x = fmaf(f.x, dn.x, yy.x); yy.y = fmaf(f.y, dn.y, yy.y);
-          yy.z = fmaf(f.z, dn.z, yy.z); yy.w = fmaf(f.w, dn.w, yy.w);
+        for (int q0 = 0; q0 < nq; q0 += QB) {
+          float4 x1[QB], x2[QB];
+#pragma unroll
+          for (int u = 0; u < QB; ++u) {
+            if (q0 + u < nq) {
+              x1[u] = *reinterpret_cast<const float4*>(d1base + (q0 + u) * qstride + off);
+              x2[u] = *reinterpret_cast<const float4*>(d2base + (q0 + u) * qstride + off);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < QB; ++u) {
+            if (q0 + u < nq) {
+              const int k = (q0 + u) * tp + c;
+              const float4 a = __ldg(reinterpret_cast<const float4*>(sc.ca + k));
+              const float4 bq = __ldg(reinterpret_cast<const float4*>(sc.cb + k));
+              const float4 e = __ldg(reinterpret_cast<const float4*>(sc.ce + k));
+              const float4 f = __ldg(reinterpret_cast<const float4*>(sc.cf + k));
+              float4 dn;
+              dn.x = fmaf(a.x, wp.x, fmaf(bq.x, x1[u].x, e.x * x2[u].x));
+              dn.y = fmaf(a.y, wp.y, fmaf(bq.y, x1[u].y, e.y * x2[u].y));
+              dn.z = fmaf(a.z, wp.z, fmaf(bq.z, x1[u].z, e.z * x2[u].z));
+              dn.w = fmaf(a.w, wp.w, fmaf(bq.w, x1[u].w, e.w * x2[u].w));
+              *reinterpret_cast<float4*>(d2base + (q0 + u) * qstride + off) = dn;
+              yy.x = fmaf(f.x, dn.x, yy.x); yy.y = fmaf(f.y, dn.y, yy.y);
+              yy.z = fmaf(f.z, dn.z, yy.z); yy.w = fmaf(f.w, dn.w, yy.w);
+            }
+          }
         }
         *reinterpret_cast<float4*>(y + off) = yy;
       }
@@ -512,10 +568,12 @@ cudaError_t launch_alpha(const Scal& sc, const double* apart, int nblk, int tp, 
 }
 cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, size_t split_stride, const float* wcur, const float* wprev,
                                   float* wnew, float* const* d1, float* const* d2, float* y, int nq,
-                                  int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s) {
+                                  int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s,
+                                  __half* planes, float* inv_scale, int64_t npad, int tn, int64_t n) {
   const int64_t qstride = rows * tp;
+  PackOut pk{planes, inv_scale, npad, tn, sqrt((double)n)};
   lanczos_update_kernel<<<stream_grid(rows, tp), kThreads, 0, s>>>(sc, p, nsplit, split_stride, wcur, wprev, wnew, d1[0], d2[0],
-                                                                    qstride, y, nq, rows, tp, bpart, final_only);
+                                                                    qstride, y, nq, rows, tp, bpart, final_only, pk);
   return cudaGetLastError();
 }
 cudaError_t launch_alpha_from_sum(const Scal& sc, const double* sums, int tp, cudaStream_t s) {
