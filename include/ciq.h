@@ -134,6 +134,12 @@ typedef struct {
   double breakdown_tol;       /* Lanczos invariant-subspace threshold, relative (default 1e-6)   */
   int32_t profile_kernels;    /* 1: bracket every MVM / update launch with CUDA events and report */
                               /*    their device time in ciq_info (small overhead; default 0)     */
+  int32_t lanczos_reuse;      /* 1: estimate lambda_min / lambda_max from the first 12 Lanczos     */
+                              /*    steps of the solve itself (Lanczos started at b, as App. D     */
+                              /*    P:1494 describes it), then replay the shifted updates of those */
+                              /*    steps: no separate ~10-MVM estimation run.  Ignored with a     */
+                              /*    preconditioner, an explicit rule/spectrum, or max_iters <= 24. */
+                              /*    Default 0 (separate estimation from lanczos_start, G5).       */
 } ciq_params;
 
 typedef struct {

@@ -59,7 +59,8 @@ class CiqParams(ctypes.Structure):
                 ("lanczos_cols", c_int32), ("lambda_min", c_double), ("lambda_max", c_double),
                 ("t", POINTER(c_double)), ("w", POINTER(c_double)), ("lanczos_start", c_void_p),
                 ("ld_start", c_int64), ("seed", c_uint64), ("mode", c_int32), ("mvm_impl", c_int32),
-                ("poll_every", c_int32), ("breakdown_tol", c_double), ("profile_kernels", c_int32)]
+                ("poll_every", c_int32), ("breakdown_tol", c_double), ("profile_kernels", c_int32),
+                ("lanczos_reuse", c_int32)]
 
 
 class CiqInfo(ctypes.Structure):
@@ -312,7 +313,7 @@ def ciq_free(ctx) -> None:
 def make_params(q: int = 8, max_iters: int = 400, tol: float = 1e-4, mode: str = "sqrt", *, lanczos_iters: int = 10,
                 lanczos_cols: int = 16, lanczos_start=None, rule=None, spectrum=None, seed: int = 2,
                 mvm_impl: str = "auto", poll_every: int = 6, breakdown_tol: float = 1e-6, profile: bool = False,
-                keep: list | None = None):
+                lanczos_reuse: bool = False, keep: list | None = None):
     """Build a CiqParams; arrays referenced by it are appended to `keep` (caller keeps them alive)."""
     keep = [] if keep is None else keep
     p = ciq_params_default()
@@ -324,6 +325,7 @@ def make_params(q: int = 8, max_iters: int = 400, tol: float = 1e-4, mode: str =
     p.poll_every = int(poll_every)
     p.breakdown_tol = float(breakdown_tol)
     p.profile_kernels = 1 if profile else 0
+    p.lanczos_reuse = 1 if lanczos_reuse else 0
     if lanczos_start is not None:
         ptr, ld, r, c = _ptr_ld(lanczos_start, "lanczos_start", keep)
         p.lanczos_start, p.ld_start = ptr, ld

@@ -111,6 +111,10 @@ struct ciq_ctx {
   int inv_scale_n = 0;
   float* psplit = nullptr;    // nsplit x rows x tp partial products
   size_t psplit_elems = 0;
+  float* stash = nullptr;     // lanczos_reuse: W_1..W_R of the warm-up steps (full height)
+  size_t stash_elems = 0;
+  double* hist = nullptr;     // lanczos_reuse: per-step scalar history [7][R][tp]
+  size_t hist_elems = 0;
   double* apart_tc = nullptr;
   size_t apart_tc_elems = 0;
   int last_nsplit = 1;
@@ -1028,6 +1032,7 @@ void ciq_free(ciq_ctx* c) {
   dfree(c->staging);
   dfree(c->kplanes);
   dfree(c->feat_a); dfree(c->feat_b); dfree(c->planes); dfree(c->inv_scale); dfree(c->psplit);
+  dfree(c->stash); dfree(c->hist);
   dfree(c->apart_tc);
   free_precond(c->pc);
   dfree(c->gsum);
@@ -1143,12 +1148,18 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     if (st != CIQ_OK) return st;
   }
 
-  // a2/a3: spectrum estimate and quadrature rule
+  // a2/a3: spectrum estimate and quadrature rule.  lanczos_reuse: the estimate comes from the
+  // first kReuse Lanczos steps of the solve itself (run below, before the shifted updates).
+  constexpr int kReuse = 12;   // a multiple of 6: the captured graph's buffer rotation is kept
+  const bool reuse = p.lanczos_reuse != 0 && p.t == nullptr && !(p.lambda_min > 0 && p.lambda_max > 0) && !P.on &&
+                     p.max_iters > 2 * kReuse;
   double t[CIQ_MAX_Q], w[CIQ_MAX_Q];
   double lmin = NAN, lmax = NAN, rmin = NAN, rmax = NAN;
   int lambda_mvms = 0;
   CUDA_TRY(c, cudaEventRecord(ev.e[1], s));
-  if (p.t != nullptr) {
+  if (reuse) {
+    // rule computed after the warm-up
+  } else if (p.t != nullptr) {
     for (int q = 0; q < nq; ++q) { t[q] = p.t[q]; w[q] = p.w[q]; }
   } else {
     if (p.lambda_min > 0 && p.lambda_max > 0) {
@@ -1162,8 +1173,10 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     int r = ciqh::hht_rule(lmin, lmax, nq, t, w);
     if (r != 0) return set_err(c, r == -1 ? CIQ_ERR_INVALID_ARG : CIQ_ERR_ELLIPTIC, "quadrature rule failed");
   }
-  CUDA_TRY(c, cudaMemcpyAsync(sc.shifts, t, nq * 8, cudaMemcpyHostToDevice, s));
-  CUDA_TRY(c, cudaMemcpyAsync(sc.weights, w, nq * 8, cudaMemcpyHostToDevice, s));
+  if (!reuse) {
+    CUDA_TRY(c, cudaMemcpyAsync(sc.shifts, t, nq * 8, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(sc.weights, w, nq * 8, cudaMemcpyHostToDevice, s));
+  }
   CUDA_TRY(c, cudaEventRecord(ev.e[2], s));
 
   // a4-a6: msMINRES iterations.  Buffers rotate with period 6 in j (W: j mod 3, D: j mod 2) and
@@ -1198,7 +1211,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     if (st != CIQ_OK) return st;
     LAUNCH(c, launch_pack_v(ws.w[1], c->op.n, c->npad, tp, sc.nrm_cur, c->planes, c->inv_scale, s));
   }
-  auto enqueue_iter = [&](int j) -> ciq_status {
+  auto enqueue_iter = [&](int j, int nqe) -> ciq_status {
     float* wcur = ws.w[j % 3];
     float* wprev = ws.w[(j + 2) % 3];
     float* wnew = ws.w[(j + 1) % 3];
@@ -1227,21 +1240,112 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     float* d2 = dslot[(j + 1) & 1];
     begin_timed(c, j, 1);
     LAUNCH(c, launch_lanczos_update(sc, pin, nsplit, (size_t)rows * tp, wcur + c->row0 * tp, wprev + c->row0 * tp,
-                                    wnew + c->row0 * tp, &d1, &d2, ws.y, nq, rows, tp, ws.bpart, 0, s,
+                                    wnew + c->row0 * tp, &d1, &d2, ws.y, nqe, rows, tp, ws.bpart, 0, s,
                                     fuse_pack ? c->planes : nullptr, c->inv_scale, c->npad, tc_chunk_cols(tp), c->op.n));
     end_timed(c);
     if (c->world == 1) {
-      LAUNCH(c, launch_givens(sc, ws.bpart, nbs, nq, tp, s));
+      LAUNCH(c, launch_givens(sc, ws.bpart, nbs, nqe, tp, s));
     } else {
       LAUNCH(c, launch_reduce_cols(ws.bpart, nbs, tp, tsum_b, 0, s));
       st2 = global_sum(c, tsum_b, tp);
       if (st2 != CIQ_OK) return st2;
-      LAUNCH(c, launch_givens(sc, tsum_b, 1, nq, tp, s));
+      LAUNCH(c, launch_givens(sc, tsum_b, 1, nqe, tp, s));
       st2 = allgather_rows(c, wnew, tp);   // next Lanczos block to every rank
       if (st2 != CIQ_OK) return st2;
     }
     return CIQ_OK;
   };
+  int j0 = 0;   // iterations already done (lanczos_reuse warm-up)
+  if (reuse) {
+    // Warm-up: kReuse plain Lanczos steps of the solve (no shifts yet: nq_eff = 0, no stopping),
+    // keeping W_j and the per-step scalars; lambda from the pooled Ritz extremes of the T_j; then
+    // the shifted QR / descent updates of those steps are replayed from the history (P:1338-1379:
+    // the Lanczos step is shift-independent; only the per-shift QR needs t_q).
+    const int R = kReuse;
+    const size_t wsz = (size_t)c->nfull * tp;
+    st = grow(c, &c->stash, &c->stash_elems, (size_t)R * wsz);
+    if (st == CIQ_OK) st = grow(c, &c->hist, &c->hist_elems, (size_t)7 * R * tp);
+    if (st != CIQ_OK) return st;
+    double* hA = c->hist;                       // alpha_j
+    double* hN = hA + (size_t)R * tp;           // nrm_j (norm of W_j)
+    double* hP = hN + (size_t)R * tp;           // nrm_{j-1}
+    double* hT = hP + (size_t)R * tp;           // beta_j (T off-diagonal before step j)
+    double* hB = hT + (size_t)R * tp;           // beta_{j+1}
+    double* hQ = hB + (size_t)R * tp;           // beta_{j+1}^2 (replay input)
+    int* hF = reinterpret_cast<int*>(hQ + (size_t)R * tp);   // frozen flags before step j
+    const int big = 1 << 30;
+    const double zero = 0.0;
+    CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->max_iters, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->tol, &zero, sizeof(double), cudaMemcpyHostToDevice, s));
+    for (int j = 1; j <= R; ++j) {
+      const size_t o = (size_t)(j - 1) * tp;
+      CUDA_TRY(c, cudaMemcpyAsync(c->stash + (size_t)(j - 1) * wsz, ws.w[j % 3], wsz * 4, cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(c, cudaMemcpyAsync(hN + o, sc.nrm_cur, tp * 8, cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(c, cudaMemcpyAsync(hP + o, sc.nrm_prev, tp * 8, cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(c, cudaMemcpyAsync(hT + o, sc.tb_cur, tp * 8, cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(c, cudaMemcpyAsync(hF + o, sc.frozen, tp * 4, cudaMemcpyDeviceToDevice, s));
+      st = enqueue_iter(j, 0);
+      if (st != CIQ_OK) return st;
+      CUDA_TRY(c, cudaMemcpyAsync(hA + o, sc.alpha, tp * 8, cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(c, cudaMemcpyAsync(hB + o, sc.tb_cur, tp * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    std::vector<double> al((size_t)R * tp), bn((size_t)R * tp);
+    std::vector<int> fr((size_t)R * tp), frz_end(tp);
+    CUDA_TRY(c, cudaMemcpyAsync(al.data(), hA, al.size() * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaMemcpyAsync(bn.data(), hB, bn.size() * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaMemcpyAsync(fr.data(), hF, fr.size() * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaMemcpyAsync(frz_end.data(), sc.frozen, tp * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    // per column: T_m with m = steps taken before the column froze (breakdown / zero column)
+    double emin_all = INFINITY, emax_all = -INFINITY;
+    std::vector<double> a(R), b(R);
+    for (int k = 0; k < (int)T; ++k) {
+      int m = 0;
+      while (m < R && fr[(size_t)m * tp + k] == 0) ++m;
+      if (m < 1) continue;
+      for (int i = 0; i < m; ++i) a[i] = al[(size_t)i * tp + k];
+      for (int i = 0; i + 1 < m; ++i) b[i] = bn[(size_t)i * tp + k];
+      double e0, e1;
+      ciqh::tridiag_extremes(a.data(), b.data(), m, &e0, &e1);
+      emin_all = std::min(emin_all, e0);
+      emax_all = std::max(emax_all, e1);
+    }
+    rmin = emin_all;
+    rmax = emax_all;
+    lmax = 1.01 * emax_all;              // reading G6, as estimate_lambda
+    lmin = 0.99 * emin_all;
+    if (c->op.diag > 0) lmin = std::min(lmin, (double)c->op.diag);
+    if (!(lmin > 0) || !std::isfinite(lmax))
+      return set_err(c, CIQ_ERR_NOT_PD, "lambda_min estimate %g <= 0: operator is not positive definite", lmin);
+    int r = ciqh::hht_rule(lmin, lmax, nq, t, w);
+    if (r != 0) return set_err(c, r == -1 ? CIQ_ERR_INVALID_ARG : CIQ_ERR_ELLIPTIC, "quadrature rule failed");
+    CUDA_TRY(c, cudaMemcpyAsync(sc.shifts, t, nq * 8, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(sc.weights, w, nq * 8, cudaMemcpyHostToDevice, s));
+    for (auto& x : bn) x = x * x;       // sqrt(fl(x^2)) == x: the replayed givens sees beta_{j+1}
+    CUDA_TRY(c, cudaMemcpyAsync(hQ, bn.data(), bn.size() * 8, cudaMemcpyHostToDevice, s));
+    // replay: fresh Givens state, then per step the recorded scalars and beta_{j+1}^2 (one block);
+    // the descent update of step k (pending) is applied with the stored v_k (W_k / nrm_k)
+    LAUNCH(c, launch_init_state(sc, nq, tp, ws.colsq, s));
+    for (int k = 1; k <= R; ++k) {
+      const size_t o = (size_t)(k - 1) * tp;
+      CUDA_TRY(c, cudaMemcpyAsync(sc.alpha, hA + o, tp * 8, cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(c, cudaMemcpyAsync(sc.nrm_cur, hN + o, tp * 8, cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(c, cudaMemcpyAsync(sc.nrm_prev, hP + o, tp * 8, cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(c, cudaMemcpyAsync(sc.tb_cur, hT + o, tp * 8, cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(c, cudaMemcpyAsync(sc.frozen, hF + o, tp * 4, cudaMemcpyDeviceToDevice, s));
+      LAUNCH(c, launch_givens(sc, hQ + o, 1, nq, tp, s));
+      if (k < R) {   // step R's update stays pending for iteration R + 1
+        float* d1 = dslot[(k + 1) & 1];
+        float* d2 = dslot[k & 1];
+        float* wk = c->stash + (size_t)(k - 1) * wsz;
+        LAUNCH(c, launch_lanczos_update(sc, nullptr, 1, 0, nullptr, wk + c->row0 * tp, nullptr, &d1, &d2, ws.y, nq,
+                                        rows, tp, nullptr, 1, s));
+      }
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->max_iters, &hctrl.max_iters, sizeof(int), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->tol, &hctrl.tol, sizeof(double), cudaMemcpyHostToDevice, s));
+    j0 = R;
+  }
   const bool use_graph = !c->profiling && getenv("CIQ_NO_GRAPH") == nullptr &&
                          (c->world == 1 || c->comm->capturable());
   int block = p.poll_every;
@@ -1258,7 +1362,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
       const int64_t l0 = c->launches;
       CUDA_TRY(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       ciq_status cst = CIQ_OK;
-      for (int k = 1; k <= block && cst == CIQ_OK; ++k) cst = enqueue_iter(k);
+      for (int k = 1; k <= block && cst == CIQ_OK; ++k) cst = enqueue_iter(k, nq);
       cudaGraph_t g = nullptr;
       cudaError_t e = cudaStreamEndCapture(s, &g);
       if (cst != CIQ_OK) { if (g) cudaGraphDestroy(g); return cst; }
@@ -1289,7 +1393,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
       return CIQ_OK;
     };
     for (;;) {
-      while ((int64_t)launched * block < p.max_iters && launched - checked < 2) {
+      while ((int64_t)launched * block < p.max_iters - j0 && launched - checked < 2) {
         st = launch_one();
         if (st != CIQ_OK) return st;
       }
@@ -1303,11 +1407,11 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     cudaEventDestroy(evp[1]);
     c->last_nsplit = loop_nsplit;
   } else {
-    int j = 0;
+    int j = j0;
     for (;;) {
       for (int k = 0; k < p.poll_every && j < p.max_iters; ++k) {
         ++j;
-        st = enqueue_iter(j);
+        st = enqueue_iter(j, nq);
         if (st != CIQ_OK) return st;
       }
       CUDA_TRY(c, cudaMemcpyAsync(&hc, sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));

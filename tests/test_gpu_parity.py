@@ -231,3 +231,47 @@ def test_cuda_graph_replay_equals_direct_launches():
     assert outs[0][1] == outs[1][1] == outs[2][1]
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
     np.testing.assert_array_equal(outs[0][0], outs[2][0])
+
+
+# ------------------------------------------------------------------------------------------------
+# lanczos_reuse: lambda from the solve's own first 12 Lanczos steps (start = b, App. D),
+# shifted updates of those steps replayed
+# ------------------------------------------------------------------------------------------------
+
+def test_lanczos_reuse_estimate_and_replay():
+    cfg = workloads.scaled(workloads.CONFIGS["C3"], n=3000, t=8)
+    inp = workloads.make_inputs(cfg)
+    op = oracle_op(cfg, inp)
+    b = inp["B"].astype(np.float64)
+    lmin, lmax, rmin, rmax = estimate_spectrum(op.mvm, b, 12, lower_bound=cfg.sigma2)
+    j = 90
+    with gpu_ctx(cfg, inp) as g:
+        out = torch.empty((cfg.n, cfg.t), device="cuda")
+        info = g.apply(dev(inp["B"]), out, q=8, max_iters=j, tol=0.0, mode="sqrt", lanczos_reuse=True)
+        rule = (np.array(info["t"][:8]), np.array(info["w"][:8]))
+        out2 = torch.empty_like(out)
+        info2 = g.apply(dev(inp["B"]), out2, q=8, max_iters=j, tol=0.0, mode="sqrt", rule=rule)
+    # no separate estimation run: J + the final K.Y
+    assert info["mvms"] == j + 1 and info["iters"] == j
+    # 12-step Ritz extremes of the 3-term fp32 recurrence vs the fp64 oracle with re-orthogonalisation
+    assert abs(info["ritz_max"] / rmax - 1) < 1e-4
+    assert abs(info["ritz_min"] / rmin - 1) < 1e-3
+    np.testing.assert_allclose(info["lambda_min"], lmin, rtol=1e-3)
+    # the replayed shifted updates equal a direct solve with the same rule
+    got = out.cpu().numpy().astype(np.float64)
+    assert relerr(got, out2.cpu().numpy()) < 1e-6
+    ref = ciq(op, b, q=8, max_iters=j, tol=0.0, mode="sqrt", rule=rule)
+    assert np.max(np.abs(ref.solve.phibar) / ref.solve.beta1) < 1e-5
+    assert relerr(got, ref.out) < 1e-4
+
+
+def test_lanczos_reuse_tolerance_stop():
+    cfg = workloads.scaled(workloads.CONFIGS["C3"], n=2000, t=4)
+    inp = workloads.make_inputs(cfg)
+    with gpu_ctx(cfg, inp) as g:
+        out = torch.empty((cfg.n, cfg.t), device="cuda")
+        a = g.apply(dev(inp["B"]), out, q=8, max_iters=400, tol=1e-4, mode="sqrt", lanczos_reuse=True)
+        b = g.apply(dev(inp["B"]), out, q=8, max_iters=400, tol=1e-4, mode="sqrt", lanczos_start=dev(inp["S"]))
+    assert a["converged"] and a["max_rel_residual"] <= 1e-4
+    assert abs(a["iters"] - b["iters"]) <= 2
+    assert a["mvms"] == a["iters"] + 1
