@@ -361,7 +361,7 @@ void mvm_geometry(const ciq_ctx* c, int tp, int* nsplit, int64_t* nblk) {
   const int chunks = tp / tc_chunk_cols(tp);
   const int nsm = sm_count();
   if (c->op.kind == CIQ_OP_DENSE) {
-    *nsplit = choose_nsplit_dense(rows, c->npad, chunks, nsm);
+    *nsplit = choose_nsplit_dense(rows, c->npad, chunks, nsm * dense_ctas_per_sm());
     *nblk = (rows + 127) / 128 * *nsplit;
   } else if (use_tc2(c)) {
     *nsplit = tc2_choose_nsplit(rows, c->op.n, chunks, nsm);

@@ -72,6 +72,7 @@ struct TcArgs {
   long long* dbg_clk;        // experiments only: per-tile clock stamps of CTA 0
 };
 int tc_chunk_cols(int tp);
+int dense_ctas_per_sm();     // resident CTAs per SM of the dense kernel
 int tc_cluster_size();       // cluster size of the matrix-free kernel (env CIQ_TC_CLUSTER overrides)
 cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, const double* nrm, __half* planes,
                           float* inv_scale, cudaStream_t s);
