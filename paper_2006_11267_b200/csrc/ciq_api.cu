@@ -309,6 +309,12 @@ bool use_tc2(const ciq_ctx* c) {
   return c->op.kind != CIQ_OP_DENSE && !v1 && c->op.n >= 256;
 }
 
+// Dense tensor-core MVM: the persistent kernel (mvm_dense2_kernel) unless CIQ_DENSE_V1=1.
+bool use_dense2() {
+  static const bool v1 = getenv("CIQ_DENSE_V1") && atoi(getenv("CIQ_DENSE_V1")) != 0;
+  return !v1;
+}
+
 int sm_count() {
   int nsm = 148, dev = 0;
   cudaGetDevice(&dev);
@@ -360,7 +366,10 @@ void mvm_geometry(const ciq_ctx* c, int tp, int* nsplit, int64_t* nblk) {
   const int64_t rows = c->row1 - c->row0;
   const int chunks = tp / tc_chunk_cols(tp);
   const int nsm = sm_count();
-  if (c->op.kind == CIQ_OP_DENSE) {
+  if (c->op.kind == CIQ_OP_DENSE && use_dense2()) {
+    *nsplit = choose_nsplit_dense(rows, c->npad, chunks, nsm);
+    *nblk = (rows + 127) / 128 * *nsplit * 4;
+  } else if (c->op.kind == CIQ_OP_DENSE) {
     *nsplit = choose_nsplit_dense(rows, c->npad, chunks, nsm * dense_ctas_per_sm());
     *nblk = (rows + 127) / 128 * *nsplit;
   } else if (use_tc2(c)) {
@@ -479,8 +488,9 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     if (a.dbg_clk) cudaMemset(a.dbg_clk, 0, 32 * 256 * sizeof(long long));
   }
   a.chunks = chunks;
-  a.nunits = v2 ? tc2_units(rows, nsplit, chunks) : 0;
-  if (dense) LAUNCH(c, launch_mvm_dense_tc(a, c->stream));
+  a.nunits = v2 ? tc2_units(rows, nsplit, chunks) : (int)((rows + 127) / 128) * nsplit * chunks;
+  if (dense && use_dense2()) LAUNCH(c, launch_mvm_dense2(a, nsm, c->stream));
+  else if (dense) LAUNCH(c, launch_mvm_dense_tc(a, c->stream));
   else if (v2) LAUNCH(c, launch_mvm_tc2(a, nsm, c->stream));
   else LAUNCH(c, launch_mvm_tc(a, c->stream));
   if (a.dbg_clk) {  // experiments only: dump the per-tile timeline of CTA (0, 0)

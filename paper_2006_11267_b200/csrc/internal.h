@@ -82,6 +82,8 @@ int tc2_units(int64_t rows, int nsplit, int chunks);
 int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm);
 cudaError_t launch_mvm_tc2(const TcArgs& a, int nsm, cudaStream_t s);
 cudaError_t launch_mvm_dense_tc(const TcArgs& a, cudaStream_t s);
+// persistent dense kernel: units = row tiles x nsplit x chunks, alpha partials [units/chunks * 4][tp]
+cudaError_t launch_mvm_dense2(const TcArgs& a, int nsm, cudaStream_t s);
 cudaError_t launch_absmax(const float* k, int64_t ldk, int64_t rows, int64_t n, unsigned int* out, cudaStream_t s);
 cudaError_t launch_split_dense(const float* k, int64_t ldk, int64_t rows, int64_t n, int64_t npad, float scale,
                                __half* hi, __half* lo, cudaStream_t s);
