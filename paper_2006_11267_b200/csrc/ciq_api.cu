@@ -1254,9 +1254,9 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
                                     fuse_pack ? c->planes : nullptr, c->inv_scale, c->npad, tc_chunk_cols(tp), c->op.n));
     end_timed(c);
     if (c->world == 1) {
-      LAUNCH(c, launch_givens(sc, ws.bpart, nbs, nqe, tp, s));
+      LAUNCH(c, launch_givens(sc, ws.bpart, update_blocks(rows), nqe, tp, s));
     } else {
-      LAUNCH(c, launch_reduce_cols(ws.bpart, nbs, tp, tsum_b, 0, s));
+      LAUNCH(c, launch_reduce_cols(ws.bpart, update_blocks(rows), tp, tsum_b, 0, s));
       st2 = global_sum(c, tsum_b, tp);
       if (st2 != CIQ_OK) return st2;
       LAUNCH(c, launch_givens(sc, tsum_b, 1, nqe, tp, s));

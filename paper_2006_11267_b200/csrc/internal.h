@@ -90,6 +90,7 @@ cudaError_t launch_split_dense(const float* k, int64_t ldk, int64_t rows, int64_
 
 // ---- vector kernels (recurrence.cu) ----
 int rowblocks(int64_t rows, int tp);   // number of CTAs of the row-streaming kernels
+int update_blocks(int64_t rows);       // CTAs (= beta^2 partial rows) of lanczos_update_kernel
 cudaError_t launch_sum_splits(const float* parts, int nsplit, size_t stride, int64_t elems, float* out,
                               cudaStream_t s);
 cudaError_t launch_load_block(const float* src, int64_t ld_src, int64_t rows, int cols, float* dst, int tp,

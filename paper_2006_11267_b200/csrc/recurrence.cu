@@ -272,8 +272,12 @@ __global__ void __launch_bounds__(kThreads, 3) lanczos_update_kernel(
         if (pk.planes != nullptr && blockIdx.x == 0 && lane_row == 0) pk.inv_scale[cc] = inv;
       }
     }
-    int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta;
-    int64_t r1 = min(rows, r0 + kRowsPerCta);
+    // grid-stride over 64-row blocks: the grid is sized to the resident CTAs (update_blocks), so
+    // the pass has no partial last wave; each CTA's beta^2 partials cover its fixed set of blocks
+    const int64_t nrb = (rows + kRowsPerCta - 1) / kRowsPerCta;
+    for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
+    const int64_t r0 = rb * kRowsPerCta;
+    const int64_t r1 = min(rows, r0 + kRowsPerCta);
     for (int64_t i = r0 + lane_row; i < r1; i += g.rpp) {
       const int64_t off = i * tp + c;
       float4 wp = *reinterpret_cast<const float4*>(wprev + off);
@@ -342,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 3) lanczos_update_kernel(
         }
         *reinterpret_cast<float4*>(y + off) = yy;
       }
+    }
     }
   }
   if (!final_only) cta_col_reduce(g, tp, acc, bpart);
@@ -512,6 +517,17 @@ inline unsigned nb_elem(int64_t e, int bs) { return (unsigned)((e + bs - 1) / bs
 
 int rowblocks(int64_t rows, int /*tp*/) { return (int)((rows + kRowsPerCta - 1) / kRowsPerCta); }
 
+int update_blocks(int64_t rows) {
+  static const int resident = [] {
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return 3 * nsm;   // __launch_bounds__(kThreads, 3)
+  }();
+  const int nrb = rowblocks(rows, 0);
+  return nrb < resident ? nrb : resident;
+}
+
 static dim3 stream_grid(int64_t rows, int tp) {
   return dim3((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((tp + kChunk - 1) / kChunk));
 }
@@ -572,7 +588,9 @@ cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, si
                                   __half* planes, float* inv_scale, int64_t npad, int tn, int64_t n) {
   const int64_t qstride = rows * tp;
   PackOut pk{planes, inv_scale, npad, tn, sqrt((double)n)};
-  lanczos_update_kernel<<<stream_grid(rows, tp), kThreads, 0, s>>>(sc, p, nsplit, split_stride, wcur, wprev, wnew, d1[0], d2[0],
+  dim3 grid = stream_grid(rows, tp);
+  grid.x = (unsigned)update_blocks(rows);
+  lanczos_update_kernel<<<grid, kThreads, 0, s>>>(sc, p, nsplit, split_stride, wcur, wprev, wnew, d1[0], d2[0],
                                                                     qstride, y, nq, rows, tp, bpart, final_only, pk);
   return cudaGetLastError();
 }
