@@ -278,7 +278,7 @@ def run_ours(args, cfg):
     if cfg.kind == "dense" and impl_used == "tc":
         kbytes = 4.0 * rows_local * n                # split fp16 planes: 4 B per entry of K, read once
         roof = {"bound": "hbm", "achieved": kbytes / (mvm_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "kernel": "mvm_dense_tc_kernel (K streamed once per MVM, tcgen05 split products)",
+                "kernel": "mvm_dense2_kernel (persistent; K streamed once per MVM, tcgen05 split products)",
                 "peak_source": f"{peaks['_source']} HBM copy bandwidth"}
     elif impl_used == "simt":
         sm_count = torch.cuda.get_device_properties(local).multi_processor_count
@@ -288,17 +288,32 @@ def run_ours(args, cfg):
                 "peak_source": f"{sm_count} SMs x 128 FP32 lanes x 2 x {peaks.get('sm_max_mhz', 1965.0)} MHz"}
     else:
         peak = peaks["bf16_tflops_sustained"]
+        # executed tensor work of mvm_tc2_kernel: per (256-row unit row) x (64-column tile) entry the
+        # distance GEMM (K = 32) and the three split products (K_hi.V_hi, K_hi.V_lo, K_lo.V_hi)
+        rows_pad, cols_pad = -(-rows_local // 256) * 256, -(-n // 64) * 64
+        exec_flops = 2.0 * rows_pad * cols_pad * (32 + 3 * (-(-tcols // 16) * 16))
         roof = {"bound": "tensor", "achieved": flops / (mvm_ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
-                "kernel": "mvm_tc_kernel (tcgen05 kind::f16, split-fp16 x3 + distance GEMM)",
+                "kernel": "mvm_tc2_kernel (tcgen05 kind::f16, split-fp16 x3 + distance GEMM, fused exp epilogue)",
                 "peak_source": f"{peaks['_source']} bf16 sustained (fp16 same rate)",
-                "note": "achieved counts only the algorithmic 2*N^2*T flops; the kernel issues ~3.5x that"}
+                "note": "achieved counts only the algorithmic 2*N^2*T flops; executed_tflops counts every MMA issued",
+                "executed_tflops": exec_flops / (mvm_ms * 1e-3) / 1e12,
+                "executed_frac_of_measured_peak": exec_flops / (mvm_ms * 1e-3) / 1e12 / peak,
+                "tensor_pipe_active_ncu": {"value": 0.61, "source": "profiles/ncu_k1_r01c.txt (sm__pipe_tensor_cycles_active)"}}
         sm_count = torch.cuda.get_device_properties(local).multi_processor_count
         sfu_peak = sm_count * 16 * peaks.get("sm_max_mhz", 1965.0) * 1e6  # MUFU.EX2 per second
         roof["sfu"] = {"achieved_evals_per_s": rows_local * n / (mvm_ms * 1e-3), "peak_evals_per_s": sfu_peak,
                        "frac": rows_local * n / (mvm_ms * 1e-3) / sfu_peak,
                        "peak_source": f"{sm_count} SMs x 16 MUFU.EX2/clk x sm_max_mhz (1 ex2 per kernel entry)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    # dram bytes per launch from one `ncu --set full` capture of the same kernel (profiles/)
+    if roof["bound"] == "hbm":
+        roof["traffic"] = 423.86e6 if cfg.name == "C2" else None
+        roof["traffic_source"] = "profiles/ncu_k2_r01f.txt (C2)"
+    elif roof["bound"] == "tensor":
+        roof["traffic"] = 32.75e6 if cfg.name == "C3" else None
+        roof["traffic_source"] = "profiles/ncu_k1_r01c.txt (C3; compute-bound: V planes / features stay in L2)"
+    else:
+        roof["traffic"] = None
     roof["ms_per_launch"] = mvm_ms
     roof["share_of_step"] = pinfo["ms_mvm"] / max(1e-9, pinfo["ms_total"])
     q = cfg.q
