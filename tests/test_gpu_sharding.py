@@ -77,3 +77,23 @@ def test_sharded_tolerance_stop_and_oracle():
     ref = ciq(op, inp["B"].astype(np.float64), q=8, max_iters=300, tol=1e-5, mode="invsqrt", lanczos_start=inp["S"])
     assert abs(infos[0]["iters"] - ref.iters) <= 1
     assert np.linalg.norm(sharded - ref.out) / np.linalg.norm(ref.out) < 1e-4
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_lanczos_reuse_equals_single_gpu(world):
+    """lambda from the solve's own Lanczos (lanczos_reuse) under row sharding: the warm-up steps use
+    the same all-gather / rank-order sums, the replay runs on the local rows."""
+    cfg = workloads.scaled(workloads.CONFIGS["C3"], n=1500, t=8)
+    inp = workloads.make_inputs(cfg)
+    kw = dict(q=8, max_iters=60, tol=0.0, mode="sqrt", lanczos_reuse=True)
+    with pb.CIQ(cfg.kind, X=dev(inp["X"]), lengthscale=cfg.lengthscale, outputscale=cfg.outputscale,
+                diag=cfg.sigma2) as g:
+        out = torch.empty((cfg.n, cfg.t), device="cuda")
+        info1 = g.apply(dev(inp["B"]), out, **kw)
+        single = out.cpu().numpy()
+    sharded, infos = run_sharded(cfg, inp, world, **kw)
+    assert np.linalg.norm(sharded - single) / np.linalg.norm(single) < 1e-5
+    assert info1["mvms"] == 61 and all(i["mvms"] == 61 for i in infos)
+    for inf in infos[1:]:
+        assert inf["lambda_max"] == infos[0]["lambda_max"] and inf["iters"] == infos[0]["iters"]
+    assert abs(infos[0]["lambda_max"] / info1["lambda_max"] - 1) < 1e-6
