@@ -100,7 +100,8 @@ struct ciq_ctx {
   // tensor-core MVM operands
   bool tc_ok = false;
   int64_t npad = 0;
-  __half* kplanes = nullptr;  // dense path: split K planes [hi | lo]
+  __half* kplanes = nullptr;  // dense path (or a materialised kernel operator): split K planes [hi | lo]
+  bool mat_ready = false;     // kernel operator: kplanes hold the materialised K (mvm_materialize)
   int64_t kplane_elems = 0;
   float kscale = 1.f;
   __half* feat_a = nullptr;   // [npad/8][4][8][8]
@@ -361,15 +362,56 @@ int choose_nsplit_dense(int64_t rows, int64_t npad, int chunks, int nsm) {
   return best;
 }
 
+// Small N, many right-hand sides (C4: N = 5000, T = 1024): the matrix-free kernel recomputes every
+// kernel tile once per 64-column chunk of T (16x for T = 1024), while the N^2 entries fit easily in
+// HBM.  Such calls materialise K once (fp32 on the CUDA cores, then the dense split-fp16 planes)
+// and run the HBM-bound dense kernel instead (north_star: "a dense-K path runs as a bandwidth-bound
+// batched GEMV/GEMM").  CIQ_NO_MATERIALIZE=1 disables it.
+constexpr int kMatMinT = 256;
+constexpr int64_t kMatMaxN = 20000;
+bool use_mat(const ciq_ctx* c, int tp) {
+  static const bool off = getenv("CIQ_NO_MATERIALIZE") != nullptr;
+  return !off && c->op.kind != CIQ_OP_DENSE && c->tc_ok && tp >= kMatMinT && c->op.n <= kMatMaxN;
+}
+
+ciq_status ensure_mat_planes(ciq_ctx* c) {
+  if (c->mat_ready) return CIQ_OK;
+  const int64_t rows = c->row1 - c->row0, n = c->op.n;
+  const int64_t npad = (n + 127) / 128 * 128;
+  const int64_t rows_pad = (rows + 127) / 128 * 128;
+  float* k = nullptr;
+  CUDA_TRY(c, dalloc(&k, (size_t)rows * n));
+  CUDA_TRY(c, launch_materialize(c->dev, c->row0, rows, k, c->stream));
+  unsigned int* mx = nullptr;
+  CUDA_TRY(c, dalloc(&mx, 1));
+  CUDA_TRY(c, cudaMemsetAsync(mx, 0, 4, c->stream));
+  CUDA_TRY(c, launch_absmax(k, n, rows, n, mx, c->stream));
+  unsigned int hbits = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&hbits, mx, 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  float amax;
+  std::memcpy(&amax, &hbits, 4);
+  if (!(amax > 0) || !std::isfinite(amax)) amax = 1.f;
+  c->kscale = std::ldexp(1.f, 14 - (int)std::ceil(std::log2(amax)));
+  c->kplane_elems = rows_pad * npad;
+  CUDA_TRY(c, dalloc(&c->kplanes, (size_t)2 * c->kplane_elems));   // [hi | lo] fp16 planes
+  CUDA_TRY(c, launch_split_dense(k, n, rows, n, npad, c->kscale, c->kplanes, c->kplanes + c->kplane_elems, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  dfree(k);
+  dfree(mx);
+  c->mat_ready = true;
+  return CIQ_OK;
+}
+
 // Column splits and number of alpha-partial rows of the tensor-core MVM for tp columns.
 void mvm_geometry(const ciq_ctx* c, int tp, int* nsplit, int64_t* nblk) {
   const int64_t rows = c->row1 - c->row0;
   const int chunks = tp / tc_chunk_cols(tp);
   const int nsm = sm_count();
-  if (c->op.kind == CIQ_OP_DENSE && use_dense2()) {
+  if ((c->op.kind == CIQ_OP_DENSE || use_mat(c, tp)) && use_dense2()) {
     *nsplit = choose_nsplit_dense(rows, c->npad, chunks, nsm);
     *nblk = (rows + 127) / 128 * *nsplit * 4;
-  } else if (c->op.kind == CIQ_OP_DENSE) {
+  } else if (c->op.kind == CIQ_OP_DENSE || use_mat(c, tp)) {
     *nsplit = choose_nsplit_dense(rows, c->npad, chunks, nsm * dense_ctas_per_sm());
     *nblk = (rows + 127) / 128 * *nsplit;
   } else if (use_tc2(c)) {
@@ -388,6 +430,10 @@ void mvm_geometry(const ciq_ctx* c, int tp, int* nsplit, int64_t* nblk) {
 // allocates).
 ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
   if (!use_tc(c, impl)) return CIQ_OK;
+  if (use_mat(c, tp)) {
+    ciq_status sm = ensure_mat_planes(c);
+    if (sm != CIQ_OK) return sm;
+  }
   const int64_t rows = c->row1 - c->row0;
   int nsplit = 1;
   int64_t nblk = 0;
@@ -427,8 +473,13 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   const int chunks = tp / tn;
   const int nsm = sm_count();
   (void)allow_split;
-  const bool dense = c->op.kind == CIQ_OP_DENSE;
-  const bool v2 = use_tc2(c);
+  const bool mat = use_mat(c, tp);
+  if (mat) {
+    ciq_status sm = ensure_mat_planes(c);
+    if (sm != CIQ_OK) return sm;
+  }
+  const bool dense = c->op.kind == CIQ_OP_DENSE || mat;
+  const bool v2 = use_tc2(c) && !mat;
   int nsplit = 1;
   int64_t nblk = 0;
   mvm_geometry(c, tp, &nsplit, &nblk);

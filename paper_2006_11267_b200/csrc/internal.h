@@ -43,6 +43,8 @@ struct Scal {
 // alpha_part (may be null): [nblk][tp] partials sum_{i in block} V[i][c] P[i][c]; nblk is
 // returned by mvm_simt_blocks.  done (may be null): skip when *done != 0.
 int mvm_simt_blocks(int64_t rows);
+// K rows [row0, row0 + rows) of a kernel operator, fp32 row-major (rows x n), without sigma^2
+cudaError_t launch_materialize(const OpDev& op, int64_t row0, int64_t rows, float* k, cudaStream_t s);
 cudaError_t launch_mvm_simt(const OpDev& op, const float* v, int tp, int64_t row0, int64_t row1,
                             float* p, int ldp, double* alpha_part, const Ctrl* done, cudaStream_t s);
 

@@ -165,6 +165,24 @@ cudaError_t launch_kind(const OpDev& op, const float* v, int tp, int64_t row0, i
   return cudaGetLastError();
 }
 
+// K[i - row0][j] = k(x_i, x_j) for rows [row0, row1) (fp32, no sigma^2): the materialised
+// operator of the small-N / many-RHS regime (mvm_materialize, ciq_api.cu).  One thread per entry.
+template <int KIND>
+__global__ void materialize_kernel(OpDev op, int64_t row0, int64_t rows, float* __restrict__ k) {
+  const int64_t n = op.n;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * n) return;
+  const int64_t i = row0 + e / n, j = e % n;
+  const float* xi = op.xs + i * op.d;
+  const float* xj = op.xs + j * op.d;
+  float r2 = 0.f;
+  for (int t = 0; t < op.d; ++t) {
+    const float dlt = xi[t] - xj[t];
+    r2 = fmaf(dlt, dlt, r2);
+  }
+  k[e] = kernel_of_r2<KIND>(r2, op.o2);
+}
+
 }  // namespace
 
 int mvm_simt_blocks(int64_t rows) { return (int)((rows + BM - 1) / BM); }
@@ -182,4 +200,18 @@ cudaError_t launch_mvm_simt(const OpDev& op, const float* v, int tp, int64_t row
   return cudaErrorInvalidValue;
 }
 
+}  // namespace ciq
+
+namespace ciq {
+cudaError_t launch_materialize(const OpDev& op, int64_t row0, int64_t rows, float* k, cudaStream_t s) {
+  const int64_t total = rows * op.n;
+  const unsigned grid = (unsigned)((total + 255) / 256);
+  switch (op.kind) {
+    case 1: materialize_kernel<1><<<grid, 256, 0, s>>>(op, row0, rows, k); break;
+    case 2: materialize_kernel<2><<<grid, 256, 0, s>>>(op, row0, rows, k); break;
+    case 3: materialize_kernel<3><<<grid, 256, 0, s>>>(op, row0, rows, k); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
 }  // namespace ciq

@@ -275,3 +275,33 @@ def test_lanczos_reuse_tolerance_stop():
     assert a["converged"] and a["max_rel_residual"] <= 1e-4
     assert abs(a["iters"] - b["iters"]) <= 2
     assert a["mvms"] == a["iters"] + 1
+
+
+# ------------------------------------------------------------------------------------------------
+# materialised kernel operator (small N, T >= 256: the C4 regime) -> persistent dense kernel
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("kind", ["rbf", "matern52"])
+def test_materialized_operator_mvm_and_solve(kind):
+    cfg = workloads.scaled(workloads.CONFIGS["C3"], n=1500, t=256, kind=kind, lengthscale=0.3)
+    inp = workloads.make_inputs(cfg)
+    op = oracle_op(cfg, inp)
+    v = workloads.rhs(cfg.n, cfg.t, seed=9)
+    ref = op.mvm(v.astype(np.float64))
+    with gpu_ctx(cfg, inp) as g:
+        out = torch.empty((cfg.n, cfg.t), device="cuda")
+        g.matvec(dev(v), out)
+        got = out.cpu().numpy().astype(np.float64)
+        assert np.abs(got - ref).max() / np.abs(ref).max() < 2e-5
+        for c in range(0, cfg.t, 37):
+            assert relerr(got[:, c], ref[:, c]) < 8e-6
+        # a full solve in this regime against the oracle (same rule, fixed J)
+        lmin, lmax, _, _ = estimate_spectrum(op.mvm, inp["S"], 10, lower_bound=cfg.sigma2)
+        rule = hht_rule(lmin, lmax, 8)
+        b = inp["B"][:, :cfg.t]
+        info = g.apply(dev(b), out, q=8, max_iters=200, tol=0.0, mode="invsqrt", rule=rule)
+        got = out.cpu().numpy().astype(np.float64)
+    cols = [0, 100, 255]
+    refs = ciq(op, b[:, cols].astype(np.float64), q=8, max_iters=200, tol=0.0, mode="invsqrt", rule=rule)
+    assert np.max(np.abs(refs.solve.phibar) / refs.solve.beta1) < 1e-5
+    assert relerr(got[:, cols], refs.out) < 1e-4
