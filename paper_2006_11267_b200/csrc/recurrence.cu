@@ -27,7 +27,7 @@ namespace {
 
 constexpr int kRowsPerCta = 64;   // rows covered by one CTA of the streaming kernels
 constexpr int kThreads = 256;
-constexpr int kChunk = 1024;      // columns per CTA (grid.y covers the rest)
+constexpr int kChunk = 256;       // columns per CTA (grid.y covers the rest: wide T -> more CTAs)
 
 // Geometry of a streaming CTA: tpr threads per row (one float4 column quad each), rpp rows per pass.
 struct Geo {
@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __re
   s = block_sum256(s);
   __shared__ double s_tbn;
   __shared__ double s_rel[8];
+  __shared__ bool s_last;
   if (threadIdx.x == 0) s_tbn = sqrt(s);
   __syncthreads();
   const double tbn = s_tbn;                      // beta_{j+1}
@@ -414,16 +415,27 @@ __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __re
     col_rel[c] = (state == 1) ? rel : 0.0;
     col_state[c] = state;
     __threadfence();
-    const unsigned int prev = atomicAdd(&ctrl->arrive, 1u);
-    if (prev == (unsigned)tp - 1) {   // last column CTA: global decision
-      __threadfence();
-      double mx = 0.0;
-      int act = 0, brk = 0;
-      for (int cc = 0; cc < tp; ++cc) {
-        const int st = ((volatile int*)col_state)[cc];
-        if (st == 1) { ++act; mx = fmax(mx, ((volatile double*)col_rel)[cc]); }
-        if (st == 2) ++brk;
-      }
+    s_last = atomicAdd(&ctrl->arrive, 1u) == (unsigned)tp - 1;
+  }
+  __syncthreads();
+  if (s_last) {   // last column CTA: global decision (max / counts: order-independent), all threads
+    __threadfence();
+    double mx = 0.0;
+    int act = 0, brk = 0;
+    for (int cc = threadIdx.x; cc < tp; cc += 256) {
+      const int st = ((volatile int*)col_state)[cc];
+      if (st == 1) { ++act; mx = fmax(mx, ((volatile double*)col_rel)[cc]); }
+      if (st == 2) ++brk;
+    }
+    mx = warp_max(mx);
+    act = __reduce_add_sync(0xffffffffu, act);
+    brk = __reduce_add_sync(0xffffffffu, brk);
+    __shared__ double s_mx[8];
+    __shared__ int s_act[8], s_brk[8];
+    if ((threadIdx.x & 31) == 0) { s_mx[threadIdx.x >> 5] = mx; s_act[threadIdx.x >> 5] = act; s_brk[threadIdx.x >> 5] = brk; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < 8; ++w) { mx = fmax(mx, s_mx[w]); act += s_act[w]; brk += s_brk[w]; }
       const int j = ctrl->iters + 1;
       ctrl->iters = j;
       ctrl->pending = 1;
