@@ -71,6 +71,21 @@ struct Bars2 {
   uint64_t a_full[2], a_empty[2];
   uint64_t pro_full, o_full[2], o_empty[2];
   uint32_t tmem_base;
+  uint32_t flags[8];   // per ring stage: the MMA issuers' schedule for that tile (written by the producer)
+};
+
+// Schedule of tile g (KV) and tile g+3 (S), computed by the producer (which has slack) so the MMA
+// issuers -- whose every instruction costs epilogue issue slots -- only test bits.
+enum : uint32_t {
+  F_ACC = 1u << 0,      // KV accumulates into O (not the first tile of its unit)
+  F_OLAST = 1u << 1,    // last tile of its unit: commit o_full after KV
+  F_OWAIT = 1u << 2,    // first tile of a unit after the first: wait o_empty (phase F_OPH)
+  F_OPH = 1u << 3,
+  F_SVALID = 1u << 4,   // S(g+3) exists
+  F_SFIRST = 1u << 5,   // S(g+3) is the first tile of its unit: wait a_full[F_KB] (phase F_APH)
+  F_APH = 1u << 6,
+  F_SLAST = 1u << 7,    // S(g+3) is the last tile of its unit: commit a_empty[F_KB]
+  F_KB = 1u << 8,       // A-rows buffer of S(g+3)'s unit
 };
 
 // Position in the flattened tile sequence of one CTA: unit u (local index k), tile jj of njt.
@@ -273,6 +288,18 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         const int st = g % C::STAGES;
         mbar_wait_backoff(&bars->empty[st], ((g / C::STAGES) & 1) ^ 1);
         T2_STAMP(0, g);
+        {
+          uint32_t fl = 0;
+          if (c.jj > 0) fl |= F_ACC;
+          if (c.jj == c.njt - 1) fl |= F_OLAST;
+          if (c.jj == 0 && c.k > 0) fl |= F_OWAIT | (((c.k - 1) & 1) ? F_OPH : 0u);
+          if (fv) {
+            fl |= F_SVALID | ((f.k & 1) ? F_KB : 0u);
+            if (f.jj == 0) fl |= F_SFIRST | (((f.k >> 1) & 1) ? F_APH : 0u);
+            if (f.jj == f.njt - 1) fl |= F_SLAST;
+          }
+          bars->flags[st] = fl;   // published to the MMA issuers by the full[st] arrive below
+        }
         uint8_t* sb = ring + st * C::STAGE;
         mbar_arrive_expect_tx(&bars->full[st], 2 * C::V_BYTES + (fv ? C::F_BYTES : 0));
         const __half* vh = args.vplanes + (size_t)c.chunk * 2 * plane + (size_t)c.J() * BN2 * TN;
@@ -320,47 +347,49 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         s.advance(args, ntiles);
       }
     }
+    // tiles of this CTA: the loop below runs on the producer's per-stage flags only
+    int ntot = 0;
+    for (int u = blockIdx.x; u < args.nunits; u += gridDim.x) {
+      const int split = (u / args.chunks) % args.nsplit;
+      ntot += ntiles * (split + 1) / args.nsplit - ntiles * split / args.nsplit;
+    }
     int st = 0, b = 0;
     uint32_t ph_st = 0, ph_b = 0;
-    for (int g = 0; kv.valid(args); ++g) {
+    for (int g = 0; g < ntot; ++g) {
       if (h == 0) T2_STAMP(1, g);
       mbar_wait(&bars->full[st], ph_st);
+      const uint32_t fl = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile uint32_t*>(&bars->flags[st]), 0);
       if (h == 0) T2_STAMP(3, g);
       mbar_wait(&bars->k_full[b][h], ph_b);
       if (h == 0) T2_STAMP(2, g);
-      if (kv.jj == 0 && kv.k > 0) mbar_wait(&bars->o_empty[h], (kv.k - 1) & 1);
+      if (fl & F_OWAIT) mbar_wait(&bars->o_empty[h], (fl & F_OPH) ? 1u : 0u);
       fence_after_sync();
       const uint32_t soff16 = (uint32_t)((st * C::STAGE) >> 4);
       // __shfl_sync(.., 0): values the compiler treats as warp-uniform (uniform registers, no
       // per-MMA R2UR / VOTEU in the issue sequence)
       const uint32_t kbu = __shfl_sync(0xffffffffu, tb_h + b * 128, 0);
       const uint64_t dvu = shfl64(dring_v + soff16);
-      const uint32_t accu = __shfl_sync(0xffffffffu, kv.jj > 0 ? 1u : 0u, 0);
-      const bool olast = kv.jj == kv.njt - 1;
       if (elect_one()) {
-        if (!(args.dbg & 1)) mma_kv12<TN>(to_h, kbu, dvu, idesc_o, accu);
-        if (olast) commit_one(&bars->o_full[h]);
+        if (!(args.dbg & 1)) mma_kv12<TN>(to_h, kbu, dvu, idesc_o, fl & F_ACC);
+        if (fl & F_OLAST) commit_one(&bars->o_full[h]);
       }
       __syncwarp();
       if (h == 0) T2_STAMP(9, g);
-      if (s.valid(args)) {   // S(g+3): its features are in stage g (skewed ring); buffer b is free
-        const int kb = s.k & 1;
-        if (s.jj == 0) mbar_wait(&bars->a_full[kb], (s.k >> 1) & 1);
+      if (fl & F_SVALID) {   // S(g+3): its features are in stage g (skewed ring); buffer b is free
+        const int kb = (fl & F_KB) ? 1 : 0;
+        if (fl & F_SFIRST) mbar_wait(&bars->a_full[kb], (fl & F_APH) ? 1u : 0u);
         const uint64_t dau = shfl64(da0 + (uint64_t)(kb * (C::A_BYTES >> 4)));
         const uint64_t dfu = shfl64(dring_f + soff16);
-        const bool last = s.jj == s.njt - 1;
         if (elect_one()) {
           mma_s2(kbu, dau, dfu, idesc_s);
           commit_one(&bars->s_full[b][h]);
-          if (last) commit_one(&bars->a_empty[kb]);
+          if (fl & F_SLAST) commit_one(&bars->a_empty[kb]);
         }
         __syncwarp();
         if (h == 0) T2_STAMP(8, g);
-        s.advance(args, ntiles);
       }
       if (elect_one()) commit_one(&bars->empty[st]);
       __syncwarp();
-      kv.advance(args, ntiles);
       if (++st == C::STAGES) { st = 0; ph_st ^= 1; }
       if (++b == NB2) { b = 0; ph_b ^= 1; }
     }
