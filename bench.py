@@ -298,7 +298,7 @@ def run_ours(args, cfg):
                 "note": "achieved counts only the algorithmic 2*N^2*T flops; executed_tflops counts every MMA issued",
                 "executed_tflops": exec_flops / (mvm_ms * 1e-3) / 1e12,
                 "executed_frac_of_measured_peak": exec_flops / (mvm_ms * 1e-3) / 1e12 / peak,
-                "tensor_pipe_active_ncu": {"value": 0.61, "source": "profiles/ncu_k1_r01c.txt (sm__pipe_tensor_cycles_active)"}}
+                "tensor_pipe_active_ncu": {"value": 0.636, "source": "profiles/ncu_k1_r01h.txt (sm__pipe_tensor_cycles_active)"}}
         sm_count = torch.cuda.get_device_properties(local).multi_processor_count
         sfu_peak = sm_count * 16 * peaks.get("sm_max_mhz", 1965.0) * 1e6  # MUFU.EX2 per second
         roof["sfu"] = {"achieved_evals_per_s": rows_local * n / (mvm_ms * 1e-3), "peak_evals_per_s": sfu_peak,
@@ -310,8 +310,8 @@ def run_ours(args, cfg):
         roof["traffic"] = 423.86e6 if cfg.name == "C2" else None
         roof["traffic_source"] = "profiles/ncu_k2_r01f.txt (C2)"
     elif roof["bound"] == "tensor":
-        roof["traffic"] = 32.75e6 if cfg.name == "C3" else None
-        roof["traffic_source"] = "profiles/ncu_k1_r01c.txt (C3; compute-bound: V planes / features stay in L2)"
+        roof["traffic"] = 33.01e6 if cfg.name == "C3" else None
+        roof["traffic_source"] = "profiles/ncu_k1_r01h.txt (C3; compute-bound: V planes / features stay in L2)"
     else:
         roof["traffic"] = None
     roof["ms_per_launch"] = mvm_ms
