@@ -29,7 +29,7 @@ import scipy.linalg
 __all__ = [
     "kernel_entries", "KernelOperator", "DenseOperator", "LowRankPlusDiag",
     "hht_rule", "lanczos", "estimate_spectrum", "msminres", "ciq",
-    "pivoted_cholesky", "precond_ciq", "MsminresResult", "CiqResult",
+    "pivoted_cholesky", "precond_ciq", "MsminresResult", "CiqResult", "ciq_vjp",
 ]
 
 
@@ -511,3 +511,31 @@ def precond_ciq(op, pre: LowRankPlusDiag, b: np.ndarray, q: int = 8, max_iters: 
     out = op.mvm(rprime_b) if mode == "sqrt" else rprime_b
     return CiqResult(out, res.t, res.w, res.lambda_min, res.lambda_max, res.iters, res.mvms,
                      res.converged, res.solve)
+
+
+# --------------------------------------------------------------------------------------------
+# Backward pass: vector-Jacobian product of K^{-1/2} b
+# --------------------------------------------------------------------------------------------
+
+def ciq_vjp(op, b: np.ndarray, v: np.ndarray, rule: tuple, max_iters: int = 400, tol: float = 0.0) -> np.ndarray:
+    """Eq. ciq_deriv: back-propagating through each term of the quadrature
+    K^{-1/2} b ~ sum_q w_q (t_q I + K)^{-1} b gives
+
+        v^T (d K^{-1/2} b / d K) ~ -1/2 sum_q w_q (t_q I + K)^{-1} (v b^T + b v^T) (t_q I + K)^{-1}
+                                 = -1/2 sum_q w_q (x_q(v) x_q(b)^T + x_q(b) x_q(v)^T)
+
+    with x_q(u) = (t_q I + K)^{-1} u the shifted solves of msMINRES: the forward pass supplies
+    x_q(b), "another call to the msMINRES algorithm" supplies x_q(v).  Columns of b / v
+    are independent problems whose gradients add (reading G15): returns the dense N x N matrix
+    G = sum_c -1/2 sum_q w_q (x_q(v_c) x_q(b_c)^T + x_q(b_c) x_q(v_c)^T)."""
+    t_q = np.asarray(rule[0], dtype=np.float64)
+    w_q = np.asarray(rule[1], dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    if b.ndim == 1:
+        b, v = b[:, None], v[:, None]
+    xb = msminres(op.mvm, b, t_q, max_iters, tol).x      # (Q, n, t)
+    xv = msminres(op.mvm, v, t_q, max_iters, tol).x
+    g = np.einsum("q,qic,qjc->ij", w_q, xv, xb)
+    return -0.5 * (g + g.T)
+
