@@ -140,6 +140,10 @@ typedef struct {
                               /*    steps: no separate ~10-MVM estimation run.  Ignored with a     */
                               /*    preconditioner, an explicit rule/spectrum, or max_iters <= 24. */
                               /*    Default 0 (separate estimation from lanczos_start, G5).       */
+  int32_t keep_shift_solutions; /* 1: also return the Q shifted solves x_q = (t_q I + K)^{-1} b   */
+  float* shift_solutions;     /*    (the forward solves the backward pass reuses) into     */
+                              /*    shift_solutions, Q x rows x T floats (row-major per shift,     */
+                              /*    ld = T; host or device).  Not with a preconditioner.           */
 } ciq_params;
 
 typedef struct {
@@ -191,6 +195,18 @@ ciq_status ciq_matvec(ciq_ctx* ctx, const float* V, int64_t ldv, int64_t T, floa
  * appending the normalised residual column.  L (N x rank, ldl >= rank, host or device) receives
  * the factor; use it as ciq_precond.L with sigma2 = op.diag for the App. A preconditioner. */
 ciq_status ciq_pivoted_cholesky(ciq_ctx* ctx, int32_t rank, float* L, int64_t ldl);
+
+/* Backward pass of K^{-1/2} B (App. B "Efficient Vector-Jacobi Products for Backpropagation",
+ * eq. ciq_deriv): with the back-propagated gradient V (rows x T, same layout as B),
+ *     G = sum_c -1/2 sum_q w_q ( x_q(v_c) x_q(b_c)^T + x_q(b_c) x_q(v_c)^T ),
+ *     x_q(u) = (t_q I + K)^{-1} u,
+ * i.e. dL/dK for L(K^{-1/2} B) with dL/d(K^{-1/2} B) = V.  Two msMINRES solves (b with the
+ * estimated or given rule, then v with the SAME rule), then the rank-2QT product on the GPU.
+ * G: N x N floats (ld = ldg >= N, host or device).  params->mode is ignored (the derivative is of
+ * K^{-1/2} b); keep_shift_solutions / shift_solutions are ignored.  Single GPU, no preconditioner
+ * (CIQ_ERR_INVALID_ARG otherwise).  info (nullable): the forward solve's info, mvms = both solves. */
+ciq_status ciq_vjp(ciq_ctx* ctx, const float* B, int64_t ldb, const float* V, int64_t ldv, int64_t T,
+                   const ciq_params* params, float* G, int64_t ldg, ciq_info* info);
 
 void ciq_free(ciq_ctx* ctx);
 

@@ -60,7 +60,7 @@ class CiqParams(ctypes.Structure):
                 ("t", POINTER(c_double)), ("w", POINTER(c_double)), ("lanczos_start", c_void_p),
                 ("ld_start", c_int64), ("seed", c_uint64), ("mode", c_int32), ("mvm_impl", c_int32),
                 ("poll_every", c_int32), ("breakdown_tol", c_double), ("profile_kernels", c_int32),
-                ("lanczos_reuse", c_int32)]
+                ("lanczos_reuse", c_int32), ("keep_shift_solutions", c_int32), ("shift_solutions", c_void_p)]
 
 
 class CiqInfo(ctypes.Structure):
@@ -102,6 +102,9 @@ def _load() -> ctypes.CDLL:
     lib.ciq_matvec.restype = c_int32
     lib.ciq_pivoted_cholesky.argtypes = [ctx_p, c_int32, c_void_p, c_int64]
     lib.ciq_pivoted_cholesky.restype = c_int32
+    lib.ciq_vjp.argtypes = [ctx_p, c_void_p, c_int64, c_void_p, c_int64, c_int64, POINTER(CiqParams), c_void_p,
+                            c_int64, POINTER(CiqInfo)]
+    lib.ciq_vjp.restype = c_int32
     lib.ciq_free.argtypes = [ctx_p]
     lib.ciq_free.restype = None
     lib.ciq_status_string.argtypes = [c_int32]
@@ -126,7 +129,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 
-EXPORTED = ["ciq_params_default", "ciq_init", "ciq_apply", "ciq_matvec", "ciq_pivoted_cholesky", "ciq_free",
+EXPORTED = ["ciq_params_default", "ciq_init", "ciq_apply", "ciq_matvec", "ciq_pivoted_cholesky", "ciq_vjp", "ciq_free",
             "ciq_status_string",
             "ciq_last_error", "ciq_shard_rows", "ciq_quadrature_rule", "ciq_tridiag_extremes",
             "ciq_nccl_unique_id", "ciq_loopback_group_create", "ciq_loopback_group_destroy"]
@@ -289,6 +292,20 @@ def ciq_apply(ctx, B, out, params: CiqParams) -> tuple[int, CiqInfo]:
     return st, info
 
 
+def ciq_vjp(ctx, B, V, G, params: CiqParams) -> tuple[int, CiqInfo]:
+    keep: list = []
+    pb, ldb, nb, t = _ptr_ld(B, "B", keep)
+    pv, ldv, nv, tv = _ptr_ld(V, "V", keep)
+    pg, ldg, ng, tg = _ptr_ld(G, "G", keep)
+    if tv != t:
+        raise CiqError(CIQ_ERR_DIM, "V must have the shape of B")
+    info = CiqInfo()
+    st = LIB.ciq_vjp(ctx, pb, ldb, pv, ldv, t, ctypes.byref(params), pg, ldg, ctypes.byref(info))
+    if st not in (CIQ_OK, CIQ_NOT_CONVERGED):
+        raise CiqError(st, LIB.ciq_last_error(ctx).decode())
+    return st, info
+
+
 def ciq_matvec(ctx, V, out, mvm_impl: str = "auto") -> None:
     keep: list = []
     pv, ldv, nv, t = _ptr_ld(V, "V", keep)
@@ -313,7 +330,7 @@ def ciq_free(ctx) -> None:
 def make_params(q: int = 8, max_iters: int = 400, tol: float = 1e-4, mode: str = "sqrt", *, lanczos_iters: int = 10,
                 lanczos_cols: int = 16, lanczos_start=None, rule=None, spectrum=None, seed: int = 2,
                 mvm_impl: str = "auto", poll_every: int = 6, breakdown_tol: float = 1e-6, profile: bool = False,
-                lanczos_reuse: bool = False, keep: list | None = None):
+                lanczos_reuse: bool = False, shift_solutions=None, keep: list | None = None):
     """Build a CiqParams; arrays referenced by it are appended to `keep` (caller keeps them alive)."""
     keep = [] if keep is None else keep
     p = ciq_params_default()
@@ -326,6 +343,13 @@ def make_params(q: int = 8, max_iters: int = 400, tol: float = 1e-4, mode: str =
     p.breakdown_tol = float(breakdown_tol)
     p.profile_kernels = 1 if profile else 0
     p.lanczos_reuse = 1 if lanczos_reuse else 0
+    if shift_solutions is not None:   # Q x rows x T (ld = T): the forward's shifted solves
+        p.keep_shift_solutions = 1
+        if isinstance(shift_solutions, np.ndarray):
+            keep.append(shift_solutions)
+            p.shift_solutions = shift_solutions.ctypes.data
+        else:
+            p.shift_solutions = shift_solutions.data_ptr()
     if lanczos_start is not None:
         ptr, ld, r, c = _ptr_ld(lanczos_start, "lanczos_start", keep)
         p.lanczos_start, p.ld_start = ptr, ld
@@ -363,6 +387,15 @@ class CIQ:
 
     def pivoted_cholesky(self, rank: int, out) -> None:
         ciq_pivoted_cholesky(self.ctx, rank, out)
+
+    def vjp(self, B, V, G, **kw) -> dict:
+        """G <- dL/dK for L(K^{-1/2} B) with back-propagated gradient V (eq. ciq_deriv)."""
+        keep: list = []
+        params, keep = make_params(keep=keep, **kw)
+        st, info = ciq_vjp(self.ctx, B, V, G, params)
+        d = info.as_dict()
+        d["status"] = st
+        return d
 
     def matvec(self, V, out, mvm_impl: str = "auto") -> None:
         ciq_matvec(self.ctx, V, out, mvm_impl)

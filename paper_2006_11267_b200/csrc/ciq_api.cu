@@ -34,6 +34,8 @@ struct Workspace {
   float* p = nullptr;
   float* d = nullptr;      // [2 slots][nq][rows][tp]
   float* y = nullptr;
+  float* xq = nullptr;     // [nq][rows][tp] kept per-shift solutions (keep_shift_solutions)
+  size_t xq_elems = 0;
   double* apart = nullptr; // [mvm blocks][tp]
   double* bpart = nullptr; // [stream blocks][tp]
   double* colsq = nullptr; // [tp]
@@ -187,7 +189,8 @@ int round16(int64_t t) { return (int)((t + 15) / 16 * 16); }
 
 void free_workspace(Workspace& ws) {
   for (auto& b : ws.w) dfree(b);
-  dfree(ws.p); dfree(ws.d); dfree(ws.y); dfree(ws.apart); dfree(ws.bpart); dfree(ws.colsq);
+  dfree(ws.p); dfree(ws.d); dfree(ws.y); dfree(ws.apart); dfree(ws.bpart); dfree(ws.colsq); dfree(ws.xq);
+  ws.xq_elems = 0;
   dfree(ws.scal_mem);
   ws.tp = ws.nq = 0;
 }
@@ -220,7 +223,7 @@ ciq_status ensure_workspace(ciq_ctx* c, int tp, int nq) {
   CUDA_TRY(c, dalloc(&ws.colsq, (size_t)tp));
   // scalar block
   size_t nd = (size_t)tp * 6 + (size_t)nq * tp * 5 + 2 * (size_t)nq;
-  size_t bytes = nd * 8 + (size_t)tp * 8 + (size_t)nq * tp * 4 * 4 + sizeof(Ctrl) + 256;
+  size_t bytes = nd * 8 + (size_t)tp * 8 + (size_t)nq * tp * 4 * 5 + sizeof(Ctrl) + 256;
   CUDA_TRY(c, dalloc(&ws.scal_mem, bytes));
   char* m = ws.scal_mem;
   auto takeD = [&](size_t k) { double* r = reinterpret_cast<double*>(m); m += k * 8; return r; };
@@ -232,6 +235,7 @@ ciq_status ensure_workspace(ciq_ctx* c, int tp, int nq) {
   auto takeF = [&](size_t k) { float* r = reinterpret_cast<float*>(m); m += k * 4; return r; };
   sc.ca = takeF((size_t)nq * tp); sc.cb = takeF((size_t)nq * tp); sc.ce = takeF((size_t)nq * tp);
   sc.cf = takeF((size_t)nq * tp);
+  sc.cphi = takeF((size_t)nq * tp);
   sc.frozen = reinterpret_cast<int*>(m); m += (size_t)tp * 4;
   sc.col_state = reinterpret_cast<int*>(m); m += (size_t)tp * 4;
   m = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(m) + 15) & ~uintptr_t(15));
@@ -1142,6 +1146,66 @@ ciq_status ciq_matvec(ciq_ctx* c, const float* V, int64_t ldv, int64_t T, float*
   return CIQ_OK;
 }
 
+ciq_status ciq_vjp(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int64_t ldv, int64_t T,
+                   const ciq_params* params, float* G, int64_t ldg, ciq_info* info) {
+  if (!c || !B || !V || !G) return CIQ_ERR_INVALID_ARG;
+  if (c->world != 1 || c->has_precond)
+    return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_vjp: single GPU, unpreconditioned operators only");
+  const int64_t n = c->op.n;
+  if (T <= 0 || ldv < T || ldb < T || ldg < n) return set_err(c, CIQ_ERR_DIM, "bad T / leading dimension");
+  ciq_params p;
+  if (params) p = *params; else ciq_params_default(&p);
+  const int nq = p.t ? p.Q : p.Q;
+  if (nq < 1 || nq > CIQ_MAX_Q) return set_err(c, CIQ_ERR_INVALID_ARG, "Q must be in [1, %d]", CIQ_MAX_Q);
+  float *xb = nullptr, *xv = nullptr, *yb = nullptr;
+  double* wd = nullptr;
+  CUDA_TRY(c, dalloc(&xb, (size_t)nq * n * T));
+  CUDA_TRY(c, dalloc(&xv, (size_t)nq * n * T));
+  CUDA_TRY(c, dalloc(&yb, (size_t)n * T));
+  CUDA_TRY(c, dalloc(&wd, (size_t)nq));
+  auto cleanup = [&]() { dfree(xb); dfree(xv); dfree(yb); dfree(wd); };
+  // forward: x_q(b) with the estimated (or given) rule
+  p.mode = CIQ_MODE_INVSQRT;
+  p.keep_shift_solutions = 1;
+  p.shift_solutions = xb;
+  ciq_info i1{};
+  ciq_status st = ciq_apply(c, B, ldb, T, yb, T, &p, &i1);
+  if (st != CIQ_OK && st != CIQ_NOT_CONVERGED) { cleanup(); return st; }
+  // backward: x_q(v) with the same rule ("another call to the msMINRES algorithm")
+  double t[CIQ_MAX_Q], w[CIQ_MAX_Q];
+  for (int q = 0; q < nq; ++q) { t[q] = i1.t[q]; w[q] = i1.w[q]; }
+  p.t = t;
+  p.w = w;
+  p.Q = nq;
+  p.lanczos_reuse = 0;
+  p.shift_solutions = xv;
+  ciq_info i2{};
+  ciq_status st2 = ciq_apply(c, V, ldv, T, yb, T, &p, &i2);
+  if (st2 != CIQ_OK && st2 != CIQ_NOT_CONVERGED) { cleanup(); return st2; }
+  CUDA_TRY(c, cudaMemcpyAsync(wd, w, nq * 8, cudaMemcpyHostToDevice, c->stream));
+  float* gdev = G;
+  float* gtmp = nullptr;
+  const bool gdevice = is_device_ptr(G);
+  if (!gdevice) {
+    CUDA_TRY(c, dalloc(&gtmp, (size_t)n * n));
+    gdev = gtmp;
+  }
+  const int64_t ld = gdevice ? ldg : n;
+  LAUNCH(c, launch_vjp_dense(xb, xv, wd, nq, n, (int)T, (int)T, gdev, ld, c->stream));
+  if (!gdevice) {
+    CUDA_TRY(c, cudaMemcpy2DAsync(G, (size_t)ldg * 4, gtmp, (size_t)n * 4, (size_t)n * 4, (size_t)n,
+                                  cudaMemcpyDeviceToHost, c->stream));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  dfree(gtmp);
+  cleanup();
+  if (info) {
+    *info = i1;
+    info->mvms = i1.mvms + i2.mvms;
+  }
+  return (st == CIQ_OK && st2 == CIQ_OK) ? CIQ_OK : CIQ_NOT_CONVERGED;
+}
+
 ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* out, int64_t ldo,
                      const ciq_params* pp, ciq_info* info) {
   if (!c) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "null ctx");
@@ -1186,6 +1250,14 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   double* tsum_a = c->tsum;        // world > 1: globally summed alpha partials
   double* tsum_b = c->tsum + tp;   // world > 1: globally summed beta^2 partials
   CUDA_TRY(c, cudaMemsetAsync(ws.y, 0, (size_t)rows * tp * 4, s));
+  const bool keep = p.keep_shift_solutions != 0 && p.shift_solutions != nullptr;
+  if (keep) {
+    if (c->pc.on) return set_err(c, CIQ_ERR_INVALID_ARG, "keep_shift_solutions: not with a preconditioner");
+    st = grow(c, &ws.xq, &ws.xq_elems, (size_t)nq * rows * tp);
+    if (st != CIQ_OK) return st;
+    CUDA_TRY(c, cudaMemsetAsync(ws.xq, 0, (size_t)nq * rows * tp * 4, s));
+  }
+  float* xqk = keep ? ws.xq : nullptr;
   CUDA_TRY(c, cudaMemsetAsync(ws.d, 0, (size_t)2 * nq * rows * tp * 4, s));
   Ctrl hctrl{};
   hctrl.max_iters = p.max_iters;
@@ -1302,7 +1374,8 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     begin_timed(c, j, 1);
     LAUNCH(c, launch_lanczos_update(sc, pin, nsplit, (size_t)rows * tp, wcur + c->row0 * tp, wprev + c->row0 * tp,
                                     wnew + c->row0 * tp, &d1, &d2, ws.y, nqe, rows, tp, ws.bpart, 0, s,
-                                    fuse_pack ? c->planes : nullptr, c->inv_scale, c->npad, tc_chunk_cols(tp), c->op.n));
+                                    fuse_pack ? c->planes : nullptr, c->inv_scale, c->npad, tc_chunk_cols(tp), c->op.n,
+                                    xqk));
     end_timed(c);
     if (c->world == 1) {
       LAUNCH(c, launch_givens(sc, ws.bpart, update_blocks(rows), nqe, tp, s));
@@ -1400,7 +1473,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
         float* d2 = dslot[k & 1];
         float* wk = c->stash + (size_t)(k - 1) * wsz;
         LAUNCH(c, launch_lanczos_update(sc, nullptr, 1, 0, nullptr, wk + c->row0 * tp, nullptr, &d1, &d2, ws.y, nq,
-                                        rows, tp, nullptr, 1, s));
+                                        rows, tp, nullptr, 1, s, nullptr, nullptr, 0, 0, 0, xqk));
       }
     }
     CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->max_iters, &hctrl.max_iters, sizeof(int), cudaMemcpyHostToDevice, s));
@@ -1417,7 +1490,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     if (st != CIQ_OK) return st;
 
     const uint64_t key[6] = {c->buf_gen, (uint64_t)tp, (uint64_t)nq, (uint64_t)p.mvm_impl, (uint64_t)block,
-                             (uint64_t)(uintptr_t)ws.d};
+                             (uint64_t)(uintptr_t)ws.d ^ ((uint64_t)(uintptr_t)xqk << 1)};
     if (c->gexec == nullptr || std::memcmp(key, c->gkey, sizeof(key)) != 0) {
       if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
       const int64_t l0 = c->launches;
@@ -1487,9 +1560,14 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     float* d2 = dslot[J & 1];        // d_{J-2}, overwritten by d_J
     float* wv = ws.w[J % 3];
     LAUNCH(c, launch_lanczos_update(sc, nullptr, 1, 0, nullptr, wv + c->row0 * tp, nullptr, &d1, &d2, ws.y, nq, rows, tp,
-                                    nullptr, 1, s));
+                                    nullptr, 1, s, nullptr, nullptr, 0, 0, 0, xqk));
   }
   CUDA_TRY(c, cudaEventRecord(ev.e[3], s));
+  if (keep)
+    for (int q = 0; q < nq; ++q) {
+      st = store_rows(c, ws.xq + (size_t)q * rows * tp, tp, rows, (int)T, p.shift_solutions + (size_t)q * rows * T, T);
+      if (st != CIQ_OK) return st;
+    }
 
   // a7: finalise.  With P: Y = M^{-1/2} b in M-space, R' b = P^{-1/2} Y (eq. precond_sqrt_inverse,
   // P:55-64) and R b = K R' b (eq. precond_sqrt).

@@ -31,6 +31,7 @@ struct Scal {
   int* frozen;        // [tp]   1: column finished (b = 0 or invariant subspace)
   double* c1; double* s1; double* c2; double* s2; double* phibar;   // [Q][tp] Givens state
   float* ca; float* cb; float* ce; float* cf;                       // [Q][tp] pending-update coefs
+  float* cphi;        // [Q][tp] phi of the pending step (x_q += phi d, kept solutions only)
   double* shifts;     // [Q]
   double* weights;    // [Q]
   double* col_rel;    // [tp]   per-column max relative residual of the last Givens step
@@ -110,7 +111,11 @@ cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, si
                                   float* wnew, float* const* d1, float* const* d2, float* y, int nq,
                                   int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s,
                                   __half* planes = nullptr, float* inv_scale = nullptr, int64_t npad = 0, int tn = 0,
-                                  int64_t n = 0);   // planes: also write W_{j+1}'s split-fp16 MVM operand
+                                  int64_t n = 0,    // planes: also write W_{j+1}'s split-fp16 MVM operand
+                                  float* xq = nullptr);   // [Q][rows][tp]: also accumulate x_q += phi_q d_q
+// Backward pass: G[i][j] = -1/2 sum_{q,c} w_q (xv[q][i][c] xb[q][j][c] + xb[q][i][c] xv[q][j][c])
+cudaError_t launch_vjp_dense(const float* xb, const float* xv, const double* w, int nq, int64_t n, int tp, int cols,
+                             float* g, int64_t ldg, cudaStream_t s);
 cudaError_t launch_alpha_from_sum(const Scal& sc, const double* sums, int tp, cudaStream_t s);
 cudaError_t launch_sum_ranks(const double* g, int world, int m, double* out, cudaStream_t s);
 cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s);

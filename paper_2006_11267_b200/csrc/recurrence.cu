@@ -174,7 +174,7 @@ __global__ void init_state_kernel(Scal sc, int nq, int tp, const double* __restr
       int k = q * tp + c;
       sc.c1[k] = 1.0; sc.s1[k] = 0.0; sc.c2[k] = 1.0; sc.s2[k] = 0.0;
       sc.phibar[k] = b1;
-      sc.ca[k] = 0.f; sc.cb[k] = 0.f; sc.ce[k] = 0.f; sc.cf[k] = 0.f;
+      sc.ca[k] = 0.f; sc.cb[k] = 0.f; sc.ce[k] = 0.f; sc.cf[k] = 0.f; sc.cphi[k] = 0.f;
     }
   }
   if (threadIdx.x == 0) {
@@ -247,7 +247,8 @@ CIQ_DEVICE float pack_scale(double nrm, double sqrt_n, float* inv) {
 __global__ void __launch_bounds__(kThreads, 3) lanczos_update_kernel(
     Scal sc, const float* __restrict__ p, int nsplit, size_t split_stride, const float* __restrict__ wcur, const float* __restrict__ wprev,
     float* __restrict__ wnew, const float* __restrict__ d1base, float* __restrict__ d2base, int64_t qstride,
-    float* __restrict__ y, int nq, int64_t rows, int tp, double* __restrict__ bpart, int final_only, PackOut pk) {
+    float* __restrict__ y, int nq, int64_t rows, int tp, double* __restrict__ bpart, int final_only, PackOut pk,
+    float* __restrict__ xq) {
   constexpr int QB = 2;
   const Ctrl* ctrl = sc.ctrl;
   if (!final_only && ctrl->done) return;
@@ -339,6 +340,13 @@ __global__ void __launch_bounds__(kThreads, 3) lanczos_update_kernel(
               dn.z = fmaf(a.z, wp.z, fmaf(bq.z, x1[u].z, e.z * x2[u].z));
               dn.w = fmaf(a.w, wp.w, fmaf(bq.w, x1[u].w, e.w * x2[u].w));
               *reinterpret_cast<float4*>(d2base + (q0 + u) * qstride + off) = dn;
+              if (xq != nullptr) {   // kept per-shift solutions (backward pass)
+                const float4 ph = __ldg(reinterpret_cast<const float4*>(sc.cphi + k));
+                float4 xx = *reinterpret_cast<const float4*>(xq + (q0 + u) * qstride + off);
+                xx.x = fmaf(ph.x, dn.x, xx.x); xx.y = fmaf(ph.y, dn.y, xx.y);
+                xx.z = fmaf(ph.z, dn.z, xx.z); xx.w = fmaf(ph.w, dn.w, xx.w);
+                *reinterpret_cast<float4*>(xq + (q0 + u) * qstride + off) = xx;
+              }
               yy.x = fmaf(f.x, dn.x, yy.x); yy.y = fmaf(f.y, dn.y, yy.y);
               yy.z = fmaf(f.z, dn.z, yy.z); yy.w = fmaf(f.w, dn.w, yy.w);
             }
@@ -376,7 +384,7 @@ __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __re
   for (int q = threadIdx.x; q < nq; q += 256) {
     const int k = q * tp + c;
     if (frozen) {
-      sc.ca[k] = 0.f; sc.cb[k] = 0.f; sc.ce[k] = 0.f; sc.cf[k] = 0.f;
+      sc.ca[k] = 0.f; sc.cb[k] = 0.f; sc.ce[k] = 0.f; sc.cf[k] = 0.f; sc.cphi[k] = 0.f;
       continue;
     }
     const double a = a_j + sc.shifts[q];
@@ -395,6 +403,7 @@ __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __re
     sc.cb[k] = (float)(-delta / gamma);
     sc.ce[k] = (float)(-eps / gamma);
     sc.cf[k] = (float)(sc.weights[q] * phi);   // Y += w_q phi d
+    sc.cphi[k] = (float)phi;                    // x_q += phi d (kept solutions)
     sc.c2[k] = c1; sc.s2[k] = s1; sc.c1[k] = cs; sc.s1[k] = sn;
     rel = fmax(rel, fabs(phib_new) / b1);
   }
@@ -523,6 +532,57 @@ __global__ void sum_splits_kernel(const float* __restrict__ parts, int nsplit, s
   reinterpret_cast<float4*>(out)[e] = acc;
 }
 
+
+// ---- backward pass ----
+// G[i][j] = -1/2 sum_q w_q sum_c (xv[q][i][c] xb[q][j][c] + xb[q][i][c] xv[q][j][c]): a 64 x 64
+// output tile per CTA, 4 x 4 per thread, contraction over (q, c) staged through shared memory in
+// steps of 16 columns; fp32 with fixed summation order (deterministic).
+__global__ void __launch_bounds__(256) vjp_dense_kernel(const float* __restrict__ xb, const float* __restrict__ xv,
+                                                        const double* __restrict__ w, int nq, int64_t n, int tp,
+                                                        int cols, float* __restrict__ g, int64_t ldg) {
+  __shared__ float av[16][65], ab[16][65], bb[16][65], bv[16][65];
+  const int64_t i0 = (int64_t)blockIdx.y * 64, j0 = (int64_t)blockIdx.x * 64;
+  const int tid = threadIdx.x, ti = tid / 16, tj = tid % 16;
+  float acc[4][4] = {};
+  for (int q = 0; q < nq; ++q) {
+    const float wq = (float)w[q];
+    const size_t qo = (size_t)q * n * tp;
+    for (int c0 = 0; c0 < cols; c0 += 16) {
+      __syncthreads();
+      for (int e = tid; e < 16 * 64; e += 256) {
+        const int cc = e / 64, r = e % 64;
+        const bool okc = c0 + cc < cols;
+        const int64_t ii = i0 + r, jj = j0 + r;
+        av[cc][r] = (okc && ii < n) ? wq * xv[qo + ii * tp + c0 + cc] : 0.f;
+        ab[cc][r] = (okc && ii < n) ? wq * xb[qo + ii * tp + c0 + cc] : 0.f;
+        bb[cc][r] = (okc && jj < n) ? xb[qo + jj * tp + c0 + cc] : 0.f;
+        bv[cc][r] = (okc && jj < n) ? xv[qo + jj * tp + c0 + cc] : 0.f;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) {
+        float a1[4], a2[4], b1[4], b2[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          a1[x] = av[cc][ti * 4 + x]; a2[x] = ab[cc][ti * 4 + x];
+          b1[x] = bb[cc][tj * 4 + x]; b2[x] = bv[cc][tj * 4 + x];
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y2 = 0; y2 < 4; ++y2) acc[x][y2] = fmaf(a1[x], b1[y2], fmaf(a2[x], b2[y2], acc[x][y2]));
+      }
+    }
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y2 = 0; y2 < 4; ++y2) {
+      const int64_t i = i0 + ti * 4 + x, j = j0 + tj * 4 + y2;
+      if (i < n && j < n) g[i * ldg + j] = -0.5f * acc[x][y2];
+    }
+}
+
 inline unsigned nb_elem(int64_t e, int bs) { return (unsigned)((e + bs - 1) / bs); }
 
 }  // namespace
@@ -597,13 +657,13 @@ cudaError_t launch_alpha(const Scal& sc, const double* apart, int nblk, int tp, 
 cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, size_t split_stride, const float* wcur, const float* wprev,
                                   float* wnew, float* const* d1, float* const* d2, float* y, int nq,
                                   int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s,
-                                  __half* planes, float* inv_scale, int64_t npad, int tn, int64_t n) {
+                                  __half* planes, float* inv_scale, int64_t npad, int tn, int64_t n, float* xq) {
   const int64_t qstride = rows * tp;
   PackOut pk{planes, inv_scale, npad, tn, sqrt((double)n)};
   dim3 grid = stream_grid(rows, tp);
   grid.x = (unsigned)update_blocks(rows);
   lanczos_update_kernel<<<grid, kThreads, 0, s>>>(sc, p, nsplit, split_stride, wcur, wprev, wnew, d1[0], d2[0],
-                                                                    qstride, y, nq, rows, tp, bpart, final_only, pk);
+                                                                    qstride, y, nq, rows, tp, bpart, final_only, pk, xq);
   return cudaGetLastError();
 }
 cudaError_t launch_alpha_from_sum(const Scal& sc, const double* sums, int tp, cudaStream_t s) {
@@ -634,6 +694,13 @@ cudaError_t launch_lanczos_coeffs(const double* h1, const double* h2, const doub
                                   int tp, double bd_tol, double* alphas, double* betas, int* len, double* inv_beta,
                                   cudaStream_t s) {
   lanczos_coeffs_kernel<<<1, 256, 0, s>>>(h1, h2, bsq, j, tp, bd_tol, alphas, betas, len, inv_beta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vjp_dense(const float* xb, const float* xv, const double* w, int nq, int64_t n, int tp, int cols,
+                             float* g, int64_t ldg, cudaStream_t s) {
+  dim3 grid((unsigned)((n + 63) / 64), (unsigned)((n + 63) / 64));
+  vjp_dense_kernel<<<grid, 256, 0, s>>>(xb, xv, w, nq, n, tp, cols, g, ldg);
   return cudaGetLastError();
 }
 

@@ -305,3 +305,58 @@ def test_materialized_operator_mvm_and_solve(kind):
     refs = ciq(op, b[:, cols].astype(np.float64), q=8, max_iters=200, tol=0.0, mode="invsqrt", rule=rule)
     assert np.max(np.abs(refs.solve.phibar) / refs.solve.beta1) < 1e-5
     assert relerr(got[:, cols], refs.out) < 1e-4
+
+
+# ------------------------------------------------------------------------------------------------
+# backward pass: kept shifted solves and the dense VJP
+# ------------------------------------------------------------------------------------------------
+
+def test_keep_shift_solutions_match_oracle_and_reuse_replay():
+    from oracle import msminres
+    cfg = workloads.scaled(workloads.CONFIGS["C3"], n=900, t=3)
+    inp = workloads.make_inputs(cfg)
+    op = oracle_op(cfg, inp)
+    lmin, lmax, _, _ = estimate_spectrum(op.mvm, inp["S"], 10, lower_bound=cfg.sigma2)
+    rule = hht_rule(lmin, lmax, 8)
+    j = 70
+    ref = msminres(op.mvm, inp["B"].astype(np.float64), rule[0], j, 0.0)
+    with gpu_ctx(cfg, inp) as g:
+        out = torch.empty((cfg.n, cfg.t), device="cuda")
+        xs = torch.zeros((8, cfg.n, cfg.t), device="cuda")
+        g.apply(dev(inp["B"]), out, q=8, max_iters=j, tol=0.0, mode="invsqrt", rule=rule, shift_solutions=xs)
+        got = xs.cpu().numpy().astype(np.float64)
+        # the lanczos_reuse warm-up + replay accumulates the same x_q
+        xs2 = torch.zeros_like(xs)
+        info = g.apply(dev(inp["B"]), out, q=8, max_iters=j, tol=0.0, mode="invsqrt", lanczos_reuse=True,
+                       shift_solutions=xs2)
+        r2 = (np.array(info["t"][:8]), np.array(info["w"][:8]))
+        xs3 = torch.zeros_like(xs)
+        g.apply(dev(inp["B"]), out, q=8, max_iters=j, tol=0.0, mode="invsqrt", rule=r2, shift_solutions=xs3)
+    assert np.max(np.abs(ref.phibar) / ref.beta1) < 1e-5
+    for q in range(8):
+        assert relerr(got[q], ref.x[q]) < 1e-4
+    assert relerr(xs2.cpu().numpy(), xs3.cpu().numpy()) < 1e-6
+    # Y = sum_q w_q x_q (eq. contour_integral_quad)
+    np.testing.assert_allclose(np.einsum("q,qnt->nt", rule[1], got), np.einsum("q,qnt->nt", rule[1], ref.x),
+                               rtol=0, atol=1e-4 * np.abs(np.einsum("q,qnt->nt", rule[1], ref.x)).max())
+
+
+def test_vjp_matches_oracle():
+    from oracle import ciq_vjp
+    cfg = workloads.scaled(workloads.CONFIGS["C3"], n=500, t=2)
+    inp = workloads.make_inputs(cfg)
+    op = oracle_op(cfg, inp)
+    v = workloads.rhs(cfg.n, cfg.t, seed=7)
+    j = 90
+    with gpu_ctx(cfg, inp) as g:
+        gmat = torch.empty((cfg.n, cfg.n), device="cuda")
+        info = g.vjp(dev(inp["B"]), dev(v), gmat, q=8, max_iters=j, tol=0.0, lanczos_start=dev(inp["S"]))
+        got = gmat.cpu().numpy().astype(np.float64)
+        ghost = np.zeros((cfg.n, cfg.n), dtype=np.float32)
+        g.vjp(inp["B"], v, ghost, q=8, max_iters=j, tol=0.0, lanczos_start=inp["S"])
+    rule = (np.array(info["t"][:8]), np.array(info["w"][:8]))
+    ref = ciq_vjp(op, inp["B"], v, rule, max_iters=j)
+    assert info["mvms"] == 2 * j + 10
+    assert relerr(got, ref) < 1e-4
+    np.testing.assert_allclose(got, got.T, rtol=0, atol=1e-6 * np.abs(got).max())
+    np.testing.assert_array_equal(ghost, gmat.cpu().numpy())
