@@ -1,0 +1,39 @@
+"""Time ciq_vjp (backward pass) on a BASELINE config: forward solve with kept shifted
+solves + the v solve with the same rule + the dense G product.  python scripts/time_vjp.py [C2]"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2006_11267_b200 as pb  # noqa: E402
+import workloads  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "C2"
+cfg = workloads.CONFIGS[name]
+inp = workloads.make_inputs(cfg)
+dv = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()  # noqa: E731
+if cfg.kind == "dense":
+    g = pb.CIQ("dense", K=dv(inp["K"]), diag=cfg.sigma2)
+else:
+    g = pb.CIQ(cfg.kind, X=dv(inp["X"]), lengthscale=cfg.lengthscale, outputscale=cfg.outputscale, diag=cfg.sigma2)
+b, v = dv(inp["B"]), dv(workloads.rhs(cfg.n, cfg.t, seed=7))
+gm = torch.empty((cfg.n, cfg.n), device="cuda")
+kw = dict(q=cfg.q, max_iters=cfg.max_iters, tol=cfg.tol, lanczos_start=dv(inp["S"]))
+out = torch.empty_like(b)
+for _ in range(2):
+    g.vjp(b, v, gm, **kw)
+e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+e0.record()
+info_f = g.apply(b, out, mode="invsqrt", **kw)
+e1.record()
+info = g.vjp(b, v, gm, **kw)
+e2.record()
+e2.synchronize()
+fwd, vjp = e0.elapsed_time(e1), e1.elapsed_time(e2)
+n, t, q = cfg.n, cfg.t, cfg.q
+gflop = 2.0 * 2.0 * n * n * q * t / 1e9
+print(json.dumps({"config": name, "forward_ms": fwd, "vjp_ms": vjp, "vjp_over_forward": vjp / fwd,
+                  "J": info["iters"], "mvms": info["mvms"], "G_product_gflop": gflop}))
