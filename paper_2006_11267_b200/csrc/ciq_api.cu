@@ -1155,7 +1155,7 @@ ciq_status ciq_vjp(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int6
   if (T <= 0 || ldv < T || ldb < T || ldg < n) return set_err(c, CIQ_ERR_DIM, "bad T / leading dimension");
   ciq_params p;
   if (params) p = *params; else ciq_params_default(&p);
-  const int nq = p.t ? p.Q : p.Q;
+  const int nq = p.Q;
   if (nq < 1 || nq > CIQ_MAX_Q) return set_err(c, CIQ_ERR_INVALID_ARG, "Q must be in [1, %d]", CIQ_MAX_Q);
   float *xb = nullptr, *xv = nullptr, *yb = nullptr;
   double* wd = nullptr;

@@ -534,23 +534,24 @@ __global__ void sum_splits_kernel(const float* __restrict__ parts, int nsplit, s
 
 
 // ---- backward pass ----
-// G[i][j] = -1/2 sum_q w_q sum_c (xv[q][i][c] xb[q][j][c] + xb[q][i][c] xv[q][j][c]): a 64 x 64
-// output tile per CTA, 4 x 4 per thread, contraction over (q, c) staged through shared memory in
-// steps of 16 columns; fp32 with fixed summation order (deterministic).
+// G[i][j] = -1/2 sum_q w_q sum_c (xv[q][i][c] xb[q][j][c] + xb[q][i][c] xv[q][j][c]): a 128 x 128
+// output tile per CTA, 8 x 8 per thread (4 FMAs per shared-memory load), contraction over (q, c)
+// staged through shared memory 16 columns at a time; fp32, fixed summation order (deterministic).
 __global__ void __launch_bounds__(256) vjp_dense_kernel(const float* __restrict__ xb, const float* __restrict__ xv,
                                                         const double* __restrict__ w, int nq, int64_t n, int tp,
                                                         int cols, float* __restrict__ g, int64_t ldg) {
-  __shared__ float av[16][65], ab[16][65], bb[16][65], bv[16][65];
-  const int64_t i0 = (int64_t)blockIdx.y * 64, j0 = (int64_t)blockIdx.x * 64;
+  constexpr int TBV = 128, KS = 16;
+  __shared__ float av[KS][TBV + 4], ab[KS][TBV + 4], bb[KS][TBV + 4], bv[KS][TBV + 4];
+  const int64_t i0 = (int64_t)blockIdx.y * TBV, j0 = (int64_t)blockIdx.x * TBV;
   const int tid = threadIdx.x, ti = tid / 16, tj = tid % 16;
-  float acc[4][4] = {};
+  float acc[8][8] = {};
   for (int q = 0; q < nq; ++q) {
     const float wq = (float)w[q];
     const size_t qo = (size_t)q * n * tp;
-    for (int c0 = 0; c0 < cols; c0 += 16) {
+    for (int c0 = 0; c0 < cols; c0 += KS) {
       __syncthreads();
-      for (int e = tid; e < 16 * 64; e += 256) {
-        const int cc = e / 64, r = e % 64;
+      for (int e = tid; e < KS * TBV; e += 256) {
+        const int r = e / KS, cc = e % KS;   // consecutive threads read consecutive columns of a row
         const bool okc = c0 + cc < cols;
         const int64_t ii = i0 + r, jj = j0 + r;
         av[cc][r] = (okc && ii < n) ? wq * xv[qo + ii * tp + c0 + cc] : 0.f;
@@ -559,28 +560,34 @@ __global__ void __launch_bounds__(256) vjp_dense_kernel(const float* __restrict_
         bv[cc][r] = (okc && jj < n) ? xv[qo + jj * tp + c0 + cc] : 0.f;
       }
       __syncthreads();
+#pragma unroll 4
+      for (int cc = 0; cc < KS; ++cc) {
+        float a1[8], a2[8], b1[8], b2[8];
 #pragma unroll
-      for (int cc = 0; cc < 16; ++cc) {
-        float a1[4], a2[4], b1[4], b2[4];
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          a1[x] = av[cc][ti * 4 + x]; a2[x] = ab[cc][ti * 4 + x];
-          b1[x] = bb[cc][tj * 4 + x]; b2[x] = bv[cc][tj * 4 + x];
+        for (int x = 0; x < 8; x += 4) {
+          *reinterpret_cast<float4*>(&a1[x]) = *reinterpret_cast<const float4*>(&av[cc][ti * 4 + x * 16]);
+          *reinterpret_cast<float4*>(&a2[x]) = *reinterpret_cast<const float4*>(&ab[cc][ti * 4 + x * 16]);
+          *reinterpret_cast<float4*>(&b1[x]) = *reinterpret_cast<const float4*>(&bb[cc][tj * 4 + x * 16]);
+          *reinterpret_cast<float4*>(&b2[x]) = *reinterpret_cast<const float4*>(&bv[cc][tj * 4 + x * 16]);
         }
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
+        for (int x = 0; x < 8; ++x)
 #pragma unroll
-          for (int y2 = 0; y2 < 4; ++y2) acc[x][y2] = fmaf(a1[x], b1[y2], fmaf(a2[x], b2[y2], acc[x][y2]));
+          for (int y2 = 0; y2 < 8; ++y2) acc[x][y2] = fmaf(a1[x], b1[y2], fmaf(a2[x], b2[y2], acc[x][y2]));
       }
     }
   }
+  // thread (ti, tj) owns rows ti*4 + {0..3} and ti*4 + 64 + {0..3}, likewise columns
 #pragma unroll
-  for (int x = 0; x < 4; ++x)
+  for (int x = 0; x < 8; ++x) {
+    const int64_t i = i0 + ti * 4 + (x & 3) + (x >> 2) * 64;
+    if (i >= n) continue;
 #pragma unroll
-    for (int y2 = 0; y2 < 4; ++y2) {
-      const int64_t i = i0 + ti * 4 + x, j = j0 + tj * 4 + y2;
-      if (i < n && j < n) g[i * ldg + j] = -0.5f * acc[x][y2];
+    for (int y2 = 0; y2 < 8; ++y2) {
+      const int64_t j = j0 + tj * 4 + (y2 & 3) + (y2 >> 2) * 64;
+      if (j < n) g[i * ldg + j] = -0.5f * acc[x][y2];
     }
+  }
 }
 
 inline unsigned nb_elem(int64_t e, int bs) { return (unsigned)((e + bs - 1) / bs); }
@@ -699,7 +706,7 @@ cudaError_t launch_lanczos_coeffs(const double* h1, const double* h2, const doub
 
 cudaError_t launch_vjp_dense(const float* xb, const float* xv, const double* w, int nq, int64_t n, int tp, int cols,
                              float* g, int64_t ldg, cudaStream_t s) {
-  dim3 grid((unsigned)((n + 63) / 64), (unsigned)((n + 63) / 64));
+  dim3 grid((unsigned)((n + 127) / 128), (unsigned)((n + 127) / 128));
   vjp_dense_kernel<<<grid, 256, 0, s>>>(xb, xv, w, nq, n, tp, cols, g, ldg);
   return cudaGetLastError();
 }
