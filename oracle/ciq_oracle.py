@@ -30,6 +30,7 @@ __all__ = [
     "kernel_entries", "KernelOperator", "DenseOperator", "LowRankPlusDiag",
     "hht_rule", "lanczos", "estimate_spectrum", "msminres", "ciq",
     "pivoted_cholesky", "precond_ciq", "MsminresResult", "CiqResult", "ciq_vjp",
+    "PosteriorOperator", "thompson_step",
 ]
 
 
@@ -539,3 +540,61 @@ def ciq_vjp(op, b: np.ndarray, v: np.ndarray, rule: tuple, max_iters: int = 400,
     g = np.einsum("q,qic,qjc->ij", w_q, xv, xb)
     return -0.5 * (g + g.T)
 
+
+
+# --------------------------------------------------------------------------------------------
+# Thompson sampling (SS5.2, eq. thompson_sample)
+# --------------------------------------------------------------------------------------------
+
+class PosteriorOperator:
+    """COV*(X*) + jitter I, the GP posterior covariance at the candidates X* given noisy training
+    data (X, y) ("posterior mean and covariance of the Gaussian process at the candidate
+    set"), from the textbook conditioning formulas:
+
+        mu*  = K*x (Kxx + noise I)^{-1} y
+        COV* = K** - K*x (Kxx + noise I)^{-1} Kx*
+
+    K** is applied matrix-free (a ``KernelOperator`` on X* whose ``sigma2`` is the jitter); the
+    training block is factorised densely once (Cholesky, n small: the paper's BO runs have <= 100
+    evaluations).  ``mvm`` is the definition written out: K** v - K*x solve(Kxx + noise I,
+    Kx* v).  ``sigma2`` = jitter is the rigorous lower bound on lambda_min (COV* is PSD; reading G6)."""
+
+    def __init__(self, x_cand, x_train, y_train, kind: str, lengthscale=1.0, outputscale: float = 1.0,
+                 noise: float = 1e-2, jitter: float = 1e-4):
+        self.kss = KernelOperator(x_cand, kind, lengthscale, outputscale, jitter)
+        self.n = self.kss.n
+        self.sigma2 = float(jitter)
+        self.noise = float(noise)
+        xt = np.asarray(x_train, dtype=np.float64)
+        self.kxx = kernel_entries(xt, xt, kind, lengthscale, outputscale) + self.noise * np.eye(xt.shape[0])
+        self.kxs = kernel_entries(xt, self.kss.x, kind, lengthscale, outputscale)      # m x N
+        self.cho = scipy.linalg.cho_factor(self.kxx, lower=True)
+        self.mean = self.kxs.T @ scipy.linalg.cho_solve(self.cho, np.asarray(y_train, dtype=np.float64))
+        self.mvm_count = 0
+
+    def mvm(self, v: np.ndarray) -> np.ndarray:
+        self.mvm_count += 1
+        v = np.asarray(v, dtype=np.float64)
+        return self.kss.mvm(v) - self.kxs.T @ scipy.linalg.cho_solve(self.cho, self.kxs @ v)
+
+    def mvm_rows(self, rows: np.ndarray, v: np.ndarray) -> np.ndarray:
+        v = np.asarray(v, dtype=np.float64)
+        rows = np.asarray(rows)
+        return self.kss.mvm_rows(rows, v) - self.kxs[:, rows].T @ scipy.linalg.cho_solve(self.cho, self.kxs @ v)
+
+    def dense(self) -> np.ndarray:
+        return self.kss.dense() - self.kxs.T @ scipy.linalg.cho_solve(self.cho, self.kxs)
+
+
+def thompson_step(post: PosteriorOperator, eps: np.ndarray, q: int = 8, max_iters: int = 400, tol: float = 1e-4,
+                  lanczos_start: np.ndarray | None = None, rule: tuple | None = None):
+    """Eq. thompson_sample: x~ = argmin( mu*(X*) + COV*(X*)^{1/2} eps ), one candidate
+    index per column of eps (each column one posterior sample), COV*^{1/2} eps by msMINRES-CIQ
+    (``ciq`` in sqrt mode on ``post``); ties broken by the lowest index.
+    Returns (indices, samples, CiqResult)."""
+    eps = np.asarray(eps, dtype=np.float64)
+    if eps.ndim == 1:
+        eps = eps[:, None]
+    r = ciq(post, eps, q=q, max_iters=max_iters, tol=tol, mode="sqrt", lanczos_start=lanczos_start, rule=rule)
+    samples = post.mean[:, None] + r.out
+    return np.argmin(samples, axis=0), samples, r

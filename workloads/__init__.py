@@ -30,6 +30,7 @@ SEED_POINTS = 0
 SEED_RHS = 1
 SEED_LANCZOS = 2
 SEED_MINIBATCH = 3
+SEED_TRAIN = 4
 
 
 def _gen(seed: int) -> torch.Generator:
@@ -186,3 +187,58 @@ def config_inputs(cfg: Config) -> dict:
 
 def kappa_hint(lambda_max: float, sigma2: float) -> float:
     return lambda_max / sigma2 if sigma2 > 0 else math.inf
+
+
+# ---- Thompson-sampling workload ----
+
+_H6_ALPHA = (1.0, 1.2, 3.0, 3.2)
+_H6_A = ((10, 3, 17, 3.5, 1.7, 8), (0.05, 10, 17, 0.1, 8, 14), (3, 3.5, 1.7, 10, 17, 8), (17, 8, 0.05, 10, 0.1, 14))
+_H6_P = ((1312, 1696, 5569, 124, 8283, 5886), (2329, 4135, 8307, 3736, 1004, 9991),
+         (2348, 1451, 3522, 2883, 3047, 6650), (4047, 8828, 8732, 5743, 1091, 381))
+
+
+def hartmann6(x: np.ndarray) -> np.ndarray:
+    """The 6-d Hartmann test function of the paper's BO experiment (its standard published
+    form): f(x) = -sum_i alpha_i exp(-sum_j A_ij (x_j - P_ij)^2) on [0,1]^6, fp64."""
+    x = np.asarray(x, dtype=np.float64)
+    f = np.zeros(x.shape[0])
+    for i in range(4):
+        a = np.asarray(_H6_A[i], dtype=np.float64)
+        p = np.asarray(_H6_P[i], dtype=np.float64) * 1e-4
+        f -= _H6_ALPHA[i] * np.exp(-np.sum(a * (x - p) ** 2, axis=1))
+    return f
+
+
+@dataclasses.dataclass(frozen=True)
+class ThompsonConfig:
+    """Thompson-sampling step on Hartmann-6: n candidates U[0,1]^6 (the
+    candidate set), m evaluated training points U[0,1]^6 with standardised Hartmann values,
+    t posterior samples.  Kernel hyper-parameters are those of C3 (the hot path's shape); `noise`
+    is the training-data noise, `jitter` the diagonal added to COV* (C3's sigma2)."""
+    name: str
+    n: int
+    m: int
+    t: int
+    kind: str = "rbf"
+    lengthscale: float = 0.15
+    outputscale: float = 1.0
+    noise: float = 1e-3
+    jitter: float = 0.05
+    q: int = 8
+    max_iters: int = 400
+    tol: float = 1e-4
+
+
+THOMPSON = {
+    "T1": ThompsonConfig("T1", 50_000, 100, 64),      # C3's shape: 50k candidates, 100 evaluations (P:743)
+}
+
+
+def thompson_inputs(cfg: ThompsonConfig) -> dict:
+    """Candidates Xs (n x 6), training Xt (m x 6), y (m, standardised Hartmann-6 values, fp64),
+    samples' eps (n x t, N(0,1)), Lanczos start S (n x 16); float32 except y."""
+    xs = points(cfg.n, 6)
+    xt = points(cfg.m, 6, seed=SEED_TRAIN)
+    f = hartmann6(xt.astype(np.float64))
+    y = (f - f.mean()) / f.std()
+    return {"Xs": xs, "Xt": xt, "y": y.astype(np.float32), "eps": rhs(cfg.n, cfg.t), "S": lanczos_start(cfg.n, 16)}
