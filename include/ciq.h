@@ -208,6 +208,31 @@ ciq_status ciq_pivoted_cholesky(ciq_ctx* ctx, int32_t rank, float* L, int64_t ld
 ciq_status ciq_vjp(ciq_ctx* ctx, const float* B, int64_t ldb, const float* V, int64_t ldv, int64_t T,
                    const ciq_params* params, float* G, int64_t ldg, ciq_info* info);
 
+/* Thompson sampling (SS5.2, eq. thompson_sample).
+ * ciq_set_posterior turns a matrix-free kernel context built on the candidate set X* (ciq_init
+ * with op.X = X*, op.diag = the jitter) into the GP posterior covariance operator at X*,
+ *     COV* + jitter I = K** + jitter I - K*x (Kxx + noise I)^{-1} Kx*,
+ * with posterior mean mu* = K*x (Kxx + noise I)^{-1} y ("posterior mean and covariance of the
+ * Gaussian process at the candidate set").  Every later ciq_apply / ciq_matvec /
+ * ciq_thompson on ctx uses this operator (lambda_min lower bound: the jitter, COV* being PSD).
+ *   Xt: m x d training inputs (row-major, ldxt >= d, host or device; same kernel and
+ *       lengthscale as the ctx), y: m training targets (host or device; NULL = zero mean),
+ *   noise > 0: the training-data noise.  1 <= m <= 4096.
+ * The training block is factorised once on the host in fp64 (Cholesky of Kxx + noise I and L^{-1});
+ * U = K*x L^{-T} (N x m, fp64) and mu* are built on the device.  Call again to replace the data.
+ * Single GPU, kernel operators, no preconditioner: CIQ_ERR_INVALID_ARG otherwise;
+ * CIQ_ERR_NOT_PD if Kxx + noise I is not positive definite in fp64. */
+ciq_status ciq_set_posterior(ciq_ctx* ctx, const float* Xt, int64_t ldxt, int64_t m, const float* y, double noise);
+
+/* One Thompson-sampling step (eq. thompson_sample): for each column c of eps (N x T, ld =
+ * ld_eps >= T, host or device; each column one standard-normal draw)
+ *     f_c = mu* + COV*^{1/2} eps_c  (msMINRES-CIQ, sqrt mode; params->mode ignored),
+ *     idx[c] = argmin_j f_c[j]  (lowest j among equal minima; int64, host or device).
+ * samples (nullable): receives f (N x T, ld = ld_samples >= T, host or device).
+ * Requires ciq_set_posterior first (CIQ_ERR_INVALID_ARG otherwise).  info as for ciq_apply. */
+ciq_status ciq_thompson(ciq_ctx* ctx, const float* eps, int64_t ld_eps, int64_t T, const ciq_params* params,
+                        int64_t* idx, float* samples, int64_t ld_samples, ciq_info* info);
+
 void ciq_free(ciq_ctx* ctx);
 
 const char* ciq_status_string(ciq_status s);

@@ -105,6 +105,11 @@ def _load() -> ctypes.CDLL:
     lib.ciq_vjp.argtypes = [ctx_p, c_void_p, c_int64, c_void_p, c_int64, c_int64, POINTER(CiqParams), c_void_p,
                             c_int64, POINTER(CiqInfo)]
     lib.ciq_vjp.restype = c_int32
+    lib.ciq_set_posterior.argtypes = [ctx_p, c_void_p, c_int64, c_int64, c_void_p, c_double]
+    lib.ciq_set_posterior.restype = c_int32
+    lib.ciq_thompson.argtypes = [ctx_p, c_void_p, c_int64, c_int64, POINTER(CiqParams), c_void_p, c_void_p, c_int64,
+                                 POINTER(CiqInfo)]
+    lib.ciq_thompson.restype = c_int32
     lib.ciq_free.argtypes = [ctx_p]
     lib.ciq_free.restype = None
     lib.ciq_status_string.argtypes = [c_int32]
@@ -129,7 +134,8 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 
-EXPORTED = ["ciq_params_default", "ciq_init", "ciq_apply", "ciq_matvec", "ciq_pivoted_cholesky", "ciq_vjp", "ciq_free",
+EXPORTED = ["ciq_params_default", "ciq_init", "ciq_apply", "ciq_matvec", "ciq_pivoted_cholesky", "ciq_vjp", "ciq_set_posterior",
+            "ciq_thompson", "ciq_free",
             "ciq_status_string",
             "ciq_last_error", "ciq_shard_rows", "ciq_quadrature_rule", "ciq_tridiag_extremes",
             "ciq_nccl_unique_id", "ciq_loopback_group_create", "ciq_loopback_group_destroy"]
@@ -306,6 +312,47 @@ def ciq_vjp(ctx, B, V, G, params: CiqParams) -> tuple[int, CiqInfo]:
     return st, info
 
 
+def ciq_set_posterior(ctx, Xt, y, noise: float) -> None:
+    """COV* + jitter I at the ctx's candidates given training data (Xt, y) (eq. thompson_sample)."""
+    keep: list = []
+    px, ldx, m, d = _ptr_ld(Xt, "Xt", keep)
+    py = None
+    if y is not None:
+        py, _, my, _ = _ptr_ld(y, "y", keep)
+        if my != m:
+            raise CiqError(CIQ_ERR_DIM, "y must have one entry per training point")
+    st = LIB.ciq_set_posterior(ctx, px, ldx, m, py, float(noise))
+    if st != CIQ_OK:
+        raise CiqError(st, LIB.ciq_last_error(ctx).decode())
+
+
+def ciq_thompson(ctx, eps, idx, samples, params: CiqParams) -> tuple[int, CiqInfo]:
+    """idx (int64, T entries, numpy or torch, host or device) <- argmin_j (mu* + COV*^{1/2} eps)_j."""
+    keep: list = []
+    pe, lde, ne, t = _ptr_ld(eps, "eps", keep)
+    ps, lds, _, ts = _ptr_ld(samples, "samples", keep)
+    if samples is not None and ts != t:
+        raise CiqError(CIQ_ERR_DIM, "samples must have the shape of eps")
+    try:
+        import torch
+        is_t = isinstance(idx, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        is_t = False
+    if is_t:
+        if idx.dtype != torch.int64 or not idx.is_contiguous() or idx.numel() != t:
+            raise TypeError("idx must be a contiguous int64 tensor with T entries")
+        pi = idx.data_ptr()
+    else:
+        if idx.dtype != np.int64 or not idx.flags.c_contiguous or idx.size != t:
+            raise TypeError("idx must be a contiguous int64 array with T entries")
+        pi = idx.ctypes.data
+    info = CiqInfo()
+    st = LIB.ciq_thompson(ctx, pe, lde, t, ctypes.byref(params), pi, ps, lds, ctypes.byref(info))
+    if st not in (CIQ_OK, CIQ_NOT_CONVERGED):
+        raise CiqError(st, LIB.ciq_last_error(ctx).decode())
+    return st, info
+
+
 def ciq_matvec(ctx, V, out, mvm_impl: str = "auto") -> None:
     keep: list = []
     pv, ldv, nv, t = _ptr_ld(V, "V", keep)
@@ -399,6 +446,20 @@ class CIQ:
 
     def matvec(self, V, out, mvm_impl: str = "auto") -> None:
         ciq_matvec(self.ctx, V, out, mvm_impl)
+
+    def set_posterior(self, Xt, y, noise: float) -> None:
+        """Make this (candidate-set) operator the GP posterior covariance COV* + jitter I."""
+        ciq_set_posterior(self.ctx, Xt, y, noise)
+
+    def thompson(self, eps, idx, samples=None, **kw) -> dict:
+        """One Thompson-sampling step (eq. thompson_sample): idx <- argmin(mu* + COV*^{1/2} eps)."""
+        keep: list = []
+        kw.pop("mode", None)
+        params, keep = make_params(keep=keep, mode="sqrt", **kw)
+        st, info = ciq_thompson(self.ctx, eps, idx, samples, params)
+        d = info.as_dict()
+        d["status"] = st
+        return d
 
     def close(self) -> None:
         if self.ctx:

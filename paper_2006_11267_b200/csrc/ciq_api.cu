@@ -78,9 +78,30 @@ struct PrecondDev {
 };
 enum { PW_INV = 0, PW_HALF = 1, PW_MHALF = 2 };
 
+// GP posterior covariance operator at the candidates (posterior.cu; ciq_set_posterior):
+// COV* + jitter I = (K** + jitter I) - U U^T with U = K*x L^{-T} (n x m, fp64).
+struct PostDev {
+  bool on = false;
+  bool inner = false;       // run_mvm re-entered for the K** part
+  int m = 0;
+  double* u = nullptr;      // n x m (fp64: the mean)
+  float* uf = nullptr;      // n x m (fp32: the per-MVM downdate)
+  float* mu = nullptr;      // n, posterior mean mu*
+  float* part = nullptr;    size_t part_cap = 0;   // U^T v partials [splits][m][tp]
+  float* h = nullptr;       size_t h_cap = 0;      // U^T v [m][tp]
+  double* bpart = nullptr;  size_t bpart_cap = 0;  // alpha partials [blocks][tp]
+  float* t = nullptr;       size_t t_cap = 0;      // K** v (rows x tp)
+  float* f = nullptr;       size_t f_cap = 0;      // thompson samples staging (n x T)
+  float* am_v = nullptr;    size_t am_v_cap = 0;   // argmin partials
+  int64_t* am_i = nullptr;  size_t am_i_cap = 0;
+  int64_t* idx = nullptr;   size_t idx_cap = 0;
+};
+
 struct ciq_ctx {
   ciq_operator op{};
   PrecondDev pc;
+  PostDev post;
+  std::vector<double> ls;     // per-coordinate lengthscales of a kernel operator (copied at init)
   OpDev dev{};
   cudaStream_t stream = nullptr;       // private non-blocking work stream (graph-capturable)
   cudaStream_t user_stream = nullptr;  // the caller's stream given to ciq_init
@@ -432,7 +453,13 @@ void mvm_geometry(const ciq_ctx* c, int tp, int* nsplit, int64_t* nblk) {
 
 // Allocate every buffer run_mvm(tp, allow_split) may need (so a CUDA-graph capture never
 // allocates).
+ciq_status post_buffers(ciq_ctx* c, int tp);
+
 ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
+  if (c->post.on) {
+    ciq_status sp = post_buffers(c, tp);
+    if (sp != CIQ_OK) return sp;
+  }
   if (!use_tc(c, impl)) return CIQ_OK;
   if (use_mat(c, tp)) {
     ciq_status sm = ensure_mat_planes(c);
@@ -459,9 +486,14 @@ ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
 
 // P (+ alpha partials) <- K V.  With the tensor-core path the result may be split into
 // `*nsplit_out` partial products (stride rows*tp) when allow_split; otherwise it is complete.
+ciq_status run_post_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, const Ctrl* done, int impl,
+                        const double* nrm, int* nsplit_out, double** apart_used, int* apart_nblk, bool skip_pack);
+
 ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, const Ctrl* done, int impl,
                    const double* nrm = nullptr, bool allow_split = false, int* nsplit_out = nullptr,
                    double** apart_used = nullptr, int* apart_nblk = nullptr, bool skip_pack = false) {
+  if (c->post.on && !c->post.inner)
+    return run_post_mvm(c, v, tp, p, apart, done, impl, nrm, nsplit_out, apart_used, apart_nblk, skip_pack);
   const int64_t rows = c->row1 - c->row0;
   if (nsplit_out) *nsplit_out = 1;
   if (!use_tc(c, impl)) {
@@ -585,6 +617,37 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   if (apart_used) *apart_used = ap;
   if (apart_nblk) *apart_nblk = (int)nblk;
   c->mvm_kind_used = 2;
+  return CIQ_OK;
+}
+
+// Work buffers of run_post_mvm at this tp (grown before any graph capture).
+ciq_status post_buffers(ciq_ctx* c, int tp) {
+  PostDev& Q = c->post;
+  const int64_t rows = c->row1 - c->row0;
+  ciq_status st = grow(c, &Q.part, &Q.part_cap, (size_t)post_splits(rows) * Q.m * tp);
+  if (st == CIQ_OK) st = grow(c, &Q.h, &Q.h_cap, (size_t)Q.m * tp);
+  if (st == CIQ_OK) st = grow(c, &Q.bpart, &Q.bpart_cap, (size_t)post_apply_blocks(rows) * tp);
+  if (st == CIQ_OK) st = grow(c, &Q.t, &Q.t_cap, (size_t)rows * tp);
+  return st;
+}
+
+// p <- (COV* + jitter I) v = (K** + jitter I) v - U (U^T v)  (eq. thompson_sample's COV*),
+// with the fixed-order fp64 partials of p . v when the caller wants alpha partials.  K** v is the
+// ordinary MVM (tcgen05 matrix-free kernel); the downdate is two skinny fp32 GEMMs (posterior.cu).
+ciq_status run_post_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, const Ctrl* done, int impl,
+                        const double* nrm, int* nsplit_out, double** apart_used, int* apart_nblk, bool skip_pack) {
+  PostDev& Q = c->post;
+  const int64_t rows = c->row1 - c->row0;
+  ciq_status st = post_buffers(c, tp);
+  if (st != CIQ_OK) return st;
+  Q.inner = true;
+  st = run_mvm(c, v, tp, Q.t, nullptr, done, impl, nrm, false, nullptr, nullptr, nullptr, skip_pack);
+  Q.inner = false;
+  if (st != CIQ_OK) return st;
+  LAUNCH(c, launch_post_downdate(Q.uf, Q.m, v, Q.t, tp, rows, Q.part, Q.h, p, apart ? Q.bpart : nullptr, c->stream));
+  if (nsplit_out) *nsplit_out = 1;
+  if (apart_used) *apart_used = apart ? Q.bpart : nullptr;
+  if (apart_nblk) *apart_nblk = post_apply_blocks(rows);
   return CIQ_OK;
 }
 
@@ -886,6 +949,20 @@ void free_precond(PrecondDev& P) {
   dfree(P.t1);
 }
 
+void free_post(PostDev& Q) {
+  dfree(Q.u); dfree(Q.uf); dfree(Q.mu); dfree(Q.part); dfree(Q.h); dfree(Q.bpart); dfree(Q.t); dfree(Q.f);
+  dfree(Q.am_v); dfree(Q.am_i); dfree(Q.idx);
+  Q = PostDev();
+}
+
+// k(r^2) of the kernel kinds, fp64 (the forms of kval / kfun on the device; reading G11)
+double kernel_r2(int kind, double r2, double o2) {
+  if (kind == CIQ_OP_RBF) return o2 * std::exp(-0.5 * r2);
+  const double r = std::sqrt(r2);
+  if (kind == CIQ_OP_MATERN52) return o2 * (1.0 + std::sqrt(5.0) * r + 5.0 / 3.0 * r2) * std::exp(-std::sqrt(5.0) * r);
+  return o2 * (1.0 + std::sqrt(3.0) * r) * std::exp(-std::sqrt(3.0) * r);
+}
+
 struct EvTimer {
   cudaEvent_t e[5];
   EvTimer() { for (auto& x : e) cudaEventCreate(&x); }
@@ -1050,6 +1127,7 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     }
     for (int64_t i = 0; i < n; ++i)
       for (int64_t k = 0; k < d; ++k) xh[i * d + k] /= op->lengthscale[op->ard ? k : 0];
+    for (int64_t k = 0; k < d; ++k) c->ls.push_back(op->lengthscale[op->ard ? k : 0]);
     if (cudaMalloc(&c->xs, (size_t)n * d * 4) != cudaSuccess) { st = CIQ_ERR_OOM; goto fail; }
     if (cudaMemcpy(c->xs, xh.data(), (size_t)n * d * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
       st = CIQ_ERR_CUDA; goto fail;
@@ -1100,6 +1178,7 @@ void ciq_free(ciq_ctx* c) {
   dfree(c->stash); dfree(c->hist);
   dfree(c->apart_tc);
   free_precond(c->pc);
+  free_post(c->post);
   dfree(c->gsum);
   dfree(c->tsum);
   delete c->comm;
@@ -1204,6 +1283,123 @@ ciq_status ciq_vjp(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int6
     info->mvms = i1.mvms + i2.mvms;
   }
   return (st == CIQ_OK && st2 == CIQ_OK) ? CIQ_OK : CIQ_NOT_CONVERGED;
+}
+
+ciq_status ciq_set_posterior(ciq_ctx* c, const float* Xt, int64_t ldxt, int64_t m, const float* y, double noise) {
+  if (!c || !Xt) return CIQ_ERR_INVALID_ARG;
+  if (c->op.kind == CIQ_OP_DENSE || c->world != 1 || c->has_precond)
+    return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_set_posterior: single-GPU kernel operators without a preconditioner");
+  const int d = (int)c->op.d;
+  if (m < 1 || m > 4096 || ldxt < d) return set_err(c, CIQ_ERR_DIM, "ciq_set_posterior: need 1 <= m <= 4096, ldxt >= d");
+  if (!(noise > 0)) return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_set_posterior: noise must be > 0");
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return set_err(c, CIQ_ERR_CUDA, "stream error");
+  // training inputs / targets to the host, scaled by the ctx's lengthscales
+  std::vector<float> xt((size_t)m * d), yh((size_t)m, 0.f);
+  if (is_device_ptr(Xt)) {
+    CUDA_TRY(c, cudaMemcpy2D(xt.data(), (size_t)d * 4, Xt, (size_t)ldxt * 4, (size_t)d * 4, (size_t)m,
+                             cudaMemcpyDeviceToHost));
+  } else {
+    for (int64_t i = 0; i < m; ++i) std::memcpy(&xt[i * d], Xt + i * ldxt, (size_t)d * 4);
+  }
+  if (y) {
+    if (is_device_ptr(y)) CUDA_TRY(c, cudaMemcpy(yh.data(), y, (size_t)m * 4, cudaMemcpyDeviceToHost));
+    else std::memcpy(yh.data(), y, (size_t)m * 4);
+  }
+  for (int64_t i = 0; i < m; ++i)
+    for (int k = 0; k < d; ++k) xt[i * d + k] = (float)((double)xt[i * d + k] / c->ls[k]);
+  // Kxx + noise I = L L^T (fp64 Cholesky, host), L^{-1} by forward substitution, z = L^{-1} y
+  const double o2 = c->op.outputscale;
+  std::vector<double> l((size_t)m * m, 0.0), linv((size_t)m * m, 0.0), z((size_t)m, 0.0);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j <= i; ++j) {
+      double r2 = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double df = (double)xt[i * d + k] - (double)xt[j * d + k];
+        r2 += df * df;
+      }
+      l[i * m + j] = kernel_r2(c->op.kind, r2, o2) + (i == j ? noise : 0.0);
+    }
+  for (int64_t j = 0; j < m; ++j) {
+    double s = l[j * m + j];
+    for (int64_t k = 0; k < j; ++k) s -= l[j * m + k] * l[j * m + k];
+    if (!(s > 0)) return set_err(c, CIQ_ERR_NOT_PD, "ciq_set_posterior: Kxx + noise I not positive definite (pivot %lld)", (long long)j);
+    const double ljj = std::sqrt(s);
+    l[j * m + j] = ljj;
+    for (int64_t i = j + 1; i < m; ++i) {
+      double t = l[i * m + j];
+      for (int64_t k = 0; k < j; ++k) t -= l[i * m + k] * l[j * m + k];
+      l[i * m + j] = t / ljj;
+    }
+  }
+  for (int64_t j = 0; j < m; ++j)       // column j of L^{-1}
+    for (int64_t i = j; i < m; ++i) {
+      double t = (i == j) ? 1.0 : 0.0;
+      for (int64_t k = j; k < i; ++k) t -= l[i * m + k] * linv[k * m + j];
+      linv[i * m + j] = t / l[i * m + i];
+    }
+  for (int64_t i = 0; i < m; ++i) {
+    double t = 0.0;
+    for (int64_t k = 0; k <= i; ++k) t += linv[i * m + k] * (double)yh[k];
+    z[i] = t;
+  }
+  free_post(c->post);
+  PostDev& Q = c->post;
+  Q.m = (int)m;
+  const int64_t n = c->op.n;
+  float* xt_d = nullptr;
+  double *linv_d = nullptr, *z_d = nullptr;
+  CUDA_TRY(c, dalloc(&Q.u, (size_t)n * m));
+  CUDA_TRY(c, dalloc(&Q.uf, (size_t)n * m));
+  CUDA_TRY(c, dalloc(&Q.mu, (size_t)n));
+  CUDA_TRY(c, dalloc(&xt_d, (size_t)m * d));
+  CUDA_TRY(c, dalloc(&linv_d, (size_t)m * m));
+  CUDA_TRY(c, dalloc(&z_d, (size_t)m));
+  CUDA_TRY(c, cudaMemcpy(xt_d, xt.data(), (size_t)m * d * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaMemcpy(linv_d, linv.data(), (size_t)m * m * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaMemcpy(z_d, z.data(), (size_t)m * 8, cudaMemcpyHostToDevice));
+  LAUNCH(c, launch_build_u(c->op.kind, c->xs, xt_d, d, n, (int)m, o2, linv_d, Q.u, Q.uf, c->stream));
+  LAUNCH(c, launch_post_mean(Q.u, z_d, n, (int)m, Q.mu, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  dfree(xt_d); dfree(linv_d); dfree(z_d);
+  Q.on = true;
+  ++c->buf_gen;   // the captured iteration graph must now include the downdate
+  return CIQ_OK;
+}
+
+ciq_status ciq_thompson(ciq_ctx* c, const float* eps, int64_t ld_eps, int64_t T, const ciq_params* params,
+                        int64_t* idx, float* samples, int64_t ld_samples, ciq_info* info) {
+  if (!c || !eps || !idx) return CIQ_ERR_INVALID_ARG;
+  if (!c->post.on) return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_thompson: call ciq_set_posterior first");
+  if (T <= 0 || ld_eps < T || (samples && ld_samples < T)) return set_err(c, CIQ_ERR_DIM, "bad T / leading dimension");
+  ciq_params p;
+  if (params) p = *params; else ciq_params_default(&p);
+  p.mode = CIQ_MODE_SQRT;
+  PostDev& Q = c->post;
+  const int64_t n = c->op.n;
+  const bool sdev = samples && is_device_ptr(samples);
+  float* f = samples;
+  int64_t ldf = ld_samples;
+  ciq_status st;
+  if (!sdev) {
+    st = grow(c, &Q.f, &Q.f_cap, (size_t)n * T);
+    if (st != CIQ_OK) return st;
+    f = Q.f;
+    ldf = T;
+  }
+  ciq_status sa = ciq_apply(c, eps, ld_eps, T, f, ldf, &p, info);   // f = COV*^{1/2} eps
+  if (sa != CIQ_OK && sa != CIQ_NOT_CONVERGED) return sa;
+  const size_t nb = (size_t)argmin_blocks(n);
+  st = grow(c, &Q.am_v, &Q.am_v_cap, nb * T);
+  if (st == CIQ_OK) st = grow(c, &Q.am_i, &Q.am_i_cap, nb * T);
+  if (st == CIQ_OK) st = grow(c, &Q.idx, &Q.idx_cap, (size_t)T);
+  if (st != CIQ_OK) return st;
+  LAUNCH(c, launch_add_mean_argmin(f, ldf, n, (int)T, Q.mu, Q.am_v, Q.am_i, Q.idx, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(idx, Q.idx, (size_t)T * 8, cudaMemcpyDefault, c->stream));
+  if (samples && !sdev)
+    CUDA_TRY(c, cudaMemcpy2DAsync(samples, (size_t)ld_samples * 4, f, (size_t)T * 4, (size_t)T * 4, (size_t)n,
+                                  cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return sa;
 }
 
 ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* out, int64_t ldo,

@@ -131,6 +131,18 @@ cudaError_t launch_lanczos_coeffs(const double* h1, const double* h2, const doub
 cudaError_t launch_scale_cols_by(const float* src, float* dst, int64_t rows, int tp, const double* inv,
                                  cudaStream_t s);
 
+// ---- Thompson sampling: GP posterior at the candidates (posterior.cu) ----
+cudaError_t launch_build_u(int kind, const float* xs, const float* xt, int d, int64_t n, int m, double o2,
+                           const double* linv, double* u, float* uf, cudaStream_t s);
+int post_splits(int64_t rows);
+int post_apply_blocks(int64_t rows);
+cudaError_t launch_post_downdate(const float* uf, int m, const float* v, const float* t, int tp, int64_t rows,
+                                 float* part, float* h, float* out, double* bpart, cudaStream_t s);
+cudaError_t launch_post_mean(const double* u, const double* z, int64_t n, int m, float* mu, cudaStream_t s);
+int argmin_blocks(int64_t n);
+cudaError_t launch_add_mean_argmin(float* samples, int64_t ld, int64_t n, int t, const float* mu, float* part_v,
+                                   int64_t* part_i, int64_t* idx, cudaStream_t s);
+
 // ---- preconditioner P = L L^T + sigma2 I (precond.cu) ----
 int utv_splits(int64_t rows);
 int uapply_blocks(int64_t rows);
