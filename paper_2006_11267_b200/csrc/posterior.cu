@@ -102,19 +102,31 @@ __global__ void __launch_bounds__(256) post_utv_kernel(const float* __restrict__
   const int64_t i_begin = rows * sp / nsplit, i_end = rows * (sp + 1) / nsplit;
   const int tid = threadIdx.x, tk = tid / 8, tc = tid % 8;
   float acc[4][8] = {};
+  // register prefetch of the next 32-row step while the current one is multiplied
+  float ru[DU_ROWS * DU_K / 256], rv[DU_ROWS * DU_C / 256];
+  auto gload = [&](int64_t i0) {
+#pragma unroll
+    for (int q = 0; q < DU_ROWS * DU_K / 256; ++q) {
+      const int e = tid + q * 256, r = e / DU_K, k = e % DU_K;
+      const int64_t i = i0 + r;
+      ru[q] = (i < i_end && k0 + k < m) ? u[i * m + k0 + k] : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < DU_ROWS * DU_C / 256; ++q) {
+      const int e = tid + q * 256, r = e / DU_C, cc = e % DU_C;
+      const int64_t i = i0 + r;
+      rv[q] = (i < i_end && c0 + cc < tp) ? v[i * tp + c0 + cc] : 0.f;
+    }
+  };
+  if (i_begin < i_end) gload(i_begin);
   for (int64_t i0 = i_begin; i0 < i_end; i0 += DU_ROWS) {
     __syncthreads();
-    for (int e = tid; e < DU_ROWS * DU_K; e += 256) {
-      const int r = e / DU_K, k = e % DU_K;
-      const int64_t i = i0 + r;
-      us[r][k] = (i < i_end && k0 + k < m) ? u[i * m + k0 + k] : 0.f;
-    }
-    for (int e = tid; e < DU_ROWS * DU_C; e += 256) {
-      const int r = e / DU_C, cc = e % DU_C;
-      const int64_t i = i0 + r;
-      vs[r][cc] = (i < i_end && c0 + cc < tp) ? v[i * tp + c0 + cc] : 0.f;
-    }
+#pragma unroll
+    for (int q = 0; q < DU_ROWS * DU_K / 256; ++q) { const int e = tid + q * 256; us[e / DU_K][e % DU_K] = ru[q]; }
+#pragma unroll
+    for (int q = 0; q < DU_ROWS * DU_C / 256; ++q) { const int e = tid + q * 256; vs[e / DU_C][e % DU_C] = rv[q]; }
     __syncthreads();
+    if (i0 + DU_ROWS < i_end) gload(i0 + DU_ROWS);
 #pragma unroll 4
     for (int r = 0; r < DU_ROWS; ++r) {
       const float4 a = *reinterpret_cast<const float4*>(&us[r][tk * 4]);
@@ -173,18 +185,29 @@ __global__ void __launch_bounds__(256) post_apply_kernel(const float* __restrict
   const int c0 = blockIdx.y * 64;
   const int tid = threadIdx.x, ti = tid / 16, tc = tid % 16;
   float acc[4][4] = {};
+  float ru[DA_ROWS * DA_K / 256], rh[DA_K * 64 / 256];   // register prefetch of the next k chunk
+  auto gload = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < DA_ROWS * DA_K / 256; ++q) {
+      const int e = tid + q * 256, r = e / DA_K, kk = e % DA_K;
+      const int64_t i = i0 + r;
+      ru[q] = (i < rows && k0 + kk < m) ? u[i * m + k0 + kk] : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < DA_K * 64 / 256; ++q) {
+      const int e = tid + q * 256, kk = e / 64, cc = e % 64;
+      rh[q] = (k0 + kk < m && c0 + cc < tp) ? h[(size_t)(k0 + kk) * tp + c0 + cc] : 0.f;
+    }
+  };
+  gload(0);
   for (int k0 = 0; k0 < m; k0 += DA_K) {
     __syncthreads();
-    for (int e = tid; e < DA_ROWS * DA_K; e += 256) {
-      const int r = e / DA_K, kk = e % DA_K;
-      const int64_t i = i0 + r;
-      us[kk][r] = (i < rows && k0 + kk < m) ? u[i * m + k0 + kk] : 0.f;
-    }
-    for (int e = tid; e < DA_K * 64; e += 256) {
-      const int kk = e / 64, cc = e % 64;
-      hs[kk][cc] = (k0 + kk < m && c0 + cc < tp) ? h[(size_t)(k0 + kk) * tp + c0 + cc] : 0.f;
-    }
+#pragma unroll
+    for (int q = 0; q < DA_ROWS * DA_K / 256; ++q) { const int e = tid + q * 256; us[e % DA_K][e / DA_K] = ru[q]; }
+#pragma unroll
+    for (int q = 0; q < DA_K * 64 / 256; ++q) { const int e = tid + q * 256; hs[e / 64][e % 64] = rh[q]; }
     __syncthreads();
+    if (k0 + DA_K < m) gload(k0 + DA_K);
 #pragma unroll 8
     for (int kk = 0; kk < DA_K; ++kk) {
       const float4 a = *reinterpret_cast<const float4*>(&us[kk][ti * 4]);
