@@ -29,10 +29,12 @@ __global__ void __launch_bounds__(256) utv_kernel(const double* __restrict__ u, 
                                                   const float* __restrict__ v, int tp, int64_t rows, int nsplit,
                                                   double* __restrict__ part) {
   __shared__ double us[KB][TB + 1];
-  __shared__ float vs[KB][TB + 1];
+  __shared__ double vs[KB][TB + 1];   // V converted to fp64 once, when staged
   const int k0 = blockIdx.x * TB, c0 = blockIdx.y * TB, sp = blockIdx.z;
   const int64_t i_begin = rows * sp / nsplit, i_end = rows * (sp + 1) / nsplit;
-  const int tid = threadIdx.x, tk = tid / 16, tc = tid % 16;  // 4x4 outputs per thread
+  // 4x4 outputs per thread: k = tk*4 + x, c = tc + 16*y (consecutive lanes read consecutive
+  // doubles of vs: no bank conflicts)
+  const int tid = threadIdx.x, tk = tid / 16, tc = tid % 16;
   double acc[4][4] = {};
   for (int64_t i0 = i_begin; i0 < i_end; i0 += KB) {
     __syncthreads();
@@ -40,14 +42,14 @@ __global__ void __launch_bounds__(256) utv_kernel(const double* __restrict__ u, 
       const int ii = e / TB, cc = e % TB;
       const int64_t i = i0 + ii;
       us[ii][cc] = (i < i_end && k0 + cc < r) ? u[i * ldu + k0 + cc] : 0.0;
-      vs[ii][cc] = (i < i_end && c0 + cc < tp) ? v[i * tp + c0 + cc] : 0.f;
+      vs[ii][cc] = (i < i_end && c0 + cc < tp) ? (double)v[i * tp + c0 + cc] : 0.0;
     }
     __syncthreads();
 #pragma unroll
     for (int ii = 0; ii < KB; ++ii) {
       double a[4], b[4];
 #pragma unroll
-      for (int x = 0; x < 4; ++x) { a[x] = us[ii][tk * 4 + x]; b[x] = (double)vs[ii][tc * 4 + x]; }
+      for (int x = 0; x < 4; ++x) { a[x] = us[ii][tk * 4 + x]; b[x] = vs[ii][tc + 16 * x]; }
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -58,7 +60,7 @@ __global__ void __launch_bounds__(256) utv_kernel(const double* __restrict__ u, 
   for (int x = 0; x < 4; ++x)
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
-      const int k = k0 + tk * 4 + x, c = c0 + tc * 4 + y;
+      const int k = k0 + tk * 4 + x, c = c0 + tc + 16 * y;
       if (k < r && c < tp) part[((size_t)sp * r + k) * tp + c] = acc[x][y];
     }
 }
@@ -75,6 +77,8 @@ __global__ void __launch_bounds__(256) uapply_kernel(const double* __restrict__ 
   __shared__ double red[16][TB];
   const int64_t i0 = (int64_t)blockIdx.x * TB;
   const int c0 = blockIdx.y * TB;
+  // 4x4 outputs per thread: rows ti*4 + p, columns tc + 16*q (conflict-free reads of hs,
+  // coalesced stores of out)
   const int tid = threadIdx.x, ti = tid / 16, tc = tid % 16;
   double acc[4][4] = {};
   for (int k0 = 0; k0 < r; k0 += KB) {
@@ -91,7 +95,7 @@ __global__ void __launch_bounds__(256) uapply_kernel(const double* __restrict__ 
     for (int kk = 0; kk < KB; ++kk) {
       double x[4], y[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) { x[q] = us[ti * 4 + q][kk]; y[q] = hs[kk][tc * 4 + q]; }
+      for (int q = 0; q < 4; ++q) { x[q] = us[ti * 4 + q][kk]; y[q] = hs[kk][tc + 16 * q]; }
 #pragma unroll
       for (int p = 0; p < 4; ++p)
 #pragma unroll
@@ -105,7 +109,7 @@ __global__ void __launch_bounds__(256) uapply_kernel(const double* __restrict__ 
     if (i >= rows) continue;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int c = c0 + tc * 4 + q;
+      const int c = c0 + tc + 16 * q;
       if (c >= tp) continue;
       const float o = (float)fma((double)a, (double)v[i * tp + c], acc[p][q]);
       out[i * tp + c] = o;
@@ -114,7 +118,7 @@ __global__ void __launch_bounds__(256) uapply_kernel(const double* __restrict__ 
   }
   if (bpart != nullptr) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) red[ti][tc * 4 + q] = part[q];
+    for (int q = 0; q < 4; ++q) red[ti][tc + 16 * q] = part[q];
     __syncthreads();
     for (int c = tid; c < TB; c += 256) {
       double s = 0.0;
