@@ -275,7 +275,18 @@ def run_ours(args, cfg):
     impl_used = pinfo["mvm_impl_used"]
     # algorithmic work per MVM launch: N^2 kernel evaluations, 2 N^2 T useful flops
     flops = 2.0 * rows_local * n * tcols        # this rank's rows of K . V
-    if cfg.kind == "dense" and impl_used == "tc":
+    if cfg.precond_rank > 0:
+        # each MVM slot applies M = P^{-1/2} K P^{-1/2}: two Woodbury applications (U^T v and U (g o H),
+        # fp64, 2 N r T flops each) around the K MVM; the fp64 GEMMs dominate (profiles/precond_sweep_r01.txt)
+        sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+        fp64_peak = sm_count * 64 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        wflops = 8.0 * rows_local * cfg.precond_rank * tcols
+        roof = {"bound": "alu", "achieved": wflops / (mvm_ms * 1e-3) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+                "kernel": "M v = P^{-1/2} K P^{-1/2} v: utv_kernel / uapply_kernel fp64 Woodbury GEMMs + the K MVM",
+                "note": "achieved = the 8 N r T fp64 flops of the two P^{-1/2} over the whole M-apply time (which also "
+                        "holds the K MVM): a lower bound on the GEMMs' own rate",
+                "peak_source": f"{sm_count} SMs x 64 DFMA/clk x 2 x sm_max_mhz (derived)"}
+    elif cfg.kind == "dense" and impl_used == "tc":
         kbytes = 4.0 * rows_local * n                # split fp16 planes: 4 B per entry of K, read once
         roof = {"bound": "hbm", "achieved": kbytes / (mvm_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "kernel": "mvm_dense2_kernel (persistent; K streamed once per MVM, tcgen05 split products)",
