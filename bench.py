@@ -121,22 +121,29 @@ def oracle_sample_rate(cfg, inp, mvms_per_call: int, rows: int = 1024, reps: int
     import numpy as np
     from threadpoolctl import threadpool_info
 
-    from oracle import KernelOperator
-    op = KernelOperator(inp["X"], cfg.kind, cfg.lengthscale, cfg.outputscale, cfg.sigma2, dense_cache_max=0,
-                        block=64)
+    from oracle import DenseOperator, KernelOperator
+    if cfg.kind == "dense":
+        rows = cfg.n   # the dense oracle MVM is cheap: time all of it
+        op = DenseOperator(inp["K"].astype(np.float64), cfg.sigma2)
+        block_rows = lambda i0, i1: op.mvm_rows(np.arange(i0, i1), v)  # noqa: E731
+    else:
+        op = KernelOperator(inp["X"], cfg.kind, cfg.lengthscale, cfg.outputscale, cfg.sigma2, dense_cache_max=0,
+                            block=64)
+        block_rows = lambda i0, i1: op.kernel_rows(i0, i1) @ v  # noqa: E731
     v = inp["B"].astype(np.float64)
     best = None
     for _ in range(reps):
         t0 = time.perf_counter()
-        for i0 in range(0, rows, op.block):
-            op.kernel_rows(i0, min(rows, i0 + op.block)) @ v
+        for i0 in range(0, rows, 64):
+            block_rows(i0, min(rows, i0 + 64))
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
     t_mvm = best * cfg.n / rows
     t_call = t_mvm * mvms_per_call
     threads = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
     return {"value": cfg.t / t_call, "unit": "RHS/s", "cores": threads, "kind": "oracle",
-            "sample": (f"oracle matrix-free MVM on {rows} of {cfg.n} rows x {cfg.t} RHS ({best:.2f} s), "
+            "sample": (f"oracle {'dense' if cfg.kind == 'dense' else 'matrix-free'} MVM on {rows} of {cfg.n} rows "
+                       f"x {cfg.t} RHS ({best:.2f} s), "
                        f"extrapolated to {mvms_per_call} MVMs per call (lambda est + J + final)"),
             "sample_seconds": best, "t_call_s": t_call}
 
