@@ -244,12 +244,18 @@ CIQ_DEVICE float pack_scale(double nrm, double sqrt_n, float* inv) {
 // only (wprev = the buffer holding nrm_J v_J).  Shifts are processed in batches of QB so that the
 // 2 QB direction loads of a row are in flight together (the loop over shifts otherwise
 // serialises on the stores to d2, which the compiler cannot reorder).
-__global__ void __launch_bounds__(kThreads, 3) lanczos_update_kernel(
+#ifndef CIQ_UPD_QB
+#define CIQ_UPD_QB 2        // shifts whose d-vector loads are in flight together
+#endif
+#ifndef CIQ_UPD_MINB
+#define CIQ_UPD_MINB 3      // resident CTAs per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(kThreads, CIQ_UPD_MINB) lanczos_update_kernel(
     Scal sc, const float* __restrict__ p, int nsplit, size_t split_stride, const float* __restrict__ wcur, const float* __restrict__ wprev,
     float* __restrict__ wnew, const float* __restrict__ d1base, float* __restrict__ d2base, int64_t qstride,
     float* __restrict__ y, int nq, int64_t rows, int tp, double* __restrict__ bpart, int final_only, PackOut pk,
     float* __restrict__ xq) {
-  constexpr int QB = 2;
+  constexpr int QB = CIQ_UPD_QB;
   const Ctrl* ctrl = sc.ctrl;
   if (!final_only && ctrl->done) return;
   const int pending = ctrl->pending;
@@ -601,7 +607,7 @@ int update_blocks(int64_t rows) {
     int nsm = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    return 3 * nsm;   // __launch_bounds__(kThreads, 3)
+    return CIQ_UPD_MINB * nsm;   // __launch_bounds__(kThreads, CIQ_UPD_MINB)
   }();
   const int nrb = rowblocks(rows, 0);
   return nrb < resident ? nrb : resident;
