@@ -136,6 +136,12 @@ struct ciq_ctx {
   float* psplit = nullptr;    // nsplit x rows x tp partial products
   size_t psplit_elems = 0;
   float* stash = nullptr;     // lanczos_reuse: W_1..W_R of the warm-up steps (full height)
+  // ciq_vjp work buffers (kept across calls: no cudaMalloc / cudaFree per call)
+  float* vjp_xb = nullptr;  size_t vjp_xb_cap = 0;
+  float* vjp_xv = nullptr;  size_t vjp_xv_cap = 0;
+  float* vjp_y = nullptr;   size_t vjp_y_cap = 0;
+  float* vjp_g = nullptr;   size_t vjp_g_cap = 0;
+  double* vjp_w = nullptr;  size_t vjp_w_cap = 0;
   size_t stash_elems = 0;
   double* hist = nullptr;     // lanczos_reuse: per-step scalar history [7][R][tp]
   size_t hist_elems = 0;
@@ -1176,6 +1182,7 @@ void ciq_free(ciq_ctx* c) {
   dfree(c->kplanes);
   dfree(c->feat_a); dfree(c->feat_b); dfree(c->planes); dfree(c->inv_scale); dfree(c->psplit);
   dfree(c->stash); dfree(c->hist);
+  dfree(c->vjp_xb); dfree(c->vjp_xv); dfree(c->vjp_y); dfree(c->vjp_g); dfree(c->vjp_w);
   dfree(c->apart_tc);
   free_precond(c->pc);
   free_post(c->post);
@@ -1236,20 +1243,20 @@ ciq_status ciq_vjp(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int6
   if (params) p = *params; else ciq_params_default(&p);
   const int nq = p.Q;
   if (nq < 1 || nq > CIQ_MAX_Q) return set_err(c, CIQ_ERR_INVALID_ARG, "Q must be in [1, %d]", CIQ_MAX_Q);
-  float *xb = nullptr, *xv = nullptr, *yb = nullptr;
-  double* wd = nullptr;
-  CUDA_TRY(c, dalloc(&xb, (size_t)nq * n * T));
-  CUDA_TRY(c, dalloc(&xv, (size_t)nq * n * T));
-  CUDA_TRY(c, dalloc(&yb, (size_t)n * T));
-  CUDA_TRY(c, dalloc(&wd, (size_t)nq));
-  auto cleanup = [&]() { dfree(xb); dfree(xv); dfree(yb); dfree(wd); };
+  ciq_status gs = grow(c, &c->vjp_xb, &c->vjp_xb_cap, (size_t)nq * n * T);
+  if (gs == CIQ_OK) gs = grow(c, &c->vjp_xv, &c->vjp_xv_cap, (size_t)nq * n * T);
+  if (gs == CIQ_OK) gs = grow(c, &c->vjp_y, &c->vjp_y_cap, (size_t)n * T);
+  if (gs == CIQ_OK) gs = grow(c, &c->vjp_w, &c->vjp_w_cap, (size_t)nq);
+  if (gs != CIQ_OK) return gs;
+  float *xb = c->vjp_xb, *xv = c->vjp_xv, *yb = c->vjp_y;
+  double* wd = c->vjp_w;
   // forward: x_q(b) with the estimated (or given) rule
   p.mode = CIQ_MODE_INVSQRT;
   p.keep_shift_solutions = 1;
   p.shift_solutions = xb;
   ciq_info i1{};
   ciq_status st = ciq_apply(c, B, ldb, T, yb, T, &p, &i1);
-  if (st != CIQ_OK && st != CIQ_NOT_CONVERGED) { cleanup(); return st; }
+  if (st != CIQ_OK && st != CIQ_NOT_CONVERGED) return st;
   // backward: x_q(v) with the same rule ("another call to the msMINRES algorithm")
   double t[CIQ_MAX_Q], w[CIQ_MAX_Q];
   for (int q = 0; q < nq; ++q) { t[q] = i1.t[q]; w[q] = i1.w[q]; }
@@ -1260,13 +1267,15 @@ ciq_status ciq_vjp(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int6
   p.shift_solutions = xv;
   ciq_info i2{};
   ciq_status st2 = ciq_apply(c, V, ldv, T, yb, T, &p, &i2);
-  if (st2 != CIQ_OK && st2 != CIQ_NOT_CONVERGED) { cleanup(); return st2; }
+  if (st2 != CIQ_OK && st2 != CIQ_NOT_CONVERGED) return st2;
   CUDA_TRY(c, cudaMemcpyAsync(wd, w, nq * 8, cudaMemcpyHostToDevice, c->stream));
   float* gdev = G;
   float* gtmp = nullptr;
   const bool gdevice = is_device_ptr(G);
   if (!gdevice) {
-    CUDA_TRY(c, dalloc(&gtmp, (size_t)n * n));
+    ciq_status g2 = grow(c, &c->vjp_g, &c->vjp_g_cap, (size_t)n * n);
+    if (g2 != CIQ_OK) return g2;
+    gtmp = c->vjp_g;
     gdev = gtmp;
   }
   const int64_t ld = gdevice ? ldg : n;
@@ -1276,8 +1285,6 @@ ciq_status ciq_vjp(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int6
                                   cudaMemcpyDeviceToHost, c->stream));
   }
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  dfree(gtmp);
-  cleanup();
   if (info) {
     *info = i1;
     info->mvms = i1.mvms + i2.mvms;
