@@ -369,6 +369,105 @@ def run_ours(args, cfg):
         torch.distributed.destroy_process_group()
 
 
+# ------------------------------------------------------------------------------------------------
+# T1: one Thompson-sampling step (eq. thompson_sample), single GPU
+# ------------------------------------------------------------------------------------------------
+
+def run_thompson(args):
+    import numpy as np
+    import torch
+
+    import paper_2006_11267_b200 as pb
+    import workloads
+    cfg = workloads.THOMPSON["T1"]
+    _, world, local = dist_env()
+    if world > 1:
+        raise SystemExit("--config T1 is single-GPU (the posterior operator is not row-sharded)")
+    torch.cuda.set_device(local)
+    inp = workloads.thompson_inputs(cfg)
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()  # noqa: E731
+    g = pb.CIQ(cfg.kind, X=dv(inp["Xs"]), lengthscale=cfg.lengthscale, outputscale=cfg.outputscale, diag=cfg.jitter)
+    g.set_posterior(dv(inp["Xt"]), dv(inp["y"]), cfg.noise)
+    eps, s0 = dv(inp["eps"]), dv(inp["S"])
+    idx = torch.empty(cfg.t, dtype=torch.int64, device="cuda")
+    samples = torch.empty_like(eps)
+    kw = dict(q=cfg.q, max_iters=cfg.max_iters, tol=cfg.tol, lanczos_start=s0, lanczos_reuse=args.lanczos == "reuse")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        g.thompson(eps, idx, samples, **kw)
+    sampler = ClockSampler(local)
+    sampler.start()
+    step_ms, infos = [], []
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        infos.append(g.thompson(eps, idx, samples, **kw))
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = statistics.mean(step_ms)
+    # e2e: eps from pinned host memory, the argmin indices back to the host (the step's result)
+    eh = torch.from_numpy(inp["eps"]).pin_memory()
+    ih = torch.empty(cfg.t, dtype=torch.int64).pin_memory()
+    e2e_ms = []
+    for _ in range(max(1, args.steps)):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.thompson(eh.numpy(), ih.numpy(), None, **kw)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e = statistics.mean(e2e_ms)
+    pinfo = g.apply(eps, samples, profile=True, mode="sqrt", **kw)
+    mvm_ms = pinfo["ms_mvm"] / max(1, pinfo["mvm_timed"])
+    peaks = load_peaks()
+    flops = 2.0 * cfg.n * cfg.n * cfg.t
+    roof = {"bound": "tensor", "achieved": flops / (mvm_ms * 1e-3) / 1e12, "peak": peaks["bf16_tflops_sustained"],
+            "unit": "TFLOP/s", "kernel": "COV* MVM = mvm_tc2_kernel (K**) + post_utv/post_reduce/post_apply downdate",
+            "peak_source": f"{peaks['_source']} bf16 sustained (fp16 same rate)", "traffic": None,
+            "ms_per_launch": mvm_ms, "share_of_step": pinfo["ms_mvm"] / max(1e-9, pinfo["ms_total"])}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    line = {"metric": "Thompson-sampling posterior samples/sec (T1: 50k Hartmann-6 candidates, m=100, Q=8)",
+            "value": cfg.t / (ms / 1000.0), "unit": "samples/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "T1: argmin(mu* + COV*^{1/2} eps) over 50,000 U[0,1]^6 candidates, 100 training "
+                                   "points (standardised Hartmann-6), RBF l=0.15, noise 1e-3, jitter 0.05, 64 samples, "
+                                   "Q=8, tol 1e-4",
+                       "J": infos[-1]["iters"], "mvms_per_step": infos[-1]["mvms"],
+                       "converged": infos[-1]["converged"], "l2": "flushed between steps (256 MiB write)"},
+            "roofline": roof,
+            "e2e": {"value": cfg.t / (e2e / 1000.0), "unit": "samples/s", "h2d_bytes_per_step": cfg.n * cfg.t * 4,
+                    "d2h_bytes_per_step": cfg.t * 8, "ms_per_step": e2e},
+            "gpu_launches": int(sum(i["kernel_launches"] for i in infos)), "clocks": clocks}
+    if not args.no_cpu_baseline:
+        # the oracle's COV* MVM on a bounded row sample, extrapolated to the step's MVM count
+        from oracle import PosteriorOperator
+        post = PosteriorOperator(inp["Xs"], inp["Xt"], inp["y"], cfg.kind, cfg.lengthscale, cfg.outputscale,
+                                 cfg.noise, cfg.jitter)
+        v = inp["eps"].astype(np.float64)
+        rows = min(args.ref_rows, cfg.n)
+        t0 = time.perf_counter()
+        for i0 in range(0, rows, 64):
+            post.mvm_rows(np.arange(i0, min(rows, i0 + 64)), v)
+        dt = time.perf_counter() - t0
+        t_call = dt * cfg.n / rows * infos[-1]["mvms"]
+        from threadpoolctl import threadpool_info
+        line["cpu_baseline"] = {"value": cfg.t / t_call, "unit": "samples/s", "kind": "oracle",
+                                "cores": max([d.get("num_threads", 1) for d in threadpool_info()] + [1]),
+                                "sample": f"oracle COV* MVM on {rows} of {cfg.n} rows x {cfg.t} samples ({dt:.2f} s), "
+                                          f"extrapolated to {infos[-1]['mvms']} MVMs per step"}
+    print(json.dumps(line), flush=True)
+    g.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -386,6 +485,13 @@ def main():
     ap.add_argument("--parallelism", default="rows", choices=["rows", "replicas"])
     args = ap.parse_args()
     import workloads
+    if args.config == "T1":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "T1 is a widening row; its oracle is timed as this "
+                                                                  "line's cpu_baseline"}))
+        else:
+            run_thompson(args)
+        return
     cfg = workloads.CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
