@@ -585,6 +585,13 @@ class PosteriorOperator:
     def dense(self) -> np.ndarray:
         return self.kss.dense() - self.kxs.T @ scipy.linalg.cho_solve(self.cho, self.kxs)
 
+    def kernel_column(self, j: int) -> np.ndarray:
+        """Column j of COV* without the jitter (what ``pivoted_cholesky`` factors)."""
+        return self.kss.kernel_column(j) - self.kxs.T @ scipy.linalg.cho_solve(self.cho, self.kxs[:, j])
+
+    def kernel_diag(self) -> np.ndarray:
+        return self.kss.kernel_diag() - np.sum(self.kxs * scipy.linalg.cho_solve(self.cho, self.kxs), axis=0)
+
 
 def thompson_step(post: PosteriorOperator, eps: np.ndarray, q: int = 8, max_iters: int = 400, tol: float = 1e-4,
                   lanczos_start: np.ndarray | None = None, rule: tuple | None = None):

@@ -104,3 +104,15 @@ def test_hartmann6_known_minimum():
     assert abs(workloads.hartmann6(xmin)[0] + 3.32237) < 1e-4
     x = np.random.default_rng(0).random((1000, 6))
     assert workloads.hartmann6(x).min() > -3.32237
+
+
+def test_posterior_kernel_column_diag_and_full_rank_pivoted_cholesky():
+    from oracle import pivoted_cholesky
+    _, _, _, post = _problem(n=60, m=8)
+    k = post.dense() - post.sigma2 * np.eye(post.n)      # COV* without the jitter
+    assert np.abs(post.kernel_column(7) - k[:, 7]).max() < 1e-12
+    assert np.abs(post.kernel_diag() - np.diag(k)).max() < 1e-12
+    lf = pivoted_cholesky(post, post.n)
+    resid = k - lf @ lf.T
+    assert np.linalg.eigvalsh(resid).min() > -1e-9       # the Schur complement stays PSD
+    assert np.trace(resid) < 1e-6 * np.trace(k)
