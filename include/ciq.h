@@ -220,7 +220,10 @@ ciq_status ciq_vjp(ciq_ctx* ctx, const float* B, int64_t ldb, const float* V, in
  *   noise > 0: the training-data noise.  1 <= m <= 4096.
  * The training block is factorised once on the host in fp64 (Cholesky of Kxx + noise I and L^{-1});
  * U = K*x L^{-T} (N x m, fp64) and mu* are built on the device.  Call again to replace the data.
- * Single GPU, kernel operators, no preconditioner: CIQ_ERR_INVALID_ARG otherwise;
+ * With a preconditioner (ciq_init's pc, sigma2 = the jitter) the solve runs on
+ * P^{-1/2} (COV* + jitter I) P^{-1/2} (App. A); ciq_pivoted_cholesky on a posterior ctx factors
+ * COV* (the Hartmann-posterior preconditioning of P:914-915).
+ * Single GPU, kernel operators: CIQ_ERR_INVALID_ARG otherwise;
  * CIQ_ERR_NOT_PD if Kxx + noise I is not positive definite in fp64. */
 ciq_status ciq_set_posterior(ciq_ctx* ctx, const float* Xt, int64_t ldxt, int64_t m, const float* y, double noise);
 

@@ -1206,7 +1206,8 @@ ciq_status ciq_pivoted_cholesky(ciq_ctx* c, int32_t rank, float* L, int64_t ldl)
   CUDA_TRY(c, dalloc(&pivval, (size_t)rank));
   CUDA_TRY(c, dalloc(&piv, (size_t)rank));
   CUDA_TRY(c, cudaMemsetAsync(ld, 0, (size_t)n * rank * 4, c->stream));
-  LAUNCH(c, launch_pivchol(c->dev, rank, ld, rank, diag, lcol, piv, pivval, c->stream));
+  LAUNCH(c, launch_pivchol(c->dev, rank, ld, rank, diag, lcol, piv, pivval, c->post.on ? c->post.u : nullptr,
+                           c->post.m, c->stream));
   ciq_status st = store_rows(c, ld, rank, n, rank, L, ldl);
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   dfree(ld); dfree(diag); dfree(lcol); dfree(pivval); dfree(piv);
@@ -1294,8 +1295,8 @@ ciq_status ciq_vjp(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int6
 
 ciq_status ciq_set_posterior(ciq_ctx* c, const float* Xt, int64_t ldxt, int64_t m, const float* y, double noise) {
   if (!c || !Xt) return CIQ_ERR_INVALID_ARG;
-  if (c->op.kind == CIQ_OP_DENSE || c->world != 1 || c->has_precond)
-    return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_set_posterior: single-GPU kernel operators without a preconditioner");
+  if (c->op.kind == CIQ_OP_DENSE || c->world != 1)
+    return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_set_posterior: single-GPU kernel operators only");
   const int d = (int)c->op.d;
   if (m < 1 || m > 4096 || ldxt < d) return set_err(c, CIQ_ERR_DIM, "ciq_set_posterior: need 1 <= m <= 4096, ldxt >= d");
   if (!(noise > 0)) return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_set_posterior: noise must be > 0");

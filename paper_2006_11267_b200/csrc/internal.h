@@ -154,6 +154,6 @@ cudaError_t launch_gram(const float* l, int ldl, int r, int64_t n, double* gram,
 cudaError_t launch_small_right_mul(const float* l, int ldl, int r, const double* wsi, int r2, int64_t n, double* u,
                                    int ldu, cudaStream_t s);
 cudaError_t launch_pivchol(const OpDev& op, int rank, float* l, int ldl, double* diag, double* lcol, int* piv,
-                           double* pivval, cudaStream_t s);
+                           double* pivval, const double* pu, int mu, cudaStream_t s);
 
 }  // namespace ciq

@@ -192,9 +192,11 @@ __device__ __forceinline__ double kval(const float* xs, int d, int64_t i, int64_
 }
 
 // column m of L: L[i][m] = (k(x_i, x_p) - sum_{l<m} L[i][l] L[p][l]) / sqrt(d_p); diag[i] -= L[i][m]^2
+// (pu, mu: the posterior downdate U (n x mu, fp64) of a Thompson-sampling ctx, or null: the factor
+// is then of COV* = k(X, X) - U U^T, posterior.cu)
 __global__ void pivchol_column_kernel(OpDev op, const int* __restrict__ piv, const double* __restrict__ pivval,
                                       int m, float* __restrict__ l, int ldl, double* __restrict__ diag,
-                                      double* __restrict__ lcol) {
+                                      double* __restrict__ lcol, const double* __restrict__ pu, int mu) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= op.n) return;
   const int p = piv[m];
@@ -204,6 +206,8 @@ __global__ void pivchol_column_kernel(OpDev op, const int* __restrict__ piv, con
   else if (op.kind == 1) kv = kval<1>(op.xs, op.d, i, p, op.o2);
   else if (op.kind == 2) kv = kval<2>(op.xs, op.d, i, p, op.o2);
   else kv = kval<3>(op.xs, op.d, i, p, op.o2);
+  if (pu != nullptr)
+    for (int k = 0; k < mu; ++k) kv -= pu[i * mu + k] * pu[(int64_t)p * mu + k];
   double s = kv;
   for (int k = 0; k < m; ++k) s -= lcol[(size_t)k * op.n + i] * lcol[(size_t)k * op.n + p];
   const double v = (dp > 0) ? s / sqrt(dp) : 0.0;
@@ -212,10 +216,13 @@ __global__ void pivchol_column_kernel(OpDev op, const int* __restrict__ piv, con
   diag[i] = (i == p) ? 0.0 : diag[i] - v * v;
 }
 
-__global__ void pivchol_init_diag(OpDev op, double* __restrict__ diag) {
+__global__ void pivchol_init_diag(OpDev op, double* __restrict__ diag, const double* __restrict__ pu, int mu) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= op.n) return;
-  diag[i] = (op.kind == 0) ? (double)op.k[i * op.ldk + i] : (double)op.o2;  // k(x, x) = o^2
+  double dv = (op.kind == 0) ? (double)op.k[i * op.ldk + i] : (double)op.o2;  // k(x, x) = o^2
+  if (pu != nullptr)
+    for (int k = 0; k < mu; ++k) dv -= pu[i * mu + k] * pu[i * mu + k];
+  diag[i] = dv;
 }
 
 inline unsigned nbk(int64_t e, int bs) { return (unsigned)((e + bs - 1) / bs); }
@@ -252,11 +259,11 @@ cudaError_t launch_small_right_mul(const float* l, int ldl, int r, const double*
 }
 
 cudaError_t launch_pivchol(const OpDev& op, int rank, float* l, int ldl, double* diag, double* lcol, int* piv,
-                           double* pivval, cudaStream_t s) {
-  pivchol_init_diag<<<nbk(op.n, 256), 256, 0, s>>>(op, diag);
+                           double* pivval, const double* pu, int mu, cudaStream_t s) {
+  pivchol_init_diag<<<nbk(op.n, 256), 256, 0, s>>>(op, diag, pu, mu);
   for (int m = 0; m < rank; ++m) {
     pivot_argmax_kernel<<<1, 1024, 0, s>>>(diag, op.n, piv, m, pivval);
-    pivchol_column_kernel<<<nbk(op.n, 256), 256, 0, s>>>(op, piv, pivval, m, l, ldl, diag, lcol);
+    pivchol_column_kernel<<<nbk(op.n, 256), 256, 0, s>>>(op, piv, pivval, m, l, ldl, diag, lcol, pu, mu);
   }
   return cudaGetLastError();
 }

@@ -23,20 +23,41 @@ PROBLEMS = [
     dict(name="N50k RBF d3 l0.2 s2 1e-3", cfg=workloads.Config("P2", 50_000, 3, "rbf", 0.2, 1.0, 1e-3, 64, 8,
                                                                  "whiten", 1500, 1e-4),
          tol=1e-4, ranks=[0, 100, 200, 400]),
+    # the paper's own case: the Hartmann-6 GP posterior covariance at 50k
+    # candidates (workloads.THOMPSON T1 with a small jitter 1e-4), sampled with R B (sqrt mode)
+    dict(name="Hartmann-6 posterior N50k jitter 1e-4 (T1)", posterior=True,
+         cfg=workloads.Config("T1p", 50_000, 6, "rbf", 0.15, 1.0, 1e-4, 64, 8, "sqrt", 1500, 1e-4),
+         tol=1e-4, ranks=[0, 200, 400]),
+    dict(name="Hartmann-6 posterior N50k l=0.5 jitter 1e-4", posterior=True,
+         cfg=workloads.Config("T1l", 50_000, 6, "rbf", 0.5, 1.0, 1e-4, 64, 8, "sqrt", 1500, 1e-4),
+         tol=1e-4, ranks=[0, 200, 400]),
 ]
 
 
 def run(prob):
     cfg = prob["cfg"]
-    inp = workloads.config_inputs(cfg)
+    post = prob.get("posterior", False)
+    if post:
+        ti = workloads.thompson_inputs(workloads.THOMPSON["T1"])
+        inp = {"X": ti["Xs"], "B": ti["eps"], "S": ti["S"]}
+        tnoise = workloads.THOMPSON["T1"].noise
+    else:
+        inp = workloads.config_inputs(cfg)
     x = dv(inp["X"])
     b = dv(inp["B"])
     s0 = dv(inp["S"])
+
+    def make(**extra):
+        gg = pb.CIQ(cfg.kind, X=x, **kw, **extra)
+        if post:
+            gg.set_posterior(dv(ti["Xt"]), dv(ti["y"]), tnoise)
+        return gg
+
     out = torch.empty_like(b)
     kw = dict(lengthscale=cfg.lengthscale, outputscale=cfg.outputscale, diag=cfg.sigma2)
     rows = []
     for r in prob["ranks"]:
-        g0 = pb.CIQ(cfg.kind, X=x, **kw)
+        g0 = make()
         if r == 0:
             g = g0
         else:
@@ -48,8 +69,8 @@ def run(prob):
             e1.synchronize()
             t_chol = e0.elapsed_time(e1)
             g0.close()
-            g = pb.CIQ(cfg.kind, X=x, precond_L=lf, precond_sigma2=cfg.sigma2, **kw)
-        call = lambda: g.apply(b, out, q=cfg.q, max_iters=cfg.max_iters, tol=prob["tol"], mode="whiten",  # noqa: E731
+            g = make(precond_L=lf, precond_sigma2=cfg.sigma2)
+        call = lambda: g.apply(b, out, q=cfg.q, max_iters=cfg.max_iters, tol=prob["tol"], mode=cfg.mode,  # noqa: E731
                                lanczos_start=s0)
         for _ in range(2):
             call()
@@ -67,5 +88,7 @@ def run(prob):
     return {"problem": prob["name"], "n": cfg.n, "t": cfg.t, "results": rows}
 
 
-for p in PROBLEMS:
-    print(json.dumps(run(p)), flush=True)
+only = sys.argv[1:]   # optional problem indices
+for i, p in enumerate(PROBLEMS):
+    if not only or str(i) in only:
+        print(json.dumps(run(p)), flush=True)

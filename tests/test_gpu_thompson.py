@@ -136,3 +136,40 @@ def test_thompson_full_size_t1():
     ref_abs = post.kss.mvm_rows(rows, np.abs(y_h)) + np.abs(post.kxs[:, rows].T) @ np.abs(
         np.linalg.solve(post.kxx, post.kxs @ y_h))
     assert (np.abs(s[rows].astype(np.float64) - ref) / (ref_abs + np.abs(post.mean[rows, None]))).max() < 6e-5
+
+
+def test_posterior_pivoted_cholesky_and_preconditioned_solve():
+    """ciq_pivoted_cholesky on a posterior ctx factors COV* (the Hartmann-posterior preconditioning
+    of P:914-915); the preconditioned whitening R'B on COV* + jitter I matches the oracle's
+    precond_ciq with the same rule and J."""
+    from oracle import LowRankPlusDiag, pivoted_cholesky, precond_ciq
+    cfg = dataclasses.replace(small_cfg(n=900, m=25, t=4), jitter=1e-3)
+    inp, post, g = setup(cfg)
+    r = 40
+    ref_l = pivoted_cholesky(post, r)
+    with g:
+        lf = torch.empty((cfg.n, r), device="cuda")
+        g.pivoted_cholesky(r, lf)
+        got_l = lf.cpu().numpy().astype(np.float64)
+    assert np.abs(got_l - ref_l).max() < 2e-6
+    pre = LowRankPlusDiag(ref_l, cfg.jitter)
+
+    class _M:
+        def mvm(self, v):
+            return pre.power(post.mvm(pre.power(v, -0.5)), -0.5)
+
+    lmin, lmax, _, _ = estimate_spectrum(_M().mvm, inp["S"], 10, lower_bound=1.0)
+    rule = hht_rule(lmin, lmax, cfg.q)
+    b = inp["eps"].astype(np.float64)
+    conv = precond_ciq(post, pre, b, q=cfg.q, max_iters=2000, tol=1e-6, mode="whiten", rule=rule)
+    j = conv.iters + 10
+    ref = precond_ciq(post, pre, b, q=cfg.q, max_iters=j, tol=0.0, mode="whiten", rule=rule)
+    gp = pb.CIQ(cfg.kind, X=dev(inp["Xs"]), lengthscale=cfg.lengthscale, outputscale=cfg.outputscale,
+                diag=cfg.jitter, precond_L=dev(got_l), precond_sigma2=cfg.jitter)
+    with gp:
+        gp.set_posterior(dev(inp["Xt"]), dev(inp["y"]), cfg.noise)
+        out = torch.empty((cfg.n, cfg.t), device="cuda")
+        info = gp.apply(dev(inp["eps"]), out, q=cfg.q, max_iters=j, tol=0.0, mode="whiten", rule=rule)
+    assert info["rotated"]
+    ev = np.linalg.eigvalsh(post.dense())   # derived fp32 bound of the preconditioned path (test_gpu_precond)
+    assert relerr(out.cpu().numpy(), ref.out) < max(1e-4, 0.05 * 1e-6 * ev[-1] / ev[0])
