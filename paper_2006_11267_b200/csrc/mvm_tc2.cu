@@ -144,7 +144,10 @@ template <int KIND>
 CIQ_DEVICE float kern(float s) {
   // s = -(log2 e / 2) r^2
   if (KIND == 1) return ex2_approx(s);
-  const float r = sqrtf(fmaxf(0.f, -1.3862943611198906f * s));  // r^2 = -2 ln2 s
+  // r^2 = -2 ln2 s; sqrt.approx (one MUFU.SQRT, ~2^-23 relative) instead of the IEEE sqrtf sequence
+  // with its slow-path call
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(0.f, -1.3862943611198906f * s)));
   if (KIND == 2) {
     const float a = 2.2360679774997896f * r;
     return (1.f + a + a * a * (1.f / 3.f)) * ex2_approx(-1.4426950408889634f * a);
