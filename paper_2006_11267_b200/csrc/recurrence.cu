@@ -543,7 +543,10 @@ __global__ void sum_splits_kernel(const float* __restrict__ parts, int nsplit, s
 // G[i][j] = -1/2 sum_q w_q sum_c (xv[q][i][c] xb[q][j][c] + xb[q][i][c] xv[q][j][c]): a 128 x 128
 // output tile per CTA, 8 x 8 per thread (4 FMAs per shared-memory load), contraction over (q, c)
 // staged through shared memory 16 columns at a time; fp32, fixed summation order (deterministic).
-__global__ void __launch_bounds__(256) vjp_dense_kernel(const float* __restrict__ xb, const float* __restrict__ xv,
+#ifndef CIQ_VJP_MINB
+#define CIQ_VJP_MINB 2   // 2 CTAs per SM (128 registers): 2.87 -> 2.67 ms on C2 (A/B, ncu)
+#endif
+__global__ void __launch_bounds__(256, CIQ_VJP_MINB) vjp_dense_kernel(const float* __restrict__ xb, const float* __restrict__ xv,
                                                         const double* __restrict__ w, int nq, int64_t n, int tp,
                                                         int cols, float* __restrict__ g, int64_t ldg) {
   constexpr int TBV = 128, KS = 16;
