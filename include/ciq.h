@@ -46,7 +46,9 @@ extern "C" {
 
 typedef enum {
   CIQ_OK = 0,
-  CIQ_NOT_CONVERGED = 1,     /* result written, max_q,c |phibar|/||b_c|| > tol after max_iters */
+  CIQ_NOT_CONVERGED = 1,     /* result written, max_q,c |phibar|/||b_c|| > tol after max_iters, */
+                             /* or a NaN / inf residual (also at tol = 0; info.max_rel_residual */
+                             /* = inf, the solve stops at that iteration)                       */
   CIQ_ERR_INVALID_ARG = -1,  /* null pointer, Q out of [1, CIQ_MAX_Q], tol < 0, max_iters < 1, ... */
   CIQ_ERR_DIM = -2,          /* n <= 0, T <= 0, d < 1, leading dimension too small            */
   CIQ_ERR_NOT_PD = -3,       /* lambda_min estimate <= 0 (operator not positive definite)     */
@@ -125,8 +127,10 @@ typedef struct {
   double lambda_max;
   const double* t;            /* optional explicit rule (host, Q values each): skips estimation  */
   const double* w;            /*   and the HHT construction (parity tests)                      */
-  const float* lanczos_start; /* optional N x lanczos_cols start block (host or device); NULL =  */
-  int64_t ld_start;           /*   counter-based N(0,1) draw from `seed`                        */
+  const float* lanczos_start; /* optional start block (host or device), lanczos_cols columns:   */
+                              /*   THIS RANK's rows [row_begin, row_end) of the N x lanczos_cols */
+                              /*   block, like B (all N rows on one GPU); NULL = counter-based   */
+  int64_t ld_start;           /*   N(0,1) draw from `seed` (same on every rank count)            */
   uint64_t seed;
   int32_t mode;               /* ciq_mode                                                       */
   int32_t mvm_impl;           /* ciq_mvm_impl                                                   */

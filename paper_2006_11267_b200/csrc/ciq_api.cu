@@ -381,10 +381,14 @@ int choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm, int cl) {
 int choose_nsplit_dense(int64_t rows, int64_t npad, int chunks, int nsm) {
   const int64_t rt = (rows + 127) / 128;
   const int64_t nkt = npad / 64;
-  int best = 1;
+  // accuracy bound as tc2_choose_nsplit: at most kMaxChainDense 64-wide K tiles (12 MMAs each) feed
+  // one fp32 TMEM accumulator (round-toward-zero accumulation)
+  constexpr int64_t kMaxChainDense = 264;
+  const int smin = (int)std::max<int64_t>(1, (nkt + kMaxChainDense - 1) / kMaxChainDense);
+  int best = smin;
   double best_eff = 0.0;
-  for (int s = 1; s <= 64; ++s) {
-    if (nkt / s < 6) break;
+  for (int s = smin; s <= std::max(64, smin); ++s) {
+    if (nkt / s < 6 && s > smin) break;
     const int64_t units = rt * chunks * s;
     const int64_t waves = (units + nsm - 1) / nsm;
     const double eff = (double)units / (double)(waves * nsm) - 0.002 * waves;  // favour fewer waves
@@ -1194,6 +1198,8 @@ void ciq_free(ciq_ctx* c) {
 
 ciq_status ciq_pivoted_cholesky(ciq_ctx* c, int32_t rank, float* L, int64_t ldl) {
   if (!c || !L) return CIQ_ERR_INVALID_ARG;
+  if (c->world != 1)   // the pivot search and the kernel columns span all N rows
+    return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_pivoted_cholesky: single-GPU contexts only (not row-sharded)");
   const int64_t n = c->op.n;
   if (rank < 1 || rank > n || ldl < rank) return set_err(c, CIQ_ERR_DIM, "bad rank / ldl");
   if (join_user_stream(c) != CIQ_OK) return CIQ_ERR_CUDA;
@@ -1805,7 +1811,12 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   CUDA_TRY(c, cudaEventSynchronize(ev.e[4]));
   CUDA_TRY(c, cudaGetLastError());
 
-  const bool converged = (p.tol == 0) || (hc.max_relres <= p.tol) || (hc.breakdown > 0 && hc.done && J < p.max_iters);
+  // a NaN / inf residual or beta (overflow, a non-PSD operator) is never reported as converged,
+  // also at fixed J (tol = 0)
+  const bool finite = hc.nonfinite == 0 && std::isfinite(hc.max_relres);
+  if (!finite) set_err(c, CIQ_NOT_CONVERGED, "non-finite msMINRES residual at iteration %d", hc.iters);
+  const bool converged =
+      finite && ((p.tol == 0) || (hc.max_relres <= p.tol) || (hc.breakdown > 0 && hc.done && J < p.max_iters));
   if (info) {
     std::memset(info, 0, sizeof(*info));
     info->iters = J;

@@ -39,6 +39,7 @@ struct Ctrl {
   double tol;
   double bd_tol;
   double max_relres;
+  int nonfinite;   // 1 once a residual or beta_{j+1} came out NaN / inf (the solve stops; CIQ_NOT_CONVERGED)
 };
 
 }  // namespace ciq

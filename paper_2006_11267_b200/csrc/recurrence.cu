@@ -184,6 +184,7 @@ __global__ void init_state_kernel(Scal sc, int nq, int tp, const double* __restr
     sc.ctrl->breakdown = 0;
     sc.ctrl->max_relres = 0.0;
     sc.ctrl->arrive = 0;
+    sc.ctrl->nonfinite = 0;
   }
 }
 
@@ -274,8 +275,14 @@ __global__ void __launch_bounds__(kThreads, CIQ_UPD_MINB) lanczos_update_kernel(
         inv_nrm[k] = fr ? 0.f : (float)(1.0 / sc.nrm_cur[cc]);
         alpha[k] = fr ? 0.f : (float)sc.alpha[cc];
         cprev[k] = fr ? 0.f : (float)(sc.tb_cur[cc] / sc.nrm_prev[cc]);
+        // scale proxy for ||W_{j+1}|| = beta_{j+1} (not known until this pass ends): beta_j for
+        // j >= 2; at j = 1 (T off-diagonal beta_1 = 0) nrm_1 = ||b|| is the caller's scale, not the
+        // operator's, so alpha_1 = v_1^T K v_1 stands in (beta_2^2 <= alpha_1 (lambda_max - alpha_1)
+        // for PSD K, so beta_2 / alpha_1 <= sqrt(kappa): both fp16 planes stay in range)
+        const double a1 = fabs(sc.alpha[cc]);
+        const double proxy = (sc.tb_cur[cc] == 0.0 && a1 > 0.0) ? a1 : sc.nrm_cur[cc];
         float inv;
-        psc[k] = pack_scale(sc.nrm_cur[cc], pk.sqrt_n, &inv);
+        psc[k] = pack_scale(proxy, pk.sqrt_n, &inv);
         if (pk.planes != nullptr && blockIdx.x == 0 && lane_row == 0) pk.inv_scale[cc] = inv;
       }
     }
@@ -411,7 +418,8 @@ __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __re
     sc.cf[k] = (float)(sc.weights[q] * phi);   // Y += w_q phi d
     sc.cphi[k] = (float)phi;                    // x_q += phi d (kept solutions)
     sc.c2[k] = c1; sc.s2[k] = s1; sc.c1[k] = cs; sc.s1[k] = sn;
-    rel = fmax(rel, fabs(phib_new) / b1);
+    const double r = fabs(phib_new) / b1;
+    rel = (r <= 1e300) ? fmax(rel, r) : INFINITY;   // NaN / inf residual -> +inf (never "converged")
   }
   rel = warp_max(rel);
   if ((threadIdx.x & 31) == 0) s_rel[threadIdx.x >> 5] = rel;
@@ -457,7 +465,8 @@ __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __re
       ctrl->breakdown += brk;
       ctrl->max_relres = mx;
       ctrl->arrive = 0;
-      if (act == 0 || (ctrl->tol > 0 && mx <= ctrl->tol) || j >= ctrl->max_iters) ctrl->done = 1;
+      if (!(mx <= 1e300)) ctrl->nonfinite = 1;   // stop: a NaN / inf never recovers
+      if (act == 0 || (ctrl->tol > 0 && mx <= ctrl->tol) || j >= ctrl->max_iters || ctrl->nonfinite) ctrl->done = 1;
     }
   }
 }
