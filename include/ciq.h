@@ -101,6 +101,13 @@ typedef struct {
   int64_t rank;
   int64_t ldl;
   float sigma2;               /* > 0                                                    */
+  int32_t matrix_free;        /* 0 (default): the fp64 route -- M = P^{-1/2} K P^{-1/2} is formed */
+                              /*   once in fp64 (N^2 doubles) and the solve runs on fp64 vectors  */
+                              /*   (precond64.cu; needed for 1e-4 parity of R'B at kappa(K)~1e6,  */
+                              /*   DESIGN.md section 5); used whenever M fits in device memory.   */
+                              /* 1: apply M matrix-free per iteration (K MVM + two Woodbury       */
+                              /*   P^{-1/2} applications, fp32 vectors): O(N) memory, accuracy    */
+                              /*   limited by the fp32 sensitivity of R'B.  */
 } ciq_precond;
 
 /* Row sharding across GPUs (one process per GPU).  NULL comm = single GPU.  Rank r
@@ -169,6 +176,7 @@ typedef struct {
   int32_t update_timed;
   int32_t mvm_impl_used;      /* ciq_mvm_impl of the loop MVMs: CIQ_MVM_SIMT or CIQ_MVM_TC       */
   int32_t mvm_splits;         /* column splits of the tensor-core MVM grid (1 = none)            */
+  int32_t fp64_route;         /* 1: preconditioned solve on the fp64 materialised M (precond64.cu) */
 } ciq_info;
 
 typedef struct ciq_ctx ciq_ctx;

@@ -29,6 +29,7 @@ thread_local std::string g_init_error;
 
 struct Workspace {
   int tp = 0, nq = 0;
+  int esz = 4;             // bytes per element of W / P / D / Y: 4 (fp32) or 8 (fp64 route)
   int64_t rows = 0;
   float* w[3] = {nullptr, nullptr, nullptr};
   float* p = nullptr;
@@ -70,6 +71,12 @@ struct PrecondDev {
   double* u = nullptr;      // n x r2 (fp64: see precond.cu)
   double* g[3] = {nullptr, nullptr, nullptr};
   float a[3] = {0.f, 0.f, 0.f};
+  double ad[3] = {0.0, 0.0, 0.0};   // the same scalars in fp64 (fp64 route)
+  // fp64 route (precond64.cu): M = P^{-1/2} K P^{-1/2} materialised in fp64, rows x ldm
+  bool matrix_free = false;         // ciq_precond.matrix_free: never materialise
+  bool m64_ready = false, m64_failed = false;
+  double* m64 = nullptr;
+  int64_t ldm = 0;
   // work
   double* part = nullptr;   size_t part_cap = 0;   // utv partials  [splits][r2][tp]
   double* h = nullptr;      size_t h_cap = 0;      // U^T v         [r2][tp]
@@ -228,28 +235,31 @@ void free_lambda(LambdaWork& lw) {
   lw.tpl = lw.nb = 0;
 }
 
-ciq_status ensure_workspace(ciq_ctx* c, int tp, int nq) {
+ciq_status ensure_workspace(ciq_ctx* c, int tp, int nq, int esz = 4) {
   Workspace& ws = c->ws;
   const int64_t rows = c->row1 - c->row0;
   const int64_t n = c->op.n;
-  if (ws.tp == tp && ws.nq >= nq && ws.rows == rows) return CIQ_OK;
+  if (ws.tp == tp && ws.nq >= nq && ws.rows == rows && ws.esz == esz) return CIQ_OK;
   ++c->buf_gen;
   free_workspace(ws);
   ws.tp = tp;
   ws.nq = nq;
   ws.rows = rows;
+  ws.esz = esz;
   // W buffers hold all N rows (the MVM input; world * per >= N with zero padding); the local
-  // block is rows [row0, row1).
+  // block is rows [row0, row1).  The fp64 route stores the same buffers as doubles (esz = 8: the
+  // float* handles then address twice as many floats).
   (void)n;
-  for (auto& b : ws.w) CUDA_TRY(c, dalloc(&b, (size_t)c->nfull * tp));
-  CUDA_TRY(c, dalloc(&ws.p, (size_t)rows * tp));
-  CUDA_TRY(c, dalloc(&ws.d, (size_t)2 * nq * rows * tp));
-  CUDA_TRY(c, dalloc(&ws.y, (size_t)rows * tp));
-  CUDA_TRY(c, dalloc(&ws.apart, (size_t)mvm_simt_blocks(rows) * tp + 64 * (size_t)tp));
+  const size_t f = (size_t)esz / 4;
+  for (auto& b : ws.w) CUDA_TRY(c, dalloc(&b, f * c->nfull * tp));
+  CUDA_TRY(c, dalloc(&ws.p, f * rows * tp));
+  CUDA_TRY(c, dalloc(&ws.d, f * 2 * nq * rows * tp));
+  CUDA_TRY(c, dalloc(&ws.y, f * rows * tp));
+  CUDA_TRY(c, dalloc(&ws.apart, (size_t)std::max(mvm_simt_blocks(rows), mvm64_blocks(rows)) * tp + 64 * (size_t)tp));
   CUDA_TRY(c, dalloc(&ws.bpart, (size_t)rowblocks(std::max(rows, c->nfull), tp) * tp));
   CUDA_TRY(c, dalloc(&ws.colsq, (size_t)tp));
   // scalar block
-  size_t nd = (size_t)tp * 6 + (size_t)nq * tp * 5 + 2 * (size_t)nq;
+  size_t nd = (size_t)tp * 6 + (size_t)nq * tp * 9 + 2 * (size_t)nq;
   size_t bytes = nd * 8 + (size_t)tp * 8 + (size_t)nq * tp * 4 * 5 + sizeof(Ctrl) + 256;
   CUDA_TRY(c, dalloc(&ws.scal_mem, bytes));
   char* m = ws.scal_mem;
@@ -259,6 +269,8 @@ ciq_status ensure_workspace(ciq_ctx* c, int tp, int nq) {
   sc.c1 = takeD((size_t)nq * tp); sc.s1 = takeD((size_t)nq * tp); sc.c2 = takeD((size_t)nq * tp);
   sc.s2 = takeD((size_t)nq * tp); sc.phibar = takeD((size_t)nq * tp);
   sc.shifts = takeD(nq); sc.weights = takeD(nq); sc.col_rel = takeD(tp);
+  sc.da = takeD((size_t)nq * tp); sc.db = takeD((size_t)nq * tp); sc.de = takeD((size_t)nq * tp);
+  sc.df = takeD((size_t)nq * tp);
   auto takeF = [&](size_t k) { float* r = reinterpret_cast<float*>(m); m += k * 4; return r; };
   sc.ca = takeF((size_t)nq * tp); sc.cb = takeF((size_t)nq * tp); sc.ce = takeF((size_t)nq * tp);
   sc.cf = takeF((size_t)nq * tp);
@@ -823,7 +835,9 @@ ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, 
   int done_mvms = 0;
   for (int j = 0; j < J; ++j) {
     const float* vj = vec(j);
-    if (c->pc.on) {
+    if (c->pc.on && c->pc.m64_ready) {   // fp64 route: Lanczos on the materialised M (fp32 basis)
+      LAUNCH(c, launch_mvm64(c->pc.m64, c->pc.ldm, rows, n, vj, false, tpl, r0, lw.p, false, nullptr, nullptr, s));
+    } else if (c->pc.on) {
       // Lanczos on M = P^{-1/2} K P^{-1/2} (App. A: the rule must cover the spectrum of M)
       PrecondDev& P = c->pc;
       ciq_status gs = grow(c, &P.t1, &P.t_cap, (size_t)2 * n * tpl);
@@ -943,6 +957,7 @@ ciq_status build_precond(ciq_ctx* c) {
     const double ap = std::pow(s2, pw[k]);
     for (int j = 0; j < r2; ++j) g[j] = std::pow(w[j] + s2, pw[k]) - ap;
     P.a[k] = (float)ap;
+    P.ad[k] = ap;
     CUDA_TRY(c, dalloc(&P.g[k], (size_t)P.r2));
     CUDA_TRY(c, cudaMemcpyAsync(P.g[k], g.data(), g.size() * 8, cudaMemcpyHostToDevice, c->stream));
   }
@@ -953,10 +968,70 @@ ciq_status build_precond(ciq_ctx* c) {
 }
 
 void free_precond(PrecondDev& P) {
-  dfree(P.l); dfree(P.u);
+  dfree(P.l); dfree(P.u); dfree(P.m64);
+  P.m64_ready = false;
   for (auto& g : P.g) dfree(g);
   dfree(P.part); dfree(P.h); dfree(P.bpart);
   dfree(P.t1);
+}
+
+// fp64 route (precond64.cu): M = P^{-1/2} (K + sigma2 I) P^{-1/2} formed once, in fp64, from fp64
+// kernel entries (the given dense K, or COV* + jitter I = K** + jitter I - U U^T for a posterior
+// ctx):  H = K U;  A = a K + U diag(g) H^T (= P^{-1/2} K);  H = A U;  M = a A + H diag(g) U^T.
+bool use_m64(const ciq_ctx* c) {
+  return c->pc.on && !c->pc.matrix_free && !c->pc.m64_failed && c->world == 1;
+}
+
+ciq_status ensure_m64(ciq_ctx* c) {
+  PrecondDev& P = c->pc;
+  if (P.m64_ready) return CIQ_OK;
+  const int64_t n = c->op.n, rows = c->row1 - c->row0;
+  const int64_t ldm = (n + 7) / 8 * 8;
+  const int r2 = P.r2;
+  cudaStream_t s = c->stream;
+  double* h = nullptr;
+  if (dalloc(&P.m64, (size_t)rows * ldm) != cudaSuccess || dalloc(&h, (size_t)n * r2) != cudaSuccess) {
+    cudaGetLastError();
+    dfree(P.m64);
+    dfree(h);
+    P.m64_failed = true;   // too large for this device: the matrix-free route (fp32 floor)
+    return CIQ_ERR_OOM;
+  }
+  P.ldm = ldm;
+  CUDA_TRY(c, cudaMemsetAsync(P.m64, 0, (size_t)rows * ldm * 8, s));
+  LAUNCH(c, launch_materialize64(c->dev, c->row0, rows, P.m64, ldm, s));
+  double* neg = nullptr;
+  if (c->post.on) {   // COV* + jitter I = K** + jitter I - U U^T  (eq. thompson_sample)
+    const int m = c->post.m;
+    std::vector<double> ones((size_t)m, -1.0);
+    CUDA_TRY(c, dalloc(&neg, (size_t)m));
+    CUDA_TRY(c, cudaMemcpyAsync(neg, ones.data(), (size_t)m * 8, cudaMemcpyHostToDevice, s));
+    LAUNCH(c, launch_gemm64(false, true, rows, n, m, c->post.u + c->row0 * m, m, c->post.u, m, neg, 1.0, P.m64, ldm, s));
+  }
+  const double a = P.ad[PW_MHALF];
+  const double* g = P.g[PW_MHALF];
+  LAUNCH(c, launch_gemm64(false, false, n, r2, n, P.m64, ldm, P.u, r2, nullptr, 0.0, h, r2, s));   // H = K U
+  LAUNCH(c, launch_gemm64(false, true, n, n, r2, P.u, r2, h, r2, g, a, P.m64, ldm, s));            // A = P^-1/2 K
+  LAUNCH(c, launch_gemm64(false, false, n, r2, n, P.m64, ldm, P.u, r2, nullptr, 0.0, h, r2, s));   // H = A U
+  LAUNCH(c, launch_gemm64(false, true, n, n, r2, h, r2, P.u, r2, g, a, P.m64, ldm, s));            // M = A P^-1/2
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  dfree(h);
+  dfree(neg);
+  P.m64_ready = true;
+  return CIQ_OK;
+}
+
+// out (fp64, rows x tp) = P^p v (fp64) for p = -1/2 (PW_MHALF) or 1/2 (PW_HALF):
+// a v + U diag(g) (U^T v), with H = U^T v in c->pc.h.
+ciq_status precond_power64(ciq_ctx* c, int which, const double* v, int tp, double* out) {
+  PrecondDev& P = c->pc;
+  const int64_t n = c->op.n;
+  ciq_status st = grow(c, &P.h, &P.h_cap, (size_t)P.r2 * tp);
+  if (st != CIQ_OK) return st;
+  LAUNCH(c, launch_gemm64(true, false, P.r2, tp, n, P.u, P.r2, v, tp, nullptr, 0.0, P.h, tp, c->stream));
+  if (out != v) CUDA_TRY(c, cudaMemcpyAsync(out, v, (size_t)n * tp * 8, cudaMemcpyDeviceToDevice, c->stream));
+  LAUNCH(c, launch_gemm64(false, false, n, tp, P.r2, P.u, P.r2, P.h, tp, P.g[which], P.ad[which], out, tp, c->stream));
+  return CIQ_OK;
 }
 
 void free_post(PostDev& Q) {
@@ -978,6 +1053,95 @@ struct EvTimer {
   EvTimer() { for (auto& x : e) cudaEventCreate(&x); }
   ~EvTimer() { for (auto& x : e) cudaEventDestroy(x); }
 };
+
+// The msMINRES iterations j0+1.. of one solve (a4-a6).  Buffers rotate with period 6 in j (W: j
+// mod 3, D: j mod 2) and every kernel reads the iteration state from device memory, so a block of
+// `poll_every` (a multiple of 6) iterations is captured once as a CUDA graph (cached in the ctx
+// under `key`) and replayed, two blocks in flight while the host checks the stopping flag of the
+// older one; iterations past the device-side stopping rule are no-ops.  Without a graph (profiling,
+// CIQ_NO_GRAPH, a non-capturable transport) the iterations are enqueued directly.
+template <class F>
+ciq_status run_iterations(ciq_ctx* c, const ciq_params& p, int j0, uint64_t key_extra, F&& enqueue_iter, Ctrl* hc,
+                          bool* replayed) {
+  const Scal& sc = c->ws.sc;
+  cudaStream_t s = c->stream;
+  const int nq = p.Q;
+  *replayed = false;
+  const bool use_graph = !c->profiling && getenv("CIQ_NO_GRAPH") == nullptr &&
+                         (c->world == 1 || c->comm->capturable());
+  if (use_graph) {
+    const int block = std::max(6, (p.poll_every + 5) / 6 * 6);
+    const uint64_t key[6] = {c->buf_gen, (uint64_t)c->ws.tp, (uint64_t)nq, key_extra, (uint64_t)block,
+                             (uint64_t)(uintptr_t)c->ws.d};
+    if (c->gexec == nullptr || std::memcmp(key, c->gkey, sizeof(key)) != 0) {
+      if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+      const int64_t l0 = c->launches;
+      CUDA_TRY(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      ciq_status cst = CIQ_OK;
+      for (int k = 1; k <= block && cst == CIQ_OK; ++k) cst = enqueue_iter(k, nq);
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(s, &g);
+      if (cst != CIQ_OK) { if (g) cudaGraphDestroy(g); return cst; }
+      CUDA_TRY(c, e);
+      e = cudaGraphInstantiate(&c->gexec, g, 0);
+      cudaGraphDestroy(g);
+      CUDA_TRY(c, e);
+      std::memcpy(c->gkey, key, sizeof(key));
+      c->graph_nodes = c->launches - l0;
+      c->launches = l0;
+    } else {
+      *replayed = true;
+    }
+    if (c->ctrl_host == nullptr) CUDA_TRY(c, cudaMallocHost(&c->ctrl_host, 2 * sizeof(Ctrl)));
+    int launched = 0, checked = 0;
+    cudaEvent_t evp[2];
+    cudaEventCreateWithFlags(&evp[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&evp[1], cudaEventDisableTiming);
+    auto launch_one = [&]() -> ciq_status {
+      const int sl = launched & 1;
+      CUDA_TRY(c, cudaGraphLaunch(c->gexec, s));
+      c->launches += c->graph_nodes;
+      CUDA_TRY(c, cudaMemcpyAsync(&c->ctrl_host[sl], sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(c, cudaEventRecord(evp[sl], s));
+      ++launched;
+      return CIQ_OK;
+    };
+    ciq_status st = CIQ_OK;
+    for (;;) {
+      while ((int64_t)launched * block < p.max_iters - j0 && launched - checked < 2) {
+        st = launch_one();
+        if (st != CIQ_OK) break;
+      }
+      if (st != CIQ_OK) break;
+      if (cudaEventSynchronize(evp[checked & 1]) != cudaSuccess) {
+        st = set_err(c, CIQ_ERR_CUDA, "graph replay failed: %s", cudaGetErrorString(cudaGetLastError()));
+        break;
+      }
+      *hc = c->ctrl_host[checked & 1];
+      ++checked;
+      if (hc->done || checked == launched) break;
+    }
+    cudaStreamSynchronize(s);
+    cudaEventDestroy(evp[0]);
+    cudaEventDestroy(evp[1]);
+    return st;
+  }
+  int j = j0;
+  for (;;) {
+    for (int k = 0; k < p.poll_every && j < p.max_iters; ++k) {
+      ++j;
+      ciq_status st = enqueue_iter(j, nq);
+      if (st != CIQ_OK) return st;
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(hc, sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (hc->done || j >= p.max_iters) break;
+  }
+  return CIQ_OK;
+}
+
+ciq_status apply_fp64(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* out, int64_t ldo, ciq_params p,
+                      ciq_info* info);
 
 }  // namespace
 
@@ -1150,6 +1314,7 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     PrecondDev& P = c->pc;
     P.rank = (int)pc->rank;
     P.sigma2 = pc->sigma2;
+    P.matrix_free = pc->matrix_free != 0;
     if (cudaMalloc(&P.l, (size_t)op->n * P.rank * 4) != cudaSuccess) { st = CIQ_ERR_OOM; goto fail; }
     const cudaMemcpyKind kind = is_device_ptr(pc->L) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if (cudaMemcpy2D(P.l, (size_t)P.rank * 4, pc->L, (size_t)pc->ldl * 4, (size_t)P.rank * 4, (size_t)op->n, kind) !=
@@ -1377,6 +1542,10 @@ ciq_status ciq_set_posterior(ciq_ctx* c, const float* Xt, int64_t ldxt, int64_t 
   dfree(xt_d); dfree(linv_d); dfree(z_d);
   Q.on = true;
   ++c->buf_gen;   // the captured iteration graph must now include the downdate
+  if (c->pc.m64_ready) {   // the fp64 route's M was formed from the prior operator: rebuild lazily
+    dfree(c->pc.m64);
+    c->pc.m64_ready = false;
+  }
   return CIQ_OK;
 }
 
@@ -1434,6 +1603,12 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   c->profiling = p.profile_kernels != 0;
   for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
   c->timed.clear();
+  if (use_m64(c)) {   // preconditioned: the fp64 route when M fits in device memory (precond64.cu)
+    const ciq_status sm = ensure_m64(c);
+    if (sm == CIQ_OK) return apply_fp64(c, B, ldb, T, out, ldo, p, info);
+    if (sm != CIQ_ERR_OOM) return sm;
+    c->err.clear();   // M does not fit: the matrix-free route below
+  }
   const int tp = round16(T);
   const int nq = p.Q;
   const int64_t n = c->op.n;
@@ -1690,78 +1865,16 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->tol, &hctrl.tol, sizeof(double), cudaMemcpyHostToDevice, s));
     j0 = R;
   }
-  const bool use_graph = !c->profiling && getenv("CIQ_NO_GRAPH") == nullptr &&
-                         (c->world == 1 || c->comm->capturable());
-  int block = p.poll_every;
-  if (use_graph) block = std::max(6, (p.poll_every + 5) / 6 * 6);
-  if (use_graph) {
-    // size every buffer the MVM may (re)allocate before capturing
-    st = prepare_mvm_buffers(c, tp, p.mvm_impl);
-    if (st != CIQ_OK) return st;
-
-    const uint64_t key[6] = {c->buf_gen, (uint64_t)tp, (uint64_t)nq, (uint64_t)p.mvm_impl, (uint64_t)block,
-                             (uint64_t)(uintptr_t)ws.d ^ ((uint64_t)(uintptr_t)xqk << 1)};
-    if (c->gexec == nullptr || std::memcmp(key, c->gkey, sizeof(key)) != 0) {
-      if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
-      const int64_t l0 = c->launches;
-      CUDA_TRY(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-      ciq_status cst = CIQ_OK;
-      for (int k = 1; k <= block && cst == CIQ_OK; ++k) cst = enqueue_iter(k, nq);
-      cudaGraph_t g = nullptr;
-      cudaError_t e = cudaStreamEndCapture(s, &g);
-      if (cst != CIQ_OK) { if (g) cudaGraphDestroy(g); return cst; }
-      CUDA_TRY(c, e);
-      e = cudaGraphInstantiate(&c->gexec, g, 0);
-      cudaGraphDestroy(g);
-      CUDA_TRY(c, e);
-      std::memcpy(c->gkey, key, sizeof(key));
-      c->graph_nodes = c->launches - l0;
-      c->launches = l0;
-    } else {
-      loop_impl = c->tc_ok && p.mvm_impl != CIQ_MVM_SIMT ? 2 : 1;
-      loop_nsplit = c->last_nsplit;
-    }
-    if (c->ctrl_host == nullptr) CUDA_TRY(c, cudaMallocHost(&c->ctrl_host, 2 * sizeof(Ctrl)));
-    // keep up to two graphs in flight: the host checks block k while block k+1 runs
-    int launched = 0, checked = 0;
-    cudaEvent_t evp[2];
-    cudaEventCreateWithFlags(&evp[0], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&evp[1], cudaEventDisableTiming);
-    auto launch_one = [&]() -> ciq_status {
-      const int sl = launched & 1;
-      CUDA_TRY(c, cudaGraphLaunch(c->gexec, s));
-      c->launches += c->graph_nodes;
-      CUDA_TRY(c, cudaMemcpyAsync(&c->ctrl_host[sl], sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
-      CUDA_TRY(c, cudaEventRecord(evp[sl], s));
-      ++launched;
-      return CIQ_OK;
-    };
-    for (;;) {
-      while ((int64_t)launched * block < p.max_iters - j0 && launched - checked < 2) {
-        st = launch_one();
-        if (st != CIQ_OK) return st;
-      }
-      CUDA_TRY(c, cudaEventSynchronize(evp[checked & 1]));
-      hc = c->ctrl_host[checked & 1];
-      ++checked;
-      if (hc.done || checked == launched) break;
-    }
-    CUDA_TRY(c, cudaStreamSynchronize(s));
-    cudaEventDestroy(evp[0]);
-    cudaEventDestroy(evp[1]);
-    c->last_nsplit = loop_nsplit;
+  st = prepare_mvm_buffers(c, tp, p.mvm_impl);   // every buffer the MVM may (re)allocate, before any capture
+  if (st != CIQ_OK) return st;
+  bool replayed = false;
+  st = run_iterations(c, p, j0, (uint64_t)p.mvm_impl ^ ((uint64_t)(uintptr_t)xqk << 1), enqueue_iter, &hc, &replayed);
+  if (st != CIQ_OK) return st;
+  if (replayed) {   // cached graph: the MVM kind / splits are those of the capture
+    loop_impl = c->tc_ok && p.mvm_impl != CIQ_MVM_SIMT ? 2 : 1;
+    loop_nsplit = c->last_nsplit;
   } else {
-    int j = j0;
-    for (;;) {
-      for (int k = 0; k < p.poll_every && j < p.max_iters; ++k) {
-        ++j;
-        st = enqueue_iter(j, nq);
-        if (st != CIQ_OK) return st;
-      }
-      CUDA_TRY(c, cudaMemcpyAsync(&hc, sc.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
-      CUDA_TRY(c, cudaStreamSynchronize(s));
-      if (hc.done || j >= p.max_iters) break;
-    }
+    c->last_nsplit = loop_nsplit;
   }
   const int J = hc.iters;
   // last pending update (step J): v_J lives in the buffer that was W_cur at iteration J
@@ -1838,6 +1951,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     info->kernel_launches = c->launches;
     info->mvm_impl_used = loop_impl;
     info->mvm_splits = loop_nsplit;
+    info->fp64_route = 0;
     for (auto& tm : c->timed) {
       if (tm.j > J) continue;  // iterations launched after convergence are no-ops
       float ms = 0.f;
@@ -1850,3 +1964,163 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
 }
 
 }  // extern "C"
+
+namespace {
+
+// The fp64 route of the preconditioned variant (precond64.cu; App. A): the same steps as
+// ciq_apply -- a1 RHS normalisation, a2/a3 lambda estimate on M and the HHT rule, a4-a6 the
+// msMINRES iterations (MVM with M, alpha, streaming update, Givens), a7 finalise -- with fp64
+// vectors and the materialised fp64 M:  R' b = P^{-1/2} M^{-1/2} b,  R b = P^{1/2} M (M^{-1/2} b).
+ciq_status apply_fp64(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* out, int64_t ldo, ciq_params p,
+                      ciq_info* info) {
+  PrecondDev& P = c->pc;
+  const int tp = round16(T);
+  const int nq = p.Q;
+  const int64_t n = c->op.n, rows = c->row1 - c->row0;
+  cudaStream_t s = c->stream;
+  ciq_status st = ensure_workspace(c, tp, nq, 8);
+  if (st != CIQ_OK) return st;
+  Workspace& ws = c->ws;
+  const Scal& sc = ws.sc;
+  auto D = [](float* f) { return reinterpret_cast<double*>(f); };
+  st = join_user_stream(c);
+  if (st != CIQ_OK) return st;
+  EvTimer ev;
+  CUDA_TRY(c, cudaEventRecord(ev.e[0], s));
+  // a1: B -> W_1 = nrm_1 v_1 (fp64)
+  for (auto& wb : ws.w) CUDA_TRY(c, cudaMemsetAsync(wb, 0, (size_t)c->nfull * tp * 8, s));
+  if (is_device_ptr(B)) {
+    LAUNCH(c, launch_f32_to_f64(B, ldb, rows, (int)T, D(ws.w[1]) + c->row0 * tp, tp, s));
+  } else {
+    st = ensure_staging(c, rows * tp);
+    if (st != CIQ_OK) return st;
+    CUDA_TRY(c, cudaMemcpy2DAsync(c->staging, (size_t)tp * 4, B, (size_t)ldb * 4, (size_t)T * 4, (size_t)rows,
+                                  cudaMemcpyHostToDevice, s));
+    LAUNCH(c, launch_f32_to_f64(c->staging, tp, rows, (int)T, D(ws.w[1]) + c->row0 * tp, tp, s));
+  }
+  CUDA_TRY(c, cudaMemsetAsync(ws.y, 0, (size_t)rows * tp * 8, s));
+  CUDA_TRY(c, cudaMemsetAsync(ws.d, 0, (size_t)2 * nq * rows * tp * 8, s));
+  Ctrl hctrl{};
+  hctrl.max_iters = p.max_iters;
+  hctrl.nq = nq;
+  hctrl.tp = tp;
+  hctrl.tol = p.tol;
+  hctrl.bd_tol = p.breakdown_tol;
+  CUDA_TRY(c, cudaMemcpyAsync(sc.ctrl, &hctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, s));
+  LAUNCH(c, launch_colsq_partials64(D(ws.w[1]) + c->row0 * tp, rows, tp, ws.bpart, s));
+  LAUNCH(c, launch_reduce_cols(ws.bpart, rowblocks(rows, tp), tp, ws.colsq, 0, s));
+  LAUNCH(c, launch_init_state(sc, nq, tp, ws.colsq, s));
+  // a2/a3: rule (lambda_min(M) >= 1: reading G6 / G13)
+  double t[CIQ_MAX_Q], w[CIQ_MAX_Q];
+  double lmin = NAN, lmax = NAN, rmin = NAN, rmax = NAN;
+  int lambda_mvms = 0;
+  CUDA_TRY(c, cudaEventRecord(ev.e[1], s));
+  if (p.t != nullptr) {
+    for (int q = 0; q < nq; ++q) { t[q] = p.t[q]; w[q] = p.w[q]; }
+  } else {
+    if (p.lambda_min > 0 && p.lambda_max > 0) {
+      lmin = p.lambda_min;
+      lmax = p.lambda_max;
+    } else {
+      st = estimate_lambda(c, &p, 1.0, &lmin, &lmax, &rmin, &rmax, &lambda_mvms);
+      if (st != CIQ_OK) return st;
+    }
+    const int r = ciqh::hht_rule(lmin, lmax, nq, t, w);
+    if (r != 0) return set_err(c, r == -1 ? CIQ_ERR_INVALID_ARG : CIQ_ERR_ELLIPTIC, "quadrature rule failed");
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(sc.shifts, t, nq * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(sc.weights, w, nq * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaEventRecord(ev.e[2], s));
+  // a4-a6
+  double* dslot[2] = {D(ws.d), D(ws.d) + (size_t)nq * rows * tp};
+  const int nb = mvm64_blocks(rows);
+  auto enqueue_iter = [&](int j, int nqe) -> ciq_status {
+    double* wcur = D(ws.w[j % 3]);
+    double* wprev = D(ws.w[(j + 2) % 3]);
+    double* wnew = D(ws.w[(j + 1) % 3]);
+    begin_timed(c, j, 0);
+    LAUNCH(c, launch_mvm64(P.m64, P.ldm, rows, n, wcur, true, tp, c->row0, D(ws.p), true, ws.apart, sc.ctrl, s));
+    end_timed(c);
+    LAUNCH(c, launch_alpha(sc, ws.apart, nb, tp, s));
+    double* d1 = dslot[j & 1];
+    double* d2 = dslot[(j + 1) & 1];
+    begin_timed(c, j, 1);
+    LAUNCH(c, launch_lanczos_update64(sc, D(ws.p), wcur + c->row0 * tp, wprev + c->row0 * tp, wnew + c->row0 * tp,
+                                      &d1, &d2, D(ws.y), nqe, rows, tp, ws.bpart, 0, s));
+    end_timed(c);
+    LAUNCH(c, launch_givens(sc, ws.bpart, update_blocks64(rows), nqe, tp, s));
+    return CIQ_OK;
+  };
+  Ctrl hc{};
+  bool replayed = false;
+  st = run_iterations(c, p, 0, 1000, enqueue_iter, &hc, &replayed);
+  if (st != CIQ_OK) return st;
+  const int J = hc.iters;
+  if (J >= 1) {   // last pending update (step J)
+    double* d1 = dslot[(J + 1) & 1];
+    double* d2 = dslot[J & 1];
+    LAUNCH(c, launch_lanczos_update64(sc, nullptr, nullptr, D(ws.w[J % 3]) + c->row0 * tp, nullptr, &d1, &d2,
+                                      D(ws.y), nq, rows, tp, nullptr, 1, s));
+  }
+  CUDA_TRY(c, cudaEventRecord(ev.e[3], s));
+  // a7: R' b = P^{-1/2} y (eq. precond_sqrt_inverse); R b = P^{1/2} (M y) (eq. precond_sqrt)
+  double* res = D(ws.w[0]);   // free after the loop (rows x tp)
+  int final_mvm = 0;
+  if (p.mode == CIQ_MODE_SQRT) {
+    LAUNCH(c, launch_mvm64(P.m64, P.ldm, rows, n, D(ws.y), true, tp, c->row0, D(ws.p), true, nullptr, nullptr, s));
+    st = precond_power64(c, PW_HALF, D(ws.p), tp, res);
+    final_mvm = 1;
+  } else {
+    st = precond_power64(c, PW_MHALF, D(ws.y), tp, res);
+  }
+  if (st != CIQ_OK) return st;
+  if (is_device_ptr(out)) {
+    LAUNCH(c, launch_f64_to_f32(res, tp, rows, (int)T, out, ldo, s));
+  } else {
+    st = ensure_staging(c, rows * tp);
+    if (st != CIQ_OK) return st;
+    LAUNCH(c, launch_f64_to_f32(res, tp, rows, (int)T, c->staging, T, s));
+    CUDA_TRY(c, cudaMemcpy2DAsync(out, (size_t)ldo * 4, c->staging, (size_t)T * 4, (size_t)T * 4, (size_t)rows,
+                                  cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_TRY(c, cudaEventRecord(ev.e[4], s));
+  CUDA_TRY(c, cudaEventSynchronize(ev.e[4]));
+  CUDA_TRY(c, cudaGetLastError());
+  const bool finite = hc.nonfinite == 0 && std::isfinite(hc.max_relres);
+  if (!finite) set_err(c, CIQ_NOT_CONVERGED, "non-finite msMINRES residual at iteration %d", hc.iters);
+  const bool converged =
+      finite && ((p.tol == 0) || (hc.max_relres <= p.tol) || (hc.breakdown > 0 && hc.done && J < p.max_iters));
+  if (info) {
+    std::memset(info, 0, sizeof(*info));
+    info->iters = J;
+    info->mvms = lambda_mvms + J + final_mvm;
+    info->converged = converged ? 1 : 0;
+    info->rotated = 1;
+    info->breakdown_cols = hc.breakdown;
+    info->Q = nq;
+    info->lambda_min = lmin;
+    info->lambda_max = lmax;
+    info->ritz_min = rmin;
+    info->ritz_max = rmax;
+    info->max_rel_residual = hc.max_relres;
+    for (int q = 0; q < nq; ++q) { info->t[q] = t[q]; info->w[q] = w[q]; }
+    cudaEventElapsedTime(&info->ms_total, ev.e[0], ev.e[4]);
+    cudaEventElapsedTime(&info->ms_lambda, ev.e[1], ev.e[2]);
+    cudaEventElapsedTime(&info->ms_loop, ev.e[2], ev.e[3]);
+    cudaEventElapsedTime(&info->ms_final, ev.e[3], ev.e[4]);
+    info->kernel_launches = c->launches;
+    info->mvm_impl_used = CIQ_MVM_SIMT;   // fp64 FMA pipe (mvm64_kernel)
+    info->mvm_splits = 1;
+    info->fp64_route = 1;
+    for (auto& tm : c->timed) {
+      if (tm.j > J) continue;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tm.a, tm.b);
+      if (tm.kind == 0) { info->ms_mvm += ms; ++info->mvm_timed; }
+      else { info->ms_update += ms; ++info->update_timed; }
+    }
+  }
+  return converged ? CIQ_OK : CIQ_NOT_CONVERGED;
+}
+
+}  // namespace

@@ -31,6 +31,7 @@ struct Scal {
   int* frozen;        // [tp]   1: column finished (b = 0 or invariant subspace)
   double* c1; double* s1; double* c2; double* s2; double* phibar;   // [Q][tp] Givens state
   float* ca; float* cb; float* ce; float* cf;                       // [Q][tp] pending-update coefs
+  double* da; double* db; double* de; double* df;                   // [Q][tp] the same in fp64 (fp64 route)
   float* cphi;        // [Q][tp] phi of the pending step (x_q += phi d, kept solutions only)
   double* shifts;     // [Q]
   double* weights;    // [Q]
@@ -94,6 +95,7 @@ cudaError_t launch_split_dense(const float* k, int64_t ldk, int64_t rows, int64_
 // ---- vector kernels (recurrence.cu) ----
 int rowblocks(int64_t rows, int tp);   // number of CTAs of the row-streaming kernels
 int update_blocks(int64_t rows);       // CTAs (= beta^2 partial rows) of lanczos_update_kernel
+int update_blocks64(int64_t rows);     // ... of its fp64 instance (launch_lanczos_update64)
 cudaError_t launch_sum_splits(const float* parts, int nsplit, size_t stride, int64_t elems, float* out,
                               cudaStream_t s);
 cudaError_t launch_load_block(const float* src, int64_t ld_src, int64_t rows, int cols, float* dst, int tp,
@@ -113,6 +115,26 @@ cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, si
                                   __half* planes = nullptr, float* inv_scale = nullptr, int64_t npad = 0, int tn = 0,
                                   int64_t n = 0,    // planes: also write W_{j+1}'s split-fp16 MVM operand
                                   float* xq = nullptr);   // [Q][rows][tp]: also accumulate x_q += phi_q d_q
+// fp64 route (preconditioned path, precond64.cu): the same streaming pass on fp64 vectors (no
+// fused packing, no kept solutions); p may be nsplit = 1 only.
+cudaError_t launch_lanczos_update64(const Scal& sc, const double* p, const double* wcur, const double* wprev,
+                                    double* wnew, double* const* d1, double* const* d2, double* y, int nq,
+                                    int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s);
+cudaError_t launch_colsq_partials64(const double* v, int64_t rows, int tp, double* part, cudaStream_t s);
+// ---- fp64 route of the preconditioned variant (precond64.cu) ----
+cudaError_t launch_materialize64(const OpDev& op, int64_t row0, int64_t rows, double* k, int64_t ldk, cudaStream_t s);
+// C = beta C + op(A) diag(g) op(B): op(A) m x kk (ta: A stored kk x m), op(B) kk x n (tb: B stored n x kk)
+cudaError_t launch_gemm64(bool ta, bool tb, int64_t m, int64_t n, int64_t kk, const double* a, int64_t lda,
+                          const double* b, int64_t ldb, const double* g, double beta, double* c, int64_t ldc,
+                          cudaStream_t s);
+// P = M V (+ alpha partials [mvm64_blocks(rows)][tp]); V (float or double) full height, P local rows
+int mvm64_blocks(int64_t rows);
+cudaError_t launch_mvm64(const double* m, int64_t ldm, int64_t rows, int64_t n, const void* v, bool v_double, int tp,
+                         int64_t row0, void* p, bool p_double, double* apart, const Ctrl* done, cudaStream_t s);
+cudaError_t launch_f32_to_f64(const float* src, int64_t ld, int64_t rows, int cols, double* dst, int tp,
+                              cudaStream_t s);
+cudaError_t launch_f64_to_f32(const double* src, int tp, int64_t rows, int cols, float* dst, int64_t ld,
+                              cudaStream_t s);
 // Backward pass: G[i][j] = -1/2 sum_{q,c} w_q (xv[q][i][c] xb[q][j][c] + xb[q][i][c] xv[q][j][c])
 cudaError_t launch_vjp_dense(const float* xb, const float* xv, const double* w, int nq, int64_t n, int tp, int cols,
                              float* g, int64_t ldg, cudaStream_t s);

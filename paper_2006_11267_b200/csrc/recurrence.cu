@@ -72,7 +72,27 @@ CIQ_DEVICE void cta_col_reduce(const Geo& g, int tp, const double (&acc)[4], dou
   for (int c = tid; c < g.cc; c += kThreads) part[(int64_t)blockIdx.x * tp + c0 + c] = sums[c];
 }
 
-__global__ void __launch_bounds__(kThreads) colsq_kernel(const float* __restrict__ v, int64_t rows, int tp,
+template <class T> struct Vec4 { T x, y, z, w; };
+template <class T> CIQ_DEVICE Vec4<T> ld4(const T* p);
+template <> CIQ_DEVICE Vec4<float> ld4<float>(const float* p) {
+  const float4 f = *reinterpret_cast<const float4*>(p);
+  return {f.x, f.y, f.z, f.w};
+}
+template <> CIQ_DEVICE Vec4<double> ld4<double>(const double* p) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+  return {a.x, a.y, b.x, b.y};
+}
+template <class T> CIQ_DEVICE void st4(T* p, const Vec4<T>& v);
+template <> CIQ_DEVICE void st4<float>(float* p, const Vec4<float>& v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v.x, v.y, v.z, v.w);
+}
+template <> CIQ_DEVICE void st4<double>(double* p, const Vec4<double>& v) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(v.x, v.y);
+  reinterpret_cast<double2*>(p)[1] = make_double2(v.z, v.w);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) colsq_kernel(const T* __restrict__ v, int64_t rows, int tp,
                                                          double* __restrict__ part) {
   Geo g(tp);
   const int tid = threadIdx.x;
@@ -82,7 +102,7 @@ __global__ void __launch_bounds__(kThreads) colsq_kernel(const float* __restrict
   if (lane_row < g.rpp) {
     int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta;
     for (int64_t i = r0 + lane_row; i < min(rows, r0 + kRowsPerCta); i += g.rpp) {
-      float4 x = *reinterpret_cast<const float4*>(v + i * tp + c);
+      const Vec4<T> x = ld4<T>(v + i * tp + c);
       acc[0] += (double)x.x * x.x; acc[1] += (double)x.y * x.y;
       acc[2] += (double)x.z * x.z; acc[3] += (double)x.w * x.w;
     }
@@ -175,6 +195,7 @@ __global__ void init_state_kernel(Scal sc, int nq, int tp, const double* __restr
       sc.c1[k] = 1.0; sc.s1[k] = 0.0; sc.c2[k] = 1.0; sc.s2[k] = 0.0;
       sc.phibar[k] = b1;
       sc.ca[k] = 0.f; sc.cb[k] = 0.f; sc.ce[k] = 0.f; sc.cf[k] = 0.f; sc.cphi[k] = 0.f;
+      sc.da[k] = 0.0; sc.db[k] = 0.0; sc.de[k] = 0.0; sc.df[k] = 0.0;
     }
   }
   if (threadIdx.x == 0) {
@@ -251,12 +272,22 @@ CIQ_DEVICE float pack_scale(double nrm, double sqrt_n, float* inv) {
 #ifndef CIQ_UPD_MINB
 #define CIQ_UPD_MINB 3      // resident CTAs per SM the register budget is sized for
 #endif
-__global__ void __launch_bounds__(kThreads, CIQ_UPD_MINB) lanczos_update_kernel(
-    Scal sc, const float* __restrict__ p, int nsplit, size_t split_stride, const float* __restrict__ wcur, const float* __restrict__ wprev,
-    float* __restrict__ wnew, const float* __restrict__ d1base, float* __restrict__ d2base, int64_t qstride,
-    float* __restrict__ y, int nq, int64_t rows, int tp, double* __restrict__ bpart, int final_only, PackOut pk,
+template <class T> CIQ_DEVICE const T* coef_sel(const float* f, const double* d);
+template <> CIQ_DEVICE const float* coef_sel<float>(const float* f, const double*) { return f; }
+template <> CIQ_DEVICE const double* coef_sel<double>(const float*, const double* d) { return d; }
+
+template <class T>
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? CIQ_UPD_MINB : 2) lanczos_update_kernel(
+    Scal sc, const T* __restrict__ p, int nsplit, size_t split_stride, const T* __restrict__ wcur, const T* __restrict__ wprev,
+    T* __restrict__ wnew, const T* __restrict__ d1base, T* __restrict__ d2base, int64_t qstride,
+    T* __restrict__ y, int nq, int64_t rows, int tp, double* __restrict__ bpart, int final_only, PackOut pk,
     float* __restrict__ xq) {
   constexpr int QB = CIQ_UPD_QB;
+  constexpr bool kF32 = sizeof(T) == 4;
+  const T* CA = coef_sel<T>(sc.ca, sc.da);
+  const T* CB = coef_sel<T>(sc.cb, sc.db);
+  const T* CE = coef_sel<T>(sc.ce, sc.de);
+  const T* CF = coef_sel<T>(sc.cf, sc.df);
   const Ctrl* ctrl = sc.ctrl;
   if (!final_only && ctrl->done) return;
   const int pending = ctrl->pending;
@@ -266,15 +297,16 @@ __global__ void __launch_bounds__(kThreads, CIQ_UPD_MINB) lanczos_update_kernel(
   const int c = blockIdx.y * kChunk + quad * 4;
   double acc[4] = {0, 0, 0, 0};
   if (lane_row < g.rpp) {
-    float inv_nrm[4], alpha[4], cprev[4], psc[4];
+    T inv_nrm[4], alpha[4], cprev[4];
+    float psc[4];
     if (!final_only) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         int cc = c + k;
         bool fr = sc.frozen[cc] != 0;
-        inv_nrm[k] = fr ? 0.f : (float)(1.0 / sc.nrm_cur[cc]);
-        alpha[k] = fr ? 0.f : (float)sc.alpha[cc];
-        cprev[k] = fr ? 0.f : (float)(sc.tb_cur[cc] / sc.nrm_prev[cc]);
+        inv_nrm[k] = fr ? T(0) : (T)(1.0 / sc.nrm_cur[cc]);
+        alpha[k] = fr ? T(0) : (T)sc.alpha[cc];
+        cprev[k] = fr ? T(0) : (T)(sc.tb_cur[cc] / sc.nrm_prev[cc]);
         // scale proxy for ||W_{j+1}|| = beta_{j+1} (not known until this pass ends): beta_j for
         // j >= 2; at j = 1 (T off-diagonal beta_1 = 0) nrm_1 = ||b|| is the caller's scale, not the
         // operator's, so alpha_1 = v_1^T K v_1 stands in (beta_2^2 <= alpha_1 (lambda_max - alpha_1)
@@ -283,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, CIQ_UPD_MINB) lanczos_update_kernel(
         const double proxy = (sc.tb_cur[cc] == 0.0 && a1 > 0.0) ? a1 : sc.nrm_cur[cc];
         float inv;
         psc[k] = pack_scale(proxy, pk.sqrt_n, &inv);
-        if (pk.planes != nullptr && blockIdx.x == 0 && lane_row == 0) pk.inv_scale[cc] = inv;
+        if (kF32 && pk.planes != nullptr && blockIdx.x == 0 && lane_row == 0) pk.inv_scale[cc] = inv;
       }
     }
     // grid-stride over 64-row blocks: the grid is sized to the resident CTAs (update_blocks), so
@@ -294,24 +326,24 @@ __global__ void __launch_bounds__(kThreads, CIQ_UPD_MINB) lanczos_update_kernel(
     const int64_t r1 = min(rows, r0 + kRowsPerCta);
     for (int64_t i = r0 + lane_row; i < r1; i += g.rpp) {
       const int64_t off = i * tp + c;
-      float4 wp = *reinterpret_cast<const float4*>(wprev + off);
+      const Vec4<T> wp = ld4<T>(wprev + off);
       if (!final_only) {
-        float4 pp = *reinterpret_cast<const float4*>(p + off);
+        Vec4<T> pp = ld4<T>(p + off);
         for (int sp = 1; sp < nsplit; ++sp) {
-          const float4 q4 = *reinterpret_cast<const float4*>(p + sp * split_stride + off);
+          const Vec4<T> q4 = ld4<T>(p + sp * split_stride + off);
           pp.x += q4.x; pp.y += q4.y; pp.z += q4.z; pp.w += q4.w;
         }
-        float4 wc = *reinterpret_cast<const float4*>(wcur + off);
-        float4 w;
-        w.x = fmaf(-cprev[0], wp.x, (pp.x - alpha[0] * wc.x) * inv_nrm[0]);
-        w.y = fmaf(-cprev[1], wp.y, (pp.y - alpha[1] * wc.y) * inv_nrm[1]);
-        w.z = fmaf(-cprev[2], wp.z, (pp.z - alpha[2] * wc.z) * inv_nrm[2]);
-        w.w = fmaf(-cprev[3], wp.w, (pp.w - alpha[3] * wc.w) * inv_nrm[3]);
-        *reinterpret_cast<float4*>(wnew + off) = w;
+        const Vec4<T> wc = ld4<T>(wcur + off);
+        Vec4<T> w;
+        w.x = fma(-cprev[0], wp.x, (pp.x - alpha[0] * wc.x) * inv_nrm[0]);
+        w.y = fma(-cprev[1], wp.y, (pp.y - alpha[1] * wc.y) * inv_nrm[1]);
+        w.z = fma(-cprev[2], wp.z, (pp.z - alpha[2] * wc.z) * inv_nrm[2]);
+        w.w = fma(-cprev[3], wp.w, (pp.w - alpha[3] * wc.w) * inv_nrm[3]);
+        st4<T>(wnew + off, w);
         acc[0] += (double)w.x * w.x; acc[1] += (double)w.y * w.y;
         acc[2] += (double)w.z * w.z; acc[3] += (double)w.w * w.w;
-        if (pk.planes != nullptr) {
-          const float x[4] = {w.x * psc[0], w.y * psc[1], w.z * psc[2], w.w * psc[3]};
+        if (kF32 && pk.planes != nullptr) {
+          const float x[4] = {(float)w.x * psc[0], (float)w.y * psc[1], (float)w.z * psc[2], (float)w.w * psc[3]};
           uint32_t hw[2], lw[2];
 #pragma unroll
           for (int k = 0; k < 4; k += 2) {
@@ -329,43 +361,43 @@ __global__ void __launch_bounds__(kThreads, CIQ_UPD_MINB) lanczos_update_kernel(
         }
       }
       if (pending) {
-        float4 yy = *reinterpret_cast<const float4*>(y + off);
+        Vec4<T> yy = ld4<T>(y + off);
         for (int q0 = 0; q0 < nq; q0 += QB) {
-          float4 x1[QB], x2[QB];
+          Vec4<T> x1[QB], x2[QB];
 #pragma unroll
           for (int u = 0; u < QB; ++u) {
             if (q0 + u < nq) {
-              x1[u] = *reinterpret_cast<const float4*>(d1base + (q0 + u) * qstride + off);
-              x2[u] = *reinterpret_cast<const float4*>(d2base + (q0 + u) * qstride + off);
+              x1[u] = ld4<T>(d1base + (q0 + u) * qstride + off);
+              x2[u] = ld4<T>(d2base + (q0 + u) * qstride + off);
             }
           }
 #pragma unroll
           for (int u = 0; u < QB; ++u) {
             if (q0 + u < nq) {
               const int k = (q0 + u) * tp + c;
-              const float4 a = __ldg(reinterpret_cast<const float4*>(sc.ca + k));
-              const float4 bq = __ldg(reinterpret_cast<const float4*>(sc.cb + k));
-              const float4 e = __ldg(reinterpret_cast<const float4*>(sc.ce + k));
-              const float4 f = __ldg(reinterpret_cast<const float4*>(sc.cf + k));
-              float4 dn;
-              dn.x = fmaf(a.x, wp.x, fmaf(bq.x, x1[u].x, e.x * x2[u].x));
-              dn.y = fmaf(a.y, wp.y, fmaf(bq.y, x1[u].y, e.y * x2[u].y));
-              dn.z = fmaf(a.z, wp.z, fmaf(bq.z, x1[u].z, e.z * x2[u].z));
-              dn.w = fmaf(a.w, wp.w, fmaf(bq.w, x1[u].w, e.w * x2[u].w));
-              *reinterpret_cast<float4*>(d2base + (q0 + u) * qstride + off) = dn;
-              if (xq != nullptr) {   // kept per-shift solutions (backward pass)
-                const float4 ph = __ldg(reinterpret_cast<const float4*>(sc.cphi + k));
-                float4 xx = *reinterpret_cast<const float4*>(xq + (q0 + u) * qstride + off);
-                xx.x = fmaf(ph.x, dn.x, xx.x); xx.y = fmaf(ph.y, dn.y, xx.y);
-                xx.z = fmaf(ph.z, dn.z, xx.z); xx.w = fmaf(ph.w, dn.w, xx.w);
-                *reinterpret_cast<float4*>(xq + (q0 + u) * qstride + off) = xx;
+              const Vec4<T> a = ld4<T>(CA + k);
+              const Vec4<T> bq = ld4<T>(CB + k);
+              const Vec4<T> e = ld4<T>(CE + k);
+              const Vec4<T> f = ld4<T>(CF + k);
+              Vec4<T> dn;
+              dn.x = fma(a.x, wp.x, fma(bq.x, x1[u].x, e.x * x2[u].x));
+              dn.y = fma(a.y, wp.y, fma(bq.y, x1[u].y, e.y * x2[u].y));
+              dn.z = fma(a.z, wp.z, fma(bq.z, x1[u].z, e.z * x2[u].z));
+              dn.w = fma(a.w, wp.w, fma(bq.w, x1[u].w, e.w * x2[u].w));
+              st4<T>(d2base + (q0 + u) * qstride + off, dn);
+              if (kF32 && xq != nullptr) {   // kept per-shift solutions (backward pass)
+                const Vec4<float> ph = ld4<float>(sc.cphi + k);
+                Vec4<float> xx = ld4<float>(xq + (q0 + u) * qstride + off);
+                xx.x = fmaf(ph.x, (float)dn.x, xx.x); xx.y = fmaf(ph.y, (float)dn.y, xx.y);
+                xx.z = fmaf(ph.z, (float)dn.z, xx.z); xx.w = fmaf(ph.w, (float)dn.w, xx.w);
+                st4<float>(xq + (q0 + u) * qstride + off, xx);
               }
-              yy.x = fmaf(f.x, dn.x, yy.x); yy.y = fmaf(f.y, dn.y, yy.y);
-              yy.z = fmaf(f.z, dn.z, yy.z); yy.w = fmaf(f.w, dn.w, yy.w);
+              yy.x = fma(f.x, dn.x, yy.x); yy.y = fma(f.y, dn.y, yy.y);
+              yy.z = fma(f.z, dn.z, yy.z); yy.w = fma(f.w, dn.w, yy.w);
             }
           }
         }
-        *reinterpret_cast<float4*>(y + off) = yy;
+        st4<T>(y + off, yy);
       }
     }
     }
@@ -398,6 +430,7 @@ __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __re
     const int k = q * tp + c;
     if (frozen) {
       sc.ca[k] = 0.f; sc.cb[k] = 0.f; sc.ce[k] = 0.f; sc.cf[k] = 0.f; sc.cphi[k] = 0.f;
+      sc.da[k] = 0.0; sc.db[k] = 0.0; sc.de[k] = 0.0; sc.df[k] = 0.0;
       continue;
     }
     const double a = a_j + sc.shifts[q];
@@ -417,6 +450,8 @@ __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __re
     sc.ce[k] = (float)(-eps / gamma);
     sc.cf[k] = (float)(sc.weights[q] * phi);   // Y += w_q phi d
     sc.cphi[k] = (float)phi;                    // x_q += phi d (kept solutions)
+    sc.da[k] = 1.0 / (gamma * nrm); sc.db[k] = -delta / gamma; sc.de[k] = -eps / gamma;
+    sc.df[k] = sc.weights[q] * phi;
     sc.c2[k] = c1; sc.s2[k] = s1; sc.c1[k] = cs; sc.s1[k] = sn;
     const double r = fabs(phib_new) / b1;
     rel = (r <= 1e300) ? fmax(rel, r) : INFINITY;   // NaN / inf residual -> +inf (never "converged")
@@ -614,13 +649,24 @@ inline unsigned nb_elem(int64_t e, int bs) { return (unsigned)((e + bs - 1) / bs
 
 int rowblocks(int64_t rows, int /*tp*/) { return (int)((rows + kRowsPerCta - 1) / kRowsPerCta); }
 
-int update_blocks(int64_t rows) {
-  static const int resident = [] {
-    int nsm = 148, dev = 0;
+static int sm_count_cached() {
+  static const int nsm = [] {
+    int v = 148, dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    return CIQ_UPD_MINB * nsm;   // __launch_bounds__(kThreads, CIQ_UPD_MINB)
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
   }();
+  return nsm;
+}
+
+int update_blocks(int64_t rows) {
+  const int resident = CIQ_UPD_MINB * sm_count_cached();   // __launch_bounds__(kThreads, CIQ_UPD_MINB)
+  const int nrb = rowblocks(rows, 0);
+  return nrb < resident ? nrb : resident;
+}
+
+int update_blocks64(int64_t rows) {
+  const int resident = 2 * sm_count_cached();   // fp64 instance: __launch_bounds__(kThreads, 2)
   const int nrb = rowblocks(rows, 0);
   return nrb < resident ? nrb : resident;
 }
@@ -651,7 +697,7 @@ cudaError_t launch_randn_fill(float* dst, int64_t rows, int cols, int tp, int64_
   return cudaGetLastError();
 }
 cudaError_t launch_colsq_partials(const float* v, int64_t rows, int tp, double* part, cudaStream_t s) {
-  colsq_kernel<<<stream_grid(rows, tp), kThreads, 0, s>>>(v, rows, tp, part);
+  colsq_kernel<float><<<stream_grid(rows, tp), kThreads, 0, s>>>(v, rows, tp, part);
   return cudaGetLastError();
 }
 cudaError_t launch_reduce_cols(const double* part, int nblk, int m, double* out, int op_sqrt, cudaStream_t s) {
@@ -687,8 +733,23 @@ cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, si
   PackOut pk{planes, inv_scale, npad, tn, sqrt((double)n)};
   dim3 grid = stream_grid(rows, tp);
   grid.x = (unsigned)update_blocks(rows);
-  lanczos_update_kernel<<<grid, kThreads, 0, s>>>(sc, p, nsplit, split_stride, wcur, wprev, wnew, d1[0], d2[0],
-                                                                    qstride, y, nq, rows, tp, bpart, final_only, pk, xq);
+  lanczos_update_kernel<float><<<grid, kThreads, 0, s>>>(sc, p, nsplit, split_stride, wcur, wprev, wnew, d1[0], d2[0],
+                                                         qstride, y, nq, rows, tp, bpart, final_only, pk, xq);
+  return cudaGetLastError();
+}
+cudaError_t launch_lanczos_update64(const Scal& sc, const double* p, const double* wcur, const double* wprev,
+                                    double* wnew, double* const* d1, double* const* d2, double* y, int nq,
+                                    int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s) {
+  const int64_t qstride = rows * tp;
+  PackOut pk{nullptr, nullptr, 0, 0, 1.0};
+  dim3 grid = stream_grid(rows, tp);
+  grid.x = (unsigned)update_blocks64(rows);
+  lanczos_update_kernel<double><<<grid, kThreads, 0, s>>>(sc, p, 1, 0, wcur, wprev, wnew, d1[0], d2[0], qstride, y, nq,
+                                                          rows, tp, bpart, final_only, pk, nullptr);
+  return cudaGetLastError();
+}
+cudaError_t launch_colsq_partials64(const double* v, int64_t rows, int tp, double* part, cudaStream_t s) {
+  colsq_kernel<double><<<stream_grid(rows, tp), kThreads, 0, s>>>(v, rows, tp, part);
   return cudaGetLastError();
 }
 cudaError_t launch_alpha_from_sum(const Scal& sc, const double* sums, int tp, cudaStream_t s) {

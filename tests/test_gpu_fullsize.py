@@ -8,7 +8,8 @@ operators), on outputs the oracle can compute one by one, plus properties that h
   result equals K times the invsqrt result of the same Krylov solve (same rule, same J), and the
   final MVM K.Y agrees with the oracle on sampled rows given the GPU's Y.
 * C4 (M = 5000, 1024 RHS, rank-200 preconditioner): seeded columns of R'B against the oracle's
-  explicit symmetric route on those columns (columns are independent; same rule and J).
+  explicit symmetric route on those columns (columns are independent; same rule and J), at the
+  flat north_star 1e-4 (the library's fp64 materialised-M route).
 Tolerances as DESIGN.md §5 derives them (full-size tcgen05 MVM: <= 6e-5 max-abs relative)."""
 import numpy as np
 import pytest
@@ -133,11 +134,8 @@ def test_c4_full_preconditioned_sampled_columns():
                 diag=cfg.sigma2, precond_L=dev(lfac), precond_sigma2=cfg.sigma2) as g:
         out = torch.empty((cfg.n, cfg.t), device="cuda")
         info = g.apply(dev(inp["B"]), out, q=cfg.q, max_iters=j, tol=0.0, mode="whiten", rule=(t, w))
-    assert info["rotated"]
+    assert info["rotated"] and info["fp64_route"]   # the fp64 materialised-M route (precond64.cu)
+    assert np.max(np.abs(ref.solve.phibar) / ref.solve.beta1) < 1e-5, "oracle not converged: raise j"
     got = out.cpu().numpy()[:, cols].astype(np.float64)
-    # derived fp32 bound of the preconditioned path: 0.05 * eps_mvm * kappa(K), with
-    # kappa(K) <= lambda_max / sigma^2 (K = K_kern + sigma^2 I)
-    _, kmax, _, _ = estimate_spectrum(op.mvm, inp["S"], 10, lower_bound=cfg.sigma2)
-    tol = max(1e-4, 0.05 * 1e-6 * kmax / cfg.sigma2)
-    for k in range(len(cols)):
-        assert relerr(got[:, k], ref.out[:, k]) < tol, (k, relerr(got[:, k], ref.out[:, k]), tol)
+    for k in range(len(cols)):   # the north_star bar, flat
+        assert relerr(got[:, k], ref.out[:, k]) < 1e-4, (k, relerr(got[:, k], ref.out[:, k]))
