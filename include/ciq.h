@@ -251,6 +251,9 @@ ciq_status ciq_thompson(ciq_ctx* ctx, const float* eps, int64_t ld_eps, int64_t 
 void ciq_free(ciq_ctx* ctx);
 
 const char* ciq_status_string(ciq_status s);
+/* sha256 prefix (16 hex digits) of the sources this library was compiled from (build.py
+ * source_hash()); lets a caller check the binary matches the committed sources. */
+const char* ciq_source_hash(void);
 const char* ciq_last_error(const ciq_ctx* ctx);   /* NULL ctx: last error of ciq_init on this thread */
 
 /* Row block [*row_begin, *row_end) owned by `rank` of `world` for a global N (multiples of 128). */

@@ -115,6 +115,8 @@ def _load() -> ctypes.CDLL:
     lib.ciq_free.restype = None
     lib.ciq_status_string.argtypes = [c_int32]
     lib.ciq_status_string.restype = c_char_p
+    lib.ciq_source_hash.argtypes = []
+    lib.ciq_source_hash.restype = c_char_p
     lib.ciq_last_error.argtypes = [ctx_p]
     lib.ciq_last_error.restype = c_char_p
     lib.ciq_shard_rows.argtypes = [c_int64, c_int32, c_int32, POINTER(c_int64), POINTER(c_int64)]
@@ -137,7 +139,7 @@ LIB = _load()
 
 EXPORTED = ["ciq_params_default", "ciq_init", "ciq_apply", "ciq_matvec", "ciq_pivoted_cholesky", "ciq_vjp", "ciq_set_posterior",
             "ciq_thompson", "ciq_free",
-            "ciq_status_string",
+            "ciq_status_string", "ciq_source_hash",
             "ciq_last_error", "ciq_shard_rows", "ciq_quadrature_rule", "ciq_tridiag_extremes",
             "ciq_nccl_unique_id", "ciq_loopback_group_create", "ciq_loopback_group_destroy"]
 
@@ -176,6 +178,11 @@ def _ptr_ld(a, name: str, keepalive: list):
         raise TypeError(f"{name} must be a C-contiguous float32 array")
     keepalive.append(arr)
     return arr.ctypes.data, arr.shape[1], arr.shape[0], arr.shape[1]
+
+
+def ciq_source_hash() -> str:
+    """The source hash compiled into the loaded libciq.so (build.py source_hash())."""
+    return LIB.ciq_source_hash().decode()
 
 
 def ciq_params_default() -> CiqParams:

@@ -123,6 +123,7 @@ struct ciq_ctx {
   double* tsum = nullptr;     // [tp] local sums
   size_t tsum_cap = 0;
   float* xs = nullptr;        // owned scaled points
+  double* xs64 = nullptr;     // owned scaled points in fp64 (exact quotients of the fp32 inputs)
   float* kcopy = nullptr;     // owned dense copy (host-provided K)
   Workspace ws;
   LambdaWork lw;
@@ -345,19 +346,20 @@ ciq_status grow(ciq_ctx* c, T** buf, size_t* cap, size_t need) {
   return CIQ_OK;
 }
 
-// Matrix-free tensor-core MVM: the persistent 256-row kernel (mvm_tc2.cu) unless CIQ_TC_V1=1
-// selects the 128-row one (mvm_tc.cu; A/B experiments).
-bool use_tc2(const ciq_ctx* c) {
-  static const bool v1 = getenv("CIQ_TC_V1") && atoi(getenv("CIQ_TC_V1")) != 0;
-  // (every unit of the persistent kernel needs >= 4 column tiles of 64: see tc2_choose_nsplit)
-  return c->op.kind != CIQ_OP_DENSE && !v1 && c->op.n >= 256;
+// A/B switches for experiments: compiled in only with -DCIQ_EXPERIMENTS (scripts/build_variant.py);
+// the shipped library ignores the environment.
+bool experiment_env(const char* name) {
+#ifdef CIQ_EXPERIMENTS
+  return getenv(name) != nullptr;
+#else
+  (void)name;
+  return false;
+#endif
 }
 
-// Dense tensor-core MVM: the persistent kernel (mvm_dense2_kernel) unless CIQ_DENSE_V1=1.
-bool use_dense2() {
-  static const bool v1 = getenv("CIQ_DENSE_V1") && atoi(getenv("CIQ_DENSE_V1")) != 0;
-  return !v1;
-}
+// The matrix-free tensor-core MVM (mvm_tc2.cu) needs >= 4 column tiles of 64 per unit
+// (tc2_choose_nsplit), i.e. N >= 256; smaller kernel operators use the fp32 SIMT kernel.
+constexpr int64_t kTcMinN = 256;
 
 int sm_count() {
   int nsm = 148, dev = 0;
@@ -368,24 +370,7 @@ int sm_count() {
 
 bool use_tc(const ciq_ctx* c, int impl) {
   if (impl == CIQ_MVM_SIMT) return false;
-  return c->tc_ok;
-}
-
-// Number of column-splits of the J range so that (row tiles x chunks x splits) fills whole waves
-// of 148 SMs (1 CTA / SM: the kernel owns all 512 TMEM columns).
-int choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm, int cl) {
-  const int64_t rt = ((rows + 127) / 128 + cl - 1) / cl * cl;
-  const int64_t ntiles = (n + 127) / 128;
-  int best = 1;
-  double best_eff = 0.0;
-  for (int s = 1; s <= 8; ++s) {
-    if (ntiles / s < 4) break;
-    const int64_t units = rt * chunks * s;
-    const int64_t waves = (units + nsm - 1) / nsm;
-    const double eff = (double)units / (double)(waves * nsm);
-    if (eff > best_eff + 0.02) { best_eff = eff; best = s; }
-  }
-  return best;
+  return c->tc_ok && (c->op.kind == CIQ_OP_DENSE || c->op.n >= kTcMinN);
 }
 
 // Dense path: split the K stream (npad/64 tiles per row block) so that row tiles x chunks x splits
@@ -417,7 +402,7 @@ int choose_nsplit_dense(int64_t rows, int64_t npad, int chunks, int nsm) {
 constexpr int kMatMinT = 256;
 constexpr int64_t kMatMaxN = 20000;
 bool use_mat(const ciq_ctx* c, int tp) {
-  static const bool off = getenv("CIQ_NO_MATERIALIZE") != nullptr;
+  const bool off = experiment_env("CIQ_NO_MATERIALIZE");
   return !off && c->op.kind != CIQ_OP_DENSE && c->tc_ok && tp >= kMatMinT && c->op.n <= kMatMaxN;
 }
 
@@ -455,21 +440,16 @@ void mvm_geometry(const ciq_ctx* c, int tp, int* nsplit, int64_t* nblk) {
   const int64_t rows = c->row1 - c->row0;
   const int chunks = tp / tc_chunk_cols(tp);
   const int nsm = sm_count();
-  if ((c->op.kind == CIQ_OP_DENSE || use_mat(c, tp)) && use_dense2()) {
+  if (c->op.kind == CIQ_OP_DENSE || use_mat(c, tp)) {
     *nsplit = choose_nsplit_dense(rows, c->npad, chunks, nsm);
     *nblk = (rows + 127) / 128 * *nsplit * 4;
-  } else if (c->op.kind == CIQ_OP_DENSE || use_mat(c, tp)) {
-    *nsplit = choose_nsplit_dense(rows, c->npad, chunks, nsm * dense_ctas_per_sm());
-    *nblk = (rows + 127) / 128 * *nsplit;
-  } else if (use_tc2(c)) {
-    *nsplit = tc2_choose_nsplit(rows, c->op.n, chunks, nsm);
-    static const int force = getenv("CIQ_TC_NSPLIT") ? atoi(getenv("CIQ_TC_NSPLIT")) : 0;   // experiments
-    if (force > 0) *nsplit = force;
-    *nblk = (rows + 255) / 256 * *nsplit * 8;
   } else {
-    const int cl = tc_cluster_size();
-    *nsplit = choose_nsplit(rows, c->op.n, chunks, nsm, cl);
-    *nblk = ((rows + 127) / 128 + cl - 1) / cl * cl * *nsplit;
+    *nsplit = tc2_choose_nsplit(rows, c->op.n, chunks, nsm);
+#ifdef CIQ_EXPERIMENTS
+    static const int force = getenv("CIQ_TC_NSPLIT") ? atoi(getenv("CIQ_TC_NSPLIT")) : 0;
+    if (force > 0) *nsplit = force;
+#endif
+    *nblk = (rows + 255) / 256 * *nsplit * 8;
   }
 }
 
@@ -537,12 +517,9 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     if (sm != CIQ_OK) return sm;
   }
   const bool dense = c->op.kind == CIQ_OP_DENSE || mat;
-  const bool v2 = use_tc2(c) && !mat;
   int nsplit = 1;
   int64_t nblk = 0;
   mvm_geometry(c, tp, &nsplit, &nblk);
-  const int cl = (dense || v2) ? 1 : tc_cluster_size();
-  const int64_t rt = ((rows + 127) / 128 + cl - 1) / cl * cl;   // 128-row tiles, padded to whole clusters
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
   if (st != CIQ_OK) return st;
   if (c->inv_scale_n < tp) {
@@ -573,8 +550,6 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   a.row1 = c->row1;
   a.tp = tp;
   a.nsplit = nsplit;
-  a.nblk_x = (int)(rt * nsplit);
-  a.cl = cl;
   a.feat_a = c->feat_a;
   a.feat_b = c->feat_b;
   a.vplanes = c->planes;
@@ -589,50 +564,32 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   a.kplanes = c->kplanes;
   a.kplane_elems = c->kplane_elems;
   a.kscale_inv = 1.f / c->kscale;
-  {
-    static const int dbg = getenv("CIQ_TC_DEBUG") ? atoi(getenv("CIQ_TC_DEBUG")) : 0;
-    a.dbg = dbg;
-    a.dbg_clk = nullptr;
-    if ((dbg & 128) && !dense) cudaMallocManaged(&a.dbg_clk, 32 * 256 * sizeof(long long));
-    if (a.dbg_clk) cudaMemset(a.dbg_clk, 0, 32 * 256 * sizeof(long long));
-  }
   a.chunks = chunks;
-  a.nunits = v2 ? tc2_units(rows, nsplit, chunks) : (int)((rows + 127) / 128) * nsplit * chunks;
-  if (dense && use_dense2()) LAUNCH(c, launch_mvm_dense2(a, nsm, c->stream));
-  else if (dense) LAUNCH(c, launch_mvm_dense_tc(a, c->stream));
-  else if (v2) LAUNCH(c, launch_mvm_tc2(a, nsm, c->stream));
-  else LAUNCH(c, launch_mvm_tc(a, c->stream));
-  if (a.dbg_clk) {  // experiments only: dump the per-tile timeline of CTA (0, 0)
+  a.nunits = dense ? (int)((rows + 127) / 128) * nsplit * chunks : tc2_units(rows, nsplit, chunks);
+#ifdef CIQ_TC_TRACE
+  a.dbg = getenv("CIQ_TC_DEBUG") ? atoi(getenv("CIQ_TC_DEBUG")) : 0;
+  if ((a.dbg & 128) && !dense) {
+    cudaMallocManaged(&a.dbg_clk, 32 * 256 * sizeof(long long));
+    cudaMemset(a.dbg_clk, 0, 32 * 256 * sizeof(long long));
+  }
+#endif
+  if (dense) LAUNCH(c, launch_mvm_dense2(a, nsm, c->stream));
+  else LAUNCH(c, launch_mvm_tc2(a, nsm, c->stream));
+#ifdef CIQ_TC_TRACE
+  if (a.dbg_clk) {  // experiments only: the per-tile timeline of CTA 0 (slots: mvm_tc2.cu T2_STAMP)
     cudaStreamSynchronize(c->stream);
-    const long long t0 = a.dbg_clk[0 * 256];
-    fprintf(stderr, "tile  prod  it_start  k0  full_ok  epi_s  epi_done  KVdone  S+3done  s_issued  kv_iss  s_commit\n");
-    for (int j = 0; j < 48; ++j) {
-      fprintf(stderr, "%4d", j);
-      for (int sl = 0; sl < 11; ++sl) {
-        const long long v = a.dbg_clk[sl * 256 + j];
-        fprintf(stderr, " %9lld", v ? v - t0 : -1LL);
-      }
-      fprintf(stderr, "\n");
-    }
-    fprintf(stderr, "tile  k0(MMA h0)  kv_iss  s_iss | w4: wait0 s_ok done | w12: wait0 s_ok done   (relative to t0)\n");
+    const long long t0 = a.dbg_clk[0];
     for (int j = 0; j < 64; ++j) {
-      const int sl[9] = {2, 9, 8, 10, 4, 5, 11, 12, 13};
       fprintf(stderr, "%4d", j);
-      for (int k = 0; k < 9; ++k) {
-        const long long v = a.dbg_clk[sl[k] * 256 + j];
+      for (int sl = 0; sl < 32; ++sl) {
+        const long long v = a.dbg_clk[sl * 256 + j];
         fprintf(stderr, " %8lld", v ? v - t0 : -1LL);
       }
       fprintf(stderr, "\n");
     }
-    fprintf(stderr, "per-warp epilogue done (warps 4..19), relative to warp 4\n");
-    for (int j = 0; j < 48; ++j) {
-      fprintf(stderr, "%4d", j);
-      const long long w4 = a.dbg_clk[16 * 256 + j];
-      for (int w = 0; w < 16; ++w) fprintf(stderr, " %6lld", a.dbg_clk[(16 + w) * 256 + j] - w4);
-      fprintf(stderr, "\n");
-    }
     cudaFree(a.dbg_clk);
   }
+#endif
   if (nsplit > 1 && nsplit_out == nullptr)  // caller wants the complete product in p
     LAUNCH(c, launch_sum_splits(c->psplit, nsplit, (size_t)rows * tp, rows * tp, p, c->stream));
   if (nsplit_out) *nsplit_out = nsplit;
@@ -1067,7 +1024,7 @@ ciq_status run_iterations(ciq_ctx* c, const ciq_params& p, int j0, uint64_t key_
   cudaStream_t s = c->stream;
   const int nq = p.Q;
   *replayed = false;
-  const bool use_graph = !c->profiling && getenv("CIQ_NO_GRAPH") == nullptr &&
+  const bool use_graph = !c->profiling && !experiment_env("CIQ_NO_GRAPH") &&
                          (c->world == 1 || c->comm->capturable());
   if (use_graph) {
     const int block = std::max(6, (p.poll_every + 5) / 6 * 6);
@@ -1161,6 +1118,11 @@ void ciq_params_default(ciq_params* p) {
   p->poll_every = 6;
   p->breakdown_tol = 1e-6;
 }
+
+#ifndef CIQ_SOURCE_HASH
+#define CIQ_SOURCE_HASH "unknown"
+#endif
+const char* ciq_source_hash(void) { return CIQ_SOURCE_HASH; }
 
 const char* ciq_status_string(ciq_status s) {
   switch (s) {
@@ -1299,6 +1261,11 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     } else {
       for (int64_t i = 0; i < n; ++i) std::memcpy(&xh[i * d], op->X + i * op->ldx, d * 4);
     }
+    // fp64 copy first: x / l of the caller's fp32 values without an fp32 rounding of the quotient
+    // (the fp64 materialised route, precond64.cu, must see the same points as an fp64 reference)
+    std::vector<double> xh64((size_t)n * d);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t k = 0; k < d; ++k) xh64[i * d + k] = (double)xh[i * d + k] / (double)op->lengthscale[op->ard ? k : 0];
     for (int64_t i = 0; i < n; ++i)
       for (int64_t k = 0; k < d; ++k) xh[i * d + k] /= op->lengthscale[op->ard ? k : 0];
     for (int64_t k = 0; k < d; ++k) c->ls.push_back(op->lengthscale[op->ard ? k : 0]);
@@ -1307,6 +1274,11 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
       st = CIQ_ERR_CUDA; goto fail;
     }
     dv.xs = c->xs;
+    if (cudaMalloc(&c->xs64, (size_t)n * d * 8) != cudaSuccess) { st = CIQ_ERR_OOM; goto fail; }
+    if (cudaMemcpy(c->xs64, xh64.data(), (size_t)n * d * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+      st = CIQ_ERR_CUDA; goto fail;
+    }
+    dv.xs64 = c->xs64;
     dv.d = (int)d;
     c->tc_ok = build_tc_features(c, xh);
   }
@@ -1346,6 +1318,7 @@ void ciq_free(ciq_ctx* c) {
   free_workspace(c->ws);
   free_lambda(c->lw);
   dfree(c->xs);
+  dfree(c->xs64);
   dfree(c->kcopy);
   dfree(c->staging);
   dfree(c->kplanes);
@@ -1723,7 +1696,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   // single GPU, tensor-core MVM: the streaming pass of iteration j writes W_{j+1}'s split-fp16
   // planes (scale from nrm_j), so no iteration packs; W_1's planes are written here, outside the
   // captured graph (graph replays and direct launches then run identical kernels)
-  const bool fuse_pack = c->world == 1 && !P.on && use_tc(c, p.mvm_impl) && getenv("CIQ_NO_FUSED_PACK") == nullptr;
+  const bool fuse_pack = c->world == 1 && !P.on && use_tc(c, p.mvm_impl) && !experiment_env("CIQ_NO_FUSED_PACK");
   if (fuse_pack) {
     st = prepare_mvm_buffers(c, tp, p.mvm_impl);
     if (st != CIQ_OK) return st;

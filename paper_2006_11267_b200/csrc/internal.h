@@ -15,6 +15,7 @@ struct OpDev {
   int64_t n;           // global N
   int d;               // point dimension (kernels)
   const float* xs;     // N x d points scaled by 1/lengthscale (row-major, ld = d)
+  const double* xs64;  // the same scaled in fp64 from the caller's fp32 points (fp64 route only)
   const float* k;      // dense: N x N (row-major, ld = ldk)
   int64_t ldk;
   float o2;            // outputscale
@@ -50,15 +51,14 @@ cudaError_t launch_materialize(const OpDev& op, int64_t row0, int64_t rows, floa
 cudaError_t launch_mvm_simt(const OpDev& op, const float* v, int tp, int64_t row0, int64_t row1,
                             float* p, int ldp, double* alpha_part, const Ctrl* done, cudaStream_t s);
 
-// tcgen05 fused kernel MVM (mvm_tc.cu).  Writes nsplit partial products P_s (row block, tp
-// columns, stride p_split_stride floats); P = sum_s P_s.  apart: [nblk_x][tp] alpha partials.
+// tcgen05 MVMs.  Matrix-free (mvm_tc2.cu): persistent 256-row units; dense (mvm_dense.cu):
+// persistent 128-row units streaming the split K planes.  Both write nsplit partial products P_s
+// (row block, tp columns, stride p_split_stride floats); P = sum_s P_s.
 struct TcArgs {
   int kind;
   int64_t n, npad, row0, row1;
-  int tp, nsplit, nblk_x;
-  int nunits, chunks;        // persistent matrix-free kernel (mvm_tc2.cu): units = row tiles x splits x chunks
-  int cl;                    // matrix-free path: CTAs per cluster along the row tiles (1, 2, 4);
-                             // nblk_x = (row tiles rounded up to cl) * nsplit
+  int tp, nsplit;
+  int nunits, chunks;        // units = row tiles x splits x chunks (round-robin over persistent CTAs)
   const __half* feat_a;      // [npad/8][4][8][8] A-role features (rows)
   const __half* feat_b;      // [npad/8][4][8][8] B-role features (columns)
   const __half* vplanes;     // [tp/TN][2][npad*TN] split V planes (pack_v)
@@ -72,21 +72,17 @@ struct TcArgs {
   const __half* kplanes;     // dense path: split K planes [hi | lo], each kplane_elems
   int64_t kplane_elems;
   float kscale_inv;          // dense path: 1 / global K scale
-  int dbg;                   // experiments only (env CIQ_TC_DEBUG): 1 skip KV MMAs, 2 skip exp math
+  int dbg;                   // experiments only (-DCIQ_TC_TRACE, env CIQ_TC_DEBUG): 1 skip KV, 2 skip exp
   long long* dbg_clk;        // experiments only: per-tile clock stamps of CTA 0
 };
 int tc_chunk_cols(int tp);
-int dense_ctas_per_sm();     // resident CTAs per SM of the dense kernel
-int tc_cluster_size();       // cluster size of the matrix-free kernel (env CIQ_TC_CLUSTER overrides)
 cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, const double* nrm, __half* planes,
                           float* inv_scale, cudaStream_t s);
-cudaError_t launch_mvm_tc(const TcArgs& a, cudaStream_t s);
-// persistent 256-row version (mvm_tc2.cu); alpha partials: [row tiles * nsplit * 8][tp]
+// persistent 256-row matrix-free kernel (mvm_tc2.cu); alpha partials: [row tiles * nsplit * 8][tp]
 int tc2_units(int64_t rows, int nsplit, int chunks);
 int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm);
 cudaError_t launch_mvm_tc2(const TcArgs& a, int nsm, cudaStream_t s);
-cudaError_t launch_mvm_dense_tc(const TcArgs& a, cudaStream_t s);
-// persistent dense kernel: units = row tiles x nsplit x chunks, alpha partials [units/chunks * 4][tp]
+// persistent dense kernel (mvm_dense.cu): alpha partials [units/chunks * 4][tp]
 cudaError_t launch_mvm_dense2(const TcArgs& a, int nsm, cudaStream_t s);
 cudaError_t launch_absmax(const float* k, int64_t ldk, int64_t rows, int64_t n, unsigned int* out, cudaStream_t s);
 cudaError_t launch_split_dense(const float* k, int64_t ldk, int64_t rows, int64_t n, int64_t npad, float scale,

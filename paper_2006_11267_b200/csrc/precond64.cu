@@ -49,7 +49,7 @@ __global__ void materialize64_kernel(OpDev op, int64_t row0, int64_t rows, doubl
   } else {
     double r2 = 0.0;
     for (int c = 0; c < op.d; ++c) {
-      const double df = (double)op.xs[gi * op.d + c] - (double)op.xs[j * op.d + c];
+      const double df = op.xs64[gi * op.d + c] - op.xs64[j * op.d + c];
       r2 = fma(df, df, r2);
     }
     v = kernel64(op.kind, r2, (double)op.o2);

@@ -115,9 +115,11 @@ def test_c5_full_solve_fixed_j():
 
 def test_c4_full_preconditioned_sampled_columns():
     cfg = workloads.CONFIGS["C4"]
+    f32 = lambda v: float(np.float32(v))  # noqa: E731  (the ABI's fp32 scalars: same inputs on both sides)
+    cfg = workloads.scaled(cfg, lengthscale=f32(cfg.lengthscale), outputscale=f32(cfg.outputscale), sigma2=f32(cfg.sigma2))
     inp = workloads.config_inputs(cfg)
     op = KernelOperator(inp["X"], cfg.kind, cfg.lengthscale, cfg.outputscale, cfg.sigma2)
-    lfac = pivoted_cholesky(op, cfg.precond_rank)
+    lfac = pivoted_cholesky(op, cfg.precond_rank).astype(np.float32).astype(np.float64)   # the fp32 L the library gets
     pre = LowRankPlusDiag(lfac, cfg.sigma2)
 
     class _M:
