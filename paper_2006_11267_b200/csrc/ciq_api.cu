@@ -131,6 +131,7 @@ struct ciq_ctx {
   // tensor-core MVM operands
   bool tc_ok = false;
   int64_t npad = 0;
+  int kf = 32;                // feature contraction of the tensor-core MVM (3 (d + 2) <= kf)
   __half* kplanes = nullptr;  // dense path (or a materialised kernel operator): split K planes [hi | lo]
   bool mat_ready = false;     // kernel operator: kplanes hold the materialised K (mvm_materialize)
   int64_t kplane_elems = 0;
@@ -368,9 +369,16 @@ int sm_count() {
   return nsm;
 }
 
-bool use_tc(const ciq_ctx* c, int impl) {
+bool use_tc3(const ciq_ctx* c, int tp);
+
+// Tensor-core MVM for tp columns: available unless the SIMT kernel is requested, the features do
+// not fit fp16 (build_tc_features), N < 256, or d > 8 (KF = 64) with a T chunk the pair kernel
+// does not take.
+bool use_tc(const ciq_ctx* c, int impl, int tp) {
   if (impl == CIQ_MVM_SIMT) return false;
-  return c->tc_ok && (c->op.kind == CIQ_OP_DENSE || c->op.n >= kTcMinN);
+  if (!c->tc_ok) return false;
+  if (c->op.kind == CIQ_OP_DENSE) return true;
+  return c->op.n >= kTcMinN && (c->kf == 32 || use_tc3(c, tp));
 }
 
 // Dense path: split the K stream (npad/64 tiles per row block) so that row tiles x chunks x splits
@@ -435,6 +443,27 @@ ciq_status ensure_mat_planes(ciq_ctx* c) {
   return CIQ_OK;
 }
 
+// The matrix-free MVM on CTA pairs (mvm_tc3.cu): the tensor-core path for d > 8 (feature
+// contraction KF = 64, which the one-CTA kernel mvm_tc2.cu does not take), for RHS chunks of 32 / 64
+// columns with enough column tiles per unit.  For d <= 8 the one-CTA kernel is faster (DESIGN.md
+// §8) and is used; CIQ_TC3=1 (experiment builds only) selects the pair kernel for A/B runs.
+bool use_tc3(const ciq_ctx* c, int tp) {
+  if (c->op.kind == CIQ_OP_DENSE || use_mat(c, tp)) return false;
+  if (c->kf == 32 && !experiment_env("CIQ_TC3")) return false;
+  const int tn = tc_chunk_cols(tp);
+  const int64_t rows = c->row1 - c->row0;
+  const int nsm = sm_count();
+  const int nsplit = tc2_choose_nsplit(rows, c->op.n, tp / tn, nsm / 2, tc3_min_tiles());
+  return tc3_supported(tn, c->op.n, nsplit);
+}
+
+// Column width of one chunk of the split V planes: the pair kernel loads half of each 64-column
+// MMA chunk per CTA, so its planes are laid out in TN/2-wide chunks.
+int plane_cols(const ciq_ctx* c, int tp) {
+  const int tn = tc_chunk_cols(tp);
+  return use_tc3(c, tp) ? tn / 2 : tn;
+}
+
 // Column splits and number of alpha-partial rows of the tensor-core MVM for tp columns.
 void mvm_geometry(const ciq_ctx* c, int tp, int* nsplit, int64_t* nblk) {
   const int64_t rows = c->row1 - c->row0;
@@ -444,7 +473,10 @@ void mvm_geometry(const ciq_ctx* c, int tp, int* nsplit, int64_t* nblk) {
     *nsplit = choose_nsplit_dense(rows, c->npad, chunks, nsm);
     *nblk = (rows + 127) / 128 * *nsplit * 4;
   } else {
-    *nsplit = tc2_choose_nsplit(rows, c->op.n, chunks, nsm);
+    // the pair kernel (mvm_tc3.cu) balances units over nsm / 2 pairs, the one-CTA kernel over nsm CTAs
+    const bool pair = use_tc3(c, tp);
+    *nsplit = pair ? tc2_choose_nsplit(rows, c->op.n, chunks, nsm / 2, tc3_min_tiles())
+                   : tc2_choose_nsplit(rows, c->op.n, chunks, nsm);
 #ifdef CIQ_EXPERIMENTS
     static const int force = getenv("CIQ_TC_NSPLIT") ? atoi(getenv("CIQ_TC_NSPLIT")) : 0;
     if (force > 0) *nsplit = force;
@@ -462,7 +494,7 @@ ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
     ciq_status sp = post_buffers(c, tp);
     if (sp != CIQ_OK) return sp;
   }
-  if (!use_tc(c, impl)) return CIQ_OK;
+  if (!use_tc(c, impl, tp)) return CIQ_OK;
   if (use_mat(c, tp)) {
     ciq_status sm = ensure_mat_planes(c);
     if (sm != CIQ_OK) return sm;
@@ -498,9 +530,10 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     return run_post_mvm(c, v, tp, p, apart, done, impl, nrm, nsplit_out, apart_used, apart_nblk, skip_pack);
   const int64_t rows = c->row1 - c->row0;
   if (nsplit_out) *nsplit_out = 1;
-  if (!use_tc(c, impl)) {
+  if (!use_tc(c, impl, tp)) {
     if (impl == CIQ_MVM_TC)
-      return set_err(c, CIQ_ERR_INVALID_ARG, "tensor-core MVM unavailable for this operator (dense, d > 8 or huge features)");
+      return set_err(c, CIQ_ERR_INVALID_ARG,
+                     "tensor-core MVM unavailable for this operator (N < 256, huge features, or d > 8 with an RHS chunk < 32)");
     LAUNCH(c, launch_mvm_simt(c->dev, v, tp, c->row0, c->row1, p, tp, apart, done, c->stream));
     if (apart_used) *apart_used = apart;
     if (apart_nblk) *apart_nblk = mvm_simt_blocks(rows);
@@ -541,7 +574,8 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     ap = c->apart_tc;
   }
   // (skip_pack: the previous streaming pass already wrote v's split planes and inv_scale)
-  if (!skip_pack) LAUNCH(c, launch_pack_v(v, c->op.n, c->npad, tp, nrm, c->planes, c->inv_scale, c->stream));
+  if (!skip_pack)
+    LAUNCH(c, launch_pack_v(v, c->op.n, c->npad, tp, plane_cols(c, tp), nrm, c->planes, c->inv_scale, c->stream));
   TcArgs a{};
   a.kind = c->op.kind;
   a.n = c->op.n;
@@ -565,24 +599,32 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   a.kplane_elems = c->kplane_elems;
   a.kscale_inv = 1.f / c->kscale;
   a.chunks = chunks;
-  a.nunits = dense ? (int)((rows + 127) / 128) * nsplit * chunks : tc2_units(rows, nsplit, chunks);
+  const bool pair = !dense && use_tc3(c, tp);
+  a.kf = c->kf;
+  a.nunits = dense ? (int)((rows + 127) / 128) * nsplit * chunks
+                   : (pair ? tc3_units(rows, nsplit, chunks) : tc2_units(rows, nsplit, chunks));
 #ifdef CIQ_TC_TRACE
   a.dbg = getenv("CIQ_TC_DEBUG") ? atoi(getenv("CIQ_TC_DEBUG")) : 0;
   if ((a.dbg & 128) && !dense) {
-    cudaMallocManaged(&a.dbg_clk, 32 * 256 * sizeof(long long));
+    cudaMalloc(&a.dbg_clk, 32 * 256 * sizeof(long long));   // device memory: stamps must be cheap stores
     cudaMemset(a.dbg_clk, 0, 32 * 256 * sizeof(long long));
   }
 #endif
   if (dense) LAUNCH(c, launch_mvm_dense2(a, nsm, c->stream));
+  else if (pair) LAUNCH(c, launch_mvm_tc3(a, nsm, c->stream));
   else LAUNCH(c, launch_mvm_tc2(a, nsm, c->stream));
 #ifdef CIQ_TC_TRACE
-  if (a.dbg_clk) {  // experiments only: the per-tile timeline of CTA 0 (slots: mvm_tc2.cu T2_STAMP)
+  if (a.dbg_clk) {  // experiments only: the per-tile timeline of CTA 0 / pair 0 (slots: T2_STAMP / T3_STAMP)
     cudaStreamSynchronize(c->stream);
-    const long long t0 = a.dbg_clk[0];
-    for (int j = 0; j < 64; ++j) {
+    std::vector<long long> h(32 * 256);
+    cudaMemcpy(h.data(), a.dbg_clk, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    long long t0 = h[0];
+    for (int sl = 0; sl < 32; ++sl)
+      if (h[sl * 256] != 0 && h[sl * 256] < t0) t0 = h[sl * 256];
+    for (int j = 0; j < 96; ++j) {
       fprintf(stderr, "%4d", j);
-      for (int sl = 0; sl < 32; ++sl) {
-        const long long v = a.dbg_clk[sl * 256 + j];
+      for (int sl = 0; sl < 14; ++sl) {
+        const long long v = h[sl * 256 + j];
         fprintf(stderr, " %8lld", v ? v - t0 : -1LL);
       }
       fprintf(stderr, "\n");
@@ -666,7 +708,8 @@ bool build_tc_features(ciq_ctx* c, const std::vector<float>& xh) {
   const int64_t n = c->op.n;
   const int d = (int)c->op.d;
   const int d2 = d + 2;
-  if (3 * d2 > 32) return false;
+  if (3 * d2 > 64) return false;
+  const int kf = 3 * d2 > 32 ? 64 : 32;   // feature contraction (64: pair kernel only)
   const int64_t npad = (n + 127) / 128 * 128;
   std::vector<double> mean(d, 0.0);
   for (int64_t i = 0; i < n; ++i)
@@ -674,7 +717,7 @@ bool build_tc_features(ciq_ctx* c, const std::vector<float>& xh) {
   for (int k = 0; k < d; ++k) mean[k] /= (double)n;
   const double sl = std::sqrt(1.4426950408889634);
   // (+256 zero rows: the 256-row units of mvm_tc2.cu may start at any 128-aligned row < npad)
-  std::vector<__half> fa((size_t)(npad + 256) * 32, __float2half(0.f)), fb((size_t)(npad + 256) * 32, __float2half(0.f));
+  std::vector<__half> fa((size_t)(npad + 256) * kf, __float2half(0.f)), fb((size_t)(npad + 256) * kf, __float2half(0.f));
   std::vector<double> a(d2), b(d2);
   double hmax = 0.0;
   auto put = [&](std::vector<__half>& f, int64_t i, int kidx, double val, bool lo) {
@@ -682,7 +725,7 @@ bool build_tc_features(ciq_ctx* c, const std::vector<float>& xh) {
     if (lo) h = __float2half_rn((float)(val - (double)__half2float(h)));
     const int64_t ng = i / 8, r = i % 8;
     const int kc = kidx / 8, kk = kidx % 8;
-    f[(size_t)((ng * 4 + kc) * 64 + r * 8 + kk)] = h;
+    f[(size_t)((ng * (kf / 8) + kc) * 64 + r * 8 + kk)] = h;
   };
   for (int64_t i = 0; i < n; ++i) {
     double hh = 0.0;
@@ -709,6 +752,7 @@ bool build_tc_features(ciq_ctx* c, const std::vector<float>& xh) {
   cudaMemcpy(c->feat_a, fa.data(), fa.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(c->feat_b, fb.data(), fb.size() * 2, cudaMemcpyHostToDevice);
   c->npad = npad;
+  c->kf = kf;
   return cudaGetLastError() == cudaSuccess;
 }
 
@@ -1696,11 +1740,11 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   // single GPU, tensor-core MVM: the streaming pass of iteration j writes W_{j+1}'s split-fp16
   // planes (scale from nrm_j), so no iteration packs; W_1's planes are written here, outside the
   // captured graph (graph replays and direct launches then run identical kernels)
-  const bool fuse_pack = c->world == 1 && !P.on && use_tc(c, p.mvm_impl) && !experiment_env("CIQ_NO_FUSED_PACK");
+  const bool fuse_pack = c->world == 1 && !P.on && use_tc(c, p.mvm_impl, tp) && !experiment_env("CIQ_NO_FUSED_PACK");
   if (fuse_pack) {
     st = prepare_mvm_buffers(c, tp, p.mvm_impl);
     if (st != CIQ_OK) return st;
-    LAUNCH(c, launch_pack_v(ws.w[1], c->op.n, c->npad, tp, sc.nrm_cur, c->planes, c->inv_scale, s));
+    LAUNCH(c, launch_pack_v(ws.w[1], c->op.n, c->npad, tp, plane_cols(c, tp), sc.nrm_cur, c->planes, c->inv_scale, s));
   }
   auto enqueue_iter = [&](int j, int nqe) -> ciq_status {
     float* wcur = ws.w[j % 3];
@@ -1732,7 +1776,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     begin_timed(c, j, 1);
     LAUNCH(c, launch_lanczos_update(sc, pin, nsplit, (size_t)rows * tp, wcur + c->row0 * tp, wprev + c->row0 * tp,
                                     wnew + c->row0 * tp, &d1, &d2, ws.y, nqe, rows, tp, ws.bpart, 0, s,
-                                    fuse_pack ? c->planes : nullptr, c->inv_scale, c->npad, tc_chunk_cols(tp), c->op.n,
+                                    fuse_pack ? c->planes : nullptr, c->inv_scale, c->npad, plane_cols(c, tp), c->op.n,
                                     xqk));
     end_timed(c);
     if (c->world == 1) {

@@ -59,6 +59,7 @@ struct TcArgs {
   int64_t n, npad, row0, row1;
   int tp, nsplit;
   int nunits, chunks;        // units = row tiles x splits x chunks (round-robin over persistent CTAs)
+  int kf;                    // feature contraction (32, or 64 for d > 8: pair kernel only)
   const __half* feat_a;      // [npad/8][4][8][8] A-role features (rows)
   const __half* feat_b;      // [npad/8][4][8][8] B-role features (columns)
   const __half* vplanes;     // [tp/TN][2][npad*TN] split V planes (pack_v)
@@ -76,12 +77,19 @@ struct TcArgs {
   long long* dbg_clk;        // experiments only: per-tile clock stamps of CTA 0
 };
 int tc_chunk_cols(int tp);
-cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, const double* nrm, __half* planes,
+// tn: column width of one layout chunk (tc_chunk_cols(tp), halved for the pair kernel)
+cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, int tn, const double* nrm, __half* planes,
                           float* inv_scale, cudaStream_t s);
 // persistent 256-row matrix-free kernel (mvm_tc2.cu); alpha partials: [row tiles * nsplit * 8][tp]
 int tc2_units(int64_t rows, int nsplit, int chunks);
-int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm);
+// min_tiles: column tiles each unit keeps (4 for mvm_tc2.cu, tc3_min_tiles() for mvm_tc3.cu)
+int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm, int min_tiles = 4);
 cudaError_t launch_mvm_tc2(const TcArgs& a, int nsm, cudaStream_t s);
+// CTA-pair kernel (mvm_tc3.cu): same units / alpha partials as tc2, V planes in TN/2-wide chunks
+bool tc3_supported(int tn, int64_t n, int nsplit);
+int tc3_min_tiles();
+int tc3_units(int64_t rows, int nsplit, int chunks);
+cudaError_t launch_mvm_tc3(const TcArgs& a, int nsm, cudaStream_t s);
 // persistent dense kernel (mvm_dense.cu): alpha partials [units/chunks * 4][tp]
 cudaError_t launch_mvm_dense2(const TcArgs& a, int nsm, cudaStream_t s);
 cudaError_t launch_absmax(const float* k, int64_t ldk, int64_t rows, int64_t n, unsigned int* out, cudaStream_t s);

@@ -315,9 +315,8 @@ int tc_chunk_cols(int tp) {
   return 16;
 }
 
-cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, const double* nrm, __half* planes,
+cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, int tn, const double* nrm, __half* planes,
                           float* inv_scale, cudaStream_t s) {
-  const int tn = tc_chunk_cols(tp);
   const int64_t total = npad * (tp / 8);
   pack_v_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(v, n, npad, tp, tn, nrm, planes, inv_scale);
   return cudaGetLastError();

@@ -543,13 +543,13 @@ cudaError_t launch2_kind(const TcArgs& a, int tn, int grid, cudaStream_t s) {
 int tc2_units(int64_t rows, int nsplit, int chunks) { return (int)((rows + BM2 - 1) / BM2) * nsplit * chunks; }
 
 // Column splits of the unit grid: enough units for the persistent CTAs to finish together
-// (max units per CTA x tiles per unit minimal), each split keeping >= 4 column tiles, and at most
+// (max units per CTA x tiles per unit minimal), each split keeping >= min_tiles column tiles, and at most
 // kMaxChain tiles per unit.  The chain bound is an accuracy bound: the tensor core adds each MMA
 // into the fp32 TMEM accumulator with a round-toward-zero bias, measured on B200 as a relative
 // shrink of ~1.1e-8 per accumulated MMA (12 per tile): 261 tiles -> -3.5e-5, 782 tiles -> -1e-4
 // (scripts/diag_mvm_n.py).  The per-split partial products are summed in
 // fp32 (round to nearest) by the consumer.
-int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm) {
+int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm, int min_tiles) {
   constexpr int64_t kMaxChain = 264;
   const int64_t nrt = (rows + BM2 - 1) / BM2;
   const int64_t ntiles = (n + BN2 - 1) / BN2;
@@ -557,7 +557,7 @@ int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm) {
   int best = smin;
   double best_cost = 1e300;
   for (int s = smin; s <= smin + 15; ++s) {
-    if (ntiles / s < 4) break;
+    if (ntiles / s < min_tiles && s > smin) break;
     const int64_t units = nrt * chunks * s;
     const int64_t per_cta = (units + nsm - 1) / nsm;
     const double cost = (double)per_cta * (double)((ntiles + s - 1) / s) * (1.0 + 0.002 * s);
