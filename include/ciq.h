@@ -110,7 +110,8 @@ typedef struct {
                               /*   limited by the fp32 sensitivity of R'B.  */
 } ciq_precond;
 
-/* Row sharding across GPUs (one process per GPU).  NULL comm = single GPU.  Rank r
+/* Row sharding across GPUs (one process per GPU).  NULL comm = single GPU; a comm
+ * with world = 1 runs the sharded code path (collectives included) on one rank.  Rank r
  * owns rows ciq_shard_rows(n, r, world); per iteration the ranks all-gather the next Lanczos
  * block and the T-sized alpha / beta^2 partial sums (summed in rank order: bit-identical scalar
  * state on every rank). */

@@ -114,6 +114,7 @@ struct ciq_ctx {
   cudaStream_t user_stream = nullptr;  // the caller's stream given to ciq_init
   cudaEvent_t join_ev = nullptr;
   int rank = 0, world = 1;
+  bool sharded = false;       // a ciq_comm was given: the row-sharded code path (also for world = 1)
   int64_t row0 = 0, row1 = 0;
   int64_t per = 0;            // rows per shard (multiple of 128; last shard may be shorter)
   int64_t nfull = 0;          // rows of the replicated (all-gathered) vectors = world * per >= n
@@ -761,7 +762,7 @@ ciq_status precond_power(ciq_ctx* c, int which, const float* v, int tp, int64_t 
 
 // vals[0..m) <- sum over ranks of vals (allgather + rank-order sum): identical on every rank.
 ciq_status global_sum(ciq_ctx* c, double* vals, int m) {
-  if (c->world == 1) return CIQ_OK;
+  if (!c->sharded) return CIQ_OK;
   ciq_status st = grow(c, &c->gsum, &c->gsum_cap, (size_t)c->world * m);
   if (st != CIQ_OK) return st;
   if (!c->comm->allgather(vals, c->gsum, (size_t)m * 8, c->stream))
@@ -772,7 +773,7 @@ ciq_status global_sum(ciq_ctx* c, double* vals, int m) {
 
 // Every rank's row block [row0, row1) of a full-height (nfull x tp) vector -> all ranks.
 ciq_status allgather_rows(ciq_ctx* c, float* full, int tp) {
-  if (c->world == 1) return CIQ_OK;
+  if (!c->sharded) return CIQ_OK;
   const size_t bytes = (size_t)c->per * tp * 4;
   if (!c->comm->allgather(full + (size_t)c->rank * c->per * tp, full, bytes, c->stream))
     return set_err(c, CIQ_ERR_NCCL, "allgather: %s", c->comm->error());
@@ -790,7 +791,7 @@ ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, 
   const int64_t nf = c->nfull;                 // basis vectors are full height (row-sharded work)
   const int64_t rows = c->row1 - c->row0;
   const int64_t r0 = c->row0;
-  if (c->world != 1 && c->pc.on)
+  if (c->sharded && c->pc.on)
     return set_err(c, CIQ_ERR_INVALID_ARG, "preconditioner with row sharding: not supported");
   LambdaWork& lw = c->lw;
   if (lw.tpl != tpl || lw.nb < J + 1 || lw.rows != rows) {
@@ -980,7 +981,7 @@ void free_precond(PrecondDev& P) {
 // kernel entries (the given dense K, or COV* + jitter I = K** + jitter I - U U^T for a posterior
 // ctx):  H = K U;  A = a K + U diag(g) H^T (= P^{-1/2} K);  H = A U;  M = a A + H diag(g) U^T.
 bool use_m64(const ciq_ctx* c) {
-  return c->pc.on && !c->pc.matrix_free && !c->pc.m64_failed && c->world == 1;
+  return c->pc.on && !c->pc.matrix_free && !c->pc.m64_failed && !c->sharded;
 }
 
 ciq_status ensure_m64(ciq_ctx* c) {
@@ -1069,7 +1070,7 @@ ciq_status run_iterations(ciq_ctx* c, const ciq_params& p, int j0, uint64_t key_
   const int nq = p.Q;
   *replayed = false;
   const bool use_graph = !c->profiling && !experiment_env("CIQ_NO_GRAPH") &&
-                         (c->world == 1 || c->comm->capturable());
+                         (!c->sharded || c->comm->capturable());
   if (use_graph) {
     const int block = std::max(6, (p.poll_every + 5) / 6 * 6);
     const uint64_t key[6] = {c->buf_gen, (uint64_t)c->ws.tp, (uint64_t)nq, key_extra, (uint64_t)block,
@@ -1235,7 +1236,7 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     if (!(pc->sigma2 > 0)) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "preconditioner sigma2 must be > 0 (S:425)");
     if (pc->rank > 2048) return set_err(nullptr, CIQ_ERR_DIM, "preconditioner rank > 2048");
   }
-  if (comm && comm->world > 1) {
+  if (comm && comm->world >= 1) {
     if (comm->rank < 0 || comm->rank >= comm->world) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "bad rank");
     if (!comm->loopback_group && !comm->nccl_unique_id)
       return set_err(nullptr, CIQ_ERR_INVALID_ARG, "row sharding needs an NCCL unique id or a loopback group");
@@ -1254,7 +1255,8 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     delete c;
     return set_err(nullptr, CIQ_ERR_CUDA, "stream creation failed");
   }
-  if (comm && comm->world > 1) {
+  if (comm && comm->world >= 1) {
+    c->sharded = true;
     c->rank = comm->rank;
     c->world = comm->world;
     ciq_shard_rows(op->n, c->rank, c->world, &c->row0, &c->row1);
@@ -1380,7 +1382,7 @@ void ciq_free(ciq_ctx* c) {
 
 ciq_status ciq_pivoted_cholesky(ciq_ctx* c, int32_t rank, float* L, int64_t ldl) {
   if (!c || !L) return CIQ_ERR_INVALID_ARG;
-  if (c->world != 1)   // the pivot search and the kernel columns span all N rows
+  if (c->sharded)   // the pivot search and the kernel columns span all N rows
     return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_pivoted_cholesky: single-GPU contexts only (not row-sharded)");
   const int64_t n = c->op.n;
   if (rank < 1 || rank > n || ldl < rank) return set_err(c, CIQ_ERR_DIM, "bad rank / ldl");
@@ -1424,7 +1426,7 @@ ciq_status ciq_matvec(ciq_ctx* c, const float* V, int64_t ldv, int64_t T, float*
 ciq_status ciq_vjp(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int64_t ldv, int64_t T,
                    const ciq_params* params, float* G, int64_t ldg, ciq_info* info) {
   if (!c || !B || !V || !G) return CIQ_ERR_INVALID_ARG;
-  if (c->world != 1 || c->has_precond)
+  if (c->sharded || c->has_precond)
     return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_vjp: single GPU, unpreconditioned operators only");
   const int64_t n = c->op.n;
   if (T <= 0 || ldv < T || ldb < T || ldg < n) return set_err(c, CIQ_ERR_DIM, "bad T / leading dimension");
@@ -1483,7 +1485,7 @@ ciq_status ciq_vjp(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int6
 
 ciq_status ciq_set_posterior(ciq_ctx* c, const float* Xt, int64_t ldxt, int64_t m, const float* y, double noise) {
   if (!c || !Xt) return CIQ_ERR_INVALID_ARG;
-  if (c->op.kind == CIQ_OP_DENSE || c->world != 1)
+  if (c->op.kind == CIQ_OP_DENSE || c->sharded)
     return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_set_posterior: single-GPU kernel operators only");
   const int d = (int)c->op.d;
   if (m < 1 || m > 4096 || ldxt < d) return set_err(c, CIQ_ERR_DIM, "ciq_set_posterior: need 1 <= m <= 4096, ldxt >= d");
@@ -1740,7 +1742,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   // single GPU, tensor-core MVM: the streaming pass of iteration j writes W_{j+1}'s split-fp16
   // planes (scale from nrm_j), so no iteration packs; W_1's planes are written here, outside the
   // captured graph (graph replays and direct launches then run identical kernels)
-  const bool fuse_pack = c->world == 1 && !P.on && use_tc(c, p.mvm_impl, tp) && !experiment_env("CIQ_NO_FUSED_PACK");
+  const bool fuse_pack = !c->sharded && !P.on && use_tc(c, p.mvm_impl, tp) && !experiment_env("CIQ_NO_FUSED_PACK");
   if (fuse_pack) {
     st = prepare_mvm_buffers(c, tp, p.mvm_impl);
     if (st != CIQ_OK) return st;
@@ -1763,7 +1765,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     const float* pin = (nsplit > 1) ? c->psplit : ws.p;
     loop_nsplit = nsplit;
     loop_impl = c->mvm_kind_used;
-    if (c->world == 1) {
+    if (!c->sharded) {
       LAUNCH(c, launch_alpha(sc, apart, nbm, tp, s));
     } else {
       LAUNCH(c, launch_reduce_cols(apart, nbm, tp, tsum_a, 0, s));
@@ -1779,7 +1781,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
                                     fuse_pack ? c->planes : nullptr, c->inv_scale, c->npad, plane_cols(c, tp), c->op.n,
                                     xqk));
     end_timed(c);
-    if (c->world == 1) {
+    if (!c->sharded) {
       LAUNCH(c, launch_givens(sc, ws.bpart, update_blocks(rows), nqe, tp, s));
     } else {
       LAUNCH(c, launch_reduce_cols(ws.bpart, update_blocks(rows), tp, tsum_b, 0, s));
@@ -1921,7 +1923,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   if (p.mode == CIQ_MODE_SQRT) {
     // K . Y: Y is this rank's row block -> all-gather it into a free full-height W buffer
     float* yfull = yout;
-    if (c->world > 1) {
+    if (c->sharded) {
       yfull = ws.w[(J + 1) % 3];
       CUDA_TRY(c, cudaMemcpyAsync(yfull + c->row0 * tp, yout, (size_t)rows * tp * 4, cudaMemcpyDeviceToDevice, s));
       st = allgather_rows(c, yfull, tp);

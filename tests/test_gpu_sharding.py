@@ -97,3 +97,28 @@ def test_sharded_lanczos_reuse_equals_single_gpu(world):
     for inf in infos[1:]:
         assert inf["lambda_max"] == infos[0]["lambda_max"] and inf["iters"] == infos[0]["iters"]
     assert abs(infos[0]["lambda_max"] / info1["lambda_max"] - 1) < 1e-6
+
+
+@pytest.mark.parametrize("dense", [False, True])
+def test_nccl_one_rank_sharded_path(dense):
+    """The NCCL transport itself (nccl_dl: dlopen of libnccl, ncclCommInitRank, ncclAllGather
+    captured in the solve's CUDA graph) on the one GPU a test box has: a world-1 communicator runs
+    the row-sharded code path (allgathered Lanczos blocks, rank-order sums of the alpha / beta^2
+    partials) and must reproduce the single-GPU result up to reduction order."""
+    cfg = workloads.scaled(workloads.CONFIGS["C2" if dense else "C3"], n=1500, t=8)
+    inp = workloads.make_inputs(cfg)
+    # converged solves (SURVEY P9: unconverged Krylov iterates amplify rounding differences -- the
+    # sharded path packs the MVM operand with its own scale -- far above the reduction-order level)
+    kw = dict(q=8, max_iters=400, tol=1e-6, mode="sqrt")
+    mk = (lambda **c: pb.CIQ("dense", K=dev(inp["K"]), diag=cfg.sigma2, **c)) if dense else \
+        (lambda **c: pb.CIQ(cfg.kind, n=cfg.n, X=dev(inp["X"]), lengthscale=cfg.lengthscale,
+                            outputscale=cfg.outputscale, diag=cfg.sigma2, **c))
+    outs = []
+    for comm in (None, (0, 1, pb.ciq_nccl_unique_id())):
+        with (mk() if comm is None else mk(comm=comm)) as g:
+            out = torch.empty((cfg.n, cfg.t), device="cuda")
+            info = g.apply(dev(inp["B"]), out, lanczos_start=dev(inp["S"]), **kw)
+            outs.append((out.cpu().numpy().astype(np.float64), info))
+    (a, ia), (b, ib) = outs
+    assert ia["converged"] and ib["converged"] and abs(ia["iters"] - ib["iters"]) <= 2
+    assert np.linalg.norm(a - b) / np.linalg.norm(a) < 1e-5
