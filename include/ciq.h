@@ -221,6 +221,20 @@ ciq_status ciq_pivoted_cholesky(ciq_ctx* ctx, int32_t rank, float* L, int64_t ld
 ciq_status ciq_vjp(ciq_ctx* ctx, const float* B, int64_t ldb, const float* V, int64_t ldv, int64_t T,
                    const ciq_params* params, float* G, int64_t ldg, ciq_info* info);
 
+/* Hyper-parameter gradient through the CIQ backward pass (eq. ciq_deriv; SURVEY
+ * §8(f) row f1): for L = sum_c v_c^T (K^{-1/2} b_c) with K = o^2 k(X, X; l) + sigma^2 I,
+ *     grad[0] = dL/dl,  grad[1] = dL/d(o^2),  grad[2] = dL/d(sigma^2)
+ * as  dL/dtheta = sum_ij G_ij dK_ij/dtheta = -sum_q w_q sum_c x_q(v_c)^T (dK/dtheta) x_q(b_c)
+ * with the shifted solves x_q(u) = (t_q I + K)^{-1} u of the forward solve and of a second solve on
+ * V with the same rule (G is never formed: O(J mvm(K)) time, O(Q N T) memory).  The
+ * bilinear forms use one matrix-free dK/dl MVM (tensor-core epilogue with the derivative of the
+ * kernel form) and one K MVM per shift, fp64 reductions.
+ *   B, V: N x T (ld >= T, host or device).  grad: 3 doubles (host).
+ * Single GPU, kernel operators with an isotropic lengthscale, no preconditioner / posterior:
+ * CIQ_ERR_INVALID_ARG otherwise.  info (nullable): the forward solve's info, mvms = all MVMs. */
+ciq_status ciq_hyper_grad(ciq_ctx* ctx, const float* B, int64_t ldb, const float* V, int64_t ldv, int64_t T,
+                          const ciq_params* params, double* grad, ciq_info* info);
+
 /* Thompson sampling (SS5.2, eq. thompson_sample).
  * ciq_set_posterior turns a matrix-free kernel context built on the candidate set X* (ciq_init
  * with op.X = X*, op.diag = the jitter) into the GP posterior covariance operator at X*,

@@ -111,6 +111,9 @@ def _load() -> ctypes.CDLL:
     lib.ciq_thompson.argtypes = [ctx_p, c_void_p, c_int64, c_int64, POINTER(CiqParams), c_void_p, c_void_p, c_int64,
                                  POINTER(CiqInfo)]
     lib.ciq_thompson.restype = c_int32
+    lib.ciq_hyper_grad.argtypes = [ctx_p, c_void_p, c_int64, c_void_p, c_int64, c_int64, POINTER(CiqParams),
+                                   POINTER(c_double), POINTER(CiqInfo)]
+    lib.ciq_hyper_grad.restype = c_int32
     lib.ciq_free.argtypes = [ctx_p]
     lib.ciq_free.restype = None
     lib.ciq_status_string.argtypes = [c_int32]
@@ -137,7 +140,8 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 
-EXPORTED = ["ciq_params_default", "ciq_init", "ciq_apply", "ciq_matvec", "ciq_pivoted_cholesky", "ciq_vjp", "ciq_set_posterior",
+EXPORTED = ["ciq_params_default", "ciq_init", "ciq_apply", "ciq_matvec", "ciq_pivoted_cholesky", "ciq_vjp", "ciq_hyper_grad",
+            "ciq_set_posterior",
             "ciq_thompson", "ciq_free",
             "ciq_status_string", "ciq_source_hash",
             "ciq_last_error", "ciq_shard_rows", "ciq_quadrature_rule", "ciq_tridiag_extremes",
@@ -322,6 +326,20 @@ def ciq_vjp(ctx, B, V, G, params: CiqParams) -> tuple[int, CiqInfo]:
     return st, info
 
 
+def ciq_hyper_grad(ctx, B, V, params: CiqParams) -> tuple[int, CiqInfo, np.ndarray]:
+    keep: list = []
+    pb, ldb, nb, t = _ptr_ld(B, "B", keep)
+    pv, ldv, nv, tv = _ptr_ld(V, "V", keep)
+    if tv != t:
+        raise CiqError(CIQ_ERR_DIM, "V must have the shape of B")
+    grad = (c_double * 3)()
+    info = CiqInfo()
+    st = LIB.ciq_hyper_grad(ctx, pb, ldb, pv, ldv, t, ctypes.byref(params), grad, ctypes.byref(info))
+    if st not in (CIQ_OK, CIQ_NOT_CONVERGED):
+        raise CiqError(st, LIB.ciq_last_error(ctx).decode())
+    return st, info, np.array(grad[:], dtype=np.float64)
+
+
 def ciq_set_posterior(ctx, Xt, y, noise: float) -> None:
     """COV* + jitter I at the ctx's candidates given training data (Xt, y) (eq. thompson_sample)."""
     keep: list = []
@@ -453,6 +471,15 @@ class CIQ:
         d = info.as_dict()
         d["status"] = st
         return d
+
+    def hyper_grad(self, B, V, **kw) -> tuple[np.ndarray, dict]:
+        """[dL/dl, dL/d(o^2), dL/d(sigma^2)] for L = sum_c v_c^T (K^{-1/2} b_c) (eq. ciq_deriv)."""
+        keep: list = []
+        params, keep = make_params(keep=keep, **kw)
+        st, info, grad = ciq_hyper_grad(self.ctx, B, V, params)
+        d = info.as_dict()
+        d["status"] = st
+        return grad, d
 
     def matvec(self, V, out, mvm_impl: str = "auto") -> None:
         ciq_matvec(self.ctx, V, out, mvm_impl)

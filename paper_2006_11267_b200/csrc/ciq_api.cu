@@ -115,6 +115,7 @@ struct ciq_ctx {
   cudaEvent_t join_ev = nullptr;
   int rank = 0, world = 1;
   bool sharded = false;       // a ciq_comm was given: the row-sharded code path (also for world = 1)
+  bool deriv = false;         // MVMs apply dK/dl instead of K (ciq_hyper_grad only)
   int64_t row0 = 0, row1 = 0;
   int64_t per = 0;            // rows per shard (multiple of 128; last shard may be shorter)
   int64_t nfull = 0;          // rows of the replicated (all-gathered) vectors = world * per >= n
@@ -412,7 +413,7 @@ constexpr int kMatMinT = 256;
 constexpr int64_t kMatMaxN = 20000;
 bool use_mat(const ciq_ctx* c, int tp) {
   const bool off = experiment_env("CIQ_NO_MATERIALIZE");
-  return !off && c->op.kind != CIQ_OP_DENSE && c->tc_ok && tp >= kMatMinT && c->op.n <= kMatMaxN;
+  return !off && !c->deriv && c->op.kind != CIQ_OP_DENSE && c->tc_ok && tp >= kMatMinT && c->op.n <= kMatMaxN;
 }
 
 ciq_status ensure_mat_planes(ciq_ctx* c) {
@@ -535,7 +536,13 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     if (impl == CIQ_MVM_TC)
       return set_err(c, CIQ_ERR_INVALID_ARG,
                      "tensor-core MVM unavailable for this operator (N < 256, huge features, or d > 8 with an RHS chunk < 32)");
-    LAUNCH(c, launch_mvm_simt(c->dev, v, tp, c->row0, c->row1, p, tp, apart, done, c->stream));
+    OpDev od = c->dev;
+    if (c->deriv) {   // dK/dl (ciq_hyper_grad): kernel kinds 4-6, o^2 / l, no sigma^2
+      od.kind += 3;
+      od.o2 = c->op.outputscale / c->ls[0];
+      od.diag = 0.f;
+    }
+    LAUNCH(c, launch_mvm_simt(od, v, tp, c->row0, c->row1, p, tp, apart, done, c->stream));
     if (apart_used) *apart_used = apart;
     if (apart_nblk) *apart_nblk = mvm_simt_blocks(rows);
     c->mvm_kind_used = 1;
@@ -578,7 +585,7 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   if (!skip_pack)
     LAUNCH(c, launch_pack_v(v, c->op.n, c->npad, tp, plane_cols(c, tp), nrm, c->planes, c->inv_scale, c->stream));
   TcArgs a{};
-  a.kind = c->op.kind;
+  a.kind = c->op.kind + (c->deriv ? 3 : 0);   // 4-6: dK/dl (ciq_hyper_grad)
   a.n = c->op.n;
   a.npad = c->npad;
   a.row0 = c->row0;
@@ -593,8 +600,8 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   a.p = pout;
   a.p_split_stride = (size_t)rows * tp;
   a.apart = ap;
-  a.o2 = c->op.outputscale;
-  a.diag = c->op.diag;
+  a.o2 = c->deriv ? c->op.outputscale / c->ls[0] : c->op.outputscale;
+  a.diag = c->deriv ? 0.f : c->op.diag;
   a.done = done;
   a.kplanes = c->kplanes;
   a.kplane_elems = c->kplane_elems;
@@ -1479,6 +1486,88 @@ ciq_status ciq_vjp(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int6
   if (info) {
     *info = i1;
     info->mvms = i1.mvms + i2.mvms;
+  }
+  return (st == CIQ_OK && st2 == CIQ_OK) ? CIQ_OK : CIQ_NOT_CONVERGED;
+}
+
+ciq_status ciq_hyper_grad(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int64_t ldv, int64_t T,
+                          const ciq_params* params, double* grad, ciq_info* info) {
+  if (!c || !B || !V || !grad) return CIQ_ERR_INVALID_ARG;
+  if (c->sharded || c->has_precond || c->post.on || c->op.kind == CIQ_OP_DENSE || c->op.ard)
+    return set_err(c, CIQ_ERR_INVALID_ARG,
+                   "ciq_hyper_grad: single-GPU, unpreconditioned, isotropic kernel operators only");
+  const int64_t n = c->op.n;
+  if (T <= 0 || ldv < T || ldb < T) return set_err(c, CIQ_ERR_DIM, "bad T / leading dimension");
+  ciq_params p;
+  if (params) p = *params; else ciq_params_default(&p);
+  const int nq = p.Q;
+  if (nq < 1 || nq > CIQ_MAX_Q) return set_err(c, CIQ_ERR_INVALID_ARG, "Q must be in [1, %d]", CIQ_MAX_Q);
+  ciq_status gs = grow(c, &c->vjp_xb, &c->vjp_xb_cap, (size_t)nq * n * T);
+  if (gs == CIQ_OK) gs = grow(c, &c->vjp_xv, &c->vjp_xv_cap, (size_t)nq * n * T);
+  if (gs == CIQ_OK) gs = grow(c, &c->vjp_y, &c->vjp_y_cap, (size_t)n * T);
+  if (gs != CIQ_OK) return gs;
+  float *xb = c->vjp_xb, *xv = c->vjp_xv, *yb = c->vjp_y;
+  // the shifted solves x_q(b) (forward) and x_q(v) (same rule), as ciq_vjp
+  p.mode = CIQ_MODE_INVSQRT;
+  p.keep_shift_solutions = 1;
+  p.shift_solutions = xb;
+  ciq_info i1{};
+  ciq_status st = ciq_apply(c, B, ldb, T, yb, T, &p, &i1);
+  if (st != CIQ_OK && st != CIQ_NOT_CONVERGED) return st;
+  double t[CIQ_MAX_Q], w[CIQ_MAX_Q];
+  for (int q = 0; q < nq; ++q) { t[q] = i1.t[q]; w[q] = i1.w[q]; }
+  p.t = t;
+  p.w = w;
+  p.Q = nq;
+  p.lanczos_reuse = 0;
+  p.shift_solutions = xv;
+  ciq_info i2{};
+  ciq_status st2 = ciq_apply(c, V, ldv, T, yb, T, &p, &i2);
+  if (st2 != CIQ_OK && st2 != CIQ_NOT_CONVERGED) return st2;
+  // dL/dtheta = -sum_q w_q sum_c x_q(v_c)^T (dK/dtheta) x_q(b_c)  (G of eq. ciq_deriv is symmetric
+  // and dK/dtheta too): one dK/dl MVM and one K MVM per shift, on the matrix-free kernels
+  const int tp = round16(T);
+  if (ensure_workspace(c, tp, std::max(1, c->ws.nq)) != CIQ_OK) return CIQ_ERR_OOM;
+  Workspace& ws = c->ws;
+  ciq_status sg = grow(c, &c->gsum, &c->gsum_cap, (size_t)3 * dot_rows_blocks());
+  if (sg != CIQ_OK) return sg;
+  std::vector<double> hpart((size_t)3 * dot_rows_blocks());
+  double dl = 0.0, dk = 0.0, dd = 0.0;
+  for (int q = 0; q < nq; ++q) {
+    const float* xbq = xb + (size_t)q * n * T;
+    const float* xvq = xv + (size_t)q * n * T;
+    ciq_status s3 = load_rows(c, xbq, T, n, (int)T, ws.w[0], tp);
+    if (s3 != CIQ_OK) return s3;
+    LAUNCH(c, launch_colsq_partials(ws.w[0], n, tp, ws.bpart, c->stream));
+    LAUNCH(c, launch_reduce_cols(ws.bpart, rowblocks(n, tp), tp, ws.colsq, 1, c->stream));
+    c->deriv = true;
+    s3 = run_mvm(c, ws.w[0], tp, ws.p, nullptr, nullptr, p.mvm_impl, ws.colsq);
+    c->deriv = false;
+    if (s3 != CIQ_OK) return s3;
+    LAUNCH(c, launch_dot_rows(xvq, T, ws.p, tp, n, (int)T, c->gsum, c->stream));
+    s3 = run_mvm(c, ws.w[0], tp, ws.p, nullptr, nullptr, p.mvm_impl, ws.colsq);
+    if (s3 != CIQ_OK) return s3;
+    LAUNCH(c, launch_dot_rows(xvq, T, ws.p, tp, n, (int)T, c->gsum + dot_rows_blocks(), c->stream));
+    LAUNCH(c, launch_dot_rows(xvq, T, xbq, T, n, (int)T, c->gsum + 2 * dot_rows_blocks(), c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(hpart.data(), c->gsum, hpart.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    double s_l = 0.0, s_k = 0.0, s_d = 0.0;   // fixed-order sums of the block partials
+    for (int b = 0; b < dot_rows_blocks(); ++b) {
+      s_l += hpart[b];
+      s_k += hpart[dot_rows_blocks() + b];
+      s_d += hpart[2 * dot_rows_blocks() + b];
+    }
+    dl += w[q] * s_l;
+    dk += w[q] * s_k;
+    dd += w[q] * s_d;
+  }
+  const double o2 = c->op.outputscale, s2 = c->op.diag;
+  grad[0] = -dl;                         // dL/dl
+  grad[1] = -(dk - s2 * dd) / o2;        // dL/d(o^2): dK/d(o^2) = (K - sigma^2 I) / o^2
+  grad[2] = -dd;                         // dL/dsigma^2: dK/dsigma^2 = I
+  if (info) {
+    *info = i1;
+    info->mvms = i1.mvms + i2.mvms + 2 * nq;
   }
   return (st == CIQ_OK && st2 == CIQ_OK) ? CIQ_OK : CIQ_NOT_CONVERGED;
 }

@@ -97,6 +97,10 @@ cudaError_t launch_split_dense(const float* k, int64_t ldk, int64_t rows, int64_
                                __half* hi, __half* lo, cudaStream_t s);
 
 // ---- vector kernels (recurrence.cu) ----
+// part[0 .. dot_rows_blocks()) fp64 partials of sum_{i < rows, c < cols} a[i][c] b[i][c] (fixed order)
+int dot_rows_blocks();
+cudaError_t launch_dot_rows(const float* a, int64_t lda, const float* b, int64_t ldb, int64_t rows, int cols,
+                            double* part, cudaStream_t s);
 int rowblocks(int64_t rows, int tp);   // number of CTAs of the row-streaming kernels
 int update_blocks(int64_t rows);       // CTAs (= beta^2 partial rows) of lanczos_update_kernel
 int update_blocks64(int64_t rows);     // ... of its fp64 instance (launch_lanczos_update64)

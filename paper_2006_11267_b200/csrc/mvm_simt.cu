@@ -27,10 +27,18 @@ CIQ_DEVICE float kernel_of_r2(float r2, float o2) {
     float r = sqrtf(r2);
     float s5 = 2.2360679774997896f * r;
     return o2 * (1.0f + s5 + s5 * s5 * (1.0f / 3.0f)) * expf(-s5);
-  } else {  // Matern-3/2
+  } else if (KIND == 3) {  // Matern-3/2
     float r = sqrtf(r2);
     float s3 = 1.7320508075688772f * r;
     return o2 * (1.0f + s3) * expf(-s3);
+  } else if (KIND == 4) {  // d/dl of RBF (o2 = o^2 / l): r^2 exp(-r^2/2)
+    return o2 * r2 * expf(-0.5f * r2);
+  } else if (KIND == 5) {  // d/dl of Matern-5/2: a^2 (1 + a) exp(-a) / 3
+    float a = 2.2360679774997896f * sqrtf(r2);
+    return o2 * a * a * (1.0f + a) * (1.0f / 3.0f) * expf(-a);
+  } else {  // d/dl of Matern-3/2: a^2 exp(-a)
+    float a = 1.7320508075688772f * sqrtf(r2);
+    return o2 * a * a * expf(-a);
   }
 }
 
@@ -196,6 +204,9 @@ cudaError_t launch_mvm_simt(const OpDev& op, const float* v, int tp, int64_t row
     case 1: return launch_kind<1>(op, v, tp, row0, row1, p, ldp, apart, done, s);
     case 2: return launch_kind<2>(op, v, tp, row0, row1, p, ldp, apart, done, s);
     case 3: return launch_kind<3>(op, v, tp, row0, row1, p, ldp, apart, done, s);
+    case 4: return launch_kind<4>(op, v, tp, row0, row1, p, ldp, apart, done, s);
+    case 5: return launch_kind<5>(op, v, tp, row0, row1, p, ldp, apart, done, s);
+    case 6: return launch_kind<6>(op, v, tp, row0, row1, p, ldp, apart, done, s);
   }
   return cudaErrorInvalidValue;
 }

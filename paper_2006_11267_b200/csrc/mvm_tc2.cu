@@ -140,10 +140,13 @@ CIQ_DEVICE uint64_t shfl64(uint64_t v) {
   return ((uint64_t)hi << 32) | lo;
 }
 
+// KIND 1-3: RBF, Matern-5/2, Matern-3/2; KIND 4-6: their lengthscale derivatives l dk/dl / o^2
+// (the hyper-parameter gradient, ciq_hyper_grad): r^2 e^{-r^2/2}, a^2 (1 + a) e^{-a} / 3, a^2 e^{-a}.
 template <int KIND>
 CIQ_DEVICE float kern(float s) {
   // s = -(log2 e / 2) r^2
   if (KIND == 1) return ex2_approx(s);
+  if (KIND == 4) return (-1.3862943611198906f * s) * ex2_approx(s);
   // r^2 = -2 ln2 s; sqrt.approx (one MUFU.SQRT, ~2^-23 relative) instead of the IEEE sqrtf sequence
   // with its slow-path call
   float r;
@@ -152,7 +155,12 @@ CIQ_DEVICE float kern(float s) {
     const float a = 2.2360679774997896f * r;
     return (1.f + a + a * a * (1.f / 3.f)) * ex2_approx(-1.4426950408889634f * a);
   }
+  if (KIND == 5) {
+    const float a = 2.2360679774997896f * r;
+    return a * a * (1.f + a) * (1.f / 3.f) * ex2_approx(-1.4426950408889634f * a);
+  }
   const float a = 1.7320508075688772f * r;
+  if (KIND == 6) return a * a * ex2_approx(-1.4426950408889634f * a);
   return (1.f + a) * ex2_approx(-1.4426950408889634f * a);
 }
 
@@ -573,6 +581,9 @@ cudaError_t launch_mvm_tc2(const TcArgs& a, int nsm, cudaStream_t s) {
     case 1: return launch2_kind<1>(a, tn, grid, s);
     case 2: return launch2_kind<2>(a, tn, grid, s);
     case 3: return launch2_kind<3>(a, tn, grid, s);
+    case 4: return launch2_kind<4>(a, tn, grid, s);
+    case 5: return launch2_kind<5>(a, tn, grid, s);
+    case 6: return launch2_kind<6>(a, tn, grid, s);
   }
   return cudaErrorInvalidValue;
 }

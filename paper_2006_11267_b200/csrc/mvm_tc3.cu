@@ -164,15 +164,21 @@ CIQ_DEVICE uint64_t shfl64_3(uint64_t v) {
 
 template <int KIND>
 CIQ_DEVICE float kern3(float s) {
-  // s = -(log2 e / 2) r^2
+  // s = -(log2 e / 2) r^2; KIND 4-6: lengthscale derivatives (as kern in mvm_tc2.cu)
   if (KIND == 1) return ex2_approx(s);
+  if (KIND == 4) return (-1.3862943611198906f * s) * ex2_approx(s);
   float r;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(0.f, -1.3862943611198906f * s)));
   if (KIND == 2) {
     const float a = 2.2360679774997896f * r;
     return (1.f + a + a * a * (1.f / 3.f)) * ex2_approx(-1.4426950408889634f * a);
   }
+  if (KIND == 5) {
+    const float a = 2.2360679774997896f * r;
+    return a * a * (1.f + a) * (1.f / 3.f) * ex2_approx(-1.4426950408889634f * a);
+  }
   const float a = 1.7320508075688772f * r;
+  if (KIND == 6) return a * a * ex2_approx(-1.4426950408889634f * a);
   return (1.f + a) * ex2_approx(-1.4426950408889634f * a);
 }
 
@@ -612,6 +618,9 @@ cudaError_t launch_mvm_tc3(const TcArgs& a, int nsm, cudaStream_t s) {
     case 1: return launch3_kf<1>(a, tn, pairs, s);
     case 2: return launch3_kf<2>(a, tn, pairs, s);
     case 3: return launch3_kf<3>(a, tn, pairs, s);
+    case 4: return launch3_kf<4>(a, tn, pairs, s);
+    case 5: return launch3_kf<5>(a, tn, pairs, s);
+    case 6: return launch3_kf<6>(a, tn, pairs, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -696,6 +696,27 @@ cudaError_t launch_randn_fill(float* dst, int64_t rows, int cols, int tp, int64_
   randn_kernel<<<nb_elem(rows * tp, 256), 256, 0, s>>>(dst, rows, cols, tp, row_offset, seed);
   return cudaGetLastError();
 }
+// part[blockIdx.x] = sum over this block's fixed rows (grid-stride) of sum_{c < cols} a[i][c] b[i][c],
+// fp64, fixed order (the bilinear forms of the hyper-parameter gradient, ciq_hyper_grad).
+__global__ void __launch_bounds__(256) dot_rows_kernel(const float* __restrict__ a, int64_t lda,
+                                                       const float* __restrict__ b, int64_t ldb, int64_t rows,
+                                                       int cols, double* __restrict__ part) {
+  double acc = 0.0;
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (int64_t)gridDim.x * 256) {
+    const int64_t i = e / cols, c = e % cols;
+    acc = fma((double)a[i * lda + c], (double)b[i * ldb + c], acc);
+  }
+  acc = block_sum256(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+int dot_rows_blocks() { return 296; }
+cudaError_t launch_dot_rows(const float* a, int64_t lda, const float* b, int64_t ldb, int64_t rows, int cols,
+                            double* part, cudaStream_t s) {
+  dot_rows_kernel<<<dot_rows_blocks(), 256, 0, s>>>(a, lda, b, ldb, rows, cols, part);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_colsq_partials(const float* v, int64_t rows, int tp, double* part, cudaStream_t s) {
   colsq_kernel<float><<<stream_grid(rows, tp), kThreads, 0, s>>>(v, rows, tp, part);
   return cudaGetLastError();
