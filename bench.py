@@ -115,35 +115,49 @@ def workload_desc(cfg) -> str:
 # reference arm / cpu baseline: the oracle on a bounded sample
 # ------------------------------------------------------------------------------------------------
 
-def oracle_sample_rate(cfg, inp, mvms_per_call: int, rows: int = 1024, reps: int = 1) -> dict:
-    """Time the oracle's matrix-free MVM on `rows` of the N rows (all N columns), extrapolate to a
-    whole call of `mvms_per_call` MVMs (the MVM is >99% of the oracle's per-iteration work)."""
+def ncu_metrics() -> dict:
+    """Per-launch ncu figures of the hot kernels ({"<kernel>/<config>": {"dram_bytes", "tensor_pipe_active",
+    "source"}}), extracted from committed `ncu --set full` captures by scripts/ncu_metrics.py."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_metrics.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def oracle_sample_rate(cfg, inp, mvms_per_call: int, rows: int = 8192, reps: int = 1) -> dict:
+    """Time the oracle's matrix-free MVM (its own threaded row-block map, one thread per host
+    core) on rows [0, `rows`) of the N rows (all N columns), extrapolate to a whole call of
+    `mvms_per_call` MVMs (the MVM is >99% of the oracle's per-iteration work).  `cores` is the
+    size of the oracle's thread pool (numpy releases the GIL in its array loops)."""
     import numpy as np
-    from threadpoolctl import threadpool_info
 
     from oracle import DenseOperator, KernelOperator
-    if cfg.kind == "dense":
-        rows = cfg.n   # the dense oracle MVM is cheap: time all of it
-        op = DenseOperator(inp["K"].astype(np.float64), cfg.sigma2)
-        block_rows = lambda i0, i1: op.mvm_rows(np.arange(i0, i1), v)  # noqa: E731
-    else:
-        op = KernelOperator(inp["X"], cfg.kind, cfg.lengthscale, cfg.outputscale, cfg.sigma2, dense_cache_max=0,
-                            block=64)
-        block_rows = lambda i0, i1: op.kernel_rows(i0, i1) @ v  # noqa: E731
+    threads = os.cpu_count() or 1
     v = inp["B"].astype(np.float64)
+    if cfg.kind == "dense":
+        rows = cfg.n   # the dense oracle MVM is cheap: time all of it (one BLAS GEMM)
+        from threadpoolctl import threadpool_info
+        threads = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+        op = DenseOperator(inp["K"].astype(np.float64), cfg.sigma2)
+        run = lambda: op.mvm(v)  # noqa: E731
+    else:
+        rows = min(rows, cfg.n)
+        op = KernelOperator(inp["X"], cfg.kind, cfg.lengthscale, cfg.outputscale, cfg.sigma2, dense_cache_max=0,
+                            threads=threads)
+        run = lambda: op.mvm_row_block(0, rows, v)  # noqa: E731
     best = None
     for _ in range(reps):
         t0 = time.perf_counter()
-        for i0 in range(0, rows, 64):
-            block_rows(i0, min(rows, i0 + 64))
+        run()
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
     t_mvm = best * cfg.n / rows
     t_call = t_mvm * mvms_per_call
-    threads = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
     return {"value": cfg.t / t_call, "unit": "RHS/s", "cores": threads, "kind": "oracle",
             "sample": (f"oracle {'dense' if cfg.kind == 'dense' else 'matrix-free'} MVM on {rows} of {cfg.n} rows "
-                       f"x {cfg.t} RHS ({best:.2f} s), "
+                       f"x {cfg.t} RHS ({best:.2f} s on {threads} threads), "
                        f"extrapolated to {mvms_per_call} MVMs per call (lambda est + J + final)"),
             "sample_seconds": best, "t_call_s": t_call}
 
@@ -315,23 +329,23 @@ def run_ours(args, cfg):
                 "peak_source": f"{peaks['_source']} bf16 sustained (fp16 same rate)",
                 "note": "achieved counts only the algorithmic 2*N^2*T flops; executed_tflops counts every MMA issued",
                 "executed_tflops": exec_flops / (mvm_ms * 1e-3) / 1e12,
-                "executed_frac_of_measured_peak": exec_flops / (mvm_ms * 1e-3) / 1e12 / peak,
-                "tensor_pipe_active_ncu": {"value": 0.636, "source": "profiles/ncu_k1_r01h.txt (sm__pipe_tensor_cycles_active)"}}
+                "executed_frac_of_measured_peak": exec_flops / (mvm_ms * 1e-3) / 1e12 / peak}
+        ncu = ncu_metrics().get(f"mvm_tc2_kernel/{cfg.name}")
+        if ncu:
+            roof["tensor_pipe_active_ncu"] = {"value": ncu["tensor_pipe_active"], "source": ncu["source"]}
         sm_count = torch.cuda.get_device_properties(local).multi_processor_count
         sfu_peak = sm_count * 16 * peaks.get("sm_max_mhz", 1965.0) * 1e6  # MUFU.EX2 per second
         roof["sfu"] = {"achieved_evals_per_s": rows_local * n / (mvm_ms * 1e-3), "peak_evals_per_s": sfu_peak,
                        "frac": rows_local * n / (mvm_ms * 1e-3) / sfu_peak,
                        "peak_source": f"{sm_count} SMs x 16 MUFU.EX2/clk x sm_max_mhz (1 ex2 per kernel entry)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    # dram bytes per launch from one `ncu --set full` capture of the same kernel (profiles/)
-    if roof["bound"] == "hbm":
-        roof["traffic"] = 423.86e6 if cfg.name == "C2" else None
-        roof["traffic_source"] = "profiles/ncu_k2_r01f.txt (C2)"
-    elif roof["bound"] == "tensor":
-        roof["traffic"] = 33.01e6 if cfg.name == "C3" else None
-        roof["traffic_source"] = "profiles/ncu_k1_r01h.txt (C3; compute-bound: V planes / features stay in L2)"
-    else:
-        roof["traffic"] = None
+    # dram bytes per launch from one `ncu --set full` capture of the same kernel at this config
+    # (profiles/ncu_metrics.json, written by scripts/ncu_metrics.py from the capture it names)
+    key = {"hbm": "mvm_dense2_kernel", "tensor": "mvm_tc2_kernel"}.get(roof["bound"])
+    ncu = ncu_metrics().get(f"{key}/{cfg.name}") if key else None
+    roof["traffic"] = ncu["dram_bytes"] if ncu else None
+    if ncu:
+        roof["traffic_source"] = ncu["source"]
     roof["ms_per_launch"] = mvm_ms
     roof["share_of_step"] = pinfo["ms_mvm"] / max(1e-9, pinfo["ms_total"])
     q = cfg.q
@@ -476,7 +490,7 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mvm", default="auto", choices=["auto", "simt", "tc"])
-    ap.add_argument("--ref-rows", type=int, default=4096)
+    ap.add_argument("--ref-rows", type=int, default=16384)
     ap.add_argument("--ref-mvms", type=int, default=166)  # C3: J=165 + 1 (final K.Y); lambda from the solve's Lanczos
     ap.add_argument("--lanczos", default="reuse", choices=["reuse", "separate"],
                     help="lambda estimate from the solve's first 12 Lanczos steps (reuse, App. D: Lanczos started "

@@ -130,6 +130,27 @@ class KernelOperator:
                 row_block(i0)
         return out + self.sigma2 * v
 
+    def mvm_row_block(self, i0: int, i1: int, v: np.ndarray) -> np.ndarray:
+        """Rows i0..i1-1 of K v, by the same (threaded) row-block map as ``mvm`` (for the bench's
+        bounded CPU baseline); does not count as an MVM."""
+        v = np.asarray(v, dtype=np.float64)
+        out = np.empty((i1 - i0,) + v.shape[1:])
+
+        def row_block(j0):
+            j1 = min(i1, j0 + self.block)
+            out[j0 - i0:j1 - i0] = self.kernel_rows(j0, j1) @ v
+
+        starts = range(i0, i1, self.block)
+        if self.threads > 1 and self._dense is None:
+            import concurrent.futures
+            with concurrent.futures.ThreadPoolExecutor(self.threads) as pool:
+                list(pool.map(row_block, starts))
+        else:
+            for j0 in starts:
+                row_block(j0)
+        out += self.sigma2 * v[i0:i1]
+        return out
+
     def mvm_rows(self, rows: np.ndarray, v: np.ndarray) -> np.ndarray:
         """(K v)[rows] -- individual outputs, one row at a time (for sampled full-size checks)."""
         v = np.asarray(v, dtype=np.float64)
