@@ -31,6 +31,7 @@ __all__ = [
     "hht_rule", "lanczos", "estimate_spectrum", "msminres", "ciq",
     "pivoted_cholesky", "precond_ciq", "MsminresResult", "CiqResult", "ciq_vjp",
     "PosteriorOperator", "thompson_step", "kernel_lengthscale_derivative", "ciq_hyper_grad",
+    "SparseOperator",
 ]
 
 
@@ -178,6 +179,40 @@ class DenseOperator:
 
     def kernel_diag(self) -> np.ndarray:
         return np.diag(self.a).copy()
+
+    def mvm(self, v):
+        self.mvm_count += 1
+        v = np.asarray(v, dtype=np.float64)
+        return self.a @ v + self.sigma2 * v
+
+    def mvm_rows(self, rows, v):
+        v = np.asarray(v, dtype=np.float64)
+        rows = np.asarray(rows)
+        return self.a[rows] @ v + self.sigma2 * v[rows]
+
+
+class SparseOperator:
+    """K = A + sigma2 I for a given sparse symmetric A in CSR form (indptr, indices, data) -- the
+    stencil precision of the Gibbs workload (Lambda = gamma_obs A^T A + gamma_prior L^T L,
+    P:995-1004) is such an operator; msMINRES-CIQ only needs its MVMs.  The MVM is
+    scipy.sparse's CSR product (a library step), in float64 on the caller's (float32) values."""
+
+    def __init__(self, indptr, indices, data, n: int, sigma2: float = 0.0):
+        import scipy.sparse
+        self.a = scipy.sparse.csr_matrix((np.asarray(data, dtype=np.float64), np.asarray(indices),
+                                          np.asarray(indptr)), shape=(n, n))
+        self.n = n
+        self.sigma2 = float(sigma2)
+        self.mvm_count = 0
+
+    def dense(self) -> np.ndarray:
+        return self.a.toarray() + self.sigma2 * np.eye(self.n)
+
+    def kernel_column(self, j: int) -> np.ndarray:
+        return self.a[:, j].toarray()[:, 0]
+
+    def kernel_diag(self) -> np.ndarray:
+        return self.a.diagonal().copy()
 
     def mvm(self, v):
         self.mvm_count += 1

@@ -242,3 +242,101 @@ def thompson_inputs(cfg: ThompsonConfig) -> dict:
     f = hartmann6(xt.astype(np.float64))
     y = (f - f.mean()) / f.std()
     return {"Xs": xs, "Xt": xt, "y": y.astype(np.float32), "eps": rhs(cfg.n, cfg.t), "S": lanczos_start(cfg.n, 16)}
+
+
+# ---- Gibbs image-reconstruction workload (§5.3, App. F) ----
+
+@dataclasses.dataclass(frozen=True)
+class GibbsConfig:
+    """The conditional precision of the paper's super-resolution Gibbs sampler,
+    Lambda = gamma_obs A^T A + gamma_prior L^T L with A = D B:
+    B = 5 x 5 Gaussian blur (std 2.5 px, normalised, reflected boundary), D = decimation of the
+    n x n image into R = 4 low-res m x m images (offsets (0,0), (0,1), (1,0), (1,1), stride n/m),
+    L = the isotropic 3 x 3 Laplacian filter of P:770-776 with reflected boundary.  Readings
+    (DESIGN.md §3 G21-G23): the prior precision is gamma_prior L^T L (the Gamma conditional uses
+    ||L x||^2; L itself is negative semi-definite), "blur radius 2.5" is the Gaussian std,
+    the four decimation offsets tile the 2 x 2 sub-pixel grid (so D^T D = I)."""
+    name: str
+    side: int = 160        # high-res image n x n (P:1005: N = 160)
+    low: int = 80          # low-res m x m (M = 80)
+    images: int = 4        # R = 4
+    gamma_obs: float = 1.0      # the data were generated with gamma_obs = 1 (P:767)
+    gamma_prior: float = 0.1   # synthetic choice (the chain samples it): kappa(Lambda) ~ 37
+    t: int = 64            # independent draws Lambda^{-1/2} eps (columns)
+    q: int = 8
+    max_iters: int = 400   # "a maximum of J = 400 msMINRES iterations" (P:779)
+    tol: float = 1e-3      # "tolerance of 0.001" (P:779)
+
+
+GIBBS = {"G1": GibbsConfig("G1")}
+
+
+def _reflect(i: np.ndarray, n: int) -> np.ndarray:
+    """Half-sample symmetric ("reflected") boundary: -1 -> 0, -2 -> 1, n -> n-1, n+1 -> n-2
+    (indices within one reflection of the image, as the 5 x 5 / 3 x 3 filters need)."""
+    i = np.where(i < 0, -i - 1, i)
+    return np.where(i >= n, 2 * n - 1 - i, i)
+
+
+def _stencil_matrix(side: int, w: np.ndarray):
+    """n^2 x n^2 sparse matrix of the correlation of an image (row-major pixels) with the odd
+    filter w under reflected boundaries: (S x)[p] = sum_o w[o] x[reflect(p + o)]."""
+    import scipy.sparse
+    r = w.shape[0] // 2
+    i, j, a, b = np.meshgrid(np.arange(side), np.arange(side), np.arange(-r, r + 1), np.arange(-r, r + 1),
+                             indexing="ij")
+    rows = (i * side + j).ravel()
+    cols = (_reflect(i + a, side) * side + _reflect(j + b, side)).ravel()
+    vals = w[a + r, b + r].ravel()
+    return scipy.sparse.csr_matrix((vals, (rows, cols)), shape=(side * side, side * side))
+
+
+def gibbs_blur_filter(std: float = 2.5, size: int = 5) -> np.ndarray:
+    """5 x 5 Gaussian blur filter, std 2.5 px, normalised to sum 1 (reading G22)."""
+    r = size // 2
+    a = np.arange(-r, r + 1, dtype=np.float64)
+    g = np.exp(-0.5 * (a[:, None] ** 2 + a[None, :] ** 2) / std ** 2)
+    return g / g.sum()
+
+
+def gibbs_laplace_filter() -> np.ndarray:
+    """The isotropic Laplacian filter of P:770-776."""
+    return np.array([[1.0, 2.0, 1.0], [2.0, -12.0, 2.0], [1.0, 2.0, 1.0]]) / 12.0
+
+
+def gibbs_decimation(side: int, low: int, images: int):
+    """D: (images m^2) x n^2 selection matrix, image r taking pixels (s i + dy_r, s j + dx_r)."""
+    import scipy.sparse
+    s = side // low
+    offs = [(0, 0), (0, 1), (1, 0), (1, 1)][:images]
+    rows, cols = [], []
+    for r, (dy, dx) in enumerate(offs):
+        for i in range(low):
+            for j in range(low):
+                rows.append(r * low * low + i * low + j)
+                cols.append((s * i + dy) * side + (s * j + dx))
+    return scipy.sparse.csr_matrix((np.ones(len(rows)), (rows, cols)), shape=(images * low * low, side * side))
+
+
+def gibbs_precision(cfg: GibbsConfig) -> dict:
+    """Lambda (fp64 assembly, returned as float32 CSR arrays: indptr int64, indices int32, data
+    float32) -- the INPUT operator of the sparse path, like the dense K of C2 -- plus the
+    factors B, D, L (fp64 scipy.sparse) for the input-pinning tests."""
+    bm = _stencil_matrix(cfg.side, gibbs_blur_filter())
+    lm = _stencil_matrix(cfg.side, gibbs_laplace_filter())
+    dm = gibbs_decimation(cfg.side, cfg.low, cfg.images)
+    am = dm @ bm
+    lam = (cfg.gamma_obs * (am.T @ am) + cfg.gamma_prior * (lm.T @ lm)).tocsr()
+    lam.sort_indices()
+    return {"indptr": lam.indptr.astype(np.int64), "indices": lam.indices.astype(np.int32),
+            "data": lam.data.astype(np.float32), "n": lam.shape[0], "B": bm, "D": dm, "L": lm}
+
+
+def gibbs_inputs(cfg: GibbsConfig) -> dict:
+    """The precision operator plus eps (n^2 x t ~ N(0,1): Lambda^{-1/2} eps is a draw from the
+    zero-mean conditional) and the Lanczos start block."""
+    out = gibbs_precision(cfg)
+    n = out["n"]
+    out["B_rhs"] = rhs(n, cfg.t)
+    out["S"] = lanczos_start(n, 16)
+    return out
