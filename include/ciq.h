@@ -156,6 +156,13 @@ typedef struct {
   float* shift_solutions;     /*    (the forward solves the backward pass reuses) into     */
                               /*    shift_solutions, Q x rows x T floats (row-major per shift,     */
                               /*    ld = T; host or device).  Not with a preconditioner.           */
+  int32_t fp64;               /* 1: accuracy mode for kernel operators without a preconditioner: */
+                              /*    K + sigma^2 I is materialised in fp64 (N^2 doubles; OOM error  */
+                              /*    if it does not fit), MVMs on the FP64 pipe, fp64 Lanczos /     */
+                              /*    msMINRES vectors (the preconditioned fp64 route, precond64.cu, */
+                              /*    with P = I).  ~30x slower than the tensor-core path; removes   */
+                              /*    the fp32 floor kappa(K) * ~1e-7 of the default. */
+                              /*    lanczos_reuse / keep_shift_solutions are ignored.  Default 0.  */
 } ciq_params;
 
 typedef struct {

@@ -116,6 +116,7 @@ struct ciq_ctx {
   int rank = 0, world = 1;
   bool sharded = false;       // a ciq_comm was given: the row-sharded code path (also for world = 1)
   bool deriv = false;         // MVMs apply dK/dl instead of K (ciq_hyper_grad only)
+  bool fp64_active = false;   // the current ciq_apply runs the fp64 route (precond64.cu)
   int64_t row0 = 0, row1 = 0;
   int64_t per = 0;            // rows per shard (multiple of 128; last shard may be shorter)
   int64_t nfull = 0;          // rows of the replicated (all-gathered) vectors = world * per >= n
@@ -844,7 +845,7 @@ ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, 
   int done_mvms = 0;
   for (int j = 0; j < J; ++j) {
     const float* vj = vec(j);
-    if (c->pc.on && c->pc.m64_ready) {   // fp64 route: Lanczos on the materialised M (fp32 basis)
+    if (c->fp64_active) {   // fp64 route: Lanczos on the materialised M (fp32 basis)
       LAUNCH(c, launch_mvm64(c->pc.m64, c->pc.ldm, rows, n, vj, false, tpl, r0, lw.p, false, nullptr, nullptr, s));
     } else if (c->pc.on) {
       // Lanczos on M = P^{-1/2} K P^{-1/2} (App. A: the rule must cover the spectrum of M)
@@ -999,7 +1000,7 @@ ciq_status ensure_m64(ciq_ctx* c) {
   const int r2 = P.r2;
   cudaStream_t s = c->stream;
   double* h = nullptr;
-  if (dalloc(&P.m64, (size_t)rows * ldm) != cudaSuccess || dalloc(&h, (size_t)n * r2) != cudaSuccess) {
+  if (dalloc(&P.m64, (size_t)rows * ldm) != cudaSuccess || (r2 > 0 && dalloc(&h, (size_t)n * r2) != cudaSuccess)) {
     cudaGetLastError();
     dfree(P.m64);
     dfree(h);
@@ -1016,6 +1017,13 @@ ciq_status ensure_m64(ciq_ctx* c) {
     CUDA_TRY(c, dalloc(&neg, (size_t)m));
     CUDA_TRY(c, cudaMemcpyAsync(neg, ones.data(), (size_t)m * 8, cudaMemcpyHostToDevice, s));
     LAUNCH(c, launch_gemm64(false, true, rows, n, m, c->post.u + c->row0 * m, m, c->post.u, m, neg, 1.0, P.m64, ldm, s));
+  }
+  if (!P.on) {   // params.fp64 without a preconditioner: M = K (+ sigma^2 I, COV* for a posterior ctx)
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    dfree(h);
+    dfree(neg);
+    P.m64_ready = true;
+    return CIQ_OK;
   }
   const double a = P.ad[PW_MHALF];
   const double* g = P.g[PW_MHALF];
@@ -1169,6 +1177,7 @@ void ciq_params_default(ciq_params* p) {
   p->mvm_impl = CIQ_MVM_AUTO;
   p->poll_every = 6;
   p->breakdown_tol = 1e-6;
+  p->fp64 = 0;
 }
 
 #ifndef CIQ_SOURCE_HASH
@@ -1711,9 +1720,22 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   c->profiling = p.profile_kernels != 0;
   for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
   c->timed.clear();
+  if (p.fp64 && !c->pc.on) {   // accuracy mode: K materialised in fp64, fp64 MVMs and vectors
+    if (c->sharded || c->op.kind == CIQ_OP_DENSE)
+      return set_err(c, CIQ_ERR_INVALID_ARG, "params.fp64: single-GPU kernel operators only");
+    const ciq_status sm = ensure_m64(c);
+    if (sm != CIQ_OK) return set_err(c, sm, "params.fp64: N^2 doubles do not fit in device memory");
+    c->fp64_active = true;
+    const ciq_status sa = apply_fp64(c, B, ldb, T, out, ldo, p, info);
+    c->fp64_active = false;
+    return sa;
+  }
   if (use_m64(c)) {   // preconditioned: the fp64 route when M fits in device memory (precond64.cu)
     const ciq_status sm = ensure_m64(c);
-    if (sm == CIQ_OK) return apply_fp64(c, B, ldb, T, out, ldo, p, info);
+    c->fp64_active = sm == CIQ_OK;
+    const ciq_status sa = sm == CIQ_OK ? apply_fp64(c, B, ldb, T, out, ldo, p, info) : sm;
+    c->fp64_active = false;
+    if (sm == CIQ_OK) return sa;
     if (sm != CIQ_ERR_OOM) return sm;
     c->err.clear();   // M does not fit: the matrix-free route below
   }
@@ -2130,7 +2152,8 @@ ciq_status apply_fp64(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float*
       lmin = p.lambda_min;
       lmax = p.lambda_max;
     } else {
-      st = estimate_lambda(c, &p, 1.0, &lmin, &lmax, &rmin, &rmax, &lambda_mvms);
+      // lambda_min bound: 1 for the preconditioned M (reading G6 / G13), sigma^2 for M = K + sigma^2 I
+      st = estimate_lambda(c, &p, P.on ? 1.0 : (double)c->op.diag, &lmin, &lmax, &rmin, &rmax, &lambda_mvms);
       if (st != CIQ_OK) return st;
     }
     const int r = ciqh::hht_rule(lmin, lmax, nq, t, w);
@@ -2176,10 +2199,13 @@ ciq_status apply_fp64(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float*
   int final_mvm = 0;
   if (p.mode == CIQ_MODE_SQRT) {
     LAUNCH(c, launch_mvm64(P.m64, P.ldm, rows, n, D(ws.y), true, tp, c->row0, D(ws.p), true, nullptr, nullptr, s));
-    st = precond_power64(c, PW_HALF, D(ws.p), tp, res);
+    if (P.on) st = precond_power64(c, PW_HALF, D(ws.p), tp, res);
+    else res = D(ws.p);   // K^{1/2} b = K y (eq. contour_integral_quad)
     final_mvm = 1;
-  } else {
+  } else if (P.on) {
     st = precond_power64(c, PW_MHALF, D(ws.y), tp, res);
+  } else {
+    res = D(ws.y);        // K^{-1/2} b = y
   }
   if (st != CIQ_OK) return st;
   if (is_device_ptr(out)) {
@@ -2203,7 +2229,7 @@ ciq_status apply_fp64(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float*
     info->iters = J;
     info->mvms = lambda_mvms + J + final_mvm;
     info->converged = converged ? 1 : 0;
-    info->rotated = 1;
+    info->rotated = P.on ? 1 : 0;
     info->breakdown_cols = hc.breakdown;
     info->Q = nq;
     info->lambda_min = lmin;

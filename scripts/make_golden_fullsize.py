@@ -6,6 +6,7 @@ Calls only ``oracle/`` and the seeded input generators (``workloads``); no value
 CUDA path.  Columns are independent in msMINRES-CIQ (reading G15), so two columns
 of the 64-column bench RHS block are checked against the same columns of the GPU's full solve.
 
+Same inputs as the library: the fp32 points, B and the fp32-rounded l, o^2, sigma^2.
 Protocol: the oracle's lambda estimate (10 Lanczos steps on the
 seeded 16-column start block, lambda_min bound sigma^2, reading G6) gives the rule (t, w); the
 solve then runs to a tight stopping tolerance (``--tol``, default 1e-8 on max_q |phibar|/beta1),
@@ -42,9 +43,12 @@ def main():
     a = ap.parse_args()
     cfg = workloads.CONFIGS[a.config]
     inp = workloads.make_inputs(cfg)
-    op = KernelOperator(inp["X"], cfg.kind, cfg.lengthscale, cfg.outputscale, cfg.sigma2, threads=a.threads)
+    # the scalars as the library receives them (the C ABI takes fp32 l, o^2, sigma^2): same inputs
+    f32 = lambda v: float(np.float32(v))  # noqa: E731
+    op = KernelOperator(inp["X"], cfg.kind, f32(cfg.lengthscale), f32(cfg.outputscale), f32(cfg.sigma2),
+                        threads=a.threads)
     t0 = time.time()
-    lmin, lmax, rmin, rmax = estimate_spectrum(op.mvm, inp["S"].astype(np.float64), 10, lower_bound=cfg.sigma2)
+    lmin, lmax, rmin, rmax = estimate_spectrum(op.mvm, inp["S"].astype(np.float64), 10, lower_bound=op.sigma2)
     t, w = hht_rule(lmin, lmax, cfg.q)
     print(f"lambda [{lmin:.6g}, {lmax:.6g}] ritz [{rmin:.6g}, {rmax:.6g}]  {time.time() - t0:.0f} s", flush=True)
     b = inp["B"][:, :a.cols].astype(np.float64)
