@@ -482,6 +482,106 @@ def run_thompson(args):
     g.close()
 
 
+# ------------------------------------------------------------------------------------------------
+# G1: draws from the Gibbs sampler's conditional N(m, Lambda^{-1}) (§5.3,
+# P:995-1009): Lambda^{-1/2} eps for 64 eps columns on the sparse stencil operator, single GPU
+# ------------------------------------------------------------------------------------------------
+
+def run_gibbs(args):
+    import numpy as np
+    import torch
+
+    import paper_2006_11267_b200 as pb
+    import workloads
+    cfg = workloads.GIBBS["G1"]
+    _, world, local = dist_env()
+    if world > 1:
+        raise SystemExit("--config G1 is single-GPU")
+    torch.cuda.set_device(local)
+    inp = workloads.gibbs_inputs(cfg)
+    n = inp["n"]
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()  # noqa: E731
+    g = pb.CIQ("sparse", K=(inp["indptr"], inp["indices"], inp["data"]))
+    eps, s0 = dv(inp["B_rhs"]), dv(inp["S"])
+    out = torch.empty_like(eps)
+    kw = dict(q=cfg.q, max_iters=cfg.max_iters, tol=cfg.tol, mode="invsqrt", lanczos_start=s0,
+              lanczos_reuse=args.lanczos == "reuse")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        g.apply(eps, out, **kw)
+    sampler = ClockSampler(local)
+    sampler.start()
+    step_ms, infos = [], []
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        infos.append(g.apply(eps, out, **kw))
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = statistics.mean(step_ms)
+    eh = torch.from_numpy(inp["B_rhs"]).pin_memory()
+    oh = torch.empty_like(eh).pin_memory()
+    e2e_ms = []
+    for _ in range(max(1, args.steps)):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.apply(eh.numpy(), oh.numpy(), **kw)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e = statistics.mean(e2e_ms)
+    pinfo = g.apply(eps, out, profile=True, **kw)
+    mvm_ms = pinfo["ms_mvm"] / max(1, pinfo["mvm_timed"])
+    peaks = load_peaks()
+    nnz = int(inp["indptr"][-1])
+    # algorithmic bytes of one SpMM: the CSR operator (4 B value + 4 B index per nonzero, 8 B per
+    # row pointer) once, V read once and P written once (N x T fp32 each)
+    sp_bytes = 8.0 * nnz + 8.0 * (n + 1) + 2.0 * 4.0 * n * cfg.t
+    roof = {"bound": "hbm", "achieved": sp_bytes / (mvm_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "kernel": "spmm_kernel (CSR, one warp per row, fp32)",
+            "peak_source": f"{peaks['_source']} HBM copy bandwidth", "traffic": None,
+            "ms_per_launch": mvm_ms, "share_of_step": pinfo["ms_mvm"] / max(1e-9, pinfo["ms_total"]),
+            "note": "operator + V + P bytes once per MVM; V rows are re-gathered from L2 per nonzero"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    line = {"metric": "Gibbs conditional draws/sec (G1: Lambda^{-1/2} eps, 160x160 super-resolution precision)",
+            "value": cfg.t / (ms / 1000.0), "unit": "samples/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"G1: Lambda = g_obs A^T A + g_prior L^T L, N = {cfg.side}^2 = {n} (P:1005), "
+                                   f"A = decimation(R={cfg.images}) x 5x5 Gaussian blur, 3x3 Laplacian, g_obs "
+                                   f"{cfg.gamma_obs}, g_prior {cfg.gamma_prior}, {cfg.t} draws, Q={cfg.q}, tol "
+                                   f"{cfg.tol}, J_max {cfg.max_iters} (P:779)",
+                       "J": infos[-1]["iters"], "mvms_per_step": infos[-1]["mvms"], "nnz": nnz,
+                       "converged": infos[-1]["converged"], "l2": "flushed between steps (256 MiB write)",
+                       "paper": "0.61 Gibbs samples/s on a Titan RTX (P:1006; one draw + mean solve + Gamma updates "
+                                "per sample: context only)"},
+            "roofline": roof,
+            "e2e": {"value": cfg.t / (e2e / 1000.0), "unit": "samples/s", "h2d_bytes_per_step": n * cfg.t * 4,
+                    "d2h_bytes_per_step": n * cfg.t * 4, "ms_per_step": e2e},
+            "gpu_launches": int(sum(i["kernel_launches"] for i in infos)), "clocks": clocks}
+    if not args.no_cpu_baseline:
+        from oracle import SparseOperator, ciq
+        op = SparseOperator(inp["indptr"], inp["indices"], inp["data"], n)
+        t0 = time.perf_counter()
+        ciq(op, inp["B_rhs"].astype(np.float64), q=cfg.q, max_iters=cfg.max_iters, tol=cfg.tol, mode="invsqrt",
+            lanczos_start=inp["S"])
+        dt = time.perf_counter() - t0
+        from threadpoolctl import threadpool_info
+        line["cpu_baseline"] = {"value": cfg.t / dt, "unit": "samples/s", "kind": "oracle",
+                                "cores": max([d.get("num_threads", 1) for d in threadpool_info()] + [1]),
+                                "sample": f"the whole oracle call on the same {n} x {cfg.t} draws ({dt:.2f} s)"}
+    print(json.dumps(line), flush=True)
+    g.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -505,6 +605,13 @@ def main():
                                                                   "line's cpu_baseline"}))
         else:
             run_thompson(args)
+        return
+    if args.config == "G1":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "G1 is a widening row; its oracle is timed as this "
+                                                                  "line's cpu_baseline"}))
+        else:
+            run_gibbs(args)
         return
     cfg = workloads.CONFIGS[args.config]
     if args.impl == "reference":

@@ -62,7 +62,10 @@ typedef enum {
   CIQ_OP_DENSE = 0,     /* K = A + diag*I for a given dense symmetric A                   */
   CIQ_OP_RBF = 1,       /* k = o^2 exp(-r^2/2)                                (reading G11)        */
   CIQ_OP_MATERN52 = 2,  /* k = o^2 (1 + sqrt5 r + 5 r^2/3) exp(-sqrt5 r)                           */
-  CIQ_OP_MATERN32 = 3   /* k = o^2 (1 + sqrt3 r) exp(-sqrt3 r);  r = ||(x - x')/l||, K += diag*I   */
+  CIQ_OP_MATERN32 = 3,  /* k = o^2 (1 + sqrt3 r) exp(-sqrt3 r);  r = ||(x - x')/l||, K += diag*I   */
+  CIQ_OP_SPARSE = 4     /* a given sparse symmetric matrix in CSR form (e.g. the stencil precision */
+                        /* Lambda = g_obs A^T A + g_prior L^T L of the Gibbs sampler),  */
+                        /* K = A + diag*I; fp32 SIMT SpMM                    */
 } ciq_op_kind;
 
 typedef enum {
@@ -91,6 +94,10 @@ typedef struct {
   float outputscale;          /* o^2 (> 0)                                                      */
   float diag;                 /* sigma^2 >= 0 added to the diagonal (noise / jitter, G12); also  */
                               /* the rigorous lower bound on lambda_min used by the estimator (G6) */
+  const int64_t* csr_indptr;  /* SPARSE: this rank's row block (all N rows on one GPU) in CSR:   */
+  const int32_t* csr_indices; /*   indptr[rows + 1] (indptr[0] = 0), global column indices and    */
+  const float* csr_values;    /*   values of the nnz = indptr[rows] entries (host or device; the */
+  int64_t nnz;                /*   ctx keeps a device copy).  The matrix must be symmetric.       */
 } ciq_operator;
 
 /* Preconditioner P = L L^T + sigma2 I, L = N x rank row-major (ld >= rank).  When L comes

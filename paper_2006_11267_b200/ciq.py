@@ -33,7 +33,7 @@ CIQ_ERR_CUDA = -5
 CIQ_ERR_NCCL = -6
 CIQ_ERR_OOM = -7
 # ciq_op_kind
-OP_KINDS = {"dense": 0, "rbf": 1, "matern52": 2, "matern32": 3}
+OP_KINDS = {"dense": 0, "rbf": 1, "matern52": 2, "matern32": 3, "sparse": 4}
 # ciq_mode
 MODES = {"sqrt": 0, "invsqrt": 1, "whiten": 2}
 # ciq_mvm_impl
@@ -43,7 +43,8 @@ MVM_IMPLS = {"auto": 0, "simt": 1, "tc": 2}
 class CiqOperator(ctypes.Structure):
     _fields_ = [("kind", c_int32), ("n", c_int64), ("K", c_void_p), ("ldk", c_int64), ("X", c_void_p),
                 ("d", c_int64), ("ldx", c_int64), ("lengthscale", POINTER(c_float)), ("ard", c_int32),
-                ("outputscale", c_float), ("diag", c_float)]
+                ("outputscale", c_float), ("diag", c_float), ("csr_indptr", c_void_p), ("csr_indices", c_void_p),
+                ("csr_values", c_void_p), ("nnz", c_int64)]
 
 
 class CiqPrecond(ctypes.Structure):
@@ -269,6 +270,17 @@ def ciq_init(kind: str, n: int, *, X=None, K=None, lengthscale=1.0, outputscale:
     if kind == "dense":
         p, ld, r, cc = _ptr_ld(K, "K", keep)
         op.K, op.ldk = p, ld
+    elif kind == "sparse":   # K = (indptr int64, indices int32, data float32) of this rank's row block
+        for name, arr, dt in (("csr_indptr", K[0], np.int64), ("csr_indices", K[1], np.int32),
+                              ("csr_values", K[2], np.float32)):
+            if isinstance(arr, np.ndarray):
+                a = np.ascontiguousarray(arr, dtype=dt)
+                keep.append(a)
+                setattr(op, name, a.ctypes.data)
+            else:   # torch tensor (device or host), contiguous, of that dtype
+                keep.append(arr)
+                setattr(op, name, arr.data_ptr())
+        op.nnz = int(K[1].shape[0])
     else:
         p, ld, r, cc = _ptr_ld(X, "X", keep)
         op.X, op.ldx, op.d = p, ld, cc
@@ -448,8 +460,8 @@ class CIQ:
 
     def __init__(self, kind: str, n: int | None = None, **kw):
         if n is None:
-            src = kw.get("X") if kind != "dense" else kw.get("K")
-            n = src.shape[0]
+            src = kw.get("X") if kind not in ("dense", "sparse") else kw.get("K")
+            n = src.shape[0] if kind != "sparse" else src[0].shape[0] - 1
         self.kind = kind
         self.n = int(n)
         self.ctx, self._keep = ciq_init(kind, self.n, **kw)

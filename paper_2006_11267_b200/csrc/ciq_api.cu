@@ -128,6 +128,9 @@ struct ciq_ctx {
   float* xs = nullptr;        // owned scaled points
   double* xs64 = nullptr;     // owned scaled points in fp64 (exact quotients of the fp32 inputs)
   float* kcopy = nullptr;     // owned dense copy (host-provided K)
+  int64_t* csr_rp = nullptr;  // owned device copy of the sparse operator's local CSR block
+  int32_t* csr_ci = nullptr;
+  float* csr_cv = nullptr;
   Workspace ws;
   LambdaWork lw;
   float* staging = nullptr;   // host-pointer staging (rows x tp)
@@ -350,6 +353,10 @@ ciq_status grow(ciq_ctx* c, T** buf, size_t* cap, size_t need) {
   return CIQ_OK;
 }
 
+bool is_kernel_op(const ciq_ctx* c) {
+  return c->op.kind == CIQ_OP_RBF || c->op.kind == CIQ_OP_MATERN52 || c->op.kind == CIQ_OP_MATERN32;
+}
+
 // A/B switches for experiments: compiled in only with -DCIQ_EXPERIMENTS (scripts/build_variant.py);
 // the shipped library ignores the environment.
 bool experiment_env(const char* name) {
@@ -539,7 +546,7 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
                      "tensor-core MVM unavailable for this operator (N < 256, huge features, or d > 8 with an RHS chunk < 32)");
     OpDev od = c->dev;
     if (c->deriv) {   // dK/dl (ciq_hyper_grad): kernel kinds 4-6, o^2 / l, no sigma^2
-      od.kind += 3;
+      od.kind += 10;   // internal kinds 11-13 (mvm_*.cu: KIND templates 4-6)
       od.o2 = c->op.outputscale / c->ls[0];
       od.diag = 0.f;
     }
@@ -586,7 +593,7 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   if (!skip_pack)
     LAUNCH(c, launch_pack_v(v, c->op.n, c->npad, tp, plane_cols(c, tp), nrm, c->planes, c->inv_scale, c->stream));
   TcArgs a{};
-  a.kind = c->op.kind + (c->deriv ? 3 : 0);   // 4-6: dK/dl (ciq_hyper_grad)
+  a.kind = c->op.kind + (c->deriv ? 10 : 0);   // 11-13: dK/dl (ciq_hyper_grad; KIND templates 4-6)
   a.n = c->op.n;
   a.npad = c->npad;
   a.row0 = c->row0;
@@ -1234,9 +1241,13 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
   if (!out || !op) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "null ctx or operator");
   *out = nullptr;
   if (op->n <= 0) return set_err(nullptr, CIQ_ERR_DIM, "n must be > 0");
-  if (op->kind < CIQ_OP_DENSE || op->kind > CIQ_OP_MATERN32) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "bad kind");
+  if (op->kind < CIQ_OP_DENSE || op->kind > CIQ_OP_SPARSE) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "bad kind");
   if (!(op->diag >= 0)) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "diag must be >= 0");
-  if (op->kind == CIQ_OP_DENSE) {
+  if (op->kind == CIQ_OP_SPARSE) {
+    if (!op->csr_indptr || !op->csr_indices || !op->csr_values || op->nnz < 0)
+      return set_err(nullptr, CIQ_ERR_INVALID_ARG, "sparse operator needs csr_indptr / csr_indices / csr_values");
+    if (pc) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "sparse operator: no preconditioner (not supported)");
+  } else if (op->kind == CIQ_OP_DENSE) {
     if (!op->K) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "dense operator needs K");
     if (op->ldk < op->n) return set_err(nullptr, CIQ_ERR_DIM, "ldk < n");
   } else {
@@ -1298,7 +1309,27 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
   dv.diag = op->diag;
   dv.o2 = op->outputscale;
   ciq_status st = CIQ_OK;
-  if (op->kind == CIQ_OP_DENSE) {
+  if (op->kind == CIQ_OP_SPARSE) {
+    // CSR of this rank's row block [row0, row1) (all rows on one GPU), copied to the device
+    const int64_t lrows = c->row1 - c->row0, nnz = op->nnz;
+    const bool dp = is_device_ptr(op->csr_indptr);
+    const cudaMemcpyKind mk = dp ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (cudaMalloc(&c->csr_rp, (size_t)(lrows + 1) * 8) != cudaSuccess ||
+        cudaMalloc(&c->csr_ci, (size_t)std::max<int64_t>(1, nnz) * 4) != cudaSuccess ||
+        cudaMalloc(&c->csr_cv, (size_t)std::max<int64_t>(1, nnz) * 4) != cudaSuccess) {
+      st = CIQ_ERR_OOM; goto fail;
+    }
+    if (cudaMemcpy(c->csr_rp, op->csr_indptr, (size_t)(lrows + 1) * 8, mk) != cudaSuccess ||
+        (nnz > 0 && cudaMemcpy(c->csr_ci, op->csr_indices, (size_t)nnz * 4,
+                               is_device_ptr(op->csr_indices) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) != cudaSuccess) ||
+        (nnz > 0 && cudaMemcpy(c->csr_cv, op->csr_values, (size_t)nnz * 4,
+                               is_device_ptr(op->csr_values) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) != cudaSuccess)) {
+      st = CIQ_ERR_CUDA; goto fail;
+    }
+    dv.rp = c->csr_rp;
+    dv.ci = c->csr_ci;
+    dv.cv = c->csr_cv;
+  } else if (op->kind == CIQ_OP_DENSE) {
     // K holds this rank's row block [row0, row1) (all rows on one GPU); the MVM kernels index it
     // by the global row, hence the pointer shift by -row0 rows.
     const int64_t lrows = c->row1 - c->row0;
@@ -1382,6 +1413,9 @@ void ciq_free(ciq_ctx* c) {
   dfree(c->xs);
   dfree(c->xs64);
   dfree(c->kcopy);
+  dfree(c->csr_rp);
+  dfree(c->csr_ci);
+  dfree(c->csr_cv);
   dfree(c->staging);
   dfree(c->kplanes);
   dfree(c->feat_a); dfree(c->feat_b); dfree(c->planes); dfree(c->inv_scale); dfree(c->psplit);
@@ -1400,6 +1434,8 @@ ciq_status ciq_pivoted_cholesky(ciq_ctx* c, int32_t rank, float* L, int64_t ldl)
   if (!c || !L) return CIQ_ERR_INVALID_ARG;
   if (c->sharded)   // the pivot search and the kernel columns span all N rows
     return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_pivoted_cholesky: single-GPU contexts only (not row-sharded)");
+  if (c->op.kind == CIQ_OP_SPARSE)
+    return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_pivoted_cholesky: kernel or dense operators only");
   const int64_t n = c->op.n;
   if (rank < 1 || rank > n || ldl < rank) return set_err(c, CIQ_ERR_DIM, "bad rank / ldl");
   if (join_user_stream(c) != CIQ_OK) return CIQ_ERR_CUDA;
@@ -1502,7 +1538,7 @@ ciq_status ciq_vjp(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int6
 ciq_status ciq_hyper_grad(ciq_ctx* c, const float* B, int64_t ldb, const float* V, int64_t ldv, int64_t T,
                           const ciq_params* params, double* grad, ciq_info* info) {
   if (!c || !B || !V || !grad) return CIQ_ERR_INVALID_ARG;
-  if (c->sharded || c->has_precond || c->post.on || c->op.kind == CIQ_OP_DENSE || c->op.ard)
+  if (c->sharded || c->has_precond || c->post.on || !is_kernel_op(c) || c->op.ard)
     return set_err(c, CIQ_ERR_INVALID_ARG,
                    "ciq_hyper_grad: single-GPU, unpreconditioned, isotropic kernel operators only");
   const int64_t n = c->op.n;
@@ -1583,7 +1619,7 @@ ciq_status ciq_hyper_grad(ciq_ctx* c, const float* B, int64_t ldb, const float* 
 
 ciq_status ciq_set_posterior(ciq_ctx* c, const float* Xt, int64_t ldxt, int64_t m, const float* y, double noise) {
   if (!c || !Xt) return CIQ_ERR_INVALID_ARG;
-  if (c->op.kind == CIQ_OP_DENSE || c->sharded)
+  if (!is_kernel_op(c) || c->sharded)
     return set_err(c, CIQ_ERR_INVALID_ARG, "ciq_set_posterior: single-GPU kernel operators only");
   const int d = (int)c->op.d;
   if (m < 1 || m > 4096 || ldxt < d) return set_err(c, CIQ_ERR_DIM, "ciq_set_posterior: need 1 <= m <= 4096, ldxt >= d");
@@ -1721,7 +1757,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
   c->timed.clear();
   if (p.fp64 && !c->pc.on) {   // accuracy mode: K materialised in fp64, fp64 MVMs and vectors
-    if (c->sharded || c->op.kind == CIQ_OP_DENSE)
+    if (c->sharded || !is_kernel_op(c))
       return set_err(c, CIQ_ERR_INVALID_ARG, "params.fp64: single-GPU kernel operators only");
     const ciq_status sm = ensure_m64(c);
     if (sm != CIQ_OK) return set_err(c, sm, "params.fp64: N^2 doubles do not fit in device memory");

@@ -20,6 +20,9 @@ struct OpDev {
   int64_t ldk;
   float o2;            // outputscale
   float diag;          // sigma^2 added to the diagonal
+  const int64_t* rp;   // sparse: CSR row pointers of the local row block (rp[0] = 0)
+  const int32_t* ci;   //         global column indices
+  const float* cv;     //         values
 };
 
 // Per-solve scalar state (device), one allocation; see recurrence.cu.
@@ -50,6 +53,10 @@ int mvm_simt_blocks(int64_t rows);
 cudaError_t launch_materialize(const OpDev& op, int64_t row0, int64_t rows, float* k, cudaStream_t s);
 cudaError_t launch_mvm_simt(const OpDev& op, const float* v, int tp, int64_t row0, int64_t row1,
                             float* p, int ldp, double* alpha_part, const Ctrl* done, cudaStream_t s);
+// sparse (CSR) operator, mvm_sparse.cu: same contract as launch_mvm_simt (alpha partials per
+// mvm_simt_blocks(rows) blocks of 64 rows)
+cudaError_t launch_spmm(const OpDev& op, const float* v, int tp, int64_t row0, int64_t row1, float* p, int ldp,
+                        double* alpha_part, const Ctrl* done, cudaStream_t s);
 
 // tcgen05 MVMs.  Matrix-free (mvm_tc2.cu): persistent 256-row units; dense (mvm_dense.cu):
 // persistent 128-row units streaming the split K planes.  Both write nsplit partial products P_s

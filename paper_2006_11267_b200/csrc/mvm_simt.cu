@@ -197,6 +197,7 @@ int mvm_simt_blocks(int64_t rows) { return (int)((rows + BM - 1) / BM); }
 
 cudaError_t launch_mvm_simt(const OpDev& op, const float* v, int tp, int64_t row0, int64_t row1, float* p,
                             int ldp, double* apart, const Ctrl* done, cudaStream_t s) {
+  if (op.kind == 4) return launch_spmm(op, v, tp, row0, row1, p, ldp, apart, done, s);   // CIQ_OP_SPARSE
   if (op.d > DMAX && op.kind != 0) return cudaErrorInvalidValue;
   if (tp % 16 != 0) return cudaErrorInvalidValue;
   switch (op.kind) {
@@ -204,9 +205,9 @@ cudaError_t launch_mvm_simt(const OpDev& op, const float* v, int tp, int64_t row
     case 1: return launch_kind<1>(op, v, tp, row0, row1, p, ldp, apart, done, s);
     case 2: return launch_kind<2>(op, v, tp, row0, row1, p, ldp, apart, done, s);
     case 3: return launch_kind<3>(op, v, tp, row0, row1, p, ldp, apart, done, s);
-    case 4: return launch_kind<4>(op, v, tp, row0, row1, p, ldp, apart, done, s);
-    case 5: return launch_kind<5>(op, v, tp, row0, row1, p, ldp, apart, done, s);
-    case 6: return launch_kind<6>(op, v, tp, row0, row1, p, ldp, apart, done, s);
+    case 11: return launch_kind<4>(op, v, tp, row0, row1, p, ldp, apart, done, s);
+    case 12: return launch_kind<5>(op, v, tp, row0, row1, p, ldp, apart, done, s);
+    case 13: return launch_kind<6>(op, v, tp, row0, row1, p, ldp, apart, done, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -581,9 +581,9 @@ cudaError_t launch_mvm_tc2(const TcArgs& a, int nsm, cudaStream_t s) {
     case 1: return launch2_kind<1>(a, tn, grid, s);
     case 2: return launch2_kind<2>(a, tn, grid, s);
     case 3: return launch2_kind<3>(a, tn, grid, s);
-    case 4: return launch2_kind<4>(a, tn, grid, s);
-    case 5: return launch2_kind<5>(a, tn, grid, s);
-    case 6: return launch2_kind<6>(a, tn, grid, s);
+    case 11: return launch2_kind<4>(a, tn, grid, s);
+    case 12: return launch2_kind<5>(a, tn, grid, s);
+    case 13: return launch2_kind<6>(a, tn, grid, s);
   }
   return cudaErrorInvalidValue;
 }

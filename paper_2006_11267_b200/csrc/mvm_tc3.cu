@@ -618,9 +618,9 @@ cudaError_t launch_mvm_tc3(const TcArgs& a, int nsm, cudaStream_t s) {
     case 1: return launch3_kf<1>(a, tn, pairs, s);
     case 2: return launch3_kf<2>(a, tn, pairs, s);
     case 3: return launch3_kf<3>(a, tn, pairs, s);
-    case 4: return launch3_kf<4>(a, tn, pairs, s);
-    case 5: return launch3_kf<5>(a, tn, pairs, s);
-    case 6: return launch3_kf<6>(a, tn, pairs, s);
+    case 11: return launch3_kf<4>(a, tn, pairs, s);
+    case 12: return launch3_kf<5>(a, tn, pairs, s);
+    case 13: return launch3_kf<6>(a, tn, pairs, s);
   }
   return cudaErrorInvalidValue;
 }
