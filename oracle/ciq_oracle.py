@@ -31,7 +31,7 @@ __all__ = [
     "hht_rule", "lanczos", "estimate_spectrum", "msminres", "ciq",
     "pivoted_cholesky", "precond_ciq", "MsminresResult", "CiqResult", "ciq_vjp",
     "PosteriorOperator", "thompson_step", "kernel_lengthscale_derivative", "ciq_hyper_grad",
-    "SparseOperator",
+    "SparseOperator", "BlockJacobi",
 ]
 
 
@@ -555,9 +555,47 @@ class LowRankPlusDiag:
         return self.l @ self.l.T + self.sigma2 * np.eye(self.l.shape[0])
 
 
-def precond_ciq(op, pre: LowRankPlusDiag, b: np.ndarray, q: int = 8, max_iters: int = 400,
+class BlockJacobi:
+    """P = blockdiag(K_11, K_22, ...): the diagonal blocks (size ``block``, the last one ragged) of
+    the operator K itself -- a preconditioner with cheap solves and MVMs (the two requirements of
+    P:71-74) whose square root has no closed form in the algorithm (the library computes P^{1/2} b
+    by CIQ on P, "nested CIQ").  Here its powers are evaluated exactly, block by block, from
+    numpy's eigh (the oracle's route is the explicit symmetric form of App. A)."""
+
+    def __init__(self, op, block: int):
+        self.n = op.n
+        self.block = int(block)
+        self.blocks = []
+        for i0 in range(0, self.n, self.block):
+            i1 = min(self.n, i0 + self.block)
+            kb = np.stack([op.kernel_column(j)[i0:i1] for j in range(i0, i1)], axis=1)
+            kb = kb + op.sigma2 * np.eye(i1 - i0)
+            lam, u = np.linalg.eigh(0.5 * (kb + kb.T))
+            self.blocks.append((i0, i1, lam, u))
+
+    def power(self, v: np.ndarray, p: float) -> np.ndarray:
+        v = np.asarray(v, dtype=np.float64)
+        out = np.empty_like(v)
+        for i0, i1, lam, u in self.blocks:
+            out[i0:i1] = u @ ((lam ** p).reshape((-1,) + (1,) * (v.ndim - 1)) * (u.T @ v[i0:i1]))
+        return out
+
+    def apply(self, v):
+        return self.power(v, 1.0)
+
+    def dense(self):
+        d = np.zeros((self.n, self.n))
+        for i0, i1, lam, u in self.blocks:
+            d[i0:i1, i0:i1] = (u * lam) @ u.T
+        return d
+
+    def spectrum(self):
+        return min(b[2][0] for b in self.blocks), max(b[2][-1] for b in self.blocks)
+
+
+def precond_ciq(op, pre, b: np.ndarray, q: int = 8, max_iters: int = 400,
                 tol: float = 1e-4, mode: str = "whiten", lanczos_start=None, lanczos_iters: int = 10,
-                rule: tuple | None = None, spectrum: tuple | None = None) -> CiqResult:
+                rule: tuple | None = None, spectrum: tuple | None = None, lower_bound: float = 1.0) -> CiqResult:
     """Preconditioned msMINRES-CIQ, oracle route = the explicit symmetric form of App. A:
 
         M = P^{-1/2} K P^{-1/2}                                    (P:8)
@@ -566,7 +604,9 @@ def precond_ciq(op, pre: LowRankPlusDiag, b: np.ndarray, q: int = 8, max_iters: 
 
     M^{-1/2} b is computed by ``ciq`` (invsqrt) on the operator M; lambda estimation runs on M with
     the rigorous bound lambda_min(M) >= 1 when P comes from a pivoted Cholesky of k(X,X) with
-    sigma2_P = sigma2 (reading G6/G13/G14).  mode 'whiten'/'invsqrt' -> R'b, 'sqrt' -> R b."""
+    sigma2_P = sigma2 (reading G6/G13/G14; ``lower_bound`` = 0 for other P, e.g. BlockJacobi).
+    ``pre`` provides power(v, p) (LowRankPlusDiag, BlockJacobi).
+    mode 'whiten'/'invsqrt' -> R'b, 'sqrt' -> R b."""
 
     class _M:
         n = op.n
@@ -581,7 +621,7 @@ def precond_ciq(op, pre: LowRankPlusDiag, b: np.ndarray, q: int = 8, max_iters: 
     if rule is None and spectrum is None:
         if lanczos_start is None:
             raise ValueError("need lanczos_start, spectrum or rule")
-        lmin, lmax, _, _ = estimate_spectrum(m.mvm, lanczos_start, lanczos_iters, lower_bound=1.0)
+        lmin, lmax, _, _ = estimate_spectrum(m.mvm, lanczos_start, lanczos_iters, lower_bound=lower_bound)
         spectrum = (lmin, lmax)
     res = ciq(m, b, q=q, max_iters=max_iters, tol=tol, mode="invsqrt", rule=rule, spectrum=spectrum)
     rprime_b = pre.power(res.out, -0.5)
