@@ -115,6 +115,14 @@ typedef struct {
                               /* 1: apply M matrix-free per iteration (K MVM + two Woodbury       */
                               /*   P^{-1/2} applications, fp32 vectors): O(N) memory, accuracy    */
                               /*   limited by the fp32 sensitivity of R'B.  */
+  int32_t kind;               /* 0 (default): P = L L^T + sigma2 I as above.                     */
+                              /* 1: block-Jacobi P = blockdiag of (K + diag I)'s own diagonal     */
+                              /*   blocks of size `block` (L, rank, sigma2, matrix_free ignored): */
+                              /*   a P without a closed-form square root -- P^{1/2} B is computed */
+                              /*   by CIQ on P ("nested CIQ") and the solve uses the P^{-1}- */
+                              /*   only recurrence on x_q = (K + t_q P)^{-1} c; */
+                              /*   fp64 throughout (K materialised: N^2 doubles), single GPU.     */
+  int64_t block;              /* kind 1: block size (>= 1; the last block is ragged)             */
 } ciq_precond;
 
 /* Row sharding across GPUs (one process per GPU).  NULL comm = single GPU; a comm
@@ -191,7 +199,9 @@ typedef struct {
   int32_t update_timed;
   int32_t mvm_impl_used;      /* ciq_mvm_impl of the loop MVMs: CIQ_MVM_SIMT or CIQ_MVM_TC       */
   int32_t mvm_splits;         /* column splits of the tensor-core MVM grid (1 = none)            */
-  int32_t fp64_route;         /* 1: preconditioned solve on the fp64 materialised M (precond64.cu) */
+  int32_t fp64_route;         /* 1: solve on fp64 vectors (precond64.cu / params.fp64 / nested)   */
+  int32_t nested_p_mvms;      /* nested CIQ (block-Jacobi P): MVMs with P spent on P^{1/2} b     */
+  int32_t nested_iters;       /*   and the inner msMINRES iterations                             */
 } ciq_info;
 
 typedef struct ciq_ctx ciq_ctx;

@@ -48,7 +48,8 @@ class CiqOperator(ctypes.Structure):
 
 
 class CiqPrecond(ctypes.Structure):
-    _fields_ = [("L", c_void_p), ("rank", c_int64), ("ldl", c_int64), ("sigma2", c_float), ("matrix_free", c_int32)]
+    _fields_ = [("L", c_void_p), ("rank", c_int64), ("ldl", c_int64), ("sigma2", c_float), ("matrix_free", c_int32),
+                ("kind", c_int32), ("block", c_int64)]
 
 
 class CiqComm(ctypes.Structure):
@@ -72,7 +73,8 @@ class CiqInfo(ctypes.Structure):
                 ("t", c_double * CIQ_MAX_Q), ("w", c_double * CIQ_MAX_Q), ("ms_total", c_float),
                 ("ms_lambda", c_float), ("ms_loop", c_float), ("ms_final", c_float), ("kernel_launches", c_int64),
                 ("ms_mvm", c_float), ("mvm_timed", c_int32), ("ms_update", c_float), ("update_timed", c_int32),
-                ("mvm_impl_used", c_int32), ("mvm_splits", c_int32), ("fp64_route", c_int32)]
+                ("mvm_impl_used", c_int32), ("mvm_splits", c_int32), ("fp64_route", c_int32),
+                ("nested_p_mvms", c_int32), ("nested_iters", c_int32)]
 
     def as_dict(self) -> dict:
         q = self.Q
@@ -85,7 +87,8 @@ class CiqInfo(ctypes.Structure):
                 "kernel_launches": self.kernel_launches, "ms_mvm": self.ms_mvm, "mvm_timed": self.mvm_timed,
                 "ms_update": self.ms_update, "update_timed": self.update_timed,
                 "mvm_impl_used": {1: "simt", 2: "tc"}.get(self.mvm_impl_used, "none"), "mvm_splits": self.mvm_splits,
-                "fp64_route": bool(self.fp64_route)}
+                "fp64_route": bool(self.fp64_route), "nested_p_mvms": self.nested_p_mvms,
+                "nested_iters": self.nested_iters}
 
 
 def _load() -> ctypes.CDLL:
@@ -259,7 +262,8 @@ def _stream_handle(stream):
 
 
 def ciq_init(kind: str, n: int, *, X=None, K=None, lengthscale=1.0, outputscale: float = 1.0, diag: float = 0.0,
-             precond_L=None, precond_sigma2: float = 0.0, precond_matrix_free: bool = False, comm: tuple | None = None,
+             precond_L=None, precond_sigma2: float = 0.0, precond_matrix_free: bool = False, precond_block: int = 0,
+             comm: tuple | None = None,
              stream=None):
     """Returns (ctx handle, keepalive list).  comm = (rank, world, unique_id_bytes) for NCCL,
     (rank, world, LoopbackGroup) for the in-process loopback transport, or None."""
@@ -291,7 +295,10 @@ def ciq_init(kind: str, n: int, *, X=None, K=None, lengthscale=1.0, outputscale:
     op.outputscale = float(outputscale)
     op.diag = float(diag)
     pc = None
-    if precond_L is not None:
+    if precond_block > 0:   # block-Jacobi P (nested CIQ); L is not used
+        pc = CiqPrecond()
+        pc.kind, pc.block = 1, int(precond_block)
+    elif precond_L is not None:
         pc = CiqPrecond()
         p, ld, r, cc = _ptr_ld(precond_L, "precond_L", keep)
         pc.L, pc.ldl, pc.rank, pc.sigma2 = p, ld, cc, float(precond_sigma2)

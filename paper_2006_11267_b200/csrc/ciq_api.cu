@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -104,9 +105,24 @@ struct PostDev {
   int64_t* idx = nullptr;   size_t idx_cap = 0;
 };
 
+// Nested-CIQ route (App. A, precond_nested.cu): block-Jacobi P = blockdiag of K's own
+// diagonal blocks; K + sigma^2 I materialised in fp64, P^{-1} blocks inverted on the host in fp64.
+struct NestedDev {
+  bool on = false;
+  int64_t block = 0;
+  std::vector<int64_t> b0;    // block starts, nb + 1 entries (b0[nb] = n)
+  bool ready = false;
+  double* k64 = nullptr;      // n x ldk: K + sigma^2 I (fp64)
+  int64_t ldk = 0;
+  double* pinv = nullptr;     // block b (size m_b) at offset b0[b] * block, row-major, ld = m_b
+  double* work = nullptr;     // fp64 vectors of pmsminres
+  size_t work_cap = 0;
+};
+
 struct ciq_ctx {
   ciq_operator op{};
   PrecondDev pc;
+  NestedDev nest;
   PostDev post;
   std::vector<double> ls;     // per-coordinate lengthscales of a kernel operator (copied at init)
   OpDev dev{};
@@ -1166,6 +1182,8 @@ ciq_status run_iterations(ciq_ctx* c, const ciq_params& p, int j0, uint64_t key_
 
 ciq_status apply_fp64(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* out, int64_t ldo, ciq_params p,
                       ciq_info* info);
+ciq_status apply_nested(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* out, int64_t ldo, ciq_params p,
+                        ciq_info* info);
 
 }  // namespace
 
@@ -1258,7 +1276,11 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     for (int k = 0; k < (op->ard ? op->d : 1); ++k)
       if (!(op->lengthscale[k] > 0)) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "lengthscale must be > 0");
   }
-  if (pc) {
+  if (pc && pc->kind == 1) {
+    if (pc->block < 1) return set_err(nullptr, CIQ_ERR_DIM, "block-Jacobi preconditioner: block must be >= 1");
+    if (comm) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "block-Jacobi preconditioner: single GPU only");
+  } else if (pc) {
+    if (pc->kind != 0) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "bad preconditioner kind");
     if (!pc->L || pc->rank < 1 || pc->ldl < pc->rank) return set_err(nullptr, CIQ_ERR_DIM, "bad preconditioner L / rank / ldl");
     if (!(pc->sigma2 > 0)) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "preconditioner sigma2 must be > 0 (S:425)");
     if (pc->rank > 2048) return set_err(nullptr, CIQ_ERR_DIM, "preconditioner rank > 2048");
@@ -1375,7 +1397,11 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     dv.d = (int)d;
     c->tc_ok = build_tc_features(c, xh);
   }
-  if (pc) {
+  if (pc && pc->kind == 1) {   // nested CIQ route: set up lazily (ensure_nested) at the first apply
+    c->nest.on = true;
+    c->nest.block = std::min<int64_t>(pc->block, op->n);
+    c->has_precond = true;
+  } else if (pc) {
     PrecondDev& P = c->pc;
     P.rank = (int)pc->rank;
     P.sigma2 = pc->sigma2;
@@ -1412,6 +1438,9 @@ void ciq_free(ciq_ctx* c) {
   free_lambda(c->lw);
   dfree(c->xs);
   dfree(c->xs64);
+  dfree(c->nest.k64);
+  dfree(c->nest.pinv);
+  dfree(c->nest.work);
   dfree(c->kcopy);
   dfree(c->csr_rp);
   dfree(c->csr_ci);
@@ -1756,6 +1785,10 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   c->profiling = p.profile_kernels != 0;
   for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
   c->timed.clear();
+  if (c->nest.on) {   // block-Jacobi P: P^{-1}-only recurrence + nested CIQ for P^{1/2} B (App. A)
+    if (c->post.on) return set_err(c, CIQ_ERR_INVALID_ARG, "block-Jacobi preconditioner: not on a posterior ctx");
+    return apply_nested(c, B, ldb, T, out, ldo, p, info);
+  }
   if (p.fp64 && !c->pc.on) {   // accuracy mode: K materialised in fp64, fp64 MVMs and vectors
     if (c->sharded || !is_kernel_op(c))
       return set_err(c, CIQ_ERR_INVALID_ARG, "params.fp64: single-GPU kernel operators only");
@@ -2289,6 +2322,398 @@ ciq_status apply_fp64(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float*
       if (tm.kind == 0) { info->ms_mvm += ms; ++info->mvm_timed; }
       else { info->ms_update += ms; ++info->update_timed; }
     }
+  }
+  return converged ? CIQ_OK : CIQ_NOT_CONVERGED;
+}
+
+
+// ---------------- nested CIQ with a block-Jacobi preconditioner (App. A) ----------------
+
+// a (m x m, row-major, SPD) <- a^{-1} in fp64: Cholesky a = L L^T, then L^{-1}, then L^{-T} L^{-1}.
+bool spd_inverse_host(std::vector<double>& a, int m) {
+  for (int j = 0; j < m; ++j) {
+    double d = a[(size_t)j * m + j];
+    for (int k = 0; k < j; ++k) d -= a[(size_t)j * m + k] * a[(size_t)j * m + k];
+    if (!(d > 0)) return false;
+    d = std::sqrt(d);
+    a[(size_t)j * m + j] = d;
+    for (int i = j + 1; i < m; ++i) {
+      double v = a[(size_t)i * m + j];
+      for (int k = 0; k < j; ++k) v -= a[(size_t)i * m + k] * a[(size_t)j * m + k];
+      a[(size_t)i * m + j] = v / d;
+    }
+  }
+  std::vector<double> li((size_t)m * m, 0.0);   // L^{-1}, lower triangular
+  for (int j = 0; j < m; ++j) {
+    li[(size_t)j * m + j] = 1.0 / a[(size_t)j * m + j];
+    for (int i = j + 1; i < m; ++i) {
+      double v = 0.0;
+      for (int k = j; k < i; ++k) v -= a[(size_t)i * m + k] * li[(size_t)k * m + j];
+      li[(size_t)i * m + j] = v / a[(size_t)i * m + i];
+    }
+  }
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double v = 0.0;
+      for (int k = i; k < m; ++k) v += li[(size_t)k * m + i] * li[(size_t)k * m + j];
+      a[(size_t)i * m + j] = v;
+      a[(size_t)j * m + i] = v;
+    }
+  return true;
+}
+
+ciq_status ensure_nested(ciq_ctx* c) {
+  NestedDev& Nd = c->nest;
+  if (Nd.ready) return CIQ_OK;
+  const int64_t n = c->op.n;
+  cudaStream_t s = c->stream;
+  Nd.ldk = (n + 7) / 8 * 8;
+  Nd.b0.clear();
+  for (int64_t i = 0; i < n; i += Nd.block) Nd.b0.push_back(i);
+  Nd.b0.push_back(n);
+  const int nb = (int)Nd.b0.size() - 1;
+  if (dalloc(&Nd.k64, (size_t)n * Nd.ldk) != cudaSuccess || dalloc(&Nd.pinv, (size_t)n * Nd.block) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(c, CIQ_ERR_OOM, "nested preconditioner: N^2 doubles do not fit in device memory");
+  }
+  CUDA_TRY(c, cudaMemsetAsync(Nd.k64, 0, (size_t)n * Nd.ldk * 8, s));
+  LAUNCH(c, launch_materialize64(c->dev, 0, n, Nd.k64, Nd.ldk, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  for (int b = 0; b < nb; ++b) {   // P_b = (K + sigma^2 I)[b, b];  P_b^{-1} on the host (fp64)
+    const int64_t i0 = Nd.b0[b];
+    const int m = (int)(Nd.b0[b + 1] - i0);
+    std::vector<double> blk((size_t)m * m);
+    CUDA_TRY(c, cudaMemcpy2D(blk.data(), (size_t)m * 8, Nd.k64 + i0 * Nd.ldk + i0, (size_t)Nd.ldk * 8, (size_t)m * 8,
+                             (size_t)m, cudaMemcpyDeviceToHost));
+    if (!spd_inverse_host(blk, m)) return set_err(c, CIQ_ERR_NOT_PD, "preconditioner block %d is not positive definite", b);
+    CUDA_TRY(c, cudaMemcpy(Nd.pinv + i0 * Nd.block, blk.data(), (size_t)m * m * 8, cudaMemcpyHostToDevice));
+  }
+  Nd.ready = true;
+  return CIQ_OK;
+}
+
+// P^{-1}-only preconditioned msMINRES (precond_nested.cu header) on columns of c0 (n x tp, fp64),
+// pencil (A, P) given as device operators; per-column scalars and the Q x tp Givens rotations on the
+// host (fp64).  Returns y = sum_q w_q x_q (x_q = (A + t_q P)^{-1} c0) in yout.  lanczos_only: run
+// `max_iters` Lanczos steps and return the per-column tridiagonal (alphas, betas) instead.
+struct PencilOps {
+  std::function<ciq_status(const double*, double*)> apply_a, apply_pinv;
+};
+
+ciq_status pmsminres(ciq_ctx* c, const PencilOps& ops, const double* c0, int tp, int cols, int nq, const double* t,
+                     const double* w, int max_iters, double tol, double* yout, int* iters, double* relres,
+                     bool lanczos_only, std::vector<std::vector<double>>* alphas, std::vector<std::vector<double>>* betas) {
+  const int64_t n = c->op.n;
+  const size_t vsz = (size_t)n * tp;
+  const int nqe = lanczos_only ? 0 : nq;
+  const int nbk = coldot64_blocks(n);
+  const size_t need = vsz * (5 + 2 * (size_t)nqe) + (size_t)nbk * tp + (size_t)4 * std::max(1, nqe) * tp + 4 * (size_t)tp;
+  NestedDev& Nd = c->nest;
+  if (Nd.work_cap < need) {
+    dfree(Nd.work);
+    Nd.work_cap = 0;
+    CUDA_TRY(c, dalloc(&Nd.work, need));
+    Nd.work_cap = need;
+  }
+  cudaStream_t s = c->stream;
+  double* r1 = Nd.work;
+  double* r2 = r1 + vsz;
+  double* yv = r2 + vsz;
+  double* v = yv + vsz;
+  double* tmp = v + vsz;
+  double* dA = tmp + vsz;                      // [nqe][n][tp]
+  double* dB = dA + (size_t)nqe * vsz;
+  double* part = dB + (size_t)nqe * vsz;
+  double* coef = part + (size_t)nbk * tp;      // [4][nqe][tp]
+  double* sca = coef + (size_t)4 * std::max(1, nqe) * tp;
+  double* scb = sca + tp;
+  double* sums = scb + tp;
+  std::vector<double> ha(tp), hb(tp), hs(tp);
+  auto coldot = [&](const double* a, const double* b, std::vector<double>& outv) -> ciq_status {
+    LAUNCH(c, launch_coldot64(a, b, n, tp, part, s));
+    LAUNCH(c, launch_reduce_cols(part, nbk, tp, sums, 0, s));
+    CUDA_TRY(c, cudaMemcpyAsync(outv.data(), sums, (size_t)tp * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    return CIQ_OK;
+  };
+  auto axpby = [&](double* out, const std::vector<double>& a, const double* x, const std::vector<double>& b,
+                   const double* y) -> ciq_status {
+    CUDA_TRY(c, cudaMemcpyAsync(sca, a.data(), (size_t)tp * 8, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(scb, b.data(), (size_t)tp * 8, cudaMemcpyHostToDevice, s));
+    LAUNCH(c, launch_axpby_cols64(out, sca, x, scb, y, n, tp, s));
+    return CIQ_OK;
+  };
+  // r1 = r2 = c0; y = P^{-1} r1; beta_1 = sqrt(r1^T y)
+  CUDA_TRY(c, cudaMemcpyAsync(r1, c0, vsz * 8, cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(r2, c0, vsz * 8, cudaMemcpyDeviceToDevice, s));
+  ciq_status st = ops.apply_pinv(r1, yv);
+  if (st != CIQ_OK) return st;
+  std::vector<double> b2(tp);
+  st = coldot(r1, yv, b2);
+  if (st != CIQ_OK) return st;
+  std::vector<double> beta1(tp), beta(tp), oldb(tp, 0.0);
+  std::vector<int> active(tp);
+  for (int k = 0; k < tp; ++k) {
+    beta1[k] = (k < cols && b2[k] > 0) ? std::sqrt(b2[k]) : 0.0;
+    beta[k] = beta1[k];
+    active[k] = beta1[k] > 0;
+  }
+  std::vector<double> c1((size_t)nq * tp, 1.0), s1((size_t)nq * tp, 0.0), c2((size_t)nq * tp, 1.0), s2((size_t)nq * tp, 0.0),
+      phib((size_t)nq * tp), hcoef((size_t)4 * std::max(1, nqe) * tp, 0.0);
+  for (int q = 0; q < nq; ++q)
+    for (int k = 0; k < tp; ++k) phib[(size_t)q * tp + k] = beta1[k];
+  if (alphas) { alphas->assign(tp, {}); betas->assign(tp, {}); }
+  if (!lanczos_only) {
+    CUDA_TRY(c, cudaMemsetAsync(dA, 0, (size_t)2 * nqe * vsz * 8, s));
+    CUDA_TRY(c, cudaMemsetAsync(yout, 0, vsz * 8, s));
+  }
+  double worst = 0.0;
+  int j = 0;
+  for (j = 1; j <= max_iters; ++j) {
+    bool any = false;
+    for (int k = 0; k < tp; ++k) any = any || active[k];
+    if (!any) { --j; break; }
+    // v = y / beta_j ; y = A v - (beta_j / beta_{j-1}) r1 ; alpha = v^T y ; y -= (alpha / beta_j) r2
+    std::vector<double> inv(tp), zero(tp, 0.0), one(tp, 1.0), m1(tp), m2(tp);
+    for (int k = 0; k < tp; ++k) inv[k] = active[k] ? 1.0 / beta[k] : 0.0;
+    st = axpby(v, inv, yv, zero, nullptr);
+    if (st != CIQ_OK) return st;
+    st = ops.apply_a(v, yv);
+    if (st != CIQ_OK) return st;
+    if (j >= 2) {
+      for (int k = 0; k < tp; ++k) m1[k] = (active[k] && oldb[k] > 0) ? -beta[k] / oldb[k] : 0.0;
+      st = axpby(yv, one, yv, m1, r1);
+      if (st != CIQ_OK) return st;
+    }
+    std::vector<double> alpha(tp);
+    st = coldot(v, yv, alpha);
+    if (st != CIQ_OK) return st;
+    for (int k = 0; k < tp; ++k) m2[k] = active[k] ? -alpha[k] / beta[k] : 0.0;
+    st = axpby(yv, one, yv, m2, r2);
+    if (st != CIQ_OK) return st;
+    std::swap(r1, r2);   // r1 <- r2 ; r2 <- y (the old r1 buffer takes y's values below)
+    CUDA_TRY(c, cudaMemcpyAsync(r2, yv, vsz * 8, cudaMemcpyDeviceToDevice, s));
+    st = ops.apply_pinv(r2, yv);
+    if (st != CIQ_OK) return st;
+    st = coldot(r2, yv, b2);
+    if (st != CIQ_OK) return st;
+    std::vector<double> bnew(tp);
+    for (int k = 0; k < tp; ++k) bnew[k] = (active[k] && b2[k] > 0) ? std::sqrt(b2[k]) : 0.0;
+    if (alphas)
+      for (int k = 0; k < cols; ++k)
+        if (active[k]) { (*alphas)[k].push_back(alpha[k]); (*betas)[k].push_back(bnew[k]); }
+    if (!lanczos_only) {   // per-shift Givens QR of column j of [T_j + t_q I; beta_{j+1} e_j^T]
+      worst = 0.0;
+      for (int q = 0; q < nq; ++q)
+        for (int k = 0; k < tp; ++k) {
+          const size_t i = (size_t)q * tp + k;
+          double* ca = &hcoef[i];
+          double* cb = &hcoef[(size_t)nq * tp + i];
+          double* ce = &hcoef[(size_t)2 * nq * tp + i];
+          double* cf = &hcoef[(size_t)3 * nq * tp + i];
+          if (!active[k]) { *ca = *cb = *ce = *cf = 0.0; continue; }
+          const double tb = j >= 2 ? beta[k] : 0.0, tbn = bnew[k];
+          const double a = alpha[k] + t[q];
+          const double eps = s2[i] * tb, dp = c2[i] * tb;
+          const double delta = c1[i] * dp + s1[i] * a, gbar = -s1[i] * dp + c1[i] * a;
+          const double gamma = std::hypot(gbar, tbn);
+          const double cs = gbar / gamma, sn = tbn / gamma;
+          const double phi = cs * phib[i];
+          phib[i] = -sn * phib[i];
+          *ca = 1.0 / gamma;
+          *cb = -delta / gamma;
+          *ce = -eps / gamma;
+          *cf = w[q] * phi;
+          c2[i] = c1[i]; s2[i] = s1[i]; c1[i] = cs; s1[i] = sn;
+          const double r = std::fabs(phib[i]) / beta1[k];
+          worst = std::isfinite(r) ? std::max(worst, r) : INFINITY;
+        }
+      CUDA_TRY(c, cudaMemcpyAsync(coef, hcoef.data(), (size_t)4 * nq * tp * 8, cudaMemcpyHostToDevice, s));
+      LAUNCH(c, launch_shift_update64(v, dA, dB, yout, coef, nq, n, tp, s));
+      std::swap(dA, dB);   // the new d (written over dB) is d_{j}: next step's d1
+    }
+    for (int k = 0; k < tp; ++k) {
+      if (!active[k]) continue;
+      if (!(bnew[k] > 1e-14 * (std::fabs(alpha[k]) + beta[k]))) active[k] = 0;   // invariant subspace: frozen
+      oldb[k] = beta[k];
+      beta[k] = bnew[k];
+    }
+    if (!lanczos_only && tol > 0 && worst <= tol) break;
+  }
+  *iters = std::min(j, max_iters);
+  *relres = worst;
+  return CIQ_OK;
+}
+
+// Extremes of the pooled Ritz values of the per-column tridiagonals (host Sturm bisection).
+void pooled_ritz(const std::vector<std::vector<double>>& al, const std::vector<std::vector<double>>& be, int cols,
+                 double* rmin, double* rmax) {
+  *rmin = INFINITY;
+  *rmax = -INFINITY;
+  for (int k = 0; k < cols; ++k) {
+    const int m = (int)al[k].size();
+    if (m == 0) continue;
+    double e0 = 0, e1 = 0;
+    if (ciqh::tridiag_extremes(al[k].data(), be[k].data(), m, &e0, &e1) == 0) {
+      *rmin = std::min(*rmin, e0);
+      *rmax = std::max(*rmax, e1);
+    }
+  }
+}
+
+ciq_status apply_nested(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* out, int64_t ldo, ciq_params p,
+                        ciq_info* info) {
+  ciq_status st = ensure_nested(c);
+  if (st != CIQ_OK) return st;
+  NestedDev& Nd = c->nest;
+  const int64_t n = c->op.n;
+  const int tp = round16(T);
+  const int nq = p.Q;
+  cudaStream_t s = c->stream;
+  st = join_user_stream(c);
+  if (st != CIQ_OK) return st;
+  EvTimer ev;
+  CUDA_TRY(c, cudaEventRecord(ev.e[0], s));
+  const size_t vsz = (size_t)n * tp;
+  double *b64 = nullptr, *c0 = nullptr, *yin = nullptr, *yout = nullptr;
+  CUDA_TRY(c, dalloc(&b64, 4 * vsz));
+  c0 = b64 + vsz;
+  yin = c0 + vsz;
+  yout = yin + vsz;
+  struct Freer { double* p; ~Freer() { dfree(p); } } fr{b64};
+  CUDA_TRY(c, cudaMemsetAsync(b64, 0, vsz * 8, s));
+  if (is_device_ptr(B)) {
+    LAUNCH(c, launch_f32_to_f64(B, ldb, n, (int)T, b64, tp, s));
+  } else {
+    st = ensure_staging(c, n * tp);
+    if (st != CIQ_OK) return st;
+    CUDA_TRY(c, cudaMemcpy2DAsync(c->staging, (size_t)tp * 4, B, (size_t)ldb * 4, (size_t)T * 4, (size_t)n,
+                                  cudaMemcpyHostToDevice, s));
+    LAUNCH(c, launch_f32_to_f64(c->staging, tp, n, (int)T, b64, tp, s));
+  }
+  int kmvms = 0, pmvms = 0;
+  auto blockdiag = [&](const double* mats, bool inverse, const double* in, double* outv) -> ciq_status {
+    for (size_t b = 0; b + 1 < Nd.b0.size(); ++b) {
+      const int64_t i0 = Nd.b0[b], m = Nd.b0[b + 1] - i0;
+      const double* a = inverse ? Nd.pinv + i0 * Nd.block : mats + i0 * Nd.ldk + i0;
+      const int64_t lda = inverse ? m : Nd.ldk;
+      LAUNCH(c, launch_gemm64(false, false, m, tp, m, a, lda, in + i0 * tp, tp, nullptr, 0.0, outv + i0 * tp, tp, s));
+    }
+    return CIQ_OK;
+  };
+  PencilOps inner{[&](const double* in, double* o) { ++pmvms; return blockdiag(Nd.k64, false, in, o); },
+                  [&](const double* in, double* o) -> ciq_status {
+                    CUDA_TRY(c, cudaMemcpyAsync(o, in, vsz * 8, cudaMemcpyDeviceToDevice, s));
+                    return CIQ_OK;
+                  }};
+  PencilOps outer{[&](const double* in, double* o) -> ciq_status {
+                    ++kmvms;
+                    LAUNCH(c, launch_mvm64(Nd.k64, Nd.ldk, n, n, in, true, tp, 0, o, true, nullptr, nullptr, s));
+                    return CIQ_OK;
+                  },
+                  [&](const double* in, double* o) { return blockdiag(nullptr, true, in, o); }};
+  const int lz = std::max(12, p.lanczos_iters + 2);
+  std::vector<std::vector<double>> al, be;
+  int it = 0;
+  double rr = 0.0;
+  // (1) c0 = P^{1/2} b by CIQ on P ("run the CIQ algorithm on P"): lambda_min(P) >= sigma^2
+  //     (P = blockdiag(K_kern) + sigma^2 I, reading G6); Q_in = max(Q, 16) so the inner quadrature
+  //     error stays far below the outer one; K-after form (reading G2): P^{1/2} b = P (P^{-1/2} b)
+  st = pmsminres(c, inner, b64, tp, (int)T, 1, nullptr, nullptr, lz, 0.0, nullptr, &it, &rr, true, &al, &be);
+  if (st != CIQ_OK) return st;
+  double pmin = 0, pmax = 0;
+  pooled_ritz(al, be, (int)T, &pmin, &pmax);
+  double plo = 0.99 * pmin, phi_ = 1.01 * pmax;
+  if (c->op.diag > 0) plo = std::min(plo, (double)c->op.diag);
+  const int qin = std::max(nq, 16);
+  double tin[CIQ_MAX_Q], win[CIQ_MAX_Q];
+  if (!(plo > 0) || ciqh::hht_rule(plo, phi_, qin, tin, win) != 0)
+    return set_err(c, CIQ_ERR_ELLIPTIC, "nested CIQ: rule for P failed (lambda [%g, %g])", plo, phi_);
+  const double tol_in = p.tol > 0 ? 0.1 * p.tol : 0.0;
+  int it_in = 0;
+  double rr_in = 0.0;
+  st = pmsminres(c, inner, b64, tp, (int)T, qin, tin, win, p.max_iters, tol_in, yin, &it_in, &rr_in, false, nullptr, nullptr);
+  if (st != CIQ_OK) return st;
+  st = inner.apply_a(yin, c0);
+  if (st != CIQ_OK) return st;
+  CUDA_TRY(c, cudaEventRecord(ev.e[1], s));
+  // (2) the rule for the pencil (K, P): explicit, or Ritz extremes of the P-Lanczos process started
+  //     at c0 (margins of reading G6; no rigorous lower bound for a block-Jacobi P)
+  double t[CIQ_MAX_Q], w[CIQ_MAX_Q], lmin = NAN, lmax = NAN, rmin = NAN, rmax = NAN;
+  int lambda_mvms = 0;
+  if (p.t != nullptr) {
+    for (int q = 0; q < nq; ++q) { t[q] = p.t[q]; w[q] = p.w[q]; }
+  } else {
+    if (p.lambda_min > 0 && p.lambda_max > 0) {
+      lmin = p.lambda_min;
+      lmax = p.lambda_max;
+    } else {
+      const int k0 = kmvms;
+      st = pmsminres(c, outer, c0, tp, (int)T, 1, nullptr, nullptr, lz, 0.0, nullptr, &it, &rr, true, &al, &be);
+      if (st != CIQ_OK) return st;
+      lambda_mvms = kmvms - k0;
+      pooled_ritz(al, be, (int)T, &rmin, &rmax);
+      lmin = 0.99 * rmin;
+      lmax = 1.01 * rmax;
+      // rigorous lower bound (reading G6 for the pencil): lambda_min(P^{-1} K) >= lambda_min(K) /
+      // lambda_max(P) >= sigma^2 / lambda_max(P) -- a few Lanczos steps overestimate lambda_min, and
+      // an overestimated kappa only costs log(kappa)
+      if (c->op.diag > 0) lmin = std::min(lmin, (double)c->op.diag / phi_);
+    }
+    if (!(lmin > 0) || ciqh::hht_rule(lmin, lmax, nq, t, w) != 0)
+      return set_err(c, CIQ_ERR_NOT_PD, "nested CIQ: lambda_min of the pencil estimate %g <= 0", lmin);
+  }
+  CUDA_TRY(c, cudaEventRecord(ev.e[2], s));
+  // (3) sum_q w_q (K + t_q P)^{-1} c0 = R' b  (eq. precond_sqrt_inverse)
+  int J = 0;
+  double relres = 0.0;
+  const int k1 = kmvms;
+  st = pmsminres(c, outer, c0, tp, (int)T, nq, t, w, p.max_iters, p.tol, yout, &J, &relres, false, nullptr, nullptr);
+  if (st != CIQ_OK) return st;
+  const int loop_mvms = kmvms - k1;
+  CUDA_TRY(c, cudaEventRecord(ev.e[3], s));
+  double* res = yout;
+  int final_mvm = 0;
+  if (p.mode == CIQ_MODE_SQRT) {   // R b = K R' b (eq. precond_sqrt)
+    st = outer.apply_a(yout, yin);
+    if (st != CIQ_OK) return st;
+    res = yin;
+    final_mvm = 1;
+  }
+  if (is_device_ptr(out)) {
+    LAUNCH(c, launch_f64_to_f32(res, tp, n, (int)T, out, ldo, s));
+  } else {
+    st = ensure_staging(c, n * tp);
+    if (st != CIQ_OK) return st;
+    LAUNCH(c, launch_f64_to_f32(res, tp, n, (int)T, c->staging, T, s));
+    CUDA_TRY(c, cudaMemcpy2DAsync(out, (size_t)ldo * 4, c->staging, (size_t)T * 4, (size_t)T * 4, (size_t)n,
+                                  cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_TRY(c, cudaEventRecord(ev.e[4], s));
+  CUDA_TRY(c, cudaEventSynchronize(ev.e[4]));
+  const bool converged = std::isfinite(relres) && (p.tol == 0 || relres <= p.tol);
+  if (info) {
+    std::memset(info, 0, sizeof(*info));
+    info->iters = J;
+    info->mvms = lambda_mvms + loop_mvms + final_mvm;   // MVMs with K (the P MVMs of the inner CIQ: nested_p_mvms)
+    info->converged = converged ? 1 : 0;
+    info->rotated = 1;
+    info->Q = nq;
+    info->lambda_min = lmin;
+    info->lambda_max = lmax;
+    info->ritz_min = rmin;
+    info->ritz_max = rmax;
+    info->max_rel_residual = relres;
+    for (int q = 0; q < nq; ++q) { info->t[q] = t[q]; info->w[q] = w[q]; }
+    cudaEventElapsedTime(&info->ms_total, ev.e[0], ev.e[4]);
+    cudaEventElapsedTime(&info->ms_lambda, ev.e[1], ev.e[2]);
+    cudaEventElapsedTime(&info->ms_loop, ev.e[2], ev.e[3]);
+    cudaEventElapsedTime(&info->ms_final, ev.e[3], ev.e[4]);
+    info->mvm_impl_used = CIQ_MVM_SIMT;
+    info->mvm_splits = 1;
+    info->fp64_route = 1;
+    info->nested_p_mvms = pmvms;
+    info->nested_iters = it_in;
   }
   return converged ? CIQ_OK : CIQ_NOT_CONVERGED;
 }

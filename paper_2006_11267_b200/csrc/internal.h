@@ -150,6 +150,16 @@ cudaError_t launch_f32_to_f64(const float* src, int64_t ld, int64_t rows, int co
                               cudaStream_t s);
 cudaError_t launch_f64_to_f32(const double* src, int tp, int64_t rows, int cols, float* dst, int64_t ld,
                               cudaStream_t s);
+// ---- P^{-1}-only preconditioned msMINRES / nested CIQ (precond_nested.cu), fp64, rows x tp ----
+int coldot64_blocks(int64_t rows);
+// part[coldot64_blocks(rows)][tp]: per-block column dot products of a and b
+cudaError_t launch_coldot64(const double* a, const double* b, int64_t rows, int tp, double* part, cudaStream_t s);
+// out = ca[c] x + cb[c] y (y may be null); ca, cb device [tp]
+cudaError_t launch_axpby_cols64(double* out, const double* ca, const double* x, const double* cb, const double* y,
+                                int64_t rows, int tp, cudaStream_t s);
+// d2_q <- ca v + cb d1_q + ce d2_q;  y += cf d2_q   (coef = [ca | cb | ce | cf], each [nq][tp])
+cudaError_t launch_shift_update64(const double* v, double* d1, double* d2, double* y, const double* coef, int nq,
+                                  int64_t rows, int tp, cudaStream_t s);
 // Backward pass: G[i][j] = -1/2 sum_{q,c} w_q (xv[q][i][c] xb[q][j][c] + xb[q][i][c] xv[q][j][c])
 cudaError_t launch_vjp_dense(const float* xb, const float* xv, const double* w, int nq, int64_t n, int tp, int cols,
                              float* g, int64_t ldg, cudaStream_t s);
