@@ -490,6 +490,10 @@ int plane_cols(const ciq_ctx* c, int tp) {
   return use_tc3(c, tp) ? tn / 2 : tn;
 }
 
+// Rows of the split V planes: npad, or the all-gathered height world * per when row-sharded (the
+// ranks all-gather their blocks of the planes in place).
+int64_t vrows(const ciq_ctx* c) { return c->sharded ? std::max(c->npad, c->nfull) : c->npad; }
+
 // Column splits and number of alpha-partial rows of the tensor-core MVM for tp columns.
 void mvm_geometry(const ciq_ctx* c, int tp, int* nsplit, int64_t* nblk) {
   const int64_t rows = c->row1 - c->row0;
@@ -529,7 +533,7 @@ ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
   int nsplit = 1;
   int64_t nblk = 0;
   mvm_geometry(c, tp, &nsplit, &nblk);
-  ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
+  ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * vrows(c) * tp);
   if (st != CIQ_OK) return st;
   if (c->inv_scale_n < tp) {
     ++c->buf_gen;
@@ -585,7 +589,7 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   int nsplit = 1;
   int64_t nblk = 0;
   mvm_geometry(c, tp, &nsplit, &nblk);
-  ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * c->npad * tp);
+  ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * vrows(c) * tp);
   if (st != CIQ_OK) return st;
   if (c->inv_scale_n < tp) {
     ++c->buf_gen;
@@ -607,11 +611,12 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   }
   // (skip_pack: the previous streaming pass already wrote v's split planes and inv_scale)
   if (!skip_pack)
-    LAUNCH(c, launch_pack_v(v, c->op.n, c->npad, tp, plane_cols(c, tp), nrm, c->planes, c->inv_scale, c->stream));
+    LAUNCH(c, launch_pack_v(v, c->op.n, vrows(c), tp, plane_cols(c, tp), nrm, c->planes, c->inv_scale, c->stream));
   TcArgs a{};
   a.kind = c->op.kind + (c->deriv ? 10 : 0);   // 11-13: dK/dl (ciq_hyper_grad; KIND templates 4-6)
   a.n = c->op.n;
   a.npad = c->npad;
+  a.vrows = vrows(c);
   a.row0 = c->row0;
   a.row1 = c->row1;
   a.tp = tp;
@@ -808,6 +813,21 @@ ciq_status allgather_rows(ciq_ctx* c, float* full, int tp) {
   const size_t bytes = (size_t)c->per * tp * 4;
   if (!c->comm->allgather(full + (size_t)c->rank * c->per * tp, full, bytes, c->stream))
     return set_err(c, CIQ_ERR_NCCL, "allgather: %s", c->comm->error());
+  return CIQ_OK;
+}
+
+// The split-fp16 V planes of this rank's rows to every rank: per layout chunk and plane (hi, lo)
+// the rows [rank * per, (rank + 1) * per) are one contiguous run of per * tn halves.
+ciq_status allgather_planes(ciq_ctx* c, int tp) {
+  if (!c->sharded) return CIQ_OK;
+  const int tn = plane_cols(c, tp);
+  const int64_t vr = vrows(c);
+  for (int ch = 0; ch < tp / tn; ++ch)
+    for (int pl = 0; pl < 2; ++pl) {
+      __half* base = c->planes + ((size_t)ch * 2 + pl) * vr * tn;
+      if (!c->comm->allgather(base + (size_t)c->rank * c->per * tn, base, (size_t)c->per * tn * 2, c->stream))
+        return set_err(c, CIQ_ERR_NCCL, "allgather (planes): %s", c->comm->error());
+    }
   return CIQ_OK;
 }
 
@@ -1922,11 +1942,13 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   // single GPU, tensor-core MVM: the streaming pass of iteration j writes W_{j+1}'s split-fp16
   // planes (scale from nrm_j), so no iteration packs; W_1's planes are written here, outside the
   // captured graph (graph replays and direct launches then run identical kernels)
-  const bool fuse_pack = !c->sharded && !P.on && use_tc(c, p.mvm_impl, tp) && !experiment_env("CIQ_NO_FUSED_PACK");
+  // (row-sharded: each rank packs its own rows and the ranks all-gather the planes instead of
+  // the fp32 block -- the same bytes, already in the MVM's operand layout)
+  const bool fuse_pack = !P.on && use_tc(c, p.mvm_impl, tp) && !experiment_env("CIQ_NO_FUSED_PACK");
   if (fuse_pack) {
     st = prepare_mvm_buffers(c, tp, p.mvm_impl);
     if (st != CIQ_OK) return st;
-    LAUNCH(c, launch_pack_v(ws.w[1], c->op.n, c->npad, tp, plane_cols(c, tp), sc.nrm_cur, c->planes, c->inv_scale, s));
+    LAUNCH(c, launch_pack_v(ws.w[1], c->op.n, vrows(c), tp, plane_cols(c, tp), sc.nrm_cur, c->planes, c->inv_scale, s));
   }
   auto enqueue_iter = [&](int j, int nqe) -> ciq_status {
     float* wcur = ws.w[j % 3];
@@ -1958,8 +1980,8 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     begin_timed(c, j, 1);
     LAUNCH(c, launch_lanczos_update(sc, pin, nsplit, (size_t)rows * tp, wcur + c->row0 * tp, wprev + c->row0 * tp,
                                     wnew + c->row0 * tp, &d1, &d2, ws.y, nqe, rows, tp, ws.bpart, 0, s,
-                                    fuse_pack ? c->planes : nullptr, c->inv_scale, c->npad, plane_cols(c, tp), c->op.n,
-                                    xqk));
+                                    fuse_pack ? c->planes : nullptr, c->inv_scale, vrows(c), plane_cols(c, tp), c->op.n,
+                                    xqk, c->row0));
     end_timed(c);
     if (!c->sharded) {
       LAUNCH(c, launch_givens(sc, ws.bpart, update_blocks(rows), nqe, tp, s));
@@ -1968,7 +1990,9 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
       st2 = global_sum(c, tsum_b, tp);
       if (st2 != CIQ_OK) return st2;
       LAUNCH(c, launch_givens(sc, tsum_b, 1, nqe, tp, s));
-      st2 = allgather_rows(c, wnew, tp);   // next Lanczos block to every rank
+      // next Lanczos block to every rank: its split-fp16 planes when the streaming
+      // pass packed them, else the fp32 rows
+      st2 = fuse_pack ? allgather_planes(c, tp) : allgather_rows(c, wnew, tp);
       if (st2 != CIQ_OK) return st2;
     }
     return CIQ_OK;

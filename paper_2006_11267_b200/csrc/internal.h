@@ -64,6 +64,7 @@ cudaError_t launch_spmm(const OpDev& op, const float* v, int tp, int64_t row0, i
 struct TcArgs {
   int kind;
   int64_t n, npad, row0, row1;
+  int64_t vrows;             // rows of the split V planes (npad; >= the all-gathered height when sharded)
   int tp, nsplit;
   int nunits, chunks;        // units = row tiles x splits x chunks (round-robin over persistent CTAs)
   int kf;                    // feature contraction (32, or 64 for d > 8: pair kernel only)
@@ -129,7 +130,8 @@ cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, si
                                   int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s,
                                   __half* planes = nullptr, float* inv_scale = nullptr, int64_t npad = 0, int tn = 0,
                                   int64_t n = 0,    // planes: also write W_{j+1}'s split-fp16 MVM operand
-                                  float* xq = nullptr);   // [Q][rows][tp]: also accumulate x_q += phi_q d_q
+                                  float* xq = nullptr,    // [Q][rows][tp]: also accumulate x_q += phi_q d_q
+                                  int64_t plane_row0 = 0);   // planes: global row of local row 0 (sharded)
 // fp64 route (preconditioned path, precond64.cu): the same streaming pass on fp64 vectors (no
 // fused packing, no kept solutions); p may be nsplit = 1 only.
 cudaError_t launch_lanczos_update64(const Scal& sc, const double* p, const double* wcur, const double* wprev,

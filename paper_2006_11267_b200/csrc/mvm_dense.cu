@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(D_THREADS, 1) mvm_dense2_kernel(TcArgs args) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nkt = (int)(args.npad / DK);
   const size_t kplane = (size_t)args.kplane_elems;
-  const size_t vplane = (size_t)args.npad * TN;
+  const size_t vplane = (size_t)args.vrows * TN;
   auto unit_geom = [&](int u, int& rt, int& split, int& chunk, int& kt0, int& nk) {
     chunk = u % args.chunks;
     const int t = u / args.chunks;

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
   __syncthreads();
   fence_after_sync();
   const uint32_t tbase = bars->tmem_base;
-  const size_t plane = (size_t)args.npad * TN;   // one plane of one chunk
+  const size_t plane = (size_t)args.vrows * TN;   // one plane of one chunk
 
   if (warp == 0) {
     // ---------------- producer (one thread) ----------------

@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(NT3, 1) mvm_tc3_kernel(TcArgs args) {
   cluster_sync();   // barriers of both CTAs initialised, TMEM allocated in both
   fence_after_sync();
   const uint32_t tbase = bars->tmem_base;
-  const size_t plane = (size_t)args.npad * TH;   // one plane of one TH-wide layout chunk
+  const size_t plane = (size_t)args.vrows * TH;   // one plane of one TH-wide layout chunk
 
   // tiles of this pair
   int ntot = 0, nunit = 0;

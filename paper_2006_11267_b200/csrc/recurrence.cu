@@ -249,9 +249,10 @@ __global__ void sum_ranks_kernel(const double* __restrict__ g, int world, int m,
 struct PackOut {
   __half* planes;      // null: no packing
   float* inv_scale;
-  int64_t npad;
+  int64_t npad;        // plane rows
   int tn;
   double sqrt_n;
+  int64_t row0;        // global row of local row 0 (row-sharded: each rank packs its rows)
 };
 
 CIQ_DEVICE float pack_scale(double nrm, double sqrt_n, float* inv) {
@@ -355,7 +356,8 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? CIQ_UPD_MINB : 2) l
           }
           const int chunk = c / pk.tn, cl = c % pk.tn;
           const size_t plane = (size_t)pk.npad * pk.tn;
-          const size_t po = (size_t)chunk * 2 * plane + ((size_t)((i / 8) * (pk.tn / 8) + cl / 8) * 64 + (i % 8) * 8 + cl % 8);
+          const int64_t ig = i + pk.row0;
+          const size_t po = (size_t)chunk * 2 * plane + ((size_t)((ig / 8) * (pk.tn / 8) + cl / 8) * 64 + (ig % 8) * 8 + cl % 8);
           *reinterpret_cast<uint2*>(pk.planes + po) = make_uint2(hw[0], hw[1]);
           *reinterpret_cast<uint2*>(pk.planes + po + plane) = make_uint2(lw[0], lw[1]);
         }
@@ -749,9 +751,10 @@ cudaError_t launch_alpha(const Scal& sc, const double* apart, int nblk, int tp, 
 cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, size_t split_stride, const float* wcur, const float* wprev,
                                   float* wnew, float* const* d1, float* const* d2, float* y, int nq,
                                   int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s,
-                                  __half* planes, float* inv_scale, int64_t npad, int tn, int64_t n, float* xq) {
+                                  __half* planes, float* inv_scale, int64_t npad, int tn, int64_t n, float* xq,
+                                  int64_t plane_row0) {
   const int64_t qstride = rows * tp;
-  PackOut pk{planes, inv_scale, npad, tn, sqrt((double)n)};
+  PackOut pk{planes, inv_scale, npad, tn, sqrt((double)n), plane_row0};
   dim3 grid = stream_grid(rows, tp);
   grid.x = (unsigned)update_blocks(rows);
   lanczos_update_kernel<float><<<grid, kThreads, 0, s>>>(sc, p, nsplit, split_stride, wcur, wprev, wnew, d1[0], d2[0],
@@ -762,7 +765,7 @@ cudaError_t launch_lanczos_update64(const Scal& sc, const double* p, const doubl
                                     double* wnew, double* const* d1, double* const* d2, double* y, int nq,
                                     int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s) {
   const int64_t qstride = rows * tp;
-  PackOut pk{nullptr, nullptr, 0, 0, 1.0};
+  PackOut pk{nullptr, nullptr, 0, 0, 1.0, 0};
   dim3 grid = stream_grid(rows, tp);
   grid.x = (unsigned)update_blocks64(rows);
   lanczos_update_kernel<double><<<grid, kThreads, 0, s>>>(sc, p, 1, 0, wcur, wprev, wnew, d1[0], d2[0], qstride, y, nq,
