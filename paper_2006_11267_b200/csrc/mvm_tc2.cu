@@ -164,12 +164,63 @@ CIQ_DEVICE float kern(float s) {
   return (1.f + a) * ex2_approx(-1.4426950408889634f * a);
 }
 
+// Matern forms for a pair of entries with packed fp32x2 arithmetic (FMUL2 / FFMA2: half the
+// FMA-pipe instructions of kern<>, whose epilogue is issue-bound); the
+// constants are folded so that sqrt gives a = sqrt(c) r directly: a^2 = -(2 ln2 c) s.
+CIQ_DEVICE uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+CIQ_DEVICE void upk2(uint64_t v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+CIQ_DEVICE uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+CIQ_DEVICE uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+template <int KIND>
+CIQ_DEVICE void kern_pair(float s0, float s1, float& k0, float& k1) {
+  // KIND 2: a = sqrt5 r, k = (1 + a + a^2/3) e^{-a};  KIND 3: a = sqrt3 r, k = (1 + a) e^{-a}
+  constexpr float c2ln2 = KIND == 2 ? -6.931471805599453f : -4.1588830833596715f;   // -(2 ln2) * 5 or * 3
+  const uint64_t x = mul2(pk2(s0, s1), pk2(c2ln2, c2ln2));
+  float x0, x1;
+  upk2(x, x0, x1);
+  float a0, a1;
+  // |x|: S can be a rounding-level negative at r ~ 0, where sqrt(|x|) ~ 0 is the right value and
+  // the absolute value is a free operand modifier of MUFU.SQRT (no FMNMX)
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(a0) : "f"(fabsf(x0)));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(a1) : "f"(fabsf(x1)));
+  const uint64_t a = pk2(a0, a1);
+  const uint64_t e = mul2(a, pk2(-1.4426950408889634f, -1.4426950408889634f));
+  float e0, e1;
+  upk2(e, e0, e1);
+  e0 = ex2_approx(e0);
+  e1 = ex2_approx(e1);
+  uint64_t poly;
+  if (KIND == 2) poly = fma2(a, fma2(a, pk2(1.f / 3.f, 1.f / 3.f), pk2(1.f, 1.f)), pk2(1.f, 1.f));
+  else poly = fma2(a, pk2(1.f, 1.f), pk2(1.f, 1.f));
+  upk2(mul2(poly, pk2(e0, e1)), k0, k1);
+}
+
 template <int KIND, bool MASK>
 CIQ_DEVICE void exp_split(const uint32_t (&sv)[32], uint32_t (&hi)[16], uint32_t (&lo)[16], int jvalid) {
 #pragma unroll
   for (int c = 0; c < 32; c += 2) {
-    float k0 = kern<KIND>(__uint_as_float(sv[c]));
-    float k1 = kern<KIND>(__uint_as_float(sv[c + 1]));
+    float k0, k1;
+#ifndef CIQ_NO_PAIR_MATERN
+    if (KIND == 2 || KIND == 3) {
+      kern_pair<KIND>(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1]), k0, k1);
+    } else
+#endif
+    {
+      k0 = kern<KIND>(__uint_as_float(sv[c]));
+      k1 = kern<KIND>(__uint_as_float(sv[c + 1]));
+    }
     if (MASK) {
       k0 = (c < jvalid) ? k0 : 0.f;
       k1 = (c + 1 < jvalid) ? k1 : 0.f;
