@@ -100,7 +100,9 @@ typedef struct {
   int64_t nnz;                /*   ctx keeps a device copy).  The matrix must be symmetric.       */
 } ciq_operator;
 
-/* Preconditioner P = L L^T + sigma2 I, L = N x rank row-major (ld >= rank).  When L comes
+/* Preconditioner P = L L^T + sigma2 I, L = N x rank row-major (ld >= rank; with row
+ * sharding: this rank's row block of L, like B -- the matrix-free route then all-reduces the
+ * rank x T products L^T W / U^T W per application).  When L comes
  * from a partial pivoted Cholesky of the kernel part of K and sigma2 = op.diag, lambda_min of
  * P^{-1/2} K P^{-1/2} is >= 1 (reading G6) and the estimator uses that bound. */
 typedef struct {

@@ -842,8 +842,6 @@ ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, 
   const int64_t nf = c->nfull;                 // basis vectors are full height (row-sharded work)
   const int64_t rows = c->row1 - c->row0;
   const int64_t r0 = c->row0;
-  if (c->sharded && c->pc.on)
-    return set_err(c, CIQ_ERR_INVALID_ARG, "preconditioner with row sharding: not supported");
   LambdaWork& lw = c->lw;
   if (lw.tpl != tpl || lw.nb < J + 1 || lw.rows != rows) {
     free_lambda(lw);
@@ -891,14 +889,17 @@ ciq_status estimate_lambda(ciq_ctx* c, const ciq_params* p, double lower_bound, 
     if (c->fp64_active) {   // fp64 route: Lanczos on the materialised M (fp32 basis)
       LAUNCH(c, launch_mvm64(c->pc.m64, c->pc.ldm, rows, n, vj, false, tpl, r0, lw.p, false, nullptr, nullptr, s));
     } else if (c->pc.on) {
-      // Lanczos on M = P^{-1/2} K P^{-1/2} (App. A: the rule must cover the spectrum of M)
+      // Lanczos on M = P^{-1/2} K P^{-1/2} (App. A: the rule must cover the spectrum of M);
+      // row-sharded: P^{-1/2} on this rank's rows, the result all-gathered for the K MVM
       PrecondDev& P = c->pc;
-      ciq_status gs = grow(c, &P.t1, &P.t_cap, (size_t)2 * n * tpl);
+      ciq_status gs = grow(c, &P.t1, &P.t_cap, (size_t)2 * nf * tpl);
       if (gs != CIQ_OK) return gs;
-      float* t2 = P.t1 + (size_t)n * tpl;
-      if (precond_power(c, PW_MHALF, vj, tpl, n, P.t1, nullptr) != CIQ_OK) return CIQ_ERR_CUDA;
+      float* t2 = P.t1 + (size_t)nf * tpl;
+      if (precond_power(c, PW_MHALF, vj + r0 * tpl, tpl, rows, P.t1 + r0 * tpl, nullptr) != CIQ_OK) return CIQ_ERR_CUDA;
+      gs = allgather_rows(c, P.t1, tpl);
+      if (gs != CIQ_OK) return gs;
       if (run_mvm(c, P.t1, tpl, t2, nullptr, nullptr, p->mvm_impl) != CIQ_OK) return CIQ_ERR_CUDA;
-      if (precond_power(c, PW_MHALF, t2, tpl, n, lw.p, nullptr) != CIQ_OK) return CIQ_ERR_CUDA;
+      if (precond_power(c, PW_MHALF, t2, tpl, rows, lw.p, nullptr) != CIQ_OK) return CIQ_ERR_CUDA;
     } else if (run_mvm(c, vj, tpl, lw.p, nullptr, nullptr, p->mvm_impl) != CIQ_OK) {
       return CIQ_ERR_CUDA;
     }
@@ -973,6 +974,8 @@ ciq_status precond_power(ciq_ctx* c, int which, const float* v, int tp, int64_t 
   if (st != CIQ_OK) return st;
   LAUNCH(c, launch_utv(P.u, P.r2, P.r2, v, tp, rows, ns, P.part, c->stream));
   LAUNCH(c, launch_reduce_cols(P.part, ns, P.r2 * tp, P.h, 0, c->stream));
+  st = global_sum(c, P.h, P.r2 * tp);   // U^T v over all ranks' rows (the L^T W sum of SURVEY §8(e))
+  if (st != CIQ_OK) return st;
   LAUNCH(c, launch_uapply(P.u, P.r2, P.r2, P.g[which], P.h, v, P.a[which], tp, rows, out, dotv,
                           dotv ? P.bpart : nullptr, c->stream));
   return CIQ_OK;
@@ -981,11 +984,13 @@ ciq_status precond_power(ciq_ctx* c, int which, const float* v, int tp, int64_t 
 // Build U, the gains and scalars from L (device, n x rank) and sigma2 (App. A).
 ciq_status build_precond(ciq_ctx* c) {
   PrecondDev& P = c->pc;
-  const int64_t n = c->op.n;
+  const int64_t n = c->row1 - c->row0;   // this rank's rows of L (all N on one GPU)
   const int r = P.rank;
   double* gram_d = nullptr;
   CUDA_TRY(c, dalloc(&gram_d, (size_t)r * r));
   LAUNCH(c, launch_gram(P.l, r, r, n, gram_d, c->stream));
+  ciq_status gs = global_sum(c, gram_d, r * r);   // L^T L = sum over the ranks' row blocks
+  if (gs != CIQ_OK) return gs;
   std::vector<double> gram((size_t)r * r), w(r), vec((size_t)r * r);
   CUDA_TRY(c, cudaMemcpyAsync(gram.data(), gram_d, gram.size() * 8, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -1309,7 +1314,6 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     if (comm->rank < 0 || comm->rank >= comm->world) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "bad rank");
     if (!comm->loopback_group && !comm->nccl_unique_id)
       return set_err(nullptr, CIQ_ERR_INVALID_ARG, "row sharding needs an NCCL unique id or a loopback group");
-    if (pc) return set_err(nullptr, CIQ_ERR_INVALID_ARG, "preconditioner with row sharding: not supported yet");
   }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -1426,9 +1430,11 @@ ciq_status ciq_init(ciq_ctx** out, const ciq_operator* op, const ciq_precond* pc
     P.rank = (int)pc->rank;
     P.sigma2 = pc->sigma2;
     P.matrix_free = pc->matrix_free != 0;
-    if (cudaMalloc(&P.l, (size_t)op->n * P.rank * 4) != cudaSuccess) { st = CIQ_ERR_OOM; goto fail; }
+    // L: this rank's row block [row0, row1) (all N rows on one GPU), like B
+    const int64_t lrows = c->row1 - c->row0;
+    if (cudaMalloc(&P.l, (size_t)lrows * P.rank * 4) != cudaSuccess) { st = CIQ_ERR_OOM; goto fail; }
     const cudaMemcpyKind kind = is_device_ptr(pc->L) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if (cudaMemcpy2D(P.l, (size_t)P.rank * 4, pc->L, (size_t)pc->ldl * 4, (size_t)P.rank * 4, (size_t)op->n, kind) !=
+    if (cudaMemcpy2D(P.l, (size_t)P.rank * 4, pc->L, (size_t)pc->ldl * 4, (size_t)P.rank * 4, (size_t)lrows, kind) !=
         cudaSuccess) { st = CIQ_ERR_CUDA; goto fail; }
     st = build_precond(c);
     if (st != CIQ_OK) {
@@ -1881,7 +1887,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     st = grow(c, &P.part, &P.part_cap, (size_t)utv_splits(rows) * P.r2 * tp);
     if (st == CIQ_OK) st = grow(c, &P.h, &P.h_cap, (size_t)P.r2 * tp);
     if (st == CIQ_OK) st = grow(c, &P.bpart, &P.bpart_cap, (size_t)uapply_blocks(rows) * tp);
-    if (st == CIQ_OK) st = grow(c, &P.t1, &P.t_cap, (size_t)2 * n * tp);
+    if (st == CIQ_OK) st = grow(c, &P.t1, &P.t_cap, (size_t)2 * c->nfull * tp);
     if (st != CIQ_OK) return st;
   }
 
@@ -1927,13 +1933,24 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   // partials of v.out (the alpha partials); the column norms of P^{-1/2} v (needed by the split-
   // fp16 packing) come from the same streaming pass.
   auto apply_m = [&](const float* v, float* out, double** apart, int* nbm) -> ciq_status {
-    ciq_status st2 = precond_power(c, PW_MHALF, v, tp, rows, P.t1, P.t1);
+    // v: full-height Lanczos block (this rank's rows valid); t1 = P^{-1/2} v on this rank's rows,
+    // all-gathered for the K MVM; out (local rows) = P^{-1/2} K t1 with the alpha partials of out.v
+    const float* vl = v + c->row0 * tp;
+    float* t1l = P.t1 + c->row0 * tp;
+    ciq_status st2 = precond_power(c, PW_MHALF, vl, tp, rows, t1l, t1l);
     if (st2 != CIQ_OK) return st2;
-    LAUNCH(c, launch_reduce_cols(P.bpart, uapply_blocks(rows), tp, ws.colsq, 1, s));
-    float* t2 = P.t1 + (size_t)n * tp;   // second half of the t1 allocation (2 n tp)
+    LAUNCH(c, launch_reduce_cols(P.bpart, uapply_blocks(rows), tp, ws.colsq, c->sharded ? 0 : 1, s));
+    if (c->sharded) {   // column norms of the full t1 (the MVM operand's pack scale) and the block
+      st2 = global_sum(c, ws.colsq, tp);
+      if (st2 != CIQ_OK) return st2;
+      LAUNCH(c, launch_sqrt_inplace(ws.colsq, tp, s));
+      st2 = allgather_rows(c, P.t1, tp);
+      if (st2 != CIQ_OK) return st2;
+    }
+    float* t2 = P.t1 + (size_t)c->nfull * tp;   // second half of the t1 allocation (2 nfull tp)
     st2 = run_mvm(c, P.t1, tp, t2, nullptr, nullptr, p.mvm_impl, ws.colsq);
     if (st2 != CIQ_OK) return st2;
-    st2 = precond_power(c, PW_MHALF, t2, tp, rows, out, v);
+    st2 = precond_power(c, PW_MHALF, t2, tp, rows, out, vl);
     if (st2 != CIQ_OK) return st2;
     *apart = P.bpart;
     *nbm = uapply_blocks(rows);

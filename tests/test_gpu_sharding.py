@@ -21,7 +21,7 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
 
 
-def run_sharded(cfg, inp, world, **kw):
+def run_sharded(cfg, inp, world, lfac=None, **kw):
     group = pb.LoopbackGroup(world)
     outs, infos, errs = [None] * world, [None] * world, []
 
@@ -29,8 +29,10 @@ def run_sharded(cfg, inp, world, **kw):
         try:
             torch.cuda.set_device(0)
             b0, b1 = pb.ciq_shard_rows(cfg.n, r, world)
+            extra = {} if lfac is None else dict(precond_L=dev(lfac[b0:b1]), precond_sigma2=cfg.sigma2,
+                                                   precond_matrix_free=True)
             g = pb.CIQ(cfg.kind, n=cfg.n, X=dev(inp["X"]), lengthscale=cfg.lengthscale, outputscale=cfg.outputscale,
-                       diag=cfg.sigma2, comm=(r, world, group))
+                       diag=cfg.sigma2, comm=(r, world, group), **extra)
             out = torch.empty((b1 - b0, cfg.t), device="cuda")
             s_rows = inp["S"][b0:b1]
             infos[r] = g.apply(dev(inp["B"][b0:b1]), out, lanczos_start=dev(s_rows), **kw)
@@ -122,3 +124,27 @@ def test_nccl_one_rank_sharded_path(dense):
     (a, ia), (b, ib) = outs
     assert ia["converged"] and ib["converged"] and abs(ia["iters"] - ib["iters"]) <= 2
     assert np.linalg.norm(a - b) / np.linalg.norm(a) < 1e-5
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("mode", ["whiten", "sqrt"])
+def test_sharded_preconditioned_equals_single_gpu(world, mode):
+    """Row sharding of the preconditioned variant (matrix-free route): each rank
+    holds its rows of L; U = L W S^{-1} from the rank-summed L^T L, and every P^{-1/2} application
+    sums U^T W over the ranks.  Same result as one GPU up to reduction order."""
+    from oracle import pivoted_cholesky
+    cfg = workloads.scaled(workloads.CONFIGS["C4"], n=1400, t=8)
+    cfg = workloads.scaled(cfg, sigma2=0.05)
+    inp = workloads.config_inputs(cfg)
+    lfac = pivoted_cholesky(KernelOperator(inp["X"], cfg.kind, cfg.lengthscale, cfg.outputscale, cfg.sigma2), 48)
+    kw = dict(q=8, max_iters=400, tol=1e-6, mode=mode, lanczos_start=None)
+    kw.pop("lanczos_start")
+    with pb.CIQ(cfg.kind, X=dev(inp["X"]), lengthscale=cfg.lengthscale, outputscale=cfg.outputscale,
+                diag=cfg.sigma2, precond_L=dev(lfac), precond_sigma2=cfg.sigma2, precond_matrix_free=True) as g:
+        out = torch.empty((cfg.n, cfg.t), device="cuda")
+        info1 = g.apply(dev(inp["B"]), out, lanczos_start=dev(inp["S"]), **kw)
+        ref = out.cpu().numpy().astype(np.float64)
+    got, infos = run_sharded(cfg, inp, world, lfac=lfac, **kw)
+    assert info1["rotated"] and all(i["rotated"] for i in infos)
+    assert abs(infos[0]["iters"] - info1["iters"]) <= 2
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-5
