@@ -234,7 +234,7 @@ def run_ours(args, cfg):
         g = pb.CIQ(cfg.kind, n=cfg.n, X=x, lengthscale=cfg.lengthscale, outputscale=cfg.outputscale,
                    diag=cfg.sigma2, comm=comm)
     kw = dict(q=cfg.q, max_iters=cfg.max_iters, tol=cfg.tol, mode=cfg.mode, lanczos_start=s, mvm_impl=args.mvm,
-              lanczos_reuse=args.lanczos == "reuse")
+              lanczos_reuse=args.lanczos == "reuse", stored_basis=args.recurrence == "stored")
     stream = torch.cuda.current_stream()
 
     for _ in range(args.warmup):
@@ -349,10 +349,14 @@ def run_ours(args, cfg):
     roof["ms_per_launch"] = mvm_ms
     roof["share_of_step"] = pinfo["ms_mvm"] / max(1e-9, pinfo["ms_total"])
     q = cfg.q
-    rec_bytes = (3 * q + 7) * rows_local * tcols * 4.0
+    # algorithmic bytes of one streaming pass: streaming = 2Q direction reads + Q writes, W_cur, W_prev,
+    # P read, W_new and its split planes written, Y read + written (3Q + 7 vectors); stored basis =
+    # the Lanczos step only (P, W_cur, W_prev read; W_new and its planes written: 5 vectors)
+    nvec = 5 if args.recurrence == "stored" else 3 * q + 7
+    rec_bytes = nvec * rows_local * tcols * 4.0
     recurrence = {"bound": "hbm", "achieved": rec_bytes / (upd_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
                   "unit": "GB/s", "kernel": "lanczos_update_kernel", "ms_per_launch": upd_ms,
-                  "algorithmic_bytes": rec_bytes}
+                  "algorithmic_bytes": rec_bytes, "vectors": nvec}
     recurrence["frac"] = recurrence["achieved"] / recurrence["peak"]
 
     line = {"metric": METRIC, "value": value, "unit": "RHS/s", "n_gpus": world, "steps": args.steps,
@@ -363,6 +367,7 @@ def run_ours(args, cfg):
                        "J": infos[-1]["iters"],
                        "mvms_per_step": infos[-1]["mvms"], "mvm_impl": impl_used,
                        "parallelism": (f"rows{world}" if sharded else f"replicas{world}") if world > 1 else "single",
+                       "recurrence": args.recurrence,
                        "l2": "flushed between steps (256 MiB write)",
                        "converged": infos[-1]["converged"], "max_rel_residual": infos[-1]["max_rel_residual"],
                        "lambda": [infos[-1]["lambda_min"], infos[-1]["lambda_max"]],
@@ -595,6 +600,9 @@ def main():
     ap.add_argument("--lanczos", default="reuse", choices=["reuse", "separate"],
                     help="lambda estimate from the solve's first 12 Lanczos steps (reuse, App. D: Lanczos started "
                          "at b) or from a separate 10-step run on a seeded start block (separate)")
+    ap.add_argument("--recurrence", default="stored", choices=["streaming", "stored"],
+                    help="streaming: the fused msMINRES update of all Q shifts per iteration (O(QNT) memory); "
+                         "stored: Lanczos basis kept, Y formed once at the end (O(JNT) memory, SURVEY f4(iii))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--parallelism", default="rows", choices=["rows", "replicas"])
     args = ap.parse_args()

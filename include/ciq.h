@@ -180,6 +180,11 @@ typedef struct {
                               /*    with P = I).  ~30x slower than the tensor-core path; removes   */
                               /*    the fp32 floor kappa(K) * ~1e-7 of the default. */
                               /*    lanczos_reuse / keep_shift_solutions are ignored.  Default 0.  */
+  int32_t stored_basis;       /* 1: keep the Lanczos basis W_1..W_J (O(J N T) memory, falls back  */
+                              /*    to the streaming recurrence if it does not fit) and form        */
+                              /*    Y = W_J z once at the end: ~5 vectors of HBM      */
+                              /*    traffic per iteration instead of 3Q + 6.  Not  */
+                              /*    with a preconditioner or keep_shift_solutions.  Default 0.     */
 } ciq_params;
 
 typedef struct {

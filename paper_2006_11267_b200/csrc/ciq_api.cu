@@ -144,6 +144,12 @@ struct ciq_ctx {
   float* xs = nullptr;        // owned scaled points
   double* xs64 = nullptr;     // owned scaled points in fp64 (exact quotients of the fp32 inputs)
   float* kcopy = nullptr;     // owned dense copy (host-provided K)
+  float* basis = nullptr;     // stored-basis variant: W_1 .. W_{J_max+1}, this rank's rows
+  size_t basis_elems = 0;
+  double* bhist = nullptr;    // stored-basis scalars [4][J_max + 1][tp] + nrm_1 / frozen_0 [2][tp]
+  size_t bhist_elems = 0;
+  float* bcoef = nullptr;     // combination coefficients [J][tp]
+  size_t bcoef_elems = 0;
   int64_t* csr_rp = nullptr;  // owned device copy of the sparse operator's local CSR block
   int32_t* csr_ci = nullptr;
   float* csr_cv = nullptr;
@@ -1205,6 +1211,67 @@ ciq_status run_iterations(ciq_ctx* c, const ciq_params& p, int j0, uint64_t key_
   return CIQ_OK;
 }
 
+// Stored-basis variant: per column, the MINRES solution of each shifted system in the Lanczos basis,
+// y_q = R_q^{-1} phi_q with R_q the Givens-QR factor of [T_J + t_q I; beta_{J+1} e_J^T] (the same
+// recurrences as givens_kernel, fp64 on the host), z = sum_q w_q y_q, and Y = sum_j (z_j / nrm_j) W_j.
+ciq_status combine_stored_basis(ciq_ctx* c, int J, int hlen, int tp, int cols, int nq, const double* t, const double* w,
+                                int64_t rows, float* y) {
+  cudaStream_t s = c->stream;
+  std::vector<double> h((size_t)4 * hlen * tp + 2 * (size_t)tp);
+  CUDA_TRY(c, cudaMemcpyAsync(h.data(), c->bhist, h.size() * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  const double* ha = h.data();
+  const double* hb = ha + (size_t)hlen * tp;
+  const double* hn = hb + (size_t)hlen * tp;
+  const double* hf = hn + (size_t)hlen * tp;
+  const double* n0 = hf + (size_t)hlen * tp;
+  const double* f0 = n0 + tp;
+  std::vector<float> coef((size_t)J * tp, 0.f);
+  std::vector<double> g(J), dl(J + 1), ep(J + 2), ph(J), yq(J + 2), z(J);
+  for (int k = 0; k < cols; ++k) {
+    if (f0[k] != 0.0) continue;   // zero column: Y = 0
+    int m = 0;                    // steps taken before the column froze (its breakdown step included)
+    while (m < J && (m == 0 || hf[(size_t)(m - 1) * tp + k] == 0.0)) ++m;
+    std::fill(z.begin(), z.end(), 0.0);
+    for (int q = 0; q < nq; ++q) {
+      double c1 = 1, s1 = 0, c2 = 1, s2 = 0, phib = n0[k];
+      for (int i = 0; i < m; ++i) {
+        const double a = ha[(size_t)i * tp + k] + t[q];
+        const double tb = i >= 1 ? hb[(size_t)(i - 1) * tp + k] : 0.0;   // beta_{i+1} of T (1-based: beta_i)
+        const double tbn = hb[(size_t)i * tp + k];
+        const double eps = s2 * tb, dp = c2 * tb;
+        const double delta = c1 * dp + s1 * a, gbar = -s1 * dp + c1 * a;
+        const double gamma = std::hypot(gbar, tbn);
+        const double cs = gbar / gamma, sn = tbn / gamma;
+        g[i] = gamma;
+        dl[i] = delta;
+        ep[i] = eps;
+        ph[i] = cs * phib;
+        phib = -sn * phib;
+        c2 = c1; s2 = s1; c1 = cs; s1 = sn;
+      }
+      // back substitution R y = phi: R column i holds (eps_i, delta_i, gamma_i) at rows i-2, i-1, i
+      yq[m] = yq[m + 1] = 0.0;
+      for (int i = m - 1; i >= 0; --i) {
+        double r = ph[i];
+        if (i + 1 < m) r -= dl[i + 1] * yq[i + 1];
+        if (i + 2 < m) r -= ep[i + 2] * yq[i + 2];
+        yq[i] = r / g[i];
+      }
+      for (int i = 0; i < m; ++i) z[i] += w[q] * yq[i];
+    }
+    for (int i = 0; i < m; ++i) {
+      const double nrm = i == 0 ? n0[k] : hn[(size_t)(i - 1) * tp + k];
+      coef[(size_t)i * tp + k] = (float)(z[i] / nrm);
+    }
+  }
+  CUDA_TRY(c, grow(c, &c->bcoef, &c->bcoef_elems, coef.size()) == CIQ_OK ? cudaSuccess : cudaErrorMemoryAllocation);
+  CUDA_TRY(c, cudaMemcpyAsync(c->bcoef, coef.data(), coef.size() * 4, cudaMemcpyHostToDevice, s));
+  LAUNCH(c, launch_combine_basis(c->basis, (size_t)rows * tp, J, c->bcoef, rows * tp, tp, y, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));   // coef (host vector) must outlive the copy
+  return CIQ_OK;
+}
+
 ciq_status apply_fp64(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* out, int64_t ldo, ciq_params p,
                       ciq_info* info);
 ciq_status apply_nested(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* out, int64_t ldo, ciq_params p,
@@ -1228,6 +1295,7 @@ void ciq_params_default(ciq_params* p) {
   p->poll_every = 6;
   p->breakdown_tol = 1e-6;
   p->fp64 = 0;
+  p->stored_basis = 0;
 }
 
 #ifndef CIQ_SOURCE_HASH
@@ -1468,6 +1536,9 @@ void ciq_free(ciq_ctx* c) {
   dfree(c->nest.pinv);
   dfree(c->nest.work);
   dfree(c->kcopy);
+  dfree(c->basis);
+  dfree(c->bhist);
+  dfree(c->bcoef);
   dfree(c->csr_rp);
   dfree(c->csr_ci);
   dfree(c->csr_cv);
@@ -1868,6 +1939,19 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     CUDA_TRY(c, cudaMemsetAsync(ws.xq, 0, (size_t)nq * rows * tp * 4, s));
   }
   float* xqk = keep ? ws.xq : nullptr;
+  // stored-basis variant: the loop runs the Lanczos step and
+  // the shifted Givens scalars only (stopping rule unchanged), keeping W_1 .. W_J; Y = sum_j coef_j
+  // W_j at the end from the per-shift MINRES on T_J (host, fp64).  ~5 vectors of HBM traffic per
+  // iteration instead of 3Q + 6, O(J N T) memory (Property 1's O(Q N T) traded away).
+  const int hlen = p.max_iters + 1;
+  bool stored = p.stored_basis != 0 && !c->pc.on && !keep;
+  if (stored) {
+    if (grow(c, &c->basis, &c->basis_elems, (size_t)hlen * rows * tp) != CIQ_OK ||
+        grow(c, &c->bhist, &c->bhist_elems, (size_t)4 * hlen * tp + 2 * (size_t)tp) != CIQ_OK) {
+      c->err.clear();   // does not fit: the streaming recurrence
+      stored = false;
+    }
+  }
   CUDA_TRY(c, cudaMemsetAsync(ws.d, 0, (size_t)2 * nq * rows * tp * 4, s));
   Ctrl hctrl{};
   hctrl.max_iters = p.max_iters;
@@ -1996,7 +2080,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     float* d2 = dslot[(j + 1) & 1];
     begin_timed(c, j, 1);
     LAUNCH(c, launch_lanczos_update(sc, pin, nsplit, (size_t)rows * tp, wcur + c->row0 * tp, wprev + c->row0 * tp,
-                                    wnew + c->row0 * tp, &d1, &d2, ws.y, nqe, rows, tp, ws.bpart, 0, s,
+                                    wnew + c->row0 * tp, &d1, &d2, ws.y, stored ? 0 : nqe, rows, tp, ws.bpart, 0, s,
                                     fuse_pack ? c->planes : nullptr, c->inv_scale, vrows(c), plane_cols(c, tp), c->op.n,
                                     xqk, c->row0));
     end_timed(c);
@@ -2012,8 +2096,16 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
       st2 = fuse_pack ? allgather_planes(c, tp) : allgather_rows(c, wnew, tp);
       if (st2 != CIQ_OK) return st2;
     }
+    if (stored)
+      LAUNCH(c, launch_store_basis(wnew + c->row0 * tp, c->basis, (size_t)rows * tp, rows * tp, sc, c->bhist, tp, hlen, s));
     return CIQ_OK;
   };
+  if (stored) {   // slot 0: W_1 (= b), and nrm_1 / the columns frozen before step 1
+    CUDA_TRY(c, cudaMemcpyAsync(c->basis, ws.w[1] + c->row0 * tp, (size_t)rows * tp * 4, cudaMemcpyDeviceToDevice, s));
+    double* h0 = c->bhist + (size_t)4 * hlen * tp;
+    CUDA_TRY(c, cudaMemcpyAsync(h0, sc.nrm_cur, (size_t)tp * 8, cudaMemcpyDeviceToDevice, s));
+    LAUNCH(c, launch_int_to_double(sc.frozen, tp, h0 + tp, s));
+  }
   int j0 = 0;   // iterations already done (lanczos_reuse warm-up)
   if (reuse) {
     // Warm-up: kReuse plain Lanczos steps of the solve (no shifts yet: nq_eff = 0, no stopping),
@@ -2093,7 +2185,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
       CUDA_TRY(c, cudaMemcpyAsync(sc.tb_cur, hT + o, tp * 8, cudaMemcpyDeviceToDevice, s));
       CUDA_TRY(c, cudaMemcpyAsync(sc.frozen, hF + o, tp * 4, cudaMemcpyDeviceToDevice, s));
       LAUNCH(c, launch_givens(sc, hQ + o, 1, nq, tp, s));
-      if (k < R) {   // step R's update stays pending for iteration R + 1
+      if (k < R && !stored) {   // step R's update stays pending for iteration R + 1
         float* d1 = dslot[(k + 1) & 1];
         float* d2 = dslot[k & 1];
         float* wk = c->stash + (size_t)(k - 1) * wsz;
@@ -2108,7 +2200,8 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   st = prepare_mvm_buffers(c, tp, p.mvm_impl);   // every buffer the MVM may (re)allocate, before any capture
   if (st != CIQ_OK) return st;
   bool replayed = false;
-  st = run_iterations(c, p, j0, (uint64_t)p.mvm_impl ^ ((uint64_t)(uintptr_t)xqk << 1), enqueue_iter, &hc, &replayed);
+  st = run_iterations(c, p, j0, (uint64_t)p.mvm_impl ^ ((uint64_t)(uintptr_t)xqk << 1) ^ (stored ? 0x10000ull : 0ull),
+                      enqueue_iter, &hc, &replayed);
   if (st != CIQ_OK) return st;
   if (replayed) {   // cached graph: the MVM kind / splits are those of the capture
     loop_impl = c->tc_ok && p.mvm_impl != CIQ_MVM_SIMT ? 2 : 1;
@@ -2117,8 +2210,12 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     c->last_nsplit = loop_nsplit;
   }
   const int J = hc.iters;
+  if (stored && J >= 1) {
+    ciq_status sb = combine_stored_basis(c, J, hlen, tp, (int)T, nq, t, w, rows, ws.y);
+    if (sb != CIQ_OK) return sb;
+  }
   // last pending update (step J): v_J lives in the buffer that was W_cur at iteration J
-  if (J >= 1) {
+  if (J >= 1 && !stored) {
     float* d1 = dslot[(J + 1) & 1];  // d_{J-1}
     float* d2 = dslot[J & 1];        // d_{J-2}, overwritten by d_J
     float* wv = ws.w[J % 3];

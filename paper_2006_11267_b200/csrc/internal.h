@@ -152,6 +152,13 @@ cudaError_t launch_f32_to_f64(const float* src, int64_t ld, int64_t rows, int co
                               cudaStream_t s);
 cudaError_t launch_f64_to_f32(const double* src, int tp, int64_t rows, int cols, float* dst, int64_t ld,
                               cudaStream_t s);
+// ---- stored-basis variant (recurrence.cu) ----
+// basis slot ctrl->iters <- w (elems floats); history [4][hlen][tp]: alpha_j, beta_{j+1}, nrm_{j+1}, frozen
+cudaError_t launch_store_basis(const float* w, float* basis, size_t stride, int64_t elems, const Scal& sc, double* hist,
+                               int tp, int hlen, cudaStream_t s);
+cudaError_t launch_int_to_double(const int* a, int m, double* out, cudaStream_t s);
+cudaError_t launch_combine_basis(const float* basis, size_t stride, int nb, const float* coef, int64_t elems, int tp,
+                                 float* y, cudaStream_t s);
 // ---- P^{-1}-only preconditioned msMINRES / nested CIQ (precond_nested.cu), fp64, rows x tp ----
 int coldot64_blocks(int64_t rows);
 // part[coldot64_blocks(rows)][tp]: per-block column dot products of a and b

@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? CIQ_UPD_MINB : 2) l
           *reinterpret_cast<uint2*>(pk.planes + po + plane) = make_uint2(lw[0], lw[1]);
         }
       }
-      if (pending) {
+      if (pending && nq > 0) {
         Vec4<T> yy = ld4<T>(y + off);
         for (int q0 = 0; q0 < nq; q0 += QB) {
           Vec4<T> x1[QB], x2[QB];
@@ -784,6 +784,63 @@ cudaError_t launch_sum_ranks(const double* g, int world, int m, double* out, cud
   sum_ranks_kernel<<<nb_elem(m, 256), 256, 0, s>>>(g, world, m, out);
   return cudaGetLastError();
 }
+// Stored-basis variant (x_J = Q_J y_J with the Lanczos basis
+// kept): after step j's givens (ctrl->iters = j) W_{j+1} (this rank's rows) goes to basis slot j
+// and the step's scalars alpha_j, beta_{j+1}, nrm_{j+1}, frozen to the history at index j - 1.
+// Reads the slot from ctrl, so a captured block of iterations replays correctly.
+__global__ void store_basis_kernel(const float* __restrict__ w, float* __restrict__ basis, size_t stride, int64_t elems,
+                                   Scal sc, double* __restrict__ hist, int tp, int hlen) {
+  const Ctrl* ctrl = sc.ctrl;
+  const int j = ctrl->iters;
+  if (j < 1 || j >= hlen) return;   // (past convergence the slot of step J is rewritten: unused)
+  float* dst = basis + (size_t)j * stride;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = w[e];
+  if (blockIdx.x == 0) {
+    double* ha = hist;                         // [hlen][tp] alpha_j
+    double* hb = ha + (size_t)hlen * tp;       // beta_{j+1}
+    double* hn = hb + (size_t)hlen * tp;       // nrm_{j+1}
+    double* hf = hn + (size_t)hlen * tp;       // frozen after step j
+    for (int c = threadIdx.x; c < tp; c += blockDim.x) {
+      const size_t o = (size_t)(j - 1) * tp + c;
+      ha[o] = sc.alpha[c];
+      hb[o] = sc.tb_cur[c];
+      hn[o] = sc.nrm_cur[c];
+      hf[o] = (double)sc.frozen[c];
+    }
+  }
+}
+
+// Y[i][c] = sum_{k < nb} coef[k][c] basis_k[i][c]  (the stored-basis solution, fp32 accumulate in
+// step order like the streaming Y += w phi d)
+__global__ void combine_basis_kernel(const float* __restrict__ basis, size_t stride, int nb, const float* __restrict__ coef,
+                                     int64_t elems, int tp, float* __restrict__ y) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % tp);
+    float acc = 0.f;
+    for (int k = 0; k < nb; ++k) acc = fmaf(coef[(size_t)k * tp + c], basis[(size_t)k * stride + e], acc);
+    y[e] = acc;
+  }
+}
+
+__global__ void int_to_double_kernel(const int* __restrict__ a, int m, double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) out[i] = (double)a[i];
+}
+cudaError_t launch_int_to_double(const int* a, int m, double* out, cudaStream_t s) {
+  int_to_double_kernel<<<(m + 255) / 256, 256, 0, s>>>(a, m, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_store_basis(const float* w, float* basis, size_t stride, int64_t elems, const Scal& sc, double* hist,
+                               int tp, int hlen, cudaStream_t s) {
+  store_basis_kernel<<<592, 256, 0, s>>>(w, basis, stride, elems, sc, hist, tp, hlen);
+  return cudaGetLastError();
+}
+cudaError_t launch_combine_basis(const float* basis, size_t stride, int nb, const float* coef, int64_t elems, int tp,
+                                 float* y, cudaStream_t s) {
+  combine_basis_kernel<<<1184, 256, 0, s>>>(basis, stride, nb, coef, elems, tp, y);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s) {
   givens_kernel<<<tp, 256, 0, s>>>(sc, bpart, nblk, nq, tp, sc.col_rel, sc.col_state);
   return cudaGetLastError();

@@ -357,3 +357,30 @@ def test_vjp_matches_oracle():
     assert relerr(got, ref) < 1e-4
     np.testing.assert_allclose(got, got.T, rtol=0, atol=1e-6 * np.abs(got).max())
     np.testing.assert_array_equal(ghost, gmat.cpu().numpy())
+
+
+# ------------------------------------------------------------------------------------------------
+# stored-basis variant: Y = W_J z from the kept Lanczos basis
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name,n,t,mode,reuse", [("C3", 2111, 21, "sqrt", False), ("C3", 1500, 64, "invsqrt", True),
+                                                 ("C2", 2048, 32, "whiten", False), ("C5", 3000, 16, "sqrt", True)])
+def test_stored_basis_equals_streaming_and_oracle(name, n, t, mode, reuse):
+    cfg = workloads.scaled(workloads.CONFIGS[name], n=n, t=t)
+    inp = workloads.config_inputs(cfg)
+    op = oracle_op(cfg, inp)
+    lmin, lmax, _, _ = estimate_spectrum(op.mvm, inp["S"], 10, lower_bound=cfg.sigma2)
+    rule = hht_rule(lmin, lmax, cfg.q)
+    conv = ciq(op, inp["B"].astype(np.float64), q=cfg.q, max_iters=2000, tol=1e-8, mode=mode, rule=rule)
+    outs = []
+    with gpu_ctx(cfg, inp) as g:
+        for stored in (False, True):
+            out = torch.empty((cfg.n, cfg.t), device="cuda")
+            kw = dict(lanczos_start=dev(inp["S"]), lanczos_reuse=True) if reuse else dict(rule=rule)
+            info = g.apply(dev(inp["B"]), out, q=cfg.q, max_iters=400, tol=1e-6, mode=mode, stored_basis=stored, **kw)
+            outs.append((out.cpu().numpy().astype(np.float64), info))
+    (a, ia), (b, ib) = outs
+    assert ia["converged"] and ib["converged"] and ia["iters"] == ib["iters"]
+    assert relerr(b, a) < 2e-6             # same Krylov iterate, combined from the basis
+    if not reuse:
+        assert relerr(b, conv.out) < 1e-4
