@@ -77,7 +77,11 @@ typedef enum {
 typedef enum {
   CIQ_MVM_AUTO = 0,      /* tensor-core path where implemented, else SIMT fp32                  */
   CIQ_MVM_SIMT = 1,      /* fp32 CUDA-core tiles (reference kernel)                             */
-  CIQ_MVM_TC = 2         /* tcgen05 split-fp16 tensor-core kernel (fails if unavailable)        */
+  CIQ_MVM_TC = 2,        /* tcgen05 split-fp16 tensor-core kernel, full tiles (fails if unavailable) */
+  CIQ_MVM_TC_SYM = 3     /* tcgen05 symmetric-tile kernel: each k(x_i, x_j), i < j, evaluated once
+                            and applied to both rows (single GPU, RBF / Matern, d <= 8, RHS chunk of
+                            16 or 32 columns; fails if unavailable).  CIQ_MVM_AUTO picks it where
+                            DESIGN.md section 8 measures it faster (RHS chunk of 16)              */
 } ciq_mvm_impl;
 
 /* The operator K (touched only through MVMs, P:397 / P:1161-1162). */

@@ -18,8 +18,8 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libciq.so")
 
-SOURCES = ["host_math.cpp", "nccl_dl.cpp", "comm.cpp", "mvm_simt.cu", "mvm_sparse.cu", "mvm_dense.cu", "mvm_tc2.cu", "mvm_tc3.cu", "recurrence.cu", "precond.cu", "precond64.cu", "precond_nested.cu", "posterior.cu", "ciq_api.cu"]
-HEADERS = ["common.cuh", "nccl_dl.h", "comm.h", "internal.h", "host_math.h", "tc_util.cuh"]
+SOURCES = ["host_math.cpp", "nccl_dl.cpp", "comm.cpp", "mvm_simt.cu", "mvm_sparse.cu", "mvm_dense.cu", "mvm_tc2.cu", "mvm_tc3.cu", "mvm_sym.cu", "recurrence.cu", "precond.cu", "precond64.cu", "precond_nested.cu", "posterior.cu", "ciq_api.cu"]
+HEADERS = ["common.cuh", "nccl_dl.h", "comm.h", "internal.h", "host_math.h", "tc_util.cuh", "kern_epi.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"] + ARCH
 # CIQ_TC_TRACE=1: compile the K1 per-tile clock stamps (experiments; see mvm_tc2.cu)

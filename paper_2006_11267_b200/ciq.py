@@ -37,7 +37,7 @@ OP_KINDS = {"dense": 0, "rbf": 1, "matern52": 2, "matern32": 3, "sparse": 4}
 # ciq_mode
 MODES = {"sqrt": 0, "invsqrt": 1, "whiten": 2}
 # ciq_mvm_impl
-MVM_IMPLS = {"auto": 0, "simt": 1, "tc": 2}
+MVM_IMPLS = {"auto": 0, "simt": 1, "tc": 2, "sym": 3}
 
 
 class CiqOperator(ctypes.Structure):
@@ -86,7 +86,7 @@ class CiqInfo(ctypes.Structure):
                 "ms_lambda": self.ms_lambda, "ms_loop": self.ms_loop, "ms_final": self.ms_final,
                 "kernel_launches": self.kernel_launches, "ms_mvm": self.ms_mvm, "mvm_timed": self.mvm_timed,
                 "ms_update": self.ms_update, "update_timed": self.update_timed,
-                "mvm_impl_used": {1: "simt", 2: "tc"}.get(self.mvm_impl_used, "none"), "mvm_splits": self.mvm_splits,
+                "mvm_impl_used": {1: "simt", 2: "tc", 3: "sym"}.get(self.mvm_impl_used, "none"), "mvm_splits": self.mvm_splits,
                 "fp64_route": bool(self.fp64_route), "nested_p_mvms": self.nested_p_mvms,
                 "nested_iters": self.nested_iters}
 

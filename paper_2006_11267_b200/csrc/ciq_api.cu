@@ -185,7 +185,15 @@ struct ciq_ctx {
   double* apart_tc = nullptr;
   size_t apart_tc_elems = 0;
   int last_nsplit = 1;
-  int mvm_kind_used = 0;      // 1 simt, 2 tc (of the last loop MVM)
+  int mvm_kind_used = 0;      // 1 simt, 2 tc, 3 symmetric-tile tc (of the last loop MVM)
+  int last_kind = 0;          // mvm_kind_used of the captured iteration graph
+  // symmetric-tile MVM (mvm_sym.cu): unit table, partial-slot prefix sums, fp32 partial products
+  int2* sym_units = nullptr;
+  int* sym_base = nullptr;
+  float* sym_part = nullptr;
+  size_t sym_part_elems = 0;
+  int64_t sym_n = -1;
+  int sym_tn = 0, sym_nb = 0, sym_ng = 0, sym_slots = 0, sym_nunits = 0;
   // CUDA graph of `poll_every` msMINRES iterations (period-6 buffer rotation => replayable)
   uint64_t buf_gen = 0;       // bumped on every device re-allocation (invalidates the graph)
   cudaGraphExec_t gexec = nullptr;
@@ -496,18 +504,64 @@ int plane_cols(const ciq_ctx* c, int tp) {
   return use_tc3(c, tp) ? tn / 2 : tn;
 }
 
+// The symmetric-tile MVM (mvm_sym.cu): every k(x_i, x_j), i < j, evaluated once
+// and applied to rows i and j.  Single GPU (it needs the whole square), RBF / Matern with d <= 8,
+// RHS chunks of 16 or 32 columns.  CIQ_MVM_AUTO takes it for 16-column chunks, where the MVM is
+// epilogue-bound with little tensor work per kernel value (C5 and T <= 16).
+constexpr int64_t kSymMinN = 1024;
+bool use_sym(const ciq_ctx* c, int impl, int tp) {
+  if (impl != CIQ_MVM_AUTO && impl != CIQ_MVM_TC_SYM) return false;
+  if (!c->tc_ok || c->sharded || c->deriv || c->kf != 32 || !is_kernel_op(c)) return false;
+  if (c->op.n < kSymMinN || c->row0 != 0 || c->row1 != c->op.n || use_mat(c, tp)) return false;
+  const int tn = tc_chunk_cols(tp);
+  if (!sym_supported(tn)) return false;
+  if (impl == CIQ_MVM_AUTO && (tn != 16 || experiment_env("CIQ_NO_SYM"))) return false;
+  return true;
+}
+
+// Unit table, slot prefix sums and partial buffer of the symmetric-tile MVM for tp columns
+// (uploaded once per N / chunk width; grown before any graph capture).
+ciq_status ensure_sym(ciq_ctx* c, int tp) {
+  const int tn = tc_chunk_cols(tp);
+  if (c->sym_n != c->op.n || c->sym_tn != tn) {
+    std::vector<int2> units;
+    std::vector<int> base;
+    int ng = 0, slots = 0;
+    sym_geometry(c->op.n, tn, &units, &base, &ng, &slots);
+    ++c->buf_gen;
+    dfree(c->sym_units);
+    dfree(c->sym_base);
+    c->sym_units = nullptr;
+    c->sym_base = nullptr;
+    CUDA_TRY(c, dalloc(&c->sym_units, units.size()));
+    CUDA_TRY(c, dalloc(&c->sym_base, base.size()));
+    CUDA_TRY(c, cudaMemcpy(c->sym_units, units.data(), units.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaMemcpy(c->sym_base, base.data(), base.size() * sizeof(int), cudaMemcpyHostToDevice));
+    c->sym_n = c->op.n;
+    c->sym_tn = tn;
+    c->sym_nb = (int)base.size() - 1;
+    c->sym_ng = ng;
+    c->sym_slots = slots;
+    c->sym_nunits = (int)units.size();
+  }
+  return grow(c, &c->sym_part, &c->sym_part_elems, (size_t)(tp / tn) * c->sym_slots * 128 * tn);
+}
+
 // Rows of the split V planes: npad, or the all-gathered height world * per when row-sharded (the
 // ranks all-gather their blocks of the planes in place).
 int64_t vrows(const ciq_ctx* c) { return c->sharded ? std::max(c->npad, c->nfull) : c->npad; }
 
 // Column splits and number of alpha-partial rows of the tensor-core MVM for tp columns.
-void mvm_geometry(const ciq_ctx* c, int tp, int* nsplit, int64_t* nblk) {
+void mvm_geometry(const ciq_ctx* c, int tp, int impl, int* nsplit, int64_t* nblk) {
   const int64_t rows = c->row1 - c->row0;
   const int chunks = tp / tc_chunk_cols(tp);
   const int nsm = sm_count();
   if (c->op.kind == CIQ_OP_DENSE || use_mat(c, tp)) {
     *nsplit = choose_nsplit_dense(rows, c->npad, chunks, nsm);
     *nblk = (rows + 127) / 128 * *nsplit * 4;
+  } else if (use_sym(c, impl, tp)) {
+    *nsplit = 1;
+    *nblk = (rows + 127) / 128;
   } else {
     // the pair kernel (mvm_tc3.cu) balances units over nsm / 2 pairs, the one-CTA kernel over nsm CTAs
     const bool pair = use_tc3(c, tp);
@@ -535,10 +589,14 @@ ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
     ciq_status sm = ensure_mat_planes(c);
     if (sm != CIQ_OK) return sm;
   }
+  if (use_sym(c, impl, tp)) {
+    ciq_status ss = ensure_sym(c, tp);
+    if (ss != CIQ_OK) return ss;
+  }
   const int64_t rows = c->row1 - c->row0;
   int nsplit = 1;
   int64_t nblk = 0;
-  mvm_geometry(c, tp, &nsplit, &nblk);
+  mvm_geometry(c, tp, impl, &nsplit, &nblk);
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * vrows(c) * tp);
   if (st != CIQ_OK) return st;
   if (c->inv_scale_n < tp) {
@@ -592,9 +650,17 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     if (sm != CIQ_OK) return sm;
   }
   const bool dense = c->op.kind == CIQ_OP_DENSE || mat;
+  const bool sym = !dense && use_sym(c, impl, tp);
+  if (impl == CIQ_MVM_TC_SYM && !sym)
+    return set_err(c, CIQ_ERR_INVALID_ARG,
+                   "symmetric-tile MVM unavailable (needs one GPU, RBF / Matern, d <= 8, N >= 1024, RHS chunk 16 or 32)");
+  if (sym) {
+    ciq_status ss = ensure_sym(c, tp);
+    if (ss != CIQ_OK) return ss;
+  }
   int nsplit = 1;
   int64_t nblk = 0;
-  mvm_geometry(c, tp, &nsplit, &nblk);
+  mvm_geometry(c, tp, impl, &nsplit, &nblk);
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * vrows(c) * tp);
   if (st != CIQ_OK) return st;
   if (c->inv_scale_n < tp) {
@@ -653,7 +719,18 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     cudaMemset(a.dbg_clk, 0, 32 * 256 * sizeof(long long));
   }
 #endif
+  if (sym) {
+    a.nunits = c->sym_nunits * chunks;
+    a.sym_units = c->sym_units;
+    a.sym_base = c->sym_base;
+    a.sym_part = c->sym_part;
+    a.sym_nb = c->sym_nb;
+    a.sym_ng = c->sym_ng;
+    a.sym_b = sym_group_blocks(tn);
+    a.sym_slots = c->sym_slots;
+  }
   if (dense) LAUNCH(c, launch_mvm_dense2(a, nsm, c->stream));
+  else if (sym) LAUNCH(c, launch_mvm_sym(a, nsm, c->stream));
   else if (pair) LAUNCH(c, launch_mvm_tc3(a, nsm, c->stream));
   else LAUNCH(c, launch_mvm_tc2(a, nsm, c->stream));
 #ifdef CIQ_TC_TRACE
@@ -680,7 +757,7 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   if (nsplit_out) *nsplit_out = nsplit;
   if (apart_used) *apart_used = ap;
   if (apart_nblk) *apart_nblk = (int)nblk;
-  c->mvm_kind_used = 2;
+  c->mvm_kind_used = sym ? 3 : 2;
   return CIQ_OK;
 }
 
@@ -1548,6 +1625,7 @@ void ciq_free(ciq_ctx* c) {
   dfree(c->stash); dfree(c->hist);
   dfree(c->vjp_xb); dfree(c->vjp_xv); dfree(c->vjp_y); dfree(c->vjp_g); dfree(c->vjp_w);
   dfree(c->apart_tc);
+  dfree(c->sym_units); dfree(c->sym_base); dfree(c->sym_part);
   free_precond(c->pc);
   free_post(c->post);
   dfree(c->gsum);
@@ -2204,10 +2282,11 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
                       enqueue_iter, &hc, &replayed);
   if (st != CIQ_OK) return st;
   if (replayed) {   // cached graph: the MVM kind / splits are those of the capture
-    loop_impl = c->tc_ok && p.mvm_impl != CIQ_MVM_SIMT ? 2 : 1;
+    loop_impl = c->last_kind;
     loop_nsplit = c->last_nsplit;
   } else {
     c->last_nsplit = loop_nsplit;
+    c->last_kind = loop_impl;
   }
   const int J = hc.iters;
   if (stored && J >= 1) {

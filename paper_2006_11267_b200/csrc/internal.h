@@ -5,6 +5,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace ciq {
@@ -83,6 +85,11 @@ struct TcArgs {
   float kscale_inv;          // dense path: 1 / global K scale
   int dbg;                   // experiments only (-DCIQ_TC_TRACE, env CIQ_TC_DEBUG): 1 skip KV, 2 skip exp
   long long* dbg_clk;        // experiments only: per-tile clock stamps of CTA 0
+  // symmetric-tile kernel (mvm_sym.cu)
+  const int2* sym_units;     // [nunits / chunks] (column group G, row range k), largest first
+  const int* sym_base;       // [sym_nb + 1] first partial slot of each 128-row block
+  float* sym_part;           // [chunks][sym_slots][128][TN] fp32 partial products
+  int sym_nb, sym_ng, sym_b, sym_slots;
 };
 int tc_chunk_cols(int tp);
 // tn: column width of one layout chunk (tc_chunk_cols(tp), halved for the pair kernel)
@@ -98,6 +105,12 @@ bool tc3_supported(int tn, int64_t n, int nsplit);
 int tc3_min_tiles();
 int tc3_units(int64_t rows, int nsplit, int chunks);
 cudaError_t launch_mvm_tc3(const TcArgs& a, int nsm, cudaStream_t s);
+// symmetric-tile matrix-free kernel (mvm_sym.cu, f4(ii)): single GPU, KF = 32, TN = 16 / 32;
+// writes the complete P and alpha partials [sym_nb][tp]
+bool sym_supported(int tn);
+int sym_group_blocks(int tn);
+void sym_geometry(int64_t n, int tn, std::vector<int2>* units, std::vector<int>* base, int* ng, int* slots);
+cudaError_t launch_mvm_sym(const TcArgs& a, int nsm, cudaStream_t s);
 // persistent dense kernel (mvm_dense.cu): alpha partials [units/chunks * 4][tp]
 cudaError_t launch_mvm_dense2(const TcArgs& a, int nsm, cudaStream_t s);
 cudaError_t launch_absmax(const float* k, int64_t ldk, int64_t rows, int64_t n, unsigned int* out, cudaStream_t s);
