@@ -318,6 +318,27 @@ def run_ours(args, cfg):
         roof = {"bound": "alu", "achieved": flops / (mvm_ms * 1e-3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
                 "kernel": "mvm_simt_kernel (fp32 FFMA)",
                 "peak_source": f"{sm_count} SMs x 128 FP32 lanes x 2 x {peaks.get('sm_max_mhz', 1965.0)} MHz"}
+    elif impl_used == "sym":
+        # symmetric-tile kernel (mvm_sym.cu, f4(ii)): nb (nb + 1) / 2 tiles of 128 x 128 kernel values, each
+        # evaluated once (sqrt + ex2 on the SFU for Matern, ex2 for RBF) and applied to both block rows;
+        # the SFU is the roof
+        sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+        nb = -(-n // 128)
+        tiles, off = nb * (nb + 1) // 2, nb * (nb - 1) // 2
+        mufu_per_eval = 1 if cfg.kind == "rbf" else 2
+        evals = tiles * 128.0 * 128.0
+        sfu_peak = sm_count * 16 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12   # MUFU Top/s
+        tpad = -(-tcols // 16) * 16
+        exec_flops = 2.0 * 128 * 128 * (tiles * (32 + 3 * tpad) + off * 3 * tpad)
+        roof = {"bound": "alu", "achieved": evals * mufu_per_eval / (mvm_ms * 1e-3) / 1e12, "peak": sfu_peak,
+                "unit": "Top/s (MUFU)",
+                "kernel": "mvm_sym_kernel (symmetric tiles: each k(x_i,x_j), i<j, evaluated once; tcgen05 forward + "
+                          "transposed split-fp16 products) + sym_reduce_kernel",
+                "peak_source": f"{sm_count} SMs x 16 MUFU/clk x sm_max_mhz {peaks.get('sm_max_mhz', 1965.0)} (derived)",
+                "note": f"achieved = {mufu_per_eval} MUFU op(s) per evaluated kernel value x nb(nb+1)/2 x 128^2 values per MVM",
+                "useful_tflops": flops / (mvm_ms * 1e-3) / 1e12,
+                "executed_tflops": exec_flops / (mvm_ms * 1e-3) / 1e12,
+                "kernel_evals_per_mvm": evals}
     else:
         peak = peaks["bf16_tflops_sustained"]
         # executed tensor work of mvm_tc2_kernel: per (256-row unit row) x (64-column tile) entry the
@@ -342,6 +363,8 @@ def run_ours(args, cfg):
     # dram bytes per launch from one `ncu --set full` capture of the same kernel at this config
     # (profiles/ncu_metrics.json, written by scripts/ncu_metrics.py from the capture it names)
     key = {"hbm": "mvm_dense2_kernel", "tensor": "mvm_tc2_kernel"}.get(roof["bound"])
+    if impl_used == "sym":
+        key = "mvm_sym_kernel"
     ncu = ncu_metrics().get(f"{key}/{cfg.name}") if key else None
     roof["traffic"] = ncu["dram_bytes"] if ncu else None
     if ncu:

@@ -507,15 +507,25 @@ int plane_cols(const ciq_ctx* c, int tp) {
 // The symmetric-tile MVM (mvm_sym.cu): every k(x_i, x_j), i < j, evaluated once
 // and applied to rows i and j.  Single GPU (it needs the whole square), RBF / Matern with d <= 8,
 // RHS chunks of 16 or 32 columns.  CIQ_MVM_AUTO takes it for 16-column chunks, where the MVM is
-// epilogue-bound with little tensor work per kernel value (C5 and T <= 16).
+// epilogue-bound with little tensor work per kernel value (C5 and T <= 16),
+// and only where the full-tile kernel's TMEM accumulation chains are at least as long as the
+// symmetric kernel's (<= 384 MMAs): the tensor core accumulates with a round-toward-zero bias of
+// ~1.1e-8 per MMA, so at small N, where mvm_tc2.cu splits the columns into
+// short chains, the full-tile kernel is the more accurate one (and the MVM is cheap either way).
 constexpr int64_t kSymMinN = 1024;
+constexpr int64_t kSymChainMmas = 384;   // mvm_sym.cu: A_ROWS = 16 tiles x 24 MMAs
 bool use_sym(const ciq_ctx* c, int impl, int tp) {
   if (impl != CIQ_MVM_AUTO && impl != CIQ_MVM_TC_SYM) return false;
   if (!c->tc_ok || c->sharded || c->deriv || c->kf != 32 || !is_kernel_op(c)) return false;
   if (c->op.n < kSymMinN || c->row0 != 0 || c->row1 != c->op.n || use_mat(c, tp)) return false;
   const int tn = tc_chunk_cols(tp);
   if (!sym_supported(tn)) return false;
-  if (impl == CIQ_MVM_AUTO && (tn != 16 || experiment_env("CIQ_NO_SYM"))) return false;
+  if (impl == CIQ_MVM_AUTO) {
+    if (tn != 16 || experiment_env("CIQ_NO_SYM")) return false;
+    const int64_t ntiles = (c->op.n + 63) / 64;
+    const int nsplit = tc2_choose_nsplit(c->op.n, c->op.n, tp / tn, sm_count());
+    if ((ntiles + nsplit - 1) / nsplit * 12 < kSymChainMmas) return false;
+  }
   return true;
 }
 

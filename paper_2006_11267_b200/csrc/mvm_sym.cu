@@ -46,6 +46,9 @@ constexpr int KFS = 32;       // feature contraction (d <= 8)
 constexpr int NTS = 640;      // 4 role warps + 16 epilogue warps
 constexpr int EPI0S = 4;
 constexpr int A_ROWS = 16;    // row blocks per unit
+#ifndef CIQ_SYM_SLEEP
+#define CIQ_SYM_SLEEP 64
+#endif
 
 template <int TN>
 struct CfgS {
@@ -70,6 +73,13 @@ struct CfgS {
 static_assert(CfgS<16>::TM_T + CfgS<16>::B * 16 <= 512, "TMEM budget");
 static_assert(CfgS<32>::TM_T + CfgS<32>::B * 32 <= 512, "TMEM budget");
 static_assert(CfgS<16>::SMEM <= 227 * 1024 && CfgS<32>::SMEM <= 227 * 1024, "shared memory budget");
+
+// Waits of the MMA issuers on the epilogue (k_full): most of their time; polled with a short
+// sleep so they do not take issue slots from the epilogue warps of their sub-partitions
+// (measured: C3-shaped, 16 RHS 0.786 -> 0.757 ms; C5 unchanged).
+CIQ_DEVICE void wait_issuer(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(CIQ_SYM_SLEEP);
+}
 
 struct BarsS {
   uint64_t full[3], empty[3];          // ring
@@ -284,7 +294,7 @@ __global__ void __launch_bounds__(NTS, 1) mvm_sym_kernel(TcArgs args) {
     for (int i = 0; i < C::NB && s.valid(args); ++i) issue_s();
     for (int g = 0; kv.valid(args); ++g) {
       const int kbuf = g % C::NB;
-      mbar_wait(&bars->k_full[kbuf], (g / C::NB) & 1);
+      wait_issuer(&bars->k_full[kbuf], (g / C::NB) & 1);
       const int fb = kv.rowseq & 1;
       const bool first = kv.row_first(), last = kv.row_last();
       if (first) mbar_wait(&bars->o_empty[fb], ((kv.rowseq >> 1) & 1) ^ 1);
@@ -312,7 +322,7 @@ __global__ void __launch_bounds__(NTS, 1) mvm_sym_kernel(TcArgs args) {
     t.start(args);
     uint32_t tused = 0, tpar = 0;
     for (int g = 0; t.valid(args); ++g) {
-      mbar_wait(&bars->k_full[g % C::NB], (g / C::NB) & 1);
+      wait_issuer(&bars->k_full[g % C::NB], (g / C::NB) & 1);
       const int rb = t.rowseq & 1;
       if (t.row_first()) mbar_wait(&bars->rfull[rb], (t.rowseq >> 1) & 1);
       const bool tv = t.tv(), tl = t.t_last(), rl = t.row_last();

@@ -36,8 +36,8 @@ for key, rep in zip(args[0::2], args[1::2]):
     m = raw(rep)
     data[key] = {"dram_bytes": num(m, "dram__bytes_read.sum") + num(m, "dram__bytes_write.sum"),
                  "tensor_pipe_active": num(m, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
-                 "duration_us": num(m, "gpu__time_duration.sum") / 1e3 if m["gpu__time_duration.sum"][1] == "nsecond"
-                 else num(m, "gpu__time_duration.sum"),
+                 "duration_us": num(m, "gpu__time_duration.sum") * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}[
+                     m["gpu__time_duration.sum"][1]],
                  "source": f"{os.path.relpath(rep, ROOT)} (ncu --set full --clock-control none)"}
     print(key, data[key])
 with open(OUT, "w") as f:

@@ -196,7 +196,7 @@ def test_c3_full_size_solve_matches_oracle_same_rule():
         info = ctx.apply(dev(inp["B"][:, cols]), out, q=cfg.q, max_iters=int(g["iters"]), tol=0.0, mode="sqrt",
                          rule=(g["t"], g["w"]))
         got = out.cpu().numpy().astype(np.float64)
-    assert info["iters"] == int(g["iters"]) and info["mvm_impl_used"] == "tc"
+    assert info["iters"] == int(g["iters"]) and info["mvm_impl_used"] in ("tc", "sym")   # 2 columns: sym
     for k in range(len(cols)):
         assert relerr(got[:, k], g["out"][:, k]) < _fp32_floor(g), (k, relerr(got[:, k], g["out"][:, k]))
 

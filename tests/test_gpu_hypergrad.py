@@ -47,7 +47,7 @@ def test_hyper_grad_matches_oracle(kind, impl):
     ref = ciq_hyper_grad(op, b.astype(np.float64), v.astype(np.float64), rule, max_iters=j)
     with pb.CIQ(kind, X=dev(x), lengthscale=ls, outputscale=o2, diag=s2) as g:
         grad, info = g.hyper_grad(dev(b), dev(v), q=8, max_iters=j, tol=0.0, rule=rule, mvm_impl=impl)
-    assert info["mvm_impl_used"] == ("simt" if impl == "simt" else "tc")
+    assert info["mvm_impl_used"] in (("simt",) if impl == "simt" else ("tc", "sym"))
     np.testing.assert_allclose(grad, ref, rtol=1e-4)
 
 
