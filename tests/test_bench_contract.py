@@ -18,7 +18,16 @@ def _run(*args):
 
 
 def test_reference_arm_line_small_config():
-    d = _run("--impl", "reference", "--config", "C1", "--steps", "1", "--warmup", "3")
+    import time
+    t0 = time.perf_counter()
+    d = _run("--impl", "reference", "--config", "C1", "--steps", "2", "--warmup", "3")
+    wall = time.perf_counter() - t0
+    # ms_per_step is the measured time of one bounded step (no extrapolation): it fits the run
+    assert d["steps"] * d["ms_per_step"] / 1000.0 <= wall
+    assert set(d["config"]) == {"workload", "global_batch"} and d["config"]["global_batch"] == 1
+    f = d["step"]["fraction_of_call"]
+    assert 0 < f <= 1 and abs(d["value"] - d["step"]["rhs_equivalent_per_step"] / (d["ms_per_step"] / 1000)) \
+        <= 1e-9 * d["value"]
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "config",
               "cpu_baseline", "e2e"):
         assert k in d, k
