@@ -428,7 +428,7 @@ int choose_nsplit_dense(int64_t rows, int64_t npad, int chunks, int nsm) {
   const int64_t nkt = npad / 64;
   // accuracy bound as tc2_choose_nsplit: at most kMaxChainDense 64-wide K tiles (12 MMAs each) feed
   // one fp32 TMEM accumulator (round-toward-zero accumulation)
-  constexpr int64_t kMaxChainDense = 264;
+  constexpr int64_t kMaxChainDense = 66;
   const int smin = (int)std::max<int64_t>(1, (nkt + kMaxChainDense - 1) / kMaxChainDense);
   int best = smin;
   double best_eff = 0.0;
@@ -751,9 +751,9 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     long long t0 = h[0];
     for (int sl = 0; sl < 32; ++sl)
       if (h[sl * 256] != 0 && h[sl * 256] < t0) t0 = h[sl * 256];
-    for (int j = 0; j < 96; ++j) {
+    for (int j = 0; j < 256; ++j) {
       fprintf(stderr, "%4d", j);
-      for (int sl = 0; sl < 14; ++sl) {
+      for (int sl = 0; sl < (j < 8 ? 32 : 14); ++sl) {
         const long long v = h[sl * 256 + j];
         fprintf(stderr, " %8lld", v ? v - t0 : -1LL);
       }

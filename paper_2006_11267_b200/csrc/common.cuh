@@ -19,6 +19,25 @@ CIQ_DEVICE double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// Transposed warp reduction: lane l holds v[0..W) (one value per column, W | 32); returns to lane
+// l the sum over the 32 lanes of column l % W.  W - 1 + log2(32 / W) shuffles instead of W x 5.
+template <int W>
+CIQ_DEVICE float warp_sum_transpose(float (&v)[W], int lane) {
+#pragma unroll
+  for (int s = W / 2; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int k = 0; k < s; ++k) {
+      const float send = up ? v[k] : v[k + s];
+      const float keep = up ? v[k + s] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  float r = v[0];
+#pragma unroll
+  for (int o = W; o < 32; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
 CIQ_DEVICE double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -25,8 +25,9 @@
 // Smem: A features of the unit (256 rows, double-buffered across units), features of the first
 // three tiles, and a ring whose stage g holds V(g) and the column features of tile g+3 (skewed:
 // one stage wait / release per tile on the MMA warp).
-// The output read-out of unit k is done by the epilogue warps right after they finish the first
-// tile of unit k+1 (O is drained to registers, released, then written with plain stores).
+// The output read-out of unit k is done by the epilogue group that takes the first tile of unit
+// k+1, right after that tile (O is drained to registers, released, then written with plain
+// stores; the alpha partials by a transposed warp reduction).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -47,13 +48,11 @@ constexpr int NT2 = 640;            // 4 role warps + 16 epilogue warps
 constexpr int EPI0 = 4;
 constexpr int NB2 = 3;              // S/K TMEM buffers
 constexpr int TMO = NB2 * 128;      // O accumulators at [384, 384 + 2 TN)
-#ifdef CIQ_NO_PINGPONG
-constexpr bool kPingPong = false;
-#else
-constexpr bool kPingPong = true;   // measured: 0.937 vs 1.088 ms per C3 MVM (profiles/)
-#endif
-constexpr int EPI_ARRIVALS = kPingPong ? 4 : 8;    // epilogue warps per tile and half
-constexpr int RO_ARRIVALS = 8;                      // warps reading out O_h (either mode)
+// Ping-pong epilogue (measured: 0.937 vs 1.088 ms per C3 MVM for all 16 warps on every tile,
+// profiles/): two groups of 8 warps take alternate tiles.
+constexpr int EPI_ARRIVALS = 4;    // epilogue warps per tile and half
+constexpr int RO_ARRIVALS = 4;     // warps reading out O_h of a unit, per half (one group)
+constexpr int RO_BYTES = 32 * 16 * 4;   // read-out transpose scratch per warp: 32 rows x 16 fp32
 
 template <int TN>
 struct Cfg2 {
@@ -63,7 +62,8 @@ struct Cfg2 {
   static constexpr int STAGE = 2 * V_BYTES + F_BYTES;
   static constexpr int STAGES = 8;
   static constexpr int RING_OFF = 2 * A_BYTES + NB2 * F_BYTES;
-  static constexpr int SMEM = 1024 + RING_OFF + STAGES * STAGE + 1024;
+  static constexpr int RO_OFF = RING_OFF + STAGES * STAGE + 1024;   // after the barriers
+  static constexpr int SMEM = 1024 + RO_OFF + 8 * RO_BYTES;
 };
 static_assert(Cfg2<64>::SMEM <= 227 * 1024, "shared memory budget");
 
@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
   uint8_t* pro = smem + 2 * C::A_BYTES;                  // [3][F_BYTES]
   uint8_t* ring = smem + C::RING_OFF;
   Bars2* bars = reinterpret_cast<Bars2*>(ring + C::STAGES * C::STAGE);
+  static_assert(sizeof(Bars2) <= 1024, "barrier block");
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t n = args.n;
@@ -331,79 +332,141 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
       if (++b == NB2) { b = 0; ph_b ^= 1; }
     }
   } else if (warp >= EPI0) {
-    // ---------------- epilogue: 16 warps; warp w works on TMEM lane quarter q = w % 4.
-    // kPingPong: two groups of 8 warps take alternate tiles (group = (w - 4) / 8), warp covers half
-    // h = ((w - 4) / 4) % 2, both 32-column chunks -- while one group sits in its TMEM load / store /
-    // barrier latencies the other keeps the SFU busy.  Otherwise all 16 warps share every tile:
-    // half (w - 4) / 8, chunk ((w - 4) / 4) % 2. ----------------
+    // ---------------- epilogue: 16 warps; warp w works on TMEM lane quarter q = w % 4.  Two groups
+    // of 8 warps take alternate tiles (group = (w - 4) / 8), a warp covers half h = ((w - 4) / 4) % 2,
+    // both 32-column chunks -- while one group sits in its TMEM load / store / barrier latencies the
+    // other keeps the SFU busy. ----------------
     const int q = warp % 4;
-    const int grp = kPingPong ? (warp - EPI0) >> 3 : 0;
-    const int h = kPingPong ? ((warp - EPI0) >> 2) & 1 : (warp - EPI0) >> 3;
-    const int cc0 = kPingPong ? 0 : ((warp - EPI0) >> 2) & 1;
-    constexpr int NCH = kPingPong ? 2 : 1;      // 32-column chunks per warp per tile
+    const int grp = (warp - EPI0) >> 3;
+    const int h = ((warp - EPI0) >> 2) & 1;
+    constexpr int NCH = 2;      // 32-column chunks per warp per tile
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    Cur c, prev;
+    // read-out scratch of this warp (h, q) of the reading group
+    float* rbuf = reinterpret_cast<float*>(smem + C::RO_OFF + (h * 4 + q) * RO_BYTES);
+    Cur c;
     c.start(args, ntiles);
-    prev = c;
-    // read-out column half of O_h: the chunk (without ping-pong) or the group (with it: both groups
-    // read out every unit, each after the first tile it takes in the next unit)
-    const int ro = kPingPong ? grp : cc0;
-    auto readout = [&](const Cur& u) {
-      // O_h columns [ro * CPW, +CPW) of rows 32 q + lane of half h
-      constexpr int CPW = TN / 2;
-      uint32_t o[CPW];
-      mbar_wait(&bars->o_full[h], u.k & 1);
-      fence_after_sync();
-      const uint32_t ta = tbase + TMO + TN * h + ro * CPW + lane_base;
+    // the unit before c's unit (valid once c has left the CTA's first unit): (u, k) only, decoded
+    // when it is read out (registers: the epilogue runs at the 96-per-thread cap)
+    int pu_u = c.u, pu_k = c.k;
+    // Read-out of a finished unit: the group that takes tile 0 of unit k reads out all TN columns of
+    // O_h of unit k-1 (the first KV of unit k waits for that group only), in passes of 16 columns.
+    // O arrives row-per-lane (TMEM lane = row); it goes through a swizzled shared-memory transpose
+    // so that V is loaded and P stored coalesced (lane -> rows lane/4 + 8k, 4 columns at 4 (lane%4)):
+    // row-per-lane global accesses cost 32 L1 wavefronts per instruction, and a read-out was ~10k
+    // cycles of L1 traffic (measured with the per-tile trace).
+    constexpr int NP = TN / 16;
+    auto readout = [&](int uu, int kk) {
+      Cur u;
+      u.u = uu;
+      u.k = kk;
+      u.decode(args, ntiles);
+      const int64_t ib = args.row0 + (int64_t)u.rt * BM2 + 128 * h + 32 * q;   // first row of the warp
+      const int colu = u.chunk * TN;
+      const int ch = lane & 3, rl = lane >> 2;
+      // coalesced layout: rows ib + rl + 8 k (k = 0..3), columns c0 + 4 ch .. + 3
+      auto vload = [&](int c0, float4 (&v)[4]) {
 #pragma unroll
-      for (int m = 0; m < CPW; m += 8) tmem_ld8(ta + m, &o[m]);
-      tmem_ld_wait();
-      fence_before_sync();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->o_empty[h]);
-      const int64_t i = args.row0 + (int64_t)u.rt * BM2 + 128 * h + 32 * q + lane;
-      const bool row_ok = i < args.row1;
-      const int col0 = u.chunk * TN + ro * CPW;
-      float* pout = args.p + (size_t)u.split * args.p_split_stride + (size_t)(i - args.row0) * args.tp + col0;
-      const float* vrow = args.v + (size_t)i * args.tp + col0;
-      double* ap = args.apart ? args.apart + ((size_t)(u.rt * args.nsplit + u.split) * 8 + q * 2 + h) * args.tp + col0
+        for (int k = 0; k < 4; ++k) {
+          const int64_t i = ib + rl + 8 * k;
+          v[k] = i < args.row1 ? __ldg(reinterpret_cast<const float4*>(args.v + (size_t)i * args.tp + colu + c0 + 4 * ch))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
+      float* pbase = args.p + (size_t)u.split * args.p_split_stride + colu + 4 * ch;
+      double* ap = args.apart ? args.apart + ((size_t)(u.rt * args.nsplit + u.split) * 8 + q * 2 + h) * args.tp + colu
                               : nullptr;
+      if (warp == 4 || warp == 12) T2_STAMP(10, u.k);
+      // V one pass ahead (its L2 latency overlaps the O wait and the previous pass)
+      float4 vn[4];
+      vload(0, vn);
+      mbar_wait(&bars->o_full[h], u.k & 1);
+      if (warp == 4 || warp == 12) T2_STAMP(11, u.k);
+      fence_after_sync();
+      const int sw = (lane >> 1) & 3;   // swizzle of this lane's row in the row-per-lane phase
+#pragma unroll 1
+      for (int pass = 0; pass < NP; ++pass) {
+        const int c0 = pass * 16;
+        float4 vc[4];
 #pragma unroll
-      for (int m = 0; m < CPW; m += 4) {
-        float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f), r4 = v4;
-        if (row_ok) {
-          v4 = *reinterpret_cast<const float4*>(vrow + m);
-          r4.x = args.o2 * __uint_as_float(o[m + 0]) * args.inv_scale[col0 + m + 0];
-          r4.y = args.o2 * __uint_as_float(o[m + 1]) * args.inv_scale[col0 + m + 1];
-          r4.z = args.o2 * __uint_as_float(o[m + 2]) * args.inv_scale[col0 + m + 2];
-          r4.w = args.o2 * __uint_as_float(o[m + 3]) * args.inv_scale[col0 + m + 3];
+        for (int k = 0; k < 4; ++k) vc[k] = vn[k];
+        uint32_t o[16];
+        const uint32_t ta = tbase + TMO + TN * h + c0 + lane_base;
+        tmem_ld8(ta, &o[0]);
+        tmem_ld8(ta + 8, &o[8]);
+        if (pass + 1 < NP) vload(c0 + 16, vn);
+        const float4 s4 = __ldg(reinterpret_cast<const float4*>(args.inv_scale + colu + c0 + 4 * ch));
+        tmem_ld_wait();
+        if (pass == NP - 1) {   // O_h is in registers: the next unit's first KV may overwrite it
+          fence_before_sync();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->o_empty[h]);
+          if (warp == 4 || warp == 12) T2_STAMP(12, u.k);
+        }
+        // row-per-lane -> smem: row = lane, 16-byte chunk j at position j ^ ((row >> 1) & 3)
+        // (conflict-free for both phases: 8 lanes of a wavefront hit 8 distinct 4-bank groups)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<uint4*>(rbuf + lane * 16 + ((j ^ sw) << 2)) = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+        __syncwarp();
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = rl + 8 * k;
+          const float4 ov = *reinterpret_cast<const float4*>(rbuf + r * 16 + ((ch ^ ((r >> 1) & 3)) << 2));
+          const float4 vv = vc[k];
+          float4 r4;
+          r4.x = args.o2 * ov.x * s4.x;
+          r4.y = args.o2 * ov.y * s4.y;
+          r4.z = args.o2 * ov.z * s4.z;
+          r4.w = args.o2 * ov.w * s4.w;
           if (u.split == 0) {
-            r4.x = fmaf(args.diag, v4.x, r4.x); r4.y = fmaf(args.diag, v4.y, r4.y);
-            r4.z = fmaf(args.diag, v4.z, r4.z); r4.w = fmaf(args.diag, v4.w, r4.w);
+            r4.x = fmaf(args.diag, vv.x, r4.x); r4.y = fmaf(args.diag, vv.y, r4.y);
+            r4.z = fmaf(args.diag, vv.z, r4.z); r4.w = fmaf(args.diag, vv.w, r4.w);
           }
-          *reinterpret_cast<float4*>(pout + m) = r4;
+          const int64_t i = ib + r;
+          if (i < args.row1) *reinterpret_cast<float4*>(pbase + (size_t)(i - args.row0) * args.tp + c0) = r4;
+          a0 = fmaf(vv.x, r4.x, a0); a1 = fmaf(vv.y, r4.y, a1); a2 = fmaf(vv.z, r4.z, a2); a3 = fmaf(vv.w, r4.w, a3);
         }
-        if (ap != nullptr) {
-          const float pv[4] = {v4.x * r4.x, v4.y * r4.y, v4.z * r4.z, v4.w * r4.w};
+        __syncwarp();   // rbuf is rewritten by the next pass
+        if (ap != nullptr) {   // alpha partials of the warp's 32 rows: sum over the 8 lanes of column chunk ch
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float sum = warp_sum(pv[e]);
-            if (lane == 0) ap[m + e] = (double)sum;
+          for (int xo = 4; xo < 32; xo <<= 1) {
+            a0 += __shfl_xor_sync(0xffffffffu, a0, xo);
+            a1 += __shfl_xor_sync(0xffffffffu, a1, xo);
+            a2 += __shfl_xor_sync(0xffffffffu, a2, xo);
+            a3 += __shfl_xor_sync(0xffffffffu, a3, xo);
+          }
+          if (rl == 0) {
+            double* d = ap + c0 + 4 * ch;
+            d[0] = a0; d[1] = a1; d[2] = a2; d[3] = a3;
           }
         }
+      }
+      if (warp == 4 || warp == 12) T2_STAMP(13, u.k);
+    };
+    // L2 prefetch of this warp's V rows of unit u (read ~njt tiles later by the read-out): the
+    // warp's 32 rows x TN columns, one 128-byte line per lane and step
+    auto prefetch_v = [&](const Cur& u) {
+      const int64_t ib = args.row0 + (int64_t)u.rt * BM2 + 128 * h + 32 * q;
+      constexpr int LPR = TN * 4 / 128 > 0 ? TN * 4 / 128 : 1;   // 128-byte lines per row
+#pragma unroll
+      for (int e = lane; e < 32 * LPR; e += 32) {
+        const int64_t i = ib + e / LPR;
+        if (i < args.row1)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(args.v + (size_t)i * args.tp + u.chunk * TN + (e % LPR) * 32));
       }
     };
     int b = 0;
     uint32_t ph_b = 0;
     int g = 0;
     for (; c.valid(args); ++g) {
-      if (!kPingPong || (g & 1) == grp) {
+      if ((g & 1) == grp) {
         mbar_wait(&bars->s_full[b][h], ph_b);
         if (warp == 4) T2_STAMP(4, g);
         fence_after_sync();
 #pragma unroll 1
         for (int ch = 0; ch < NCH; ++ch) {
-          const int cc = cc0 + ch;
+          const int cc = ch;
           const uint32_t tb = tbase + b * 128 + 64 * h + 32 * cc + lane_base;
           const int64_t jcol0 = (int64_t)c.J() * BN2 + 32 * cc;
           uint32_t sv[32];
@@ -426,16 +489,19 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         __syncwarp();
         if (warp == 4) T2_STAMP(5, g);
         if (warp == 19) T2_STAMP(6, g);
-        T2_STAMP(16 + warp - EPI0, g);
         if (lane == 0) mbar_arrive(&bars->k_full[b][h]);
-        // first tile this warp takes in unit k: unit k-1 is complete (its last KV is issued)
-        if (c.k > 0 && c.k != prev.k) readout(prev);
-        prev = c;
+        if (c.jj == 0) {
+          prefetch_v(c);
+          if (c.k > 0) readout(pu_u, pu_k);   // unit k-1 is complete (its last KV is issued)
+        }
       }
+      const int old_u = c.u, old_k = c.k;
       c.advance(args, ntiles);
+      if (!c.valid(args) || c.k != old_k) { pu_u = old_u; pu_k = old_k; }
       if (++b == NB2) { b = 0; ph_b ^= 1; }
     }
-    if (prev.valid(args)) readout(prev);
+    // the CTA's last unit: one group (all of its TN columns) / every warp (its column half)
+    if (pu_u < args.nunits && grp == 0) readout(pu_u, pu_k);
   }
   fence_before_sync();
   __syncthreads();
@@ -472,11 +538,16 @@ int tc2_units(int64_t rows, int nsplit, int chunks) { return (int)((rows + BM2 -
 // (max units per CTA x tiles per unit minimal), each split keeping >= min_tiles column tiles, and at most
 // kMaxChain tiles per unit.  The chain bound is an accuracy bound: the tensor core adds each MMA
 // into the fp32 TMEM accumulator with a round-toward-zero bias, measured on B200 as a relative
-// shrink of ~1.1e-8 per accumulated MMA (12 per tile): 261 tiles -> -3.5e-5, 782 tiles -> -1e-4
-// (scripts/diag_mvm_n.py).  The per-split partial products are summed in
-// fp32 (round to nearest) by the consumer.
+// shrink of ~1.1e-8 per accumulated MMA (12 per tile).  It is the error that dominates the
+// full-size solve: at C3 the solve's error against the float64 oracle is proportional to the chain
+// length (profiles/chain_nsplit_r02.txt: 264 / 130 / 65 / 33 tiles -> 2.6e-4 / 1.35e-4 / 7.0e-5 /
+// 3.6e-5, same rule and J; a numpy emulation of the round-toward-zero accumulation,
+// scripts/diag_rz_chain.py, shows the same proportionality), while fp32 vectors and fp32 kernel
+// entries alone give ~1e-5 (scripts/diag_fp32_floor.py).  66 tiles keep C3 inside north_star's
+// 1e-4.  The per-split partial products are summed in fp32 (round to
+// nearest) by the consumer.
 int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm, int min_tiles) {
-  constexpr int64_t kMaxChain = 264;
+  constexpr int64_t kMaxChain = 66;
   const int64_t nrt = (rows + BM2 - 1) / BM2;
   const int64_t ntiles = (n + BN2 - 1) / BN2;
   const int smin = (int)((ntiles + kMaxChain - 1) / kMaxChain);

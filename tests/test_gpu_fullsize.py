@@ -10,11 +10,12 @@ operators), on outputs the oracle can compute one by one, plus properties that h
 * Full solve against the float64 oracle at C3's FULL size (tests/golden/c3_full_cols.npz, written
   by scripts/make_golden_fullsize.py from oracle/ only: the oracle's lambda estimate and rule, its
   msMINRES run to max relres 1e-8 (J = 307), K^{1/2}b for the first two columns of C3's B):
-  (a) params.fp64 (the accuracy mode), same rule and J: 1e-6, far inside north_star's 1e-4
-  ("up to N = 50,000 ... 4 decimal places"); (b) the default fp32 tensor-core path, same
-  rule and J, and (c) the bench configuration itself (64 columns, own lambda estimate from the
-  solve's first 12 Lanczos steps, tol 1e-4): within the derived fp32 floor kappa(K) 2^-22
-  (_fp32_floor).
+  (a) params.fp64 (the accuracy mode), same rule and J: 1e-6; (b) the default fp32 tensor-core
+  path, same rule and J (2 columns: the symmetric-tile kernel; 64 columns: the bench's full-tile
+  kernel), and (c) the bench configuration itself (64 columns, own lambda estimate from the
+  solve's first 12 Lanczos steps, tol 1e-4): north_star's flat 1e-4 ("up to N = 50,000
+  ... 4 decimal places").  The fp32 paths meet it because the TMEM accumulation chains are capped
+  at 66 tiles (the round-toward-zero bias).
 * C4 (M = 5000, 1024 RHS, rank-200 preconditioner): seeded columns of R'B against the oracle's
   explicit symmetric route on those columns (columns are independent; same rule and J), at the
   flat north_star 1e-4 (the library's fp64 materialised-M route).
@@ -32,9 +33,10 @@ import paper_2006_11267_b200 as pb  # noqa: E402
 
 # max |err| / max |ref| over the sampled rows, derived in DESIGN.md section 5: the tcgen05 fp32
 # accumulation shrinks each accumulated MMA by <= 1.3e-8 (round toward zero, measured), the
-# partial products are at most 264 tiles x 12 MMAs long (tc2_choose_nsplit) -> <= 4.1e-5, plus
-# <= 2e-5 for the split-fp16 operands (the bound the small-size parity tests use).
-MVM_TOL = 6e-5
+# partial products are at most 66 tiles x 12 MMAs long (tc2_choose_nsplit, choose_nsplit_dense;
+# the symmetric-tile kernel: <= 384 MMAs) -> <= 1.1e-5, plus <= 2e-5 for the split-fp16 operands
+# (the bound the small-size parity tests use).
+MVM_TOL = 3.5e-5
 
 
 def dev(a):
@@ -157,14 +159,7 @@ def _golden_c3():
     return np.load(path)
 
 
-def _fp32_floor(g):
-    """Derived bound for an fp32 evaluation of K at full size: every fp32
-    scheme carries kernel entries to ~22-24 significant bits (split-fp16 k_hi + k_lo: 2^-22), and
-    an entry-wise relative perturbation eps of K moves K^{+-1/2} b by up to ~kappa(K) eps, kappa
-    from the oracle's own spectrum estimate (C3: 1788 -> 4.3e-4).  Measured at C3: tensor core
-    2.6e-4, fp32 SIMT 2.1-2.7e-4 (scripts/diag_golden_c3.py); params.fp64 removes the floor (next
-    tests: 6e-8)."""
-    return float(g["lambda_max"] / g["lambda_min"]) * 2.0 ** -22
+NORTH_STAR = 1e-4   # relative L2 error vs the float64 oracle (BASELINE.json north_star)
 
 
 def test_c3_full_size_fp64_mode_matches_oracle():
@@ -185,33 +180,41 @@ def test_c3_full_size_fp64_mode_matches_oracle():
                 assert relerr(got[:, k], g[key][:, k]) < 1e-6, (mode, k, relerr(got[:, k], g[key][:, k]))
 
 
-def test_c3_full_size_solve_matches_oracle_same_rule():
-    """The default fp32 tensor-core path at full size, same rule and J, within the fp32 floor."""
+@pytest.mark.parametrize("ncols", [2, 64])
+def test_c3_full_size_solve_matches_oracle_same_rule(ncols):
+    """The default fp32 tensor-core path at full size, same rule and J: 2 columns (16-column
+    chunks: the symmetric-tile kernel) and 64 columns (the bench's full-tile kernel, 12 column
+    splits of <= 66 tiles), north_star's flat 1e-4 on the golden columns."""
     g = _golden_c3()
     cfg = workloads.CONFIGS["C3"]
     inp = workloads.make_inputs(cfg)
     cols = g["cols"]
+    b = inp["B"][:, :ncols] if ncols > len(cols) else inp["B"][:, cols]
     with full_ctx(cfg, inp) as ctx:
-        out = torch.empty((cfg.n, len(cols)), device="cuda")
-        info = ctx.apply(dev(inp["B"][:, cols]), out, q=cfg.q, max_iters=int(g["iters"]), tol=0.0, mode="sqrt",
+        out = torch.empty((cfg.n, b.shape[1]), device="cuda")
+        info = ctx.apply(dev(b), out, q=cfg.q, max_iters=int(g["iters"]), tol=0.0, mode="sqrt",
                          rule=(g["t"], g["w"]))
         got = out.cpu().numpy().astype(np.float64)
-    assert info["iters"] == int(g["iters"]) and info["mvm_impl_used"] in ("tc", "sym")   # 2 columns: sym
-    for k in range(len(cols)):
-        assert relerr(got[:, k], g["out"][:, k]) < _fp32_floor(g), (k, relerr(got[:, k], g["out"][:, k]))
+    assert info["iters"] == int(g["iters"])
+    assert info["mvm_impl_used"] == ("tc" if ncols == 64 else "sym"), info["mvm_impl_used"]
+    for i, k in enumerate(cols):
+        kk = k if ncols > len(cols) else i
+        assert relerr(got[:, kk], g["out"][:, i]) < NORTH_STAR, (k, relerr(got[:, kk], g["out"][:, i]))
 
 
 def test_c3_full_size_bench_configuration_matches_oracle():
-    """The exact call bench.py times: 64 columns, lanczos_reuse, tol 1e-4, own rule (the rule
-    differs from the oracle's by the lambda estimates: quadrature error ~1e-6 at Q = 8)."""
+    """The exact call bench.py times: 64 columns, lanczos_reuse, stored basis, tol 1e-4, own rule
+    (the rule differs from the oracle's by the lambda estimates: quadrature error ~1e-6 at Q = 8),
+    north_star's flat 1e-4."""
     g = _golden_c3()
     cfg = workloads.CONFIGS["C3"]
     inp = workloads.make_inputs(cfg)
     with full_ctx(cfg, inp) as ctx:
         out = torch.empty((cfg.n, cfg.t), device="cuda")
         info = ctx.apply(dev(inp["B"]), out, q=cfg.q, max_iters=cfg.max_iters, tol=cfg.tol, mode="sqrt",
-                         lanczos_start=dev(inp["S"]), lanczos_reuse=True)
+                         lanczos_start=dev(inp["S"]), lanczos_reuse=True, stored_basis=True)
         got = out.cpu().numpy().astype(np.float64)
     assert info["converged"] and info["max_rel_residual"] <= cfg.tol
-    for k in g["cols"]:
-        assert relerr(got[:, k], g["out"][:, k]) < _fp32_floor(g), (k, relerr(got[:, k], g["out"][:, k]))
+    assert info["mvm_impl_used"] == "tc" and info["mvm_splits"] >= 12
+    for i, k in enumerate(g["cols"]):
+        assert relerr(got[:, k], g["out"][:, i]) < NORTH_STAR, (k, relerr(got[:, k], g["out"][:, i]))
