@@ -184,6 +184,12 @@ struct ciq_ctx {
   size_t hist_elems = 0;
   double* apart_tc = nullptr;
   size_t apart_tc_elems = 0;
+  // fused alpha of the full-tile kernel (TcArgs::alpha_out): set by the recurrence around its MVM
+  const Scal* alpha_fuse = nullptr;
+  bool alpha_fused = false;        // the last run_mvm computed alpha itself
+  double* cta_part = nullptr;      // [SMs][tp]
+  size_t cta_part_elems = 0;
+  unsigned* ticket = nullptr;      // zero between launches
   int last_nsplit = 1;
   int mvm_kind_used = 0;      // 1 simt, 2 tc, 3 symmetric-tile tc (of the last loop MVM)
   int last_kind = 0;          // mvm_kind_used of the captured iteration graph
@@ -619,6 +625,12 @@ ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
     st = grow(c, &c->psplit, &c->psplit_elems, (size_t)nsplit * rows * tp);
     if (st != CIQ_OK) return st;
   }
+  st = grow(c, &c->cta_part, &c->cta_part_elems, (size_t)sm_count() * tp);
+  if (st != CIQ_OK) return st;
+  if (c->ticket == nullptr) {
+    CUDA_TRY(c, cudaMalloc(&c->ticket, sizeof(unsigned)));
+    CUDA_TRY(c, cudaMemset(c->ticket, 0, sizeof(unsigned)));
+  }
   return grow(c, &c->apart_tc, &c->apart_tc_elems, (size_t)nblk * tp);
 }
 
@@ -738,6 +750,17 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     a.sym_ng = c->sym_ng;
     a.sym_b = sym_group_blocks(tn);
     a.sym_slots = c->sym_slots;
+  }
+  c->alpha_fused = false;
+  if (!dense && !sym && !pair && ap != nullptr && c->alpha_fuse != nullptr && !c->sharded && !c->post.on &&
+      !c->deriv && c->cta_part != nullptr &&
+      c->cta_part_elems >= (size_t)nsm * tp && c->ticket != nullptr) {
+    a.alpha_out = c->alpha_fuse->alpha;
+    a.alpha_nrm = c->alpha_fuse->nrm_cur;
+    a.alpha_frozen = c->alpha_fuse->frozen;
+    a.cta_part = c->cta_part;
+    a.ticket = c->ticket;
+    c->alpha_fused = true;
   }
   if (dense) LAUNCH(c, launch_mvm_dense2(a, nsm, c->stream));
   else if (sym) LAUNCH(c, launch_mvm_sym(a, nsm, c->stream));
@@ -1634,7 +1657,7 @@ void ciq_free(ciq_ctx* c) {
   dfree(c->feat_a); dfree(c->feat_b); dfree(c->planes); dfree(c->inv_scale); dfree(c->psplit);
   dfree(c->stash); dfree(c->hist);
   dfree(c->vjp_xb); dfree(c->vjp_xv); dfree(c->vjp_y); dfree(c->vjp_g); dfree(c->vjp_w);
-  dfree(c->apart_tc);
+  dfree(c->apart_tc); dfree(c->cta_part); dfree(c->ticket);
   dfree(c->sym_units); dfree(c->sym_base); dfree(c->sym_part);
   free_precond(c->pc);
   free_post(c->post);
@@ -2148,16 +2171,20 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     double* apart = nullptr;
     // single GPU, tensor-core MVM: the streaming pass of iteration j writes W_{j+1}'s split-fp16
     // planes, so iteration j+1 skips pack_v (the first iteration of a block always packs)
+    c->alpha_fuse = P.on ? nullptr : &sc;   // the full-tile kernel computes alpha_j in its tail
     ciq_status st2 = P.on ? apply_m(wcur, ws.p, &apart, &nbm)
                           : run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit,
                                     &apart, &nbm, fuse_pack);
+    c->alpha_fuse = nullptr;
+    const bool alpha_done = !P.on && c->alpha_fused;
+    c->alpha_fused = false;
     end_timed(c);
     if (st2 != CIQ_OK) return st2;
     const float* pin = (nsplit > 1) ? c->psplit : ws.p;
     loop_nsplit = nsplit;
     loop_impl = c->mvm_kind_used;
     if (!c->sharded) {
-      LAUNCH(c, launch_alpha(sc, apart, nbm, tp, s));
+      if (!alpha_done) LAUNCH(c, launch_alpha(sc, apart, nbm, tp, s));
     } else {
       LAUNCH(c, launch_reduce_cols(apart, nbm, tp, tsum_a, 0, s));
       st2 = global_sum(c, tsum_a, tp);
@@ -2170,22 +2197,22 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     LAUNCH(c, launch_lanczos_update(sc, pin, nsplit, (size_t)rows * tp, wcur + c->row0 * tp, wprev + c->row0 * tp,
                                     wnew + c->row0 * tp, &d1, &d2, ws.y, stored ? 0 : nqe, rows, tp, ws.bpart, 0, s,
                                     fuse_pack ? c->planes : nullptr, c->inv_scale, vrows(c), plane_cols(c, tp), c->op.n,
-                                    xqk, c->row0));
+                                    xqk, c->row0, stored ? c->basis : nullptr, (size_t)rows * tp, hlen));
     end_timed(c);
+    // stored basis: the streaming pass wrote W_{j+1} to its basis slot, the Givens pass writes the
+    // step's scalars (no separate copy pass)
     if (!c->sharded) {
-      LAUNCH(c, launch_givens(sc, ws.bpart, update_blocks(rows), nqe, tp, s));
+      LAUNCH(c, launch_givens(sc, ws.bpart, update_blocks(rows), nqe, tp, s, stored ? c->bhist : nullptr, hlen));
     } else {
       LAUNCH(c, launch_reduce_cols(ws.bpart, update_blocks(rows), tp, tsum_b, 0, s));
       st2 = global_sum(c, tsum_b, tp);
       if (st2 != CIQ_OK) return st2;
-      LAUNCH(c, launch_givens(sc, tsum_b, 1, nqe, tp, s));
+      LAUNCH(c, launch_givens(sc, tsum_b, 1, nqe, tp, s, stored ? c->bhist : nullptr, hlen));
       // next Lanczos block to every rank: its split-fp16 planes when the streaming
       // pass packed them, else the fp32 rows
       st2 = fuse_pack ? allgather_planes(c, tp) : allgather_rows(c, wnew, tp);
       if (st2 != CIQ_OK) return st2;
     }
-    if (stored)
-      LAUNCH(c, launch_store_basis(wnew + c->row0 * tp, c->basis, (size_t)rows * tp, rows * tp, sc, c->bhist, tp, hlen, s));
     return CIQ_OK;
   };
   if (stored) {   // slot 0: W_1 (= b), and nrm_1 / the columns frozen before step 1

@@ -90,6 +90,15 @@ struct TcArgs {
   const int* sym_base;       // [sym_nb + 1] first partial slot of each 128-row block
   float* sym_part;           // [chunks][sym_slots][128][TN] fp32 partial products
   int sym_nb, sym_ng, sym_b, sym_slots;
+  // fused alpha (mvm_tc2.cu, single-GPU recurrence; null: off): after its read-outs each CTA sums
+  // its own units' alpha partials into cta_part[blockIdx][tp] (unit order, slot order); the last CTA
+  // to finish (ticket) sums those in CTA order and writes alpha_out[c] = sum / nrm[c]^2 (0 for
+  // frozen columns) -- the alpha_kernel pass without its launch
+  double* alpha_out;
+  const double* alpha_nrm;
+  const int* alpha_frozen;
+  double* cta_part;
+  unsigned* ticket;
 };
 int tc_chunk_cols(int tp);
 // tn: column width of one layout chunk (tc_chunk_cols(tp), halved for the pair kernel)
@@ -144,7 +153,9 @@ cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, si
                                   __half* planes = nullptr, float* inv_scale = nullptr, int64_t npad = 0, int tn = 0,
                                   int64_t n = 0,    // planes: also write W_{j+1}'s split-fp16 MVM operand
                                   float* xq = nullptr,    // [Q][rows][tp]: also accumulate x_q += phi_q d_q
-                                  int64_t plane_row0 = 0);   // planes: global row of local row 0 (sharded)
+                                  int64_t plane_row0 = 0,   // planes: global row of local row 0 (sharded)
+                                  float* basis = nullptr, size_t basis_stride = 0,   // stored basis: W_{j+1} to slot j
+                                  int hlen = 0);
 // fp64 route (preconditioned path, precond64.cu): the same streaming pass on fp64 vectors (no
 // fused packing, no kept solutions); p may be nsplit = 1 only.
 cudaError_t launch_lanczos_update64(const Scal& sc, const double* p, const double* wcur, const double* wprev,
@@ -167,8 +178,6 @@ cudaError_t launch_f64_to_f32(const double* src, int tp, int64_t rows, int cols,
                               cudaStream_t s);
 // ---- stored-basis variant (recurrence.cu) ----
 // basis slot ctrl->iters <- w (elems floats); history [4][hlen][tp]: alpha_j, beta_{j+1}, nrm_{j+1}, frozen
-cudaError_t launch_store_basis(const float* w, float* basis, size_t stride, int64_t elems, const Scal& sc, double* hist,
-                               int tp, int hlen, cudaStream_t s);
 cudaError_t launch_int_to_double(const int* a, int m, double* out, cudaStream_t s);
 cudaError_t launch_combine_basis(const float* basis, size_t stride, int nb, const float* coef, int64_t elems, int tp,
                                  float* y, cudaStream_t s);
@@ -187,7 +196,9 @@ cudaError_t launch_vjp_dense(const float* xb, const float* xv, const double* w, 
                              float* g, int64_t ldg, cudaStream_t s);
 cudaError_t launch_alpha_from_sum(const Scal& sc, const double* sums, int tp, cudaStream_t s);
 cudaError_t launch_sum_ranks(const double* g, int world, int m, double* out, cudaStream_t s);
-cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s);
+// hist (stored basis, may be null): the step's alpha_j, beta_{j+1}, nrm_{j+1}, frozen at slot j - 1
+cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s,
+                          double* hist = nullptr, int hlen = 0);
 // Lambda-estimation Lanczos (full re-orthogonalisation)
 cudaError_t launch_basis_dots(const float* basis, int64_t bstride, int nb, int64_t rows, int tp, const float* p,
                               double* part, cudaStream_t s);

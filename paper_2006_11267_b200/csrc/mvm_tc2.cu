@@ -509,6 +509,35 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
     fence_after_sync();
     tmem_dealloc<512>(tbase);
   }
+  if (args.alpha_out != nullptr) {   // fused alpha (TcArgs): this CTA's read-outs are complete
+    const int tp = args.tp;
+    for (int col = threadIdx.x; col < tp; col += NT2) {
+      double sum = 0.0;
+      for (int u = blockIdx.x; u < args.nunits; u += gridDim.x) {
+        const int chunk = u % args.chunks;
+        if (col / TN != chunk) continue;
+        const size_t r0 = (size_t)(u / args.chunks) * 8;   // rows (rt * nsplit + split) * 8 + (q, h) slot
+#pragma unroll
+        for (int sl = 0; sl < 8; ++sl) sum += args.apart[(r0 + sl) * tp + col];
+      }
+      args.cta_part[(size_t)blockIdx.x * tp + col] = sum;
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) s_last = atomicAdd(args.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      for (int col = threadIdx.x; col < tp; col += NT2) {
+        double sum = 0.0;
+        for (int b = 0; b < (int)gridDim.x; ++b) sum += ((volatile double*)args.cta_part)[(size_t)b * tp + col];
+        const double nr = args.alpha_nrm[col];
+        args.alpha_out[col] = args.alpha_frozen[col] ? 0.0 : sum / (nr * nr);
+      }
+      if (threadIdx.x == 0) *args.ticket = 0u;   // for the next launch (stream-ordered)
+    }
+  }
 }
 
 template <int KIND, int TN>

@@ -246,6 +246,16 @@ __global__ void sum_ranks_kernel(const double* __restrict__ g, int world, int m,
 // stands in for beta_{j+1}, which is not known yet (any power of two that keeps both fp16 halves
 // in range gives the same product: scaling by 2^e is exact).  Layout as pack_v (mvm_tc.cu):
 // [chunk][hi|lo][npad/8][tn/8][8][8].
+// Stored-basis output of the streaming / Givens passes (params.stored_basis): W_{j+1} to slot j of
+// basis (stride elements per slot), and the step's scalars to hist = [alpha | beta_{j+1} | nrm_{j+1} |
+// frozen] x [hlen][tp] at slot j - 1.  basis / hist null: not stored.
+struct BasisOut {
+  float* basis;
+  size_t stride;
+  double* hist;
+  int hlen;
+};
+
 struct PackOut {
   __half* planes;      // null: no packing
   float* inv_scale;
@@ -282,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? CIQ_UPD_MINB : 2) l
     Scal sc, const T* __restrict__ p, int nsplit, size_t split_stride, const T* __restrict__ wcur, const T* __restrict__ wprev,
     T* __restrict__ wnew, const T* __restrict__ d1base, T* __restrict__ d2base, int64_t qstride,
     T* __restrict__ y, int nq, int64_t rows, int tp, double* __restrict__ bpart, int final_only, PackOut pk,
-    float* __restrict__ xq) {
+    float* __restrict__ xq, BasisOut bo) {
   constexpr int QB = CIQ_UPD_QB;
   constexpr bool kF32 = sizeof(T) == 4;
   const T* CA = coef_sel<T>(sc.ca, sc.da);
@@ -292,6 +302,13 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? CIQ_UPD_MINB : 2) l
   const Ctrl* ctrl = sc.ctrl;
   if (!final_only && ctrl->done) return;
   const int pending = ctrl->pending;
+  // stored-basis variant: W_{j+1} also goes to basis slot j (= Givens steps done + 1; the Givens
+  // pass of step j runs after this one), so no separate copy pass (store_basis) per iteration
+  T* bslot = nullptr;
+  if (bo.basis != nullptr && !final_only) {
+    const int j = ctrl->iters + 1;
+    if (j >= 1 && j < bo.hlen) bslot = reinterpret_cast<T*>(bo.basis) + (size_t)j * bo.stride;
+  }
   Geo g(tp);
   const int tid = threadIdx.x;
   const int lane_row = tid / g.tpr, quad = tid % g.tpr;
@@ -341,6 +358,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? CIQ_UPD_MINB : 2) l
         w.z = fma(-cprev[2], wp.z, (pp.z - alpha[2] * wc.z) * inv_nrm[2]);
         w.w = fma(-cprev[3], wp.w, (pp.w - alpha[3] * wc.w) * inv_nrm[3]);
         st4<T>(wnew + off, w);
+        if (bslot != nullptr) st4<T>(bslot + off, w);
         acc[0] += (double)w.x * w.x; acc[1] += (double)w.y * w.y;
         acc[2] += (double)w.z * w.z; acc[3] += (double)w.w * w.w;
         if (kF32 && pk.planes != nullptr) {
@@ -412,10 +430,12 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? CIQ_UPD_MINB : 2) l
 // go to col_rel / col_state and the last CTA to finish (atomic arrival count) takes the global
 // decision -- max and counts are order-independent, so the outcome is deterministic.
 __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __restrict__ bpart, int nblk, int nq,
-                                                     int tp, double* __restrict__ col_rel, int* __restrict__ col_state) {
+                                                     int tp, double* __restrict__ col_rel, int* __restrict__ col_state,
+                                                     BasisOut bo) {
   Ctrl* ctrl = sc.ctrl;
   if (ctrl->done) return;
   const int c = blockIdx.x;
+  const int jstep = ctrl->iters + 1;   // this step (the last CTA increments ctrl->iters after every CTA read it)
   double s = 0.0;
   for (int b = threadIdx.x; b < nblk; b += 256) s += bpart[(int64_t)b * tp + c];
   s = block_sum256(s);
@@ -471,6 +491,17 @@ __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __re
       sc.nrm_prev[c] = nrm;
       sc.nrm_cur[c] = broke ? 1.0 : tbn;
       sc.tb_cur[c] = tbn;
+    }
+    if (bo.hist != nullptr && jstep < bo.hlen) {   // stored basis: the step's scalars (slot j - 1)
+      double* ha = bo.hist;                          // alpha_j
+      double* hb = ha + (size_t)bo.hlen * tp;        // beta_{j+1}
+      double* hn = hb + (size_t)bo.hlen * tp;        // nrm_{j+1}
+      double* hf = hn + (size_t)bo.hlen * tp;        // frozen after step j
+      const size_t o = (size_t)(jstep - 1) * tp + c;
+      ha[o] = a_j;
+      hb[o] = sc.tb_cur[c];
+      hn[o] = sc.nrm_cur[c];
+      hf[o] = (double)sc.frozen[c];
     }
     col_rel[c] = (state == 1) ? rel : 0.0;
     col_state[c] = state;
@@ -752,13 +783,14 @@ cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, si
                                   float* wnew, float* const* d1, float* const* d2, float* y, int nq,
                                   int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s,
                                   __half* planes, float* inv_scale, int64_t npad, int tn, int64_t n, float* xq,
-                                  int64_t plane_row0) {
+                                  int64_t plane_row0, float* basis, size_t basis_stride, int hlen) {
   const int64_t qstride = rows * tp;
   PackOut pk{planes, inv_scale, npad, tn, sqrt((double)n), plane_row0};
   dim3 grid = stream_grid(rows, tp);
   grid.x = (unsigned)update_blocks(rows);
   lanczos_update_kernel<float><<<grid, kThreads, 0, s>>>(sc, p, nsplit, split_stride, wcur, wprev, wnew, d1[0], d2[0],
-                                                         qstride, y, nq, rows, tp, bpart, final_only, pk, xq);
+                                                         qstride, y, nq, rows, tp, bpart, final_only, pk, xq,
+                                                         BasisOut{basis, basis_stride, nullptr, hlen});
   return cudaGetLastError();
 }
 cudaError_t launch_lanczos_update64(const Scal& sc, const double* p, const double* wcur, const double* wprev,
@@ -769,7 +801,8 @@ cudaError_t launch_lanczos_update64(const Scal& sc, const double* p, const doubl
   dim3 grid = stream_grid(rows, tp);
   grid.x = (unsigned)update_blocks64(rows);
   lanczos_update_kernel<double><<<grid, kThreads, 0, s>>>(sc, p, 1, 0, wcur, wprev, wnew, d1[0], d2[0], qstride, y, nq,
-                                                          rows, tp, bpart, final_only, pk, nullptr);
+                                                          rows, tp, bpart, final_only, pk, nullptr,
+                                                          BasisOut{nullptr, 0, nullptr, 0});
   return cudaGetLastError();
 }
 cudaError_t launch_colsq_partials64(const double* v, int64_t rows, int tp, double* part, cudaStream_t s) {
@@ -788,29 +821,6 @@ cudaError_t launch_sum_ranks(const double* g, int world, int m, double* out, cud
 // kept): after step j's givens (ctrl->iters = j) W_{j+1} (this rank's rows) goes to basis slot j
 // and the step's scalars alpha_j, beta_{j+1}, nrm_{j+1}, frozen to the history at index j - 1.
 // Reads the slot from ctrl, so a captured block of iterations replays correctly.
-__global__ void store_basis_kernel(const float* __restrict__ w, float* __restrict__ basis, size_t stride, int64_t elems,
-                                   Scal sc, double* __restrict__ hist, int tp, int hlen) {
-  const Ctrl* ctrl = sc.ctrl;
-  const int j = ctrl->iters;
-  if (j < 1 || j >= hlen) return;   // (past convergence the slot of step J is rewritten: unused)
-  float* dst = basis + (size_t)j * stride;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += (int64_t)gridDim.x * blockDim.x)
-    dst[e] = w[e];
-  if (blockIdx.x == 0) {
-    double* ha = hist;                         // [hlen][tp] alpha_j
-    double* hb = ha + (size_t)hlen * tp;       // beta_{j+1}
-    double* hn = hb + (size_t)hlen * tp;       // nrm_{j+1}
-    double* hf = hn + (size_t)hlen * tp;       // frozen after step j
-    for (int c = threadIdx.x; c < tp; c += blockDim.x) {
-      const size_t o = (size_t)(j - 1) * tp + c;
-      ha[o] = sc.alpha[c];
-      hb[o] = sc.tb_cur[c];
-      hn[o] = sc.nrm_cur[c];
-      hf[o] = (double)sc.frozen[c];
-    }
-  }
-}
-
 // Y[i][c] = sum_{k < nb} coef[k][c] basis_k[i][c]  (the stored-basis solution, fp32 accumulate in
 // step order like the streaming Y += w phi d)
 __global__ void combine_basis_kernel(const float* __restrict__ basis, size_t stride, int nb, const float* __restrict__ coef,
@@ -830,19 +840,15 @@ cudaError_t launch_int_to_double(const int* a, int m, double* out, cudaStream_t 
   int_to_double_kernel<<<(m + 255) / 256, 256, 0, s>>>(a, m, out);
   return cudaGetLastError();
 }
-cudaError_t launch_store_basis(const float* w, float* basis, size_t stride, int64_t elems, const Scal& sc, double* hist,
-                               int tp, int hlen, cudaStream_t s) {
-  store_basis_kernel<<<592, 256, 0, s>>>(w, basis, stride, elems, sc, hist, tp, hlen);
-  return cudaGetLastError();
-}
 cudaError_t launch_combine_basis(const float* basis, size_t stride, int nb, const float* coef, int64_t elems, int tp,
                                  float* y, cudaStream_t s) {
   combine_basis_kernel<<<1184, 256, 0, s>>>(basis, stride, nb, coef, elems, tp, y);
   return cudaGetLastError();
 }
 
-cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s) {
-  givens_kernel<<<tp, 256, 0, s>>>(sc, bpart, nblk, nq, tp, sc.col_rel, sc.col_state);
+cudaError_t launch_givens(const Scal& sc, const double* bpart, int nblk, int nq, int tp, cudaStream_t s, double* hist,
+                          int hlen) {
+  givens_kernel<<<tp, 256, 0, s>>>(sc, bpart, nblk, nq, tp, sc.col_rel, sc.col_state, BasisOut{nullptr, 0, hist, hlen});
   return cudaGetLastError();
 }
 cudaError_t launch_basis_dots(const float* basis, int64_t bstride, int nb, int64_t rows, int tp, const float* p,
