@@ -389,8 +389,10 @@ def run_ours(args, cfg):
     q = cfg.q
     # algorithmic bytes of one streaming pass: streaming = 2Q direction reads + Q writes, W_cur, W_prev,
     # P read, W_new and its split planes written, Y read + written (3Q + 7 vectors); stored basis =
-    # the Lanczos step only (P, W_cur, W_prev read; W_new and its planes written: 5 vectors)
-    nvec = 5 if args.recurrence == "stored" else 3 * q + 7
+    # the Lanczos step only (P, W_cur, W_prev read; W_new, its planes and its basis-slot copy
+    # written: 6 vectors).  The MVM's column-split partial products (nsplit - 1 extra reads of P)
+    # are not algorithmic bytes.
+    nvec = 6 if args.recurrence == "stored" else 3 * q + 7
     rec_bytes = nvec * rows_local * tcols * 4.0
     recurrence = {"bound": "hbm", "achieved": rec_bytes / (upd_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
                   "unit": "GB/s", "kernel": "lanczos_update_kernel", "ms_per_launch": upd_ms,
@@ -404,6 +406,7 @@ def run_ours(args, cfg):
             "config": static_config(cfg, 1 if sharded else world) | {"l2": "flushed between steps (256 MiB write)"},
             "run": {"J": infos[-1]["iters"],
                     "mvms_per_step": infos[-1]["mvms"], "mvm_impl": impl_used,
+                    "mvm_splits": infos[-1].get("mvm_splits"),
                     "parallelism": (f"rows{world}" if sharded else f"replicas{world}") if world > 1 else "single",
                     "recurrence": args.recurrence,
                     "converged": infos[-1]["converged"], "max_rel_residual": infos[-1]["max_rel_residual"],
