@@ -311,9 +311,19 @@ def run_ours(args, cfg):
     impl_used = pinfo["mvm_impl_used"]
     # algorithmic work per MVM launch: N^2 kernel evaluations, 2 N^2 T useful flops
     flops = 2.0 * rows_local * n * tcols        # this rank's rows of K . V
-    if cfg.precond_rank > 0:
-        # each MVM slot applies M = P^{-1/2} K P^{-1/2}: two Woodbury applications (U^T v and U (g o H),
-        # fp64, 2 N r T flops each) around the K MVM; the fp64 GEMMs dominate (profiles/precond_sweep_r01.txt)
+    if cfg.precond_rank > 0 and pinfo.get("fp64_route"):
+        # fp64 route (precond64.cu): every MVM slot is P = M V with M = P^{-1/2} (K + s2 I) P^{-1/2}
+        # materialised in fp64 -- a dense fp64 contraction, 2 N^2 T flops, on the FP64 tensor pipe (DMMA).
+        # Peak: the DMMA rate measured on this B200 SKU by scripts/ubench_dmma.cu (MEASURED_PEAKS.json has
+        # no fp64 entry and B200_PROFILING.md gives no fp64 ratio)
+        dmma_peak = 37.17   # TFLOP/s, scripts/ubench_dmma.cu (8 warps/CTA x 296 CTAs), profiles/ubench_dmma_r02.txt
+        roof = {"bound": "tensor", "achieved": flops / (mvm_ms * 1e-3) / 1e12, "peak": dmma_peak, "unit": "TFLOP/s",
+                "kernel": "mvm64_kernel (fp64 M = P^-1/2 K P^-1/2 materialised; mma.sync m8n8k4 f64 / DMMA, "
+                          "3-stage cp.async ring)",
+                "peak_source": "measured DMMA m8n8k4 throughput, scripts/ubench_dmma.cu (profiles/ubench_dmma_r02.txt)"}
+    elif cfg.precond_rank > 0:
+        # matrix-free fp32 route: each MVM slot applies M = P^{-1/2} K P^{-1/2}: two Woodbury applications
+        # (U^T v and U (g o H), fp64, 2 N r T flops each) around the K MVM
         sm_count = torch.cuda.get_device_properties(local).multi_processor_count
         fp64_peak = sm_count * 64 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         wflops = 8.0 * rows_local * cfg.precond_rank * tcols

@@ -118,125 +118,138 @@ __global__ void __launch_bounds__(256) gemm64_kernel(int64_t m, int64_t n, int64
 
 // ---- the solve's MVM on the materialised M: P = M V (+ fixed-order alpha partials) ----
 // M: rows x n (ld ldm, even, columns [n, ldm) zero), fp64.  V: n x tp (TV = float or double; rows >= n are never read).
-// P: rows x tp (TP).  128 x 128 output tile per CTA, 256 threads with 8 x 8 outputs each
-// (4 FMAs per shared-memory load), contraction staged 8 at a time, double-buffered through
-// registers.  apart[blockIdx.x][c] = sum_{i in the tile} V[row0 + i][c] P[i][c] (fixed order).
-constexpr int MB = 128, MK = 8;
+// P: rows x tp (TP).  On the FP64 tensor pipe: DMMA (mma.sync m8n8k4 f64; measured on this B200
+// 37.2 TFLOP/s vs 33.9 for DFMA, scripts/ubench_dmma.cu), 64 x 64 output tile per CTA, 8 warps of
+// 32 x 16 (4 x 2 DMMA tiles), contraction staged 16 at a time through a 3-stage cp.async ring
+// (no staging registers: 3 CTAs per SM; C4's 79 x 16 tiles fill 2.85 waves of 444).  Shared
+// layouts: A[m][k] with a 20-double row (k + 4 pad), B[k][c] with a 68-double row -- the fragment
+// loads (lane -> m = lane / 4, k = lane % 4 for A; k = lane % 4, c = lane / 4 for B) hit 16
+// distinct 2-bank pairs per half-warp.  apart[rb][c] = sum_{i in the tile} V[row0 + i][c] P[i][c]
+// (fixed order).  The round-1/2 SIMT kernel (128 x 128 tiles, 8 x 8 DFMA per thread) ran C4's M MVM
+// at 12 TFLOP/s (32% of the FP64 pipe: one CTA per SM, 2.16 waves).
+constexpr int MB = 64, MBN = 64, MK = 16, MST = 3;
+constexpr int SA = MK + 4;      // A row (doubles)
+constexpr int SB = MBN + 4;     // B row (elements)
+
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = ok ? 16 : 0;   // zero fill out of range
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
 
 template <class TV>
-__device__ __forceinline__ void ld2(const TV* p, double& x, double& y);
-template <>
-__device__ __forceinline__ void ld2<float>(const float* p, double& x, double& y) {
-  const float2 f = *reinterpret_cast<const float2*>(p);
-  x = f.x; y = f.y;
-}
-template <>
-__device__ __forceinline__ void ld2<double>(const double* p, double& x, double& y) {
-  const double2 f = *reinterpret_cast<const double2*>(p);
-  x = f.x; y = f.y;
-}
+__device__ __forceinline__ double ldv(const TV* p) { return (double)*p; }
 
 template <class TV, class TP>
-__global__ void __launch_bounds__(256) mvm64_kernel(const double* __restrict__ mtx, int64_t ldm, int64_t rows, int64_t n,
-                                                    const TV* __restrict__ v, int tp, int64_t row0,
-                                                    TP* __restrict__ p, double* __restrict__ apart,
-                                                    const Ctrl* __restrict__ done) {
+__global__ void __launch_bounds__(256, 3) mvm64_kernel(const double* __restrict__ mtx, int64_t ldm, int64_t rows, int64_t n,
+                                                       const TV* __restrict__ v, int tp, int64_t row0,
+                                                       TP* __restrict__ p, double* __restrict__ apart,
+                                                       const Ctrl* __restrict__ done) {
   if (done != nullptr && done->done) return;
-  __shared__ double as[2][MK][MB];
-  __shared__ double bs[2][MK][MB];
-  double (*red)[MB] = reinterpret_cast<double (*)[MB]>(&as[0][0][0]);   // epilogue reuse: 16 x MB
-  const int64_t i0 = (int64_t)blockIdx.x * MB;
-  const int c0 = blockIdx.y * MB;
-  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
-  // global -> register staging: A (128 rows x 8 k) and B (8 k x 128 cols), 2 double pairs each
-  double ra[4], rb[4];
-  auto load = [&](int64_t k0) {
-#pragma unroll
-    for (int it = 0; it < 2; ++it) {
-      const int e = tid + it * 256;
-      const int r = e / 4, kq = (e % 4) * 2;          // A: row r, k pair kq
-      const int64_t i = i0 + r, k = k0 + kq;
-      double x = 0.0, y = 0.0;
-      if (i < rows) {
-        // ldm even (padded): the pair is aligned; columns in [n, ldm) are zero
-        if (k < n) { const double2 f = *reinterpret_cast<const double2*>(mtx + i * ldm + k); x = f.x; y = f.y; }
-      }
-      ra[2 * it] = x; ra[2 * it + 1] = y;
-      const int kb = e / 64, cq = (e % 64) * 2;          // B: k row kb, column pair cq
-      const int64_t kr = k0 + kb;
-      const int cc = c0 + cq;
-      double bx = 0.0, by = 0.0;
-      if (kr < n && cc < tp) ld2<TV>(v + kr * tp + cc, bx, by);   // tp % 16 == 0: pairs never straddle
-      rb[2 * it] = bx; rb[2 * it + 1] = by;
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int it = 0; it < 2; ++it) {
-      const int e = tid + it * 256;
-      const int r = e / 4, kq = (e % 4) * 2;
-      as[buf][kq][r] = ra[2 * it];
-      as[buf][kq + 1][r] = ra[2 * it + 1];
-      const int kb = e / 64, cq = (e % 64) * 2;
-      bs[buf][kb][cq] = rb[2 * it];
-      bs[buf][kb][cq + 1] = rb[2 * it + 1];
-    }
-  };
-  double acc[8][8] = {};
+  extern __shared__ __align__(16) uint8_t smem64[];
+  double* As = reinterpret_cast<double*>(smem64);                       // [MST][MB][SA]
+  TV* Bs = reinterpret_cast<TV*>(smem64 + (size_t)MST * MB * SA * 8);   // [MST][MK][SB]
+  const int c0 = blockIdx.x * MBN;
+  const int rb = blockIdx.y;
+  const int64_t i0 = (int64_t)rb * MB;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 2, wn = warp & 3;        // warp tile rows wm*32.., cols wn*16..
   const int64_t nk = (n + MK - 1) / MK;
-  load(0);
-  store(0);
-  __syncthreads();
-  for (int64_t kt = 0; kt < nk; ++kt) {
-    const int buf = (int)(kt & 1);
-    if (kt + 1 < nk) load((kt + 1) * MK);
+  // one stage: A 64 rows x 16 k = 128 x 16 B (thread: row tid / 4 ... two chunks), B 16 k x 64 cols
+  auto issue = [&](int64_t kt, int st) {
+    const int64_t k0 = kt * MK;
+    double* a = As + (size_t)st * MB * SA;
 #pragma unroll
-    for (int k = 0; k < MK; ++k) {
-      double x[8], y[8];
-      // rows ty*4 + {0..3} and 64 + ty*4 + {0..3}; columns tx*4 + {0..3} and 64 + tx*4 + {0..3}
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const double2 a01 = *reinterpret_cast<const double2*>(&as[buf][k][h * 64 + ty * 4]);
-        const double2 a23 = *reinterpret_cast<const double2*>(&as[buf][k][h * 64 + ty * 4 + 2]);
-        const double2 b01 = *reinterpret_cast<const double2*>(&bs[buf][k][h * 64 + tx * 4]);
-        const double2 b23 = *reinterpret_cast<const double2*>(&bs[buf][k][h * 64 + tx * 4 + 2]);
-        x[4 * h + 0] = a01.x; x[4 * h + 1] = a01.y; x[4 * h + 2] = a23.x; x[4 * h + 3] = a23.y;
-        y[4 * h + 0] = b01.x; y[4 * h + 1] = b01.y; y[4 * h + 2] = b23.x; y[4 * h + 3] = b23.y;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int w = 0; w < 8; ++w) acc[u][w] = fma(x[u], y[w], acc[u][w]);
+    for (int e = tid; e < MB * (MK / 2); e += 256) {   // 512 chunks of 2 doubles
+      const int r = e >> 3, kc = (e & 7) * 2;
+      const int64_t i = i0 + r, k = k0 + kc;
+      const bool ok = i < rows && k < ldm;
+      cp16(a + r * SA + kc, ok ? (const void*)(mtx + i * ldm + k) : (const void*)mtx, ok);
     }
-    if (kt + 1 < nk) store(buf ^ 1);
-    __syncthreads();
+    TV* bsm = Bs + (size_t)st * MK * SB;
+    constexpr int EPC = 16 / sizeof(TV);               // elements per 16-byte chunk
+    constexpr int CPR = MBN / EPC;                     // chunks per k row
+#pragma unroll
+    for (int e = tid; e < MK * CPR; e += 256) {
+      const int kr = e / CPR, cc = (e % CPR) * EPC;
+      const int64_t k = k0 + kr;
+      const int col = c0 + cc;
+      const bool ok = k < n && col < tp;
+      cp16(bsm + kr * SB + cc, ok ? (const void*)(v + k * tp + col) : (const void*)v, ok);
+    }
+  };
+  double acc[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < MST - 1; ++st) {
+    if (st < nk) issue(st, st);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  // epilogue: write P, alpha partials over this tile's rows (fixed order: rows within a thread,
-  // then the 16 row-groups in order)
-  double cs[8];
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(MST - 2) : "memory");
+    __syncthreads();   // stage kt landed for every thread; stage kt - 1 is free for reuse
+    if (kt + MST - 1 < nk) issue(kt + MST - 1, (int)((kt + MST - 1) % MST));
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const int st = (int)(kt % MST);
+    const double* a = As + (size_t)st * MB * SA + (wm * 32 + fr) * SA + fk;
+    const TV* bsm = Bs + (size_t)st * MK * SB + fk * SB + wn * 16 + fr;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) cs[w] = 0.0;
+    for (int kk = 0; kk < MK; kk += 4) {
+      double af[4], bf[2];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int64_t i = i0 + (u / 4) * 64 + ty * 4 + (u % 4);
+      for (int mb = 0; mb < 4; ++mb) af[mb] = a[mb * 8 * SA + kk];
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) bf[nb] = ldv<TV>(bsm + kk * SB + nb * 8);
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[mb][nb][0]), "+d"(acc[mb][nb][1])
+                       : "d"(af[mb]), "d"(bf[nb]));
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  // epilogue: D fragment (row fr, columns 2 fk, 2 fk + 1 of each 8 x 8 tile); alpha partials in a
+  // fixed order (m-blocks of the lane, then lanes of a column chunk, then the two warp rows)
+  double cs[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int mb = 0; mb < 4; ++mb) {
+    const int64_t i = i0 + wm * 32 + mb * 8 + fr;
     if (i >= rows) continue;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      const int c = c0 + (w / 4) * 64 + tx * 4 + (w % 4);
+    for (int nb = 0; nb < 2; ++nb) {
+      const int c = c0 + wn * 16 + nb * 8 + 2 * fk;
       if (c >= tp) continue;
-      p[i * tp + c] = (TP)acc[u][w];
-      if (apart != nullptr) cs[w] = fma((double)v[(row0 + i) * tp + c], acc[u][w], cs[w]);
+      p[i * tp + c] = (TP)acc[mb][nb][0];
+      p[i * tp + c + 1] = (TP)acc[mb][nb][1];
+      if (apart != nullptr) {
+        cs[nb][0] = fma(ldv<TV>(v + (row0 + i) * tp + c), acc[mb][nb][0], cs[nb][0]);
+        cs[nb][1] = fma(ldv<TV>(v + (row0 + i) * tp + c + 1), acc[mb][nb][1], cs[nb][1]);
+      }
     }
   }
   if (apart != nullptr) {
 #pragma unroll
-    for (int w = 0; w < 8; ++w) red[ty][(w / 4) * 64 + tx * 4 + (w % 4)] = cs[w];
-    __syncthreads();
-    if (tid < MB) {
-      double s = 0.0;
-      for (int r = 0; r < 16; ++r) s += red[r][tid];
-      if (c0 + tid < tp) apart[(int64_t)blockIdx.x * tp + c0 + tid] = s;
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int xo = 4; xo < 32; xo <<= 1) cs[nb][e] += __shfl_xor_sync(0xffffffffu, cs[nb][e], xo);
+    __syncthreads();   // the ring is free: reuse it for the two warp rows' partials
+    double* red = reinterpret_cast<double*>(smem64);   // [2][MBN]
+    if (lane < 4) {
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) red[wm * MBN + wn * 16 + nb * 8 + 2 * lane + e] = cs[nb][e];
     }
+    __syncthreads();
+    if (tid < MBN && c0 + tid < tp) apart[(int64_t)rb * tp + c0 + tid] = red[tid] + red[MBN + tid];
   }
 }
 
@@ -281,19 +294,26 @@ cudaError_t launch_gemm64(bool ta, bool tb, int64_t m, int64_t n, int64_t kk, co
 
 int mvm64_blocks(int64_t rows) { return (int)((rows + MB - 1) / MB); }
 
+template <class TV, class TP>
+cudaError_t launch_mvm64_t(const double* m, int64_t ldm, int64_t rows, int64_t n, const TV* v, int tp, int64_t row0,
+                           TP* p, double* apart, const Ctrl* done, cudaStream_t s) {
+  const size_t smem = (size_t)MST * MB * SA * 8 + (size_t)MST * MK * SB * sizeof(TV);
+  auto k = mvm64_kernel<TV, TP>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(nblk(tp, MBN), (unsigned)mvm64_blocks(rows));   // column tiles fastest: a row block's M stays in L2
+  k<<<grid, 256, smem, s>>>(m, ldm, rows, n, v, tp, row0, p, apart, done);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mvm64(const double* m, int64_t ldm, int64_t rows, int64_t n, const void* v, bool v_double, int tp,
                          int64_t row0, void* p, bool p_double, double* apart, const Ctrl* done, cudaStream_t s) {
-  if (ldm % 2 != 0) return cudaErrorInvalidValue;
-  dim3 grid((unsigned)mvm64_blocks(rows), nblk(tp, MB));
+  if (ldm % 2 != 0 || tp % 16 != 0) return cudaErrorInvalidValue;
   if (v_double && p_double)
-    mvm64_kernel<double, double><<<grid, 256, 0, s>>>(m, ldm, rows, n, (const double*)v, tp, row0, (double*)p, apart, done);
-  else if (v_double)
-    mvm64_kernel<double, float><<<grid, 256, 0, s>>>(m, ldm, rows, n, (const double*)v, tp, row0, (float*)p, apart, done);
-  else if (p_double)
-    mvm64_kernel<float, double><<<grid, 256, 0, s>>>(m, ldm, rows, n, (const float*)v, tp, row0, (double*)p, apart, done);
-  else
-    mvm64_kernel<float, float><<<grid, 256, 0, s>>>(m, ldm, rows, n, (const float*)v, tp, row0, (float*)p, apart, done);
-  return cudaGetLastError();
+    return launch_mvm64_t(m, ldm, rows, n, (const double*)v, tp, row0, (double*)p, apart, done, s);
+  if (v_double) return launch_mvm64_t(m, ldm, rows, n, (const double*)v, tp, row0, (float*)p, apart, done, s);
+  if (p_double) return launch_mvm64_t(m, ldm, rows, n, (const float*)v, tp, row0, (double*)p, apart, done, s);
+  return launch_mvm64_t(m, ldm, rows, n, (const float*)v, tp, row0, (float*)p, apart, done, s);
 }
 
 cudaError_t launch_f32_to_f64(const float* src, int64_t ld, int64_t rows, int cols, double* dst, int tp,
