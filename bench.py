@@ -390,6 +390,8 @@ def run_ours(args, cfg):
     key = {"hbm": "mvm_dense2_kernel", "tensor": "mvm_tc2_kernel"}.get(roof["bound"])
     if impl_used == "sym":
         key = "mvm_sym_kernel"
+    if cfg.precond_rank > 0 and pinfo.get("fp64_route"):
+        key = "mvm64_kernel"
     ncu = ncu_metrics().get(f"{key}/{cfg.name}") if key else None
     roof["traffic"] = ncu["dram_bytes"] if ncu else None
     if ncu:
