@@ -78,10 +78,12 @@ typedef enum {
   CIQ_MVM_AUTO = 0,      /* tensor-core path where implemented, else SIMT fp32                  */
   CIQ_MVM_SIMT = 1,      /* fp32 CUDA-core tiles (reference kernel)                             */
   CIQ_MVM_TC = 2,        /* tcgen05 split-fp16 tensor-core kernel, full tiles (fails if unavailable) */
-  CIQ_MVM_TC_SYM = 3     /* tcgen05 symmetric-tile kernel: each k(x_i, x_j), i < j, evaluated once
+  CIQ_MVM_TC_SYM = 3,    /* tcgen05 symmetric-tile kernel: each k(x_i, x_j), i < j, evaluated once
                             and applied to both rows (single GPU, RBF / Matern, d <= 8, RHS chunk of
                             16 or 32 columns; fails if unavailable).  CIQ_MVM_AUTO picks it where
                             DESIGN.md section 8 measures it faster (RHS chunk of 16)              */
+  CIQ_MVM_FP64_TC = 4    /* reported only (ciq_info.mvm_impl_used): the fp64 route's materialised-M
+                            MVM on the FP64 tensor pipe (DMMA; params.fp64 / preconditioned)      */
 } ciq_mvm_impl;
 
 /* The operator K (touched only through MVMs, P:397 / P:1161-1162). */
@@ -208,11 +210,13 @@ typedef struct {
   int32_t mvm_timed;          /*   number of loop MVMs timed (= iters)                          */
   float ms_update;            /* profile_kernels: summed device time of the streaming updates    */
   int32_t update_timed;
-  int32_t mvm_impl_used;      /* ciq_mvm_impl of the loop MVMs: CIQ_MVM_SIMT or CIQ_MVM_TC       */
+  int32_t mvm_impl_used;      /* ciq_mvm_impl of the loop MVMs: SIMT, TC, TC_SYM or FP64_TC      */
   int32_t mvm_splits;         /* column splits of the tensor-core MVM grid (1 = none)            */
   int32_t fp64_route;         /* 1: solve on fp64 vectors (precond64.cu / params.fp64 / nested)   */
   int32_t nested_p_mvms;      /* nested CIQ (block-Jacobi P): MVMs with P spent on P^{1/2} b     */
   int32_t nested_iters;       /*   and the inner msMINRES iterations                             */
+  int32_t overlap;            /* row-sharded: 1 if the Lanczos-block all-gather ran next to the
+                                 local diagonal block's MVM */
 } ciq_info;
 
 typedef struct ciq_ctx ciq_ctx;

@@ -137,6 +137,16 @@ struct ciq_ctx {
   int64_t per = 0;            // rows per shard (multiple of 128; last shard may be shorter)
   int64_t nfull = 0;          // rows of the replicated (all-gathered) vectors = world * per >= n
   Comm* comm = nullptr;
+  // row-sharded overlap: the MVM's local column block runs on s2 while the
+  // Lanczos block's planes are all-gathered on `stream`; run_mvm applies mvm_win when on
+  struct MvmWinArgs {
+    bool on = false;
+    int lo = 0, hi = 0, skip_lo = 0, skip_hi = 0, no_diag = 0, grid_cap = 0;
+    int p_split_off = 0;       // first partial-product slot written
+    int64_t ap_row_off = 0;    // first alpha-partial row written
+  } mvm_win;
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* gsum = nullptr;     // [world][m] allgather buffer of cross-rank partial sums
   size_t gsum_cap = 0;
   double* tsum = nullptr;     // [tp] local sums
@@ -510,6 +520,14 @@ int plane_cols(const ciq_ctx* c, int tp) {
   return use_tc3(c, tp) ? tn / 2 : tn;
 }
 
+// Row-sharded overlap of the Lanczos-block all-gather with the local diagonal block's MVM (the
+// full-tile kernel on this rank's own column tiles, whose planes the streaming pass just wrote):
+// kernel operators on the tensor-core path, no preconditioner / posterior / derivative.
+bool use_overlap(const ciq_ctx* c, int impl, int tp) {
+  if (!c->sharded || !use_tc(c, impl, tp) || !is_kernel_op(c) || use_mat(c, tp) || use_tc3(c, tp)) return false;
+  return !c->pc.on && !c->post.on && !c->deriv && !experiment_env("CIQ_NO_OVERLAP");
+}
+
 // The symmetric-tile MVM (mvm_sym.cu): every k(x_i, x_j), i < j, evaluated once
 // and applied to rows i and j.  Single GPU (it needs the whole square), RBF / Matern with d <= 8,
 // RHS chunks of 16 or 32 columns.  CIQ_MVM_AUTO takes it for 16-column chunks, where the MVM is
@@ -591,6 +609,33 @@ void mvm_geometry(const ciq_ctx* c, int tp, int impl, int* nsplit, int64_t* nblk
   }
 }
 
+// Row-sharded overlap geometry (full-tile kernel only): this rank's rows [row0, row1) are also the
+// column tiles [lo, hi) of K whose V planes exist before the all-gather.  The remote launch covers
+// the other tiles ([0, lo) and [hi, ntiles)) with nsr splits / nbr alpha rows, the local launch the
+// window with nsl / nbl; the consumer sums nsr + nsl partial products, alpha nbr + nbl rows.
+struct OverlapGeo {
+  int lo, hi, nsr, nsl;
+  int64_t nbr, nbl;
+};
+constexpr int kOverlapReservedSMs = 16;   // SMs left to the concurrent all-gather (NCCL kernels)
+bool use_overlap(const ciq_ctx* c, int impl, int tp);
+OverlapGeo overlap_geometry(const ciq_ctx* c, int tp) {
+  OverlapGeo g{};
+  const int64_t rows = c->row1 - c->row0;
+  const int chunks = tp / tc_chunk_cols(tp);
+  const int nsm = sm_count();
+  const int ntiles = (int)((c->op.n + 63) / 64);
+  g.lo = (int)(c->row0 / 64);
+  g.hi = (int)std::min<int64_t>(ntiles, (c->row1 + 63) / 64);
+  const int nloc = g.hi - g.lo, nrem = ntiles - nloc;
+  const int capl = std::max(1, nsm - kOverlapReservedSMs);
+  g.nsl = tc2_choose_nsplit(rows, (int64_t)nloc * 64, chunks, capl);
+  g.nsr = nrem > 0 ? tc2_choose_nsplit(rows, (int64_t)nrem * 64, chunks, nsm) : 0;
+  g.nbl = (rows + 255) / 256 * g.nsl * 8;
+  g.nbr = (rows + 255) / 256 * g.nsr * 8;
+  return g;
+}
+
 // Allocate every buffer run_mvm(tp, allow_split) may need (so a CUDA-graph capture never
 // allocates).
 ciq_status post_buffers(ciq_ctx* c, int tp);
@@ -620,6 +665,16 @@ ciq_status prepare_mvm_buffers(ciq_ctx* c, int tp, int impl) {
     dfree(c->inv_scale);
     CUDA_TRY(c, dalloc(&c->inv_scale, (size_t)tp));
     c->inv_scale_n = tp;
+  }
+  if (use_overlap(c, impl, tp)) {   // the two windowed launches' partial products / alpha rows
+    const OverlapGeo og = overlap_geometry(c, tp);
+    nsplit = std::max(nsplit, og.nsr + og.nsl);
+    nblk = std::max<int64_t>(nblk, og.nbr + og.nbl);
+    if (c->s2 == nullptr) {
+      CUDA_TRY(c, cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
   }
   if (nsplit > 1) {
     st = grow(c, &c->psplit, &c->psplit_elems, (size_t)nsplit * rows * tp);
@@ -683,6 +738,15 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   int nsplit = 1;
   int64_t nblk = 0;
   mvm_geometry(c, tp, impl, &nsplit, &nblk);
+  const bool win = c->mvm_win.on && !dense && !sym && !use_tc3(c, tp) && nsplit_out != nullptr;
+  if (c->mvm_win.on && !win) return set_err(c, CIQ_ERR_INVALID_ARG, "internal: windowed MVM needs the full-tile kernel");
+  if (win) {   // one column window of the row-sharded overlap (overlap_geometry)
+    const ciq_ctx::MvmWinArgs& w = c->mvm_win;
+    const int ntw = (w.hi - w.lo) - (w.skip_hi - w.skip_lo);
+    const int capw = w.grid_cap > 0 ? std::min(w.grid_cap, nsm) : nsm;
+    nsplit = tc2_choose_nsplit(rows, (int64_t)ntw * 64, chunks, capw);
+    nblk = (rows + 255) / 256 * nsplit * 8;
+  }
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * vrows(c) * tp);
   if (st != CIQ_OK) return st;
   if (c->inv_scale_n < tp) {
@@ -692,16 +756,18 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     c->inv_scale_n = tp;
   }
   float* pout = p;
-  if (nsplit > 1) {
-    st = grow(c, &c->psplit, &c->psplit_elems, (size_t)nsplit * rows * tp);
+  if (nsplit > 1 || win) {
+    const size_t off = win ? (size_t)c->mvm_win.p_split_off : 0;
+    st = grow(c, &c->psplit, &c->psplit_elems, (off + nsplit) * rows * tp);
     if (st != CIQ_OK) return st;
-    pout = c->psplit;
+    pout = c->psplit + off * rows * tp;
   }
   double* ap = apart;
   if (apart != nullptr) {
-    st = grow(c, &c->apart_tc, &c->apart_tc_elems, (size_t)nblk * tp);
+    const size_t off = win ? (size_t)c->mvm_win.ap_row_off : 0;
+    st = grow(c, &c->apart_tc, &c->apart_tc_elems, (off + nblk) * tp);
     if (st != CIQ_OK) return st;
-    ap = c->apart_tc;
+    ap = c->apart_tc + off * tp;
   }
   // (skip_pack: the previous streaming pass already wrote v's split planes and inv_scale)
   if (!skip_pack)
@@ -734,6 +800,14 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   a.kf = c->kf;
   a.nunits = dense ? (int)((rows + 127) / 128) * nsplit * chunks
                    : (pair ? tc3_units(rows, nsplit, chunks) : tc2_units(rows, nsplit, chunks));
+  if (win) {
+    a.win_lo = c->mvm_win.lo;
+    a.win_hi = c->mvm_win.hi;
+    a.skip_lo = c->mvm_win.skip_lo;
+    a.skip_hi = c->mvm_win.skip_hi;
+    a.no_diag = c->mvm_win.no_diag;
+    a.grid_cap = c->mvm_win.grid_cap;
+  }
 #ifdef CIQ_TC_TRACE
   a.dbg = getenv("CIQ_TC_DEBUG") ? atoi(getenv("CIQ_TC_DEBUG")) : 0;
   if ((a.dbg & 128) && !dense) {
@@ -1658,6 +1732,9 @@ void ciq_free(ciq_ctx* c) {
   dfree(c->stash); dfree(c->hist);
   dfree(c->vjp_xb); dfree(c->vjp_xv); dfree(c->vjp_y); dfree(c->vjp_g); dfree(c->vjp_w);
   dfree(c->apart_tc); dfree(c->cta_part); dfree(c->ticket);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->s2) cudaStreamDestroy(c->s2);
   dfree(c->sym_units); dfree(c->sym_base); dfree(c->sym_part);
   free_precond(c->pc);
   free_post(c->post);
@@ -2162,6 +2239,8 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     if (st != CIQ_OK) return st;
     LAUNCH(c, launch_pack_v(ws.w[1], c->op.n, vrows(c), tp, plane_cols(c, tp), sc.nrm_cur, c->planes, c->inv_scale, s));
   }
+  const bool overlap = fuse_pack && use_overlap(c, p.mvm_impl, tp);
+  const OverlapGeo og = overlap ? overlap_geometry(c, tp) : OverlapGeo{};
   auto enqueue_iter = [&](int j, int nqe) -> ciq_status {
     float* wcur = ws.w[j % 3];
     float* wprev = ws.w[(j + 2) % 3];
@@ -2171,16 +2250,51 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     double* apart = nullptr;
     // single GPU, tensor-core MVM: the streaming pass of iteration j writes W_{j+1}'s split-fp16
     // planes, so iteration j+1 skips pack_v (the first iteration of a block always packs)
-    c->alpha_fuse = P.on ? nullptr : &sc;   // the full-tile kernel computes alpha_j in its tail
-    ciq_status st2 = P.on ? apply_m(wcur, ws.p, &apart, &nbm)
-                          : run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit,
-                                    &apart, &nbm, fuse_pack);
-    c->alpha_fuse = nullptr;
+    ciq_status st2 = CIQ_OK;
+    if (overlap) {
+      // row-sharded overlap: W_j's planes of this rank's rows were written by the
+      // previous streaming pass, so the MVM of the local diagonal block (K[rows, rows] W_j[rows],
+      // on s2, sigma^2 W_j included) runs while the ranks all-gather W_j's planes on `stream`;
+      // then the remote column tiles.  The consumer sums both launches' partial products.
+      CUDA_TRY(c, cudaEventRecord(c->ev_fork, s));
+      CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_fork, 0));
+      int nsl = 0, nbl = 0;
+      double* apl = nullptr;
+      c->mvm_win = ciq_ctx::MvmWinArgs{true, og.lo, og.hi, 0, 0, 0, std::max(1, sm_count() - kOverlapReservedSMs),
+                                       og.nsr, og.nbr};
+      c->stream = c->s2;
+      st2 = run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsl, &apl, &nbl, true);
+      c->stream = s;
+      c->mvm_win = ciq_ctx::MvmWinArgs{};
+      if (st2 != CIQ_OK) return st2;
+      CUDA_TRY(c, cudaEventRecord(c->ev_join, c->s2));
+      st2 = allgather_planes(c, tp);
+      if (st2 != CIQ_OK) return st2;
+      CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_join, 0));
+      if (og.nsr > 0) {
+        int nsr = 0, nbr = 0;
+        double* apr = nullptr;
+        c->mvm_win = ciq_ctx::MvmWinArgs{true, 0, 0, og.lo, og.hi, 1, 0, 0, 0};
+        c->mvm_win.hi = (int)((c->op.n + 63) / 64);
+        st2 = run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsr, &apr, &nbr, true);
+        c->mvm_win = ciq_ctx::MvmWinArgs{};
+        if (st2 != CIQ_OK) return st2;
+      }
+      nsplit = og.nsr + og.nsl;
+      nbm = (int)(og.nbr + og.nbl);
+      apart = c->apart_tc;
+    } else {
+      c->alpha_fuse = P.on ? nullptr : &sc;   // the full-tile kernel computes alpha_j in its tail
+      st2 = P.on ? apply_m(wcur, ws.p, &apart, &nbm)
+                 : run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit,
+                           &apart, &nbm, fuse_pack);
+      c->alpha_fuse = nullptr;
+    }
     const bool alpha_done = !P.on && c->alpha_fused;
     c->alpha_fused = false;
     end_timed(c);
     if (st2 != CIQ_OK) return st2;
-    const float* pin = (nsplit > 1) ? c->psplit : ws.p;
+    const float* pin = (nsplit > 1 || overlap) ? c->psplit : ws.p;
     loop_nsplit = nsplit;
     loop_impl = c->mvm_kind_used;
     if (!c->sharded) {
@@ -2209,9 +2323,12 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
       if (st2 != CIQ_OK) return st2;
       LAUNCH(c, launch_givens(sc, tsum_b, 1, nqe, tp, s, stored ? c->bhist : nullptr, hlen));
       // next Lanczos block to every rank: its split-fp16 planes when the streaming
-      // pass packed them, else the fp32 rows
-      st2 = fuse_pack ? allgather_planes(c, tp) : allgather_rows(c, wnew, tp);
-      if (st2 != CIQ_OK) return st2;
+      // pass packed them, else the fp32 rows (overlap: the planes at the start of the next
+      // iteration, next to the local block's MVM)
+      if (!overlap) {
+        st2 = fuse_pack ? allgather_planes(c, tp) : allgather_rows(c, wnew, tp);
+        if (st2 != CIQ_OK) return st2;
+      }
     }
     return CIQ_OK;
   };
@@ -2403,6 +2520,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     cudaEventElapsedTime(&info->ms_final, ev.e[3], ev.e[4]);
     info->kernel_launches = c->launches;
     info->mvm_impl_used = loop_impl;
+    info->overlap = overlap ? 1 : 0;
     info->mvm_splits = loop_nsplit;
     info->fp64_route = 0;
     for (auto& tm : c->timed) {
@@ -2566,7 +2684,7 @@ ciq_status apply_fp64(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float*
     cudaEventElapsedTime(&info->ms_loop, ev.e[2], ev.e[3]);
     cudaEventElapsedTime(&info->ms_final, ev.e[3], ev.e[4]);
     info->kernel_launches = c->launches;
-    info->mvm_impl_used = CIQ_MVM_SIMT;   // fp64 FMA pipe (mvm64_kernel)
+    info->mvm_impl_used = CIQ_MVM_FP64_TC;   // FP64 tensor pipe (mvm64_kernel, DMMA)
     info->mvm_splits = 1;
     info->fp64_route = 1;
     for (auto& tm : c->timed) {
@@ -2963,7 +3081,7 @@ ciq_status apply_nested(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, floa
     cudaEventElapsedTime(&info->ms_lambda, ev.e[1], ev.e[2]);
     cudaEventElapsedTime(&info->ms_loop, ev.e[2], ev.e[3]);
     cudaEventElapsedTime(&info->ms_final, ev.e[3], ev.e[4]);
-    info->mvm_impl_used = CIQ_MVM_SIMT;
+    info->mvm_impl_used = CIQ_MVM_FP64_TC;   // K MVMs on the FP64 tensor pipe (mvm64_kernel, DMMA)
     info->mvm_splits = 1;
     info->fp64_route = 1;
     info->nested_p_mvms = pmvms;

@@ -99,7 +99,20 @@ struct TcArgs {
   const int* alpha_frozen;
   double* cta_part;
   unsigned* ticket;
+  // column window of the full-tile kernel (row-sharded overlap): the launch covers the
+  // 64-column tiles [win_lo, win_hi) minus [skip_lo, skip_hi) (win_hi = 0: all tiles, no skip);
+  // no_diag: do not add sigma^2 V (another launch of the same product adds it); grid_cap: at most
+  // that many CTAs (0: one per SM) -- leaves SMs to a concurrent collective
+  int win_lo, win_hi, skip_lo, skip_hi, no_diag, grid_cap;
 };
+// tiles of a (possibly windowed) full-tile launch
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int tc2_window_tiles(const TcArgs& a) {
+  const int all = (int)((a.n + 63) / 64);
+  return (a.win_hi > 0 ? a.win_hi - a.win_lo : all) - (a.skip_hi - a.skip_lo);
+}
 int tc_chunk_cols(int tp);
 // tn: column width of one layout chunk (tc_chunk_cols(tp), halved for the pair kernel)
 cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, int tn, const double* nrm, __half* planes,

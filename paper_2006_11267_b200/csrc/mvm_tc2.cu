@@ -90,6 +90,13 @@ enum : uint32_t {
   F_KB = 1u << 8,       // A-rows buffer of S(g+3)'s unit
 };
 
+// 64-column tile of K of the launch's t-th tile (its column window, TcArgs::win_* / skip_*)
+CIQ_DEVICE int window_tile(const TcArgs& a, int t) {
+  int j = (a.win_hi > 0 ? a.win_lo : 0) + t;
+  if (a.skip_hi > a.skip_lo && j >= a.skip_lo) j += a.skip_hi - a.skip_lo;
+  return j;
+}
+
 // Position in the flattened tile sequence of one CTA: unit u (local index k), tile jj of njt.
 struct Cur {
   int k, u, jj, njt, jt0, split, chunk, rt;
@@ -116,7 +123,7 @@ struct Cur {
       if (u < a.nunits) decode(a, ntiles);
     }
   }
-  CIQ_DEVICE int J() const { return jt0 + jj; }
+  CIQ_DEVICE int J(const TcArgs& a) const { return window_tile(a, jt0 + jj); }
 };
 
 // KV(J) of one half: O_h (+)= K_h . V_J, 4 K-steps x (k_hi.v_hi, k_hi.v_lo, k_lo.v_hi) = 12 TS MMAs,
@@ -179,7 +186,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t n = args.n;
-  const int ntiles = (int)((n + BN2 - 1) / BN2);
+  const int ntiles = tc2_window_tiles(args);   // this launch's column tiles
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 2); }
@@ -210,7 +217,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         const int npro = c.njt < NB2 ? c.njt : NB2;
         mbar_arrive_expect_tx(&bars->pro_full, npro * C::F_BYTES);
         for (int i = 0; i < npro; ++i)
-          bulk_g2s(pro + i * C::F_BYTES, args.feat_b + (size_t)(c.jt0 + i) * BN2 * KF2, C::F_BYTES, &bars->pro_full);
+          bulk_g2s(pro + i * C::F_BYTES, args.feat_b + (size_t)window_tile(args, c.jt0 + i) * BN2 * KF2, C::F_BYTES, &bars->pro_full);
         f = c;
         for (int i = 0; i < NB2; ++i) f.advance(args, ntiles);
       }
@@ -240,10 +247,10 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         }
         uint8_t* sb = ring + st * C::STAGE;
         mbar_arrive_expect_tx(&bars->full[st], 2 * C::V_BYTES + (fv ? C::F_BYTES : 0));
-        const __half* vh = args.vplanes + (size_t)c.chunk * 2 * plane + (size_t)c.J() * BN2 * TN;
+        const __half* vh = args.vplanes + (size_t)c.chunk * 2 * plane + (size_t)c.J(args) * BN2 * TN;
         bulk_g2s(sb, vh, C::V_BYTES, &bars->full[st]);
         bulk_g2s(sb + C::V_BYTES, vh + plane, C::V_BYTES, &bars->full[st]);
-        if (fv) bulk_g2s(sb + 2 * C::V_BYTES, args.feat_b + (size_t)f.J() * BN2 * KF2, C::F_BYTES, &bars->full[st]);
+        if (fv) bulk_g2s(sb + 2 * C::V_BYTES, args.feat_b + (size_t)f.J(args) * BN2 * KF2, C::F_BYTES, &bars->full[st]);
         c.advance(args, ntiles);
         if (fv) f.advance(args, ntiles);
       }
@@ -419,7 +426,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
           r4.y = args.o2 * ov.y * s4.y;
           r4.z = args.o2 * ov.z * s4.z;
           r4.w = args.o2 * ov.w * s4.w;
-          if (u.split == 0) {
+          if (u.split == 0 && !args.no_diag) {
             r4.x = fmaf(args.diag, vv.x, r4.x); r4.y = fmaf(args.diag, vv.y, r4.y);
             r4.z = fmaf(args.diag, vv.z, r4.z); r4.w = fmaf(args.diag, vv.w, r4.w);
           }
@@ -468,7 +475,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         for (int ch = 0; ch < NCH; ++ch) {
           const int cc = ch;
           const uint32_t tb = tbase + b * 128 + 64 * h + 32 * cc + lane_base;
-          const int64_t jcol0 = (int64_t)c.J() * BN2 + 32 * cc;
+          const int64_t jcol0 = (int64_t)c.J(args) * BN2 + 32 * cc;
           uint32_t sv[32];
           tmem_ld32(tb, sv);
           tmem_ld_wait();
@@ -594,7 +601,8 @@ int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm, int min_tile
 
 cudaError_t launch_mvm_tc2(const TcArgs& a, int nsm, cudaStream_t s) {
   const int tn = tc_chunk_cols(a.tp);
-  const int grid = a.nunits < nsm ? a.nunits : nsm;
+  const int cap = a.grid_cap > 0 && a.grid_cap < nsm ? a.grid_cap : nsm;
+  const int grid = a.nunits < cap ? a.nunits : cap;
   switch (a.kind) {
     case 1: return launch2_kind<1>(a, tn, grid, s);
     case 2: return launch2_kind<2>(a, tn, grid, s);

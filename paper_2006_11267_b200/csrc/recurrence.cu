@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? CIQ_UPD_MINB : 2) l
       const Vec4<T> wp = ld4<T>(wprev + off);
       if (!final_only) {
         Vec4<T> pp = ld4<T>(p + off);
-        for (int sp = 1; sp < nsplit; ++sp) {
+        for (int sp = 1; sp < nsplit; ++sp) {   // the MVM's column-split partial products, split order
           const Vec4<T> q4 = ld4<T>(p + sp * split_stride + off);
           pp.x += q4.x; pp.y += q4.y; pp.z += q4.z; pp.w += q4.w;
         }
@@ -608,9 +608,14 @@ __global__ void sum_splits_kernel(const float* __restrict__ parts, int nsplit, s
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n4) return;
   float4 acc = reinterpret_cast<const float4*>(parts)[e];
-  for (int s = 1; s < nsplit; ++s) {
-    const float4 q = reinterpret_cast<const float4*>(parts + s * stride)[e];
-    acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+  for (int s = 1; s < nsplit; s += 4) {   // split order; 4 loads in flight
+    float4 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (s + u < nsplit) q[u] = reinterpret_cast<const float4*>(parts + (s + u) * stride)[e];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (s + u < nsplit) { acc.x += q[u].x; acc.y += q[u].y; acc.z += q[u].z; acc.w += q[u].w; }
   }
   reinterpret_cast<float4*>(out)[e] = acc;
 }

@@ -69,6 +69,8 @@ def test_sharded_equals_single_gpu(world, impl):
     for inf in infos[1:]:
         assert inf["lambda_max"] == infos[0]["lambda_max"] and inf["iters"] == infos[0]["iters"]
     assert abs(infos[0]["lambda_max"] / info1["lambda_max"] - 1) < 1e-6
+    # the tensor-core path all-gathers the Lanczos block next to the local diagonal block's MVM
+    assert all(inf["overlap"] == (impl == "tc") for inf in infos), [inf["overlap"] for inf in infos]
 
 
 def test_sharded_tolerance_stop_and_oracle():
@@ -124,6 +126,9 @@ def test_nccl_one_rank_sharded_path(dense):
     (a, ia), (b, ib) = outs
     assert ia["converged"] and ib["converged"] and abs(ia["iters"] - ib["iters"]) <= 2
     assert np.linalg.norm(a - b) / np.linalg.norm(a) < 1e-5
+    # matrix-free: the captured iteration graph forks the local block's MVM onto a side stream next
+    # to the NCCL all-gather (world 1: the local block is every column tile)
+    assert ib["overlap"] == (not dense) and not ia["overlap"]
 
 
 @pytest.mark.parametrize("world", [2, 3])
