@@ -280,6 +280,9 @@ CIQ_DEVICE float pack_scale(double nrm, double sqrt_n, float* inv) {
 #ifndef CIQ_UPD_QB
 #define CIQ_UPD_QB 2        // shifts whose d-vector loads are in flight together
 #endif
+#ifndef CIQ_UPD_SG
+#define CIQ_UPD_SG 1        // partial-product loads grouped per iteration (A/B: scripts/ab_update_sg.sh)
+#endif
 #ifndef CIQ_UPD_MINB
 #define CIQ_UPD_MINB 3      // resident CTAs per SM the register budget is sized for
 #endif
@@ -347,9 +350,15 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? CIQ_UPD_MINB : 2) l
       const Vec4<T> wp = ld4<T>(wprev + off);
       if (!final_only) {
         Vec4<T> pp = ld4<T>(p + off);
-        for (int sp = 1; sp < nsplit; ++sp) {   // the MVM's column-split partial products, split order
-          const Vec4<T> q4 = ld4<T>(p + sp * split_stride + off);
-          pp.x += q4.x; pp.y += q4.y; pp.z += q4.z; pp.w += q4.w;
+        // the MVM's column-split partial products, summed in split order, CIQ_UPD_SG loads in flight
+        for (int sp = 1; sp < nsplit; sp += CIQ_UPD_SG) {
+          Vec4<T> q4[CIQ_UPD_SG];
+#pragma unroll
+          for (int u = 0; u < CIQ_UPD_SG; ++u)
+            if (sp + u < nsplit) q4[u] = ld4<T>(p + (sp + u) * split_stride + off);
+#pragma unroll
+          for (int u = 0; u < CIQ_UPD_SG; ++u)
+            if (sp + u < nsplit) { pp.x += q4[u].x; pp.y += q4[u].y; pp.z += q4[u].z; pp.w += q4[u].w; }
         }
         const Vec4<T> wc = ld4<T>(wcur + off);
         Vec4<T> w;
