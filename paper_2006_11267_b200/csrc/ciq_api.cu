@@ -826,7 +826,10 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     a.sym_slots = c->sym_slots;
   }
   c->alpha_fused = false;
-  if (!dense && !sym && !pair && ap != nullptr && c->alpha_fuse != nullptr && !c->sharded && !c->post.on &&
+#ifdef CIQ_NO_ALPHA_FUSE
+  c->alpha_fuse = nullptr;   // experiments only: the separate alpha pass
+#endif
+  if (!dense && !sym && !pair && !win && ap != nullptr && c->alpha_fuse != nullptr && !c->sharded && !c->post.on &&
       !c->deriv && c->cta_part != nullptr &&
       c->cta_part_elems >= (size_t)nsm * tp && c->ticket != nullptr) {
     a.alpha_out = c->alpha_fuse->alpha;

@@ -90,7 +90,7 @@ struct TcArgs {
   const int* sym_base;       // [sym_nb + 1] first partial slot of each 128-row block
   float* sym_part;           // [chunks][sym_slots][128][TN] fp32 partial products
   int sym_nb, sym_ng, sym_b, sym_slots;
-  // fused alpha (mvm_tc2.cu, single-GPU recurrence; null: off): after its read-outs each CTA sums
+  // fused alpha (mvm_tc2.cu; single-GPU recurrence; null: off): after its read-outs each CTA sums
   // its own units' alpha partials into cta_part[blockIdx][tp] (unit order, slot order); the last CTA
   // to finish (ticket) sums those in CTA order and writes alpha_out[c] = sum / nrm[c]^2 (0 for
   // frozen columns) -- the alpha_kernel pass without its launch

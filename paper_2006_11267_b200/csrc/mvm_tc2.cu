@@ -536,11 +536,37 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
     __syncthreads();
     if (s_last) {
       __threadfence();
-      for (int col = threadIdx.x; col < tp; col += NT2) {
+      // the CTAs' rows in G = NT2 / tp contiguous groups (fixed), each summed in CTA order by one
+      // thread per column (L2 loads, __ldcg: published by the other CTAs' fence + ticket), then the
+      // groups in order
+      double* s_grp = reinterpret_cast<double*>(smem);   // [NT2]: the ring is free now
+      const int nb = (int)gridDim.x;
+      const int G = tp <= NT2 ? NT2 / tp : 1;
+      const int grp = threadIdx.x / tp, col = threadIdx.x % tp;
+      if (grp < G) {
+        const int b0 = nb * grp / G, b1 = nb * (grp + 1) / G;
         double sum = 0.0;
-        for (int b = 0; b < (int)gridDim.x; ++b) sum += ((volatile double*)args.cta_part)[(size_t)b * tp + col];
-        const double nr = args.alpha_nrm[col];
-        args.alpha_out[col] = args.alpha_frozen[col] ? 0.0 : sum / (nr * nr);
+        int b = b0;
+        for (; b + 4 <= b1; b += 4) {
+          double x[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) x[e] = __ldcg(args.cta_part + (size_t)(b + e) * tp + col);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sum += x[e];
+        }
+        for (; b < b1; ++b) sum += __ldcg(args.cta_part + (size_t)b * tp + col);
+        if (tp <= NT2) s_grp[threadIdx.x] = sum;
+      }
+      __syncthreads();
+      for (int cc = threadIdx.x; cc < tp; cc += NT2) {
+        double sum = 0.0;
+        if (tp <= NT2) {
+          for (int gg = 0; gg < G; ++gg) sum += s_grp[gg * tp + cc];
+        } else {
+          for (int bb = 0; bb < nb; ++bb) sum += __ldcg(args.cta_part + (size_t)bb * tp + cc);
+        }
+        const double nr = args.alpha_nrm[cc];
+        args.alpha_out[cc] = args.alpha_frozen[cc] ? 0.0 : sum / (nr * nr);
       }
       if (threadIdx.x == 0) *args.ticket = 0u;   // for the next launch (stream-ordered)
     }
