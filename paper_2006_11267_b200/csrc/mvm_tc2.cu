@@ -46,8 +46,20 @@ constexpr int BN2 = 64;             // columns per tile
 constexpr int KF2 = 32;             // feature contraction
 constexpr int NT2 = 640;            // 4 role warps + 16 epilogue warps
 constexpr int EPI0 = 4;
-constexpr int NB2 = 3;              // S/K TMEM buffers
-constexpr int TMO = NB2 * 128;      // O accumulators at [384, 384 + 2 TN)
+// TMEM: S/K buffers x 128 columns + O slots x 2 TN.  Round 2, with the 66-tile accumulation chains
+// (16 units per CTA at C3): 2 S/K buffers + 2 O slots beat 3 + 1 (MVM 0.99-1.00 vs 1.01-1.02 ms,
+// profiles/ab_k1_oslots_r02.txt) -- the unit read-out no longer stalls the next unit's first KV,
+// which outweighs the shallower S look-ahead.
+#ifndef CIQ_TC2_NB
+#define CIQ_TC2_NB 2
+#endif
+#ifndef CIQ_TC2_OSLOTS
+#define CIQ_TC2_OSLOTS 2
+#endif
+constexpr int NB2 = CIQ_TC2_NB;     // S/K TMEM buffers
+constexpr int NO2 = CIQ_TC2_OSLOTS; // O accumulator slots (2: the next unit's KV never waits for a read-out)
+constexpr int TMO = NB2 * 128;      // O slot s, half h at TMO + s 2 TN + h TN
+static_assert(NB2 * 128 + NO2 * 128 <= 512 && NO2 >= 1 && NO2 <= 2, "TMEM budget (TN <= 64)");
 // Ping-pong epilogue (measured: 0.937 vs 1.088 ms per C3 MVM for all 16 warps on every tile,
 // profiles/): two groups of 8 warps take alternate tiles.
 constexpr int EPI_ARRIVALS = 4;    // epilogue warps per tile and half
@@ -71,7 +83,7 @@ struct Bars2 {
   uint64_t full[8], empty[8];              // smem ring (empty: one commit per MMA warp)
   uint64_t s_full[NB2][2], k_full[NB2][2];   // per TMEM buffer and 128-row half
   uint64_t a_full[2], a_empty[2];
-  uint64_t pro_full, o_full[2], o_empty[2];
+  uint64_t pro_full, o_full[NO2][2], o_empty[NO2][2];
   uint32_t tmem_base;
   uint32_t flags[8];   // per ring stage: the MMA issuers' schedule for that tile (written by the producer)
 };
@@ -88,6 +100,7 @@ enum : uint32_t {
   F_APH = 1u << 6,
   F_SLAST = 1u << 7,    // S(g+3) is the last tile of its unit: commit a_empty[F_KB]
   F_KB = 1u << 8,       // A-rows buffer of S(g+3)'s unit
+  F_OSLOT = 1u << 9,    // O slot of tile g's unit (NO2 = 2)
 };
 
 // 64-column tile of K of the launch's t-th tile (its column window, TcArgs::win_* / skip_*)
@@ -194,7 +207,8 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
       for (int h = 0; h < 2; ++h) { mbar_init(&bars->s_full[b][h], 1); mbar_init(&bars->k_full[b][h], EPI_ARRIVALS); }
     for (int b = 0; b < 2; ++b) { mbar_init(&bars->a_full[b], 1); mbar_init(&bars->a_empty[b], 2); }
     mbar_init(&bars->pro_full, 1);
-    for (int h = 0; h < 2; ++h) { mbar_init(&bars->o_full[h], 1); mbar_init(&bars->o_empty[h], RO_ARRIVALS); }
+    for (int o = 0; o < NO2; ++o)
+      for (int h = 0; h < 2; ++h) { mbar_init(&bars->o_full[o][h], 1); mbar_init(&bars->o_empty[o][h], RO_ARRIVALS); }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
@@ -237,7 +251,9 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
           uint32_t fl = 0;
           if (c.jj > 0) fl |= F_ACC;
           if (c.jj == c.njt - 1) fl |= F_OLAST;
-          if (c.jj == 0 && c.k > 0) fl |= F_OWAIT | (((c.k - 1) & 1) ? F_OPH : 0u);
+          // the first KV of unit k overwrites O slot k % NO2: unit k - NO2 must be read out
+          if (c.jj == 0 && c.k >= NO2) fl |= F_OWAIT | ((((c.k - NO2) / NO2) & 1) ? F_OPH : 0u);
+          if (NO2 > 1 && (c.k & 1)) fl |= F_OSLOT;
           if (fv) {
             fl |= F_SVALID | ((f.k & 1) ? F_KB : 0u);
             if (f.jj == 0) fl |= F_SFIRST | (((f.k >> 1) & 1) ? F_APH : 0u);
@@ -274,7 +290,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
     const uint64_t dring_f = smem_desc(smem_u32(ring) + 2 * C::V_BYTES, 128, (KF2 / 8) * 128);
     const uint64_t dring_v = smem_desc(smem_u32(ring), (TN / 8) * 128, 128);
     const uint32_t tb_h = tbase + 64 * h;         // half h of every S / K buffer
-    const uint32_t to_h = tbase + TMO + TN * h;   // O_h
+    const uint32_t to_h0 = tbase + TMO + TN * h;   // O_h of slot 0 (slot 1 at + 2 TN)
     if (kv.valid(args)) {
       mbar_wait(&bars->a_full[0], 0);
       mbar_wait(&bars->pro_full, 0);
@@ -307,7 +323,9 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
       if (h == 0) T2_STAMP(3, g);
       mbar_wait(&bars->k_full[b][h], ph_b);
       if (h == 0) T2_STAMP(2, g);
-      if (fl & F_OWAIT) mbar_wait(&bars->o_empty[h], (fl & F_OPH) ? 1u : 0u);
+      const int oslot = (fl & F_OSLOT) ? 1 : 0;
+      if (fl & F_OWAIT) mbar_wait(&bars->o_empty[oslot][h], (fl & F_OPH) ? 1u : 0u);
+      const uint32_t to_h = to_h0 + oslot * 2 * TN;
       fence_after_sync();
       const uint32_t soff16 = (uint32_t)((st * C::STAGE) >> 4);
       // __shfl_sync(.., 0): values the compiler treats as warp-uniform (uniform registers, no
@@ -316,7 +334,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
       const uint64_t dvu = shfl64(dring_v + soff16);
       if (elect_one()) {
         if (!(args.dbg & 1)) mma_kv12<TN>(to_h, kbu, dvu, idesc_o, fl & F_ACC);
-        if (fl & F_OLAST) commit_one(&bars->o_full[h]);
+        if (fl & F_OLAST) commit_one(&bars->o_full[oslot][h]);
       }
       __syncwarp();
       if (h == 0) T2_STAMP(9, g);
@@ -386,7 +404,8 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
       // V one pass ahead (its L2 latency overlaps the O wait and the previous pass)
       float4 vn[4];
       vload(0, vn);
-      mbar_wait(&bars->o_full[h], u.k & 1);
+      const int oslot = u.k % NO2;
+      mbar_wait(&bars->o_full[oslot][h], (u.k / NO2) & 1);
       if (warp == 4 || warp == 12) T2_STAMP(11, u.k);
       fence_after_sync();
       const int sw = (lane >> 1) & 3;   // swizzle of this lane's row in the row-per-lane phase
@@ -397,7 +416,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) vc[k] = vn[k];
         uint32_t o[16];
-        const uint32_t ta = tbase + TMO + TN * h + c0 + lane_base;
+        const uint32_t ta = tbase + TMO + oslot * 2 * TN + TN * h + c0 + lane_base;
         tmem_ld8(ta, &o[0]);
         tmem_ld8(ta + 8, &o[8]);
         if (pass + 1 < NP) vload(c0 + 16, vn);
@@ -406,7 +425,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         if (pass == NP - 1) {   // O_h is in registers: the next unit's first KV may overwrite it
           fence_before_sync();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&bars->o_empty[h]);
+          if (lane == 0) mbar_arrive(&bars->o_empty[oslot][h]);
           if (warp == 4 || warp == 12) T2_STAMP(12, u.k);
         }
         // row-per-lane -> smem: row = lane, 16-byte chunk j at position j ^ ((row >> 1) & 3)
