@@ -59,14 +59,6 @@ constexpr int EPI0 = 4;
 constexpr int NB2 = CIQ_TC2_NB;     // S/K TMEM buffers
 constexpr int NO2 = CIQ_TC2_OSLOTS; // O accumulator slots (2: the next unit's KV never waits for a read-out)
 constexpr int TMO = NB2 * 128;      // O slot s, half h at TMO + s 2 TN + h TN
-// CIQ_TC2_ALT (experiments): the two O slots alternate by tile WITHIN a unit (two accumulation
-// chains of half the unit, summed in fp32 at the read-out) instead of by unit
-#ifdef CIQ_TC2_ALT
-constexpr bool kAlt = true;
-#else
-constexpr bool kAlt = false;
-#endif
-static_assert(!kAlt || NO2 == 2, "alternating accumulators need two O slots");
 static_assert(NB2 * 128 + NO2 * 128 <= 512 && NO2 >= 1 && NO2 <= 2, "TMEM budget (TN <= 64)");
 // Ping-pong epilogue (measured: 0.937 vs 1.088 ms per C3 MVM for all 16 warps on every tile,
 // profiles/): two groups of 8 warps take alternate tiles.
@@ -257,16 +249,11 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         T2_STAMP(0, g);
         {
           uint32_t fl = 0;
-          if (c.jj >= (kAlt ? 2 : 1)) fl |= F_ACC;
+          if (c.jj > 0) fl |= F_ACC;
           if (c.jj == c.njt - 1) fl |= F_OLAST;
           // the first KV of unit k overwrites O slot k % NO2: unit k - NO2 must be read out
-          if (kAlt) {   // both slots belong to the unit: its first KV waits for unit k - 1's read-out
-            if (c.jj == 0 && c.k >= 1) fl |= F_OWAIT | (((c.k - 1) & 1) ? F_OPH : 0u);
-            if (c.jj & 1) fl |= F_OSLOT;
-          } else {
-            if (c.jj == 0 && c.k >= NO2) fl |= F_OWAIT | ((((c.k - NO2) / NO2) & 1) ? F_OPH : 0u);
-            if (NO2 > 1 && (c.k & 1)) fl |= F_OSLOT;
-          }
+          if (c.jj == 0 && c.k >= NO2) fl |= F_OWAIT | ((((c.k - NO2) / NO2) & 1) ? F_OPH : 0u);
+          if (NO2 > 1 && (c.k & 1)) fl |= F_OSLOT;
           if (fv) {
             fl |= F_SVALID | ((f.k & 1) ? F_KB : 0u);
             if (f.jj == 0) fl |= F_SFIRST | (((f.k >> 1) & 1) ? F_APH : 0u);
@@ -337,8 +324,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
       mbar_wait(&bars->k_full[b][h], ph_b);
       if (h == 0) T2_STAMP(2, g);
       const int oslot = (fl & F_OSLOT) ? 1 : 0;
-      const int obar = kAlt ? 0 : oslot;   // alternating: one full / empty pair per unit
-      if (fl & F_OWAIT) mbar_wait(&bars->o_empty[obar][h], (fl & F_OPH) ? 1u : 0u);
+      if (fl & F_OWAIT) mbar_wait(&bars->o_empty[oslot][h], (fl & F_OPH) ? 1u : 0u);
       const uint32_t to_h = to_h0 + oslot * 2 * TN;
       fence_after_sync();
       const uint32_t soff16 = (uint32_t)((st * C::STAGE) >> 4);
@@ -348,7 +334,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
       const uint64_t dvu = shfl64(dring_v + soff16);
       if (elect_one()) {
         if (!(args.dbg & 1)) mma_kv12<TN>(to_h, kbu, dvu, idesc_o, fl & F_ACC);
-        if (fl & F_OLAST) commit_one(&bars->o_full[obar][h]);
+        if (fl & F_OLAST) commit_one(&bars->o_full[oslot][h]);
       }
       __syncwarp();
       if (h == 0) T2_STAMP(9, g);
@@ -418,8 +404,8 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
       // V one pass ahead (its L2 latency overlaps the O wait and the previous pass)
       float4 vn[4];
       vload(0, vn);
-      const int oslot = kAlt ? 0 : u.k % NO2;
-      mbar_wait(&bars->o_full[oslot][h], kAlt ? (u.k & 1) : ((u.k / NO2) & 1));
+      const int oslot = u.k % NO2;
+      mbar_wait(&bars->o_full[oslot][h], (u.k / NO2) & 1);
       if (warp == 4 || warp == 12) T2_STAMP(11, u.k);
       fence_after_sync();
       const int sw = (lane >> 1) & 3;   // swizzle of this lane's row in the row-per-lane phase
@@ -433,18 +419,9 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         const uint32_t ta = tbase + TMO + oslot * 2 * TN + TN * h + c0 + lane_base;
         tmem_ld8(ta, &o[0]);
         tmem_ld8(ta + 8, &o[8]);
-        uint32_t o1[kAlt ? 16 : 1];
-        if (kAlt && u.njt > 1) {   // the second accumulator (odd tiles of the unit)
-          tmem_ld8(ta + 2 * TN, &o1[0]);
-          tmem_ld8(ta + 2 * TN + 8, &o1[8]);
-        }
         if (pass + 1 < NP) vload(c0 + 16, vn);
         const float4 s4 = __ldg(reinterpret_cast<const float4*>(args.inv_scale + colu + c0 + 4 * ch));
         tmem_ld_wait();
-        if (kAlt && u.njt > 1) {
-#pragma unroll
-          for (int m = 0; m < 16; ++m) o[m] = __float_as_uint(__uint_as_float(o[m]) + __uint_as_float(o1[m]));
-        }
         if (pass == NP - 1) {   // O_h is in registers: the next unit's first KV may overwrite it
           fence_before_sync();
           __syncwarp();
@@ -651,7 +628,7 @@ int tc2_units(int64_t rows, int nsplit, int chunks) { return (int)((rows + BM2 -
 // 1e-4.  The per-split partial products are summed in fp32 (round to
 // nearest) by the consumer.
 int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm, int min_tiles) {
-  constexpr int64_t kMaxChain = kAlt ? 132 : 66;   // tiles per unit (kAlt: two alternating chains of <= 66)
+  constexpr int64_t kMaxChain = 66;
   const int64_t nrt = (rows + BM2 - 1) / BM2;
   const int64_t ntiles = (n + BN2 - 1) / BN2;
   const int smin = (int)((ntiles + kMaxChain - 1) / kMaxChain);
