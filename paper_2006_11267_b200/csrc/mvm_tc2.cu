@@ -20,14 +20,16 @@
 //       split k = k_hi + k_lo (fp16) -> tcgen05.st in place (chunk c -> hi at [32c, 32c+16),
 //       lo at [32c+16, 32c+32));
 //   (3) O_h += K_h . V_J (TS: A from TMEM, B = V_J MN-major): k_hi.v_hi + k_hi.v_lo + k_lo.v_hi.
-// TMEM (512 columns): S/K buffers b = 0..2 at [128 b, 128 b + 128) (half h at +64 h), O_h at
-// 384 + TN h.  S runs three tiles ahead of KV.
+// TMEM (512 columns): NB2 S/K buffers b at [128 b, 128 b + 128) (half h at +64 h), then NO2 O
+// slots (slot s, half h at 128 NB2 + 2 TN s + TN h; units alternate slots).  S runs NB2 tiles ahead
+// of KV.  Default NB2 = NO2 = 2 (see CIQ_TC2_NB below).
 // Smem: A features of the unit (256 rows, double-buffered across units), features of the first
-// three tiles, and a ring whose stage g holds V(g) and the column features of tile g+3 (skewed:
-// one stage wait / release per tile on the MMA warp).
+// NB2 tiles, and a ring whose stage g holds V(g) and the column features of tile g+NB2 (skewed:
+// one stage wait / release per tile on the MMA warp), and per reading warp a 2 KB transpose buffer.
 // The output read-out of unit k is done by the epilogue group that takes the first tile of unit
-// k+1, right after that tile (O is drained to registers, released, then written with plain
-// stores; the alpha partials by a transposed warp reduction).
+// k+1, right after that tile (O is drained to registers through the smem transpose, released,
+// then written with coalesced stores; the alpha partials by lane-group shuffles); the CTA's alpha
+// partials are reduced in the kernel tail when the recurrence asks for it (TcArgs::alpha_out).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
