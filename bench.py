@@ -419,6 +419,8 @@ def run_ours(args, cfg):
             "run": {"J": infos[-1]["iters"],
                     "mvms_per_step": infos[-1]["mvms"], "mvm_impl": impl_used,
                     "mvm_splits": infos[-1].get("mvm_splits"),
+                    "mvm_schedule": "relaxed inexact Krylov: 66-tile chains until max relres <= 0.1, then 264 "
+                                    "(params.mvm_relax, DESIGN.md section 5)",
                     "parallelism": (f"rows{world}" if sharded else f"replicas{world}") if world > 1 else "single",
                     "recurrence": args.recurrence,
                     "converged": infos[-1]["converged"], "max_rel_residual": infos[-1]["max_rel_residual"],

@@ -63,7 +63,7 @@ class CiqParams(ctypes.Structure):
                 ("ld_start", c_int64), ("seed", c_uint64), ("mode", c_int32), ("mvm_impl", c_int32),
                 ("poll_every", c_int32), ("breakdown_tol", c_double), ("profile_kernels", c_int32),
                 ("lanczos_reuse", c_int32), ("keep_shift_solutions", c_int32), ("shift_solutions", c_void_p),
-                ("fp64", c_int32), ("stored_basis", c_int32)]
+                ("fp64", c_int32), ("stored_basis", c_int32), ("mvm_relax", c_int32)]
 
 
 class CiqInfo(ctypes.Structure):
@@ -426,7 +426,7 @@ def make_params(q: int = 8, max_iters: int = 400, tol: float = 1e-4, mode: str =
                 lanczos_cols: int = 16, lanczos_start=None, rule=None, spectrum=None, seed: int = 2,
                 mvm_impl: str = "auto", poll_every: int = 6, breakdown_tol: float = 1e-6, profile: bool = False,
                 lanczos_reuse: bool = False, shift_solutions=None, keep: list | None = None, fp64: bool = False,
-                stored_basis: bool = False):
+                stored_basis: bool = False, mvm_relax: bool = True):
     """Build a CiqParams; arrays referenced by it are appended to `keep` (caller keeps them alive)."""
     keep = [] if keep is None else keep
     p = ciq_params_default()
@@ -441,6 +441,7 @@ def make_params(q: int = 8, max_iters: int = 400, tol: float = 1e-4, mode: str =
     p.lanczos_reuse = 1 if lanczos_reuse else 0
     p.fp64 = 1 if fp64 else 0
     p.stored_basis = 1 if stored_basis else 0
+    p.mvm_relax = 1 if mvm_relax else 0
     if shift_solutions is not None:   # Q x rows x T (ld = T): the forward's shifted solves
         p.keep_shift_solutions = 1
         if isinstance(shift_solutions, np.ndarray):

@@ -147,6 +147,12 @@ struct ciq_ctx {
   } mvm_win;
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // relaxed MVM schedule (params.mvm_relax): the next run_mvm launches the full-tile kernel with
+  // `nsplit` column splits, or `nsplit_alt` once ctrl->relaxed (chosen by the kernel at launch)
+  struct MvmGate {
+    bool on = false;
+    int nsplit = 0, nsplit_alt = 0;
+  } mvm_gate;
   double* gsum = nullptr;     // [world][m] allgather buffer of cross-rank partial sums
   size_t gsum_cap = 0;
   double* tsum = nullptr;     // [tp] local sums
@@ -747,6 +753,11 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     nsplit = tc2_choose_nsplit(rows, (int64_t)ntw * 64, chunks, capw);
     nblk = (rows + 255) / 256 * nsplit * 8;
   }
+  const bool gated = c->mvm_gate.on && !dense && !sym && !win && !use_tc3(c, tp) && done != nullptr;
+  if (gated) {   // the relaxed schedule's accurate grid (buffers sized for it; the alternative is smaller)
+    nsplit = c->mvm_gate.nsplit;
+    nblk = (rows + 255) / 256 * nsplit * 8;
+  }
   ciq_status st = grow(c, &c->planes, &c->planes_elems, (size_t)2 * vrows(c) * tp);
   if (st != CIQ_OK) return st;
   if (c->inv_scale_n < tp) {
@@ -800,6 +811,11 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   a.kf = c->kf;
   a.nunits = dense ? (int)((rows + 127) / 128) * nsplit * chunks
                    : (pair ? tc3_units(rows, nsplit, chunks) : tc2_units(rows, nsplit, chunks));
+  if (gated) {
+    a.gate = &done->relaxed;
+    a.nsplit_alt = c->mvm_gate.nsplit_alt;
+    a.nunits_alt = tc2_units(rows, c->mvm_gate.nsplit_alt, chunks);
+  }
   if (win) {
     a.win_lo = c->mvm_win.lo;
     a.win_hi = c->mvm_win.hi;
@@ -1483,6 +1499,7 @@ void ciq_params_default(ciq_params* p) {
   p->breakdown_tol = 1e-6;
   p->fp64 = 0;
   p->stored_basis = 0;
+  p->mvm_relax = 1;
 }
 
 #ifndef CIQ_SOURCE_HASH
@@ -2243,6 +2260,28 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     LAUNCH(c, launch_pack_v(ws.w[1], c->op.n, vrows(c), tp, plane_cols(c, tp), sc.nrm_cur, c->planes, c->inv_scale, s));
   }
   const bool overlap = fuse_pack && use_overlap(c, p.mvm_impl, tp);
+  // Relaxed inexact Krylov (params.mvm_relax; Simoncini & Szyld): the MVM's
+  // error may grow as 1 / ||r_j|| without moving the result, so once the max relative residual is
+  // <= kRelaxThr the full-tile kernel runs with 4x longer TMEM accumulation chains (kTc2RelaxedChain:
+  // 4x the round-toward-zero bias, fewer column splits and partial products)
+  constexpr double kRelaxThr = 0.1;
+  int ns_acc = 0, ns_rel = 0;
+  bool relax = false;
+#ifndef CIQ_NO_ALPHA_FUSE
+  if (p.mvm_relax && !P.on && !overlap && !c->sharded && !c->post.on && !c->deriv && use_tc(c, p.mvm_impl, tp) &&
+      is_kernel_op(c) && !use_mat(c, tp) && !use_sym(c, p.mvm_impl, tp) && !use_tc3(c, tp)) {
+    int64_t nb = 0;
+    mvm_geometry(c, tp, p.mvm_impl, &ns_acc, &nb);
+    ns_rel = tc2_choose_nsplit(rows, c->op.n, tp / tc_chunk_cols(tp), sm_count(), 4, kTc2RelaxedChain);
+    relax = ns_rel < ns_acc;
+  }
+#endif
+  {
+    const double thr = relax ? kRelaxThr : 0.0;
+    const int zero = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->relax_thr, &thr, sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->relaxed, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+  }
   const OverlapGeo og = overlap ? overlap_geometry(c, tp) : OverlapGeo{};
   auto enqueue_iter = [&](int j, int nqe) -> ciq_status {
     float* wcur = ws.w[j % 3];
@@ -2286,6 +2325,18 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
       nsplit = og.nsr + og.nsl;
       nbm = (int)(og.nbr + og.nbl);
       apart = c->apart_tc;
+    } else if (relax) {
+      // relaxed schedule (params.mvm_relax): the kernel takes the accurate or the relaxed column
+      // splits from ctrl->relaxed (set by the Givens pass once max relres <= relax_thr); alpha_j in
+      // its tail either way (the consumer's split count follows the same flag)
+      c->alpha_fuse = &sc;
+      c->mvm_gate = ciq_ctx::MvmGate{true, ns_acc, ns_rel};
+      st2 = run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit, &apart, &nbm,
+                    fuse_pack);
+      if (st2 == CIQ_OK && !c->alpha_fused)
+        st2 = set_err(c, CIQ_ERR_INVALID_ARG, "internal: relaxed MVM schedule without the fused alpha");
+      c->mvm_gate = ciq_ctx::MvmGate{};
+      c->alpha_fuse = nullptr;
     } else {
       c->alpha_fuse = P.on ? nullptr : &sc;   // the full-tile kernel computes alpha_j in its tail
       st2 = P.on ? apply_m(wcur, ws.p, &apart, &nbm)
@@ -2314,7 +2365,8 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     LAUNCH(c, launch_lanczos_update(sc, pin, nsplit, (size_t)rows * tp, wcur + c->row0 * tp, wprev + c->row0 * tp,
                                     wnew + c->row0 * tp, &d1, &d2, ws.y, stored ? 0 : nqe, rows, tp, ws.bpart, 0, s,
                                     fuse_pack ? c->planes : nullptr, c->inv_scale, vrows(c), plane_cols(c, tp), c->op.n,
-                                    xqk, c->row0, stored ? c->basis : nullptr, (size_t)rows * tp, hlen));
+                                    xqk, c->row0, stored ? c->basis : nullptr, (size_t)rows * tp, hlen,
+                                    relax ? ns_rel : 0));
     end_timed(c);
     // stored basis: the streaming pass wrote W_{j+1} to its basis slot, the Givens pass writes the
     // step's scalars (no separate copy pass)

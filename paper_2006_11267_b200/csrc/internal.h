@@ -104,6 +104,10 @@ struct TcArgs {
   // no_diag: do not add sigma^2 V (another launch of the same product adds it); grid_cap: at most
   // that many CTAs (0: one per SM) -- leaves SMs to a concurrent collective
   int win_lo, win_hi, skip_lo, skip_hi, no_diag, grid_cap;
+  // relaxed MVM schedule (params.mvm_relax, full-tile kernel): when *gate != 0 the launch uses
+  // nsplit_alt column splits / nunits_alt units (longer accumulation chains); null: never
+  const int* gate;
+  int nsplit_alt, nunits_alt;
 };
 // tiles of a (possibly windowed) full-tile launch
 #ifdef __CUDACC__
@@ -120,7 +124,9 @@ cudaError_t launch_pack_v(const float* v, int64_t n, int64_t npad, int tp, int t
 // persistent 256-row matrix-free kernel (mvm_tc2.cu); alpha partials: [row tiles * nsplit * 8][tp]
 int tc2_units(int64_t rows, int nsplit, int chunks);
 // min_tiles: column tiles each unit keeps (4 for mvm_tc2.cu, tc3_min_tiles() for mvm_tc3.cu)
-int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm, int min_tiles = 4);
+int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm, int min_tiles = 4, int64_t max_chain = 0);
+constexpr int64_t kTc2MaxChain = 66;          // accurate TMEM accumulation chain (tiles), mvm_tc2.cu
+constexpr int64_t kTc2RelaxedChain = 264;     // the relaxed schedule's chain (4x)
 cudaError_t launch_mvm_tc2(const TcArgs& a, int nsm, cudaStream_t s);
 // CTA-pair kernel (mvm_tc3.cu): same units / alpha partials as tc2, V planes in TN/2-wide chunks
 bool tc3_supported(int tn, int64_t n, int nsplit);
@@ -168,7 +174,8 @@ cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, si
                                   float* xq = nullptr,    // [Q][rows][tp]: also accumulate x_q += phi_q d_q
                                   int64_t plane_row0 = 0,   // planes: global row of local row 0 (sharded)
                                   float* basis = nullptr, size_t basis_stride = 0,   // stored basis: W_{j+1} to slot j
-                                  int hlen = 0);
+                                  int hlen = 0,
+                                  int nsplit_relaxed = 0);   // > 0: nsplit_relaxed partial products once ctrl->relaxed
 // fp64 route (preconditioned path, precond64.cu): the same streaming pass on fp64 vectors (no
 // fused packing, no kept solutions); p may be nsplit = 1 only.
 cudaError_t launch_lanczos_update64(const Scal& sc, const double* p, const double* wcur, const double* wprev,

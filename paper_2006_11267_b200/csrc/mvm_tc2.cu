@@ -87,6 +87,7 @@ struct Bars2 {
   uint64_t a_full[2], a_empty[2];
   uint64_t pro_full, o_full[NO2][2], o_empty[NO2][2];
   uint32_t tmem_base;
+  int eff_nsplit, eff_nunits;   // this launch's unit grid (Sched)
   uint32_t flags[8];   // per ring stage: the MMA issuers' schedule for that tile (written by the producer)
 };
 
@@ -113,29 +114,38 @@ CIQ_DEVICE int window_tile(const TcArgs& a, int t) {
 }
 
 // Position in the flattened tile sequence of one CTA: unit u (local index k), tile jj of njt.
+// The launch's unit grid: column splits x units (TcArgs::nsplit / nunits, or the relaxed
+// schedule's nsplit_alt / nunits_alt when *gate != 0 -- chosen once per launch, kept in smem).
+struct Sched {
+  const volatile int* g;   // -> Bars2::eff_nsplit, eff_nunits (read at each use: no pinned registers)
+  int chunks;
+  CIQ_DEVICE int nsplit() const { return g[0]; }
+  CIQ_DEVICE int nunits() const { return g[1]; }
+};
+
 struct Cur {
   int k, u, jj, njt, jt0, split, chunk, rt;
-  CIQ_DEVICE void decode(const TcArgs& a, int ntiles) {
+  CIQ_DEVICE void decode(const Sched& a, int ntiles) {
     chunk = u % a.chunks;
     const int t = u / a.chunks;
-    split = t % a.nsplit;
-    rt = t / a.nsplit;
-    jt0 = ntiles * split / a.nsplit;          // ntiles * nsplit < 2^31 (checked on the host)
-    njt = ntiles * (split + 1) / a.nsplit - jt0;
+    split = t % a.nsplit();
+    rt = t / a.nsplit();
+    jt0 = ntiles * split / a.nsplit();          // ntiles * nsplit < 2^31 (checked on the host)
+    njt = ntiles * (split + 1) / a.nsplit() - jt0;
   }
-  CIQ_DEVICE void start(const TcArgs& a, int ntiles) {
+  CIQ_DEVICE void start(const Sched& a, int ntiles) {
     k = 0;
     u = blockIdx.x;
     jj = 0;
-    if (u < a.nunits) decode(a, ntiles);
+    if (u < a.nunits()) decode(a, ntiles);
   }
-  CIQ_DEVICE bool valid(const TcArgs& a) const { return u < a.nunits; }
-  CIQ_DEVICE void advance(const TcArgs& a, int ntiles) {
+  CIQ_DEVICE bool valid(const Sched& a) const { return u < a.nunits(); }
+  CIQ_DEVICE void advance(const Sched& a, int ntiles) {
     if (++jj == njt) {
       jj = 0;
       ++k;
       u += gridDim.x;
-      if (u < a.nunits) decode(a, ntiles);
+      if (u < a.nunits()) decode(a, ntiles);
     }
   }
   CIQ_DEVICE int J(const TcArgs& a) const { return window_tile(a, jt0 + jj); }
@@ -204,6 +214,9 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
   const int ntiles = tc2_window_tiles(args);   // this launch's column tiles
 
   if (threadIdx.x == 0) {
+    const bool alt = args.gate != nullptr && *args.gate != 0;   // relaxed schedule (params.mvm_relax)
+    bars->eff_nsplit = alt ? args.nsplit_alt : args.nsplit;
+    bars->eff_nunits = alt ? args.nunits_alt : args.nunits;
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 2); }
     for (int b = 0; b < NB2; ++b)
       for (int h = 0; h < 2; ++h) { mbar_init(&bars->s_full[b][h], 1); mbar_init(&bars->k_full[b][h], EPI_ARRIVALS); }
@@ -218,14 +231,15 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
   __syncthreads();
   fence_after_sync();
   const uint32_t tbase = bars->tmem_base;
+  const Sched sch{&bars->eff_nsplit, args.chunks};
   const size_t plane = (size_t)args.vrows * TN;   // one plane of one chunk
 
   if (warp == 0) {
     // ---------------- producer (one thread) ----------------
     if (lane == 0) {
       Cur c, f;
-      c.start(args, ntiles);
-      if (c.valid(args)) {
+      c.start(sch, ntiles);
+      if (c.valid(sch)) {
         // prologue: A rows of unit 0 and the column features of its first three tiles (njt >= 4)
         const int64_t i0 = args.row0 + (int64_t)c.rt * BM2;
         mbar_arrive_expect_tx(&bars->a_full[0], C::A_BYTES);
@@ -235,10 +249,10 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         for (int i = 0; i < npro; ++i)
           bulk_g2s(pro + i * C::F_BYTES, args.feat_b + (size_t)window_tile(args, c.jt0 + i) * BN2 * KF2, C::F_BYTES, &bars->pro_full);
         f = c;
-        for (int i = 0; i < NB2; ++i) f.advance(args, ntiles);
+        for (int i = 0; i < NB2; ++i) f.advance(sch, ntiles);
       }
-      for (int g = 0; c.valid(args); ++g) {
-        const bool fv = f.valid(args);
+      for (int g = 0; c.valid(sch); ++g) {
+        const bool fv = f.valid(sch);
         if (fv && f.jj == 0 && f.k > 0) {   // S of unit f.k starts with tile g+3: its A rows
           const int kb = f.k & 1;
           mbar_wait_backoff(&bars->a_empty[kb], ((f.k >> 1) & 1) ^ 1);
@@ -269,8 +283,8 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         bulk_g2s(sb, vh, C::V_BYTES, &bars->full[st]);
         bulk_g2s(sb + C::V_BYTES, vh + plane, C::V_BYTES, &bars->full[st]);
         if (fv) bulk_g2s(sb + 2 * C::V_BYTES, args.feat_b + (size_t)f.J(args) * BN2 * KF2, C::F_BYTES, &bars->full[st]);
-        c.advance(args, ntiles);
-        if (fv) f.advance(args, ntiles);
+        c.advance(sch, ntiles);
+        if (fv) f.advance(sch, ntiles);
       }
     }
   } else if (warp == 1 || warp == 2) {
@@ -283,7 +297,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
     constexpr uint32_t idesc_s = idesc_f16(128, BN2, 0, 0);   // A, B K-major, N = 64
     constexpr uint32_t idesc_o = idesc_f16(128, TN, 0, 1);    // A (TMEM) K-major, B MN-major
     Cur kv, s;
-    kv.start(args, ntiles);
+    kv.start(sch, ntiles);
     s = kv;
     // K-major features: LBO = 128 B (K-adjacent core), SBO = KF/8 * 128 B (8-row groups);
     // V planes MN-major: LBO = TN/8 * 128 B, SBO = 128 B.
@@ -293,11 +307,11 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
     const uint64_t dring_v = smem_desc(smem_u32(ring), (TN / 8) * 128, 128);
     const uint32_t tb_h = tbase + 64 * h;         // half h of every S / K buffer
     const uint32_t to_h0 = tbase + TMO + TN * h;   // O_h of slot 0 (slot 1 at + 2 TN)
-    if (kv.valid(args)) {
+    if (kv.valid(sch)) {
       mbar_wait(&bars->a_full[0], 0);
       mbar_wait(&bars->pro_full, 0);
       fence_after_sync();
-      for (int i = 0; i < NB2 && s.valid(args) && s.k == 0; ++i) {
+      for (int i = 0; i < NB2 && s.valid(sch) && s.k == 0; ++i) {
         const uint32_t d = __shfl_sync(0xffffffffu, tb_h + i * 128, 0);
         const uint64_t db = shfl64(dpro + (uint64_t)((i * C::F_BYTES) >> 4));
         const bool last = s.jj == s.njt - 1;
@@ -307,14 +321,14 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
           if (last) commit_one(&bars->a_empty[0]);
         }
         __syncwarp();
-        s.advance(args, ntiles);
+        s.advance(sch, ntiles);
       }
     }
     // tiles of this CTA: the loop below runs on the producer's per-stage flags only
     int ntot = 0;
-    for (int u = blockIdx.x; u < args.nunits; u += gridDim.x) {
-      const int split = (u / args.chunks) % args.nsplit;
-      ntot += ntiles * (split + 1) / args.nsplit - ntiles * split / args.nsplit;
+    for (int u = blockIdx.x; u < sch.nunits(); u += gridDim.x) {
+      const int split = (u / sch.chunks) % sch.nsplit();
+      ntot += ntiles * (split + 1) / sch.nsplit() - ntiles * split / sch.nsplit();
     }
     int st = 0, b = 0;
     uint32_t ph_st = 0, ph_b = 0;
@@ -371,7 +385,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
     // read-out scratch of this warp (h, q) of the reading group
     float* rbuf = reinterpret_cast<float*>(smem + C::RO_OFF + (h * 4 + q) * RO_BYTES);
     Cur c;
-    c.start(args, ntiles);
+    c.start(sch, ntiles);
     // the unit before c's unit (valid once c has left the CTA's first unit): (u, k) only, decoded
     // when it is read out (registers: the epilogue runs at the 96-per-thread cap)
     int pu_u = c.u, pu_k = c.k;
@@ -386,7 +400,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
       Cur u;
       u.u = uu;
       u.k = kk;
-      u.decode(args, ntiles);
+      u.decode(sch, ntiles);
       const int64_t ib = args.row0 + (int64_t)u.rt * BM2 + 128 * h + 32 * q;   // first row of the warp
       const int colu = u.chunk * TN;
       const int ch = lane & 3, rl = lane >> 2;
@@ -400,7 +414,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         }
       };
       float* pbase = args.p + (size_t)u.split * args.p_split_stride + colu + 4 * ch;
-      double* ap = args.apart ? args.apart + ((size_t)(u.rt * args.nsplit + u.split) * 8 + q * 2 + h) * args.tp + colu
+      double* ap = args.apart ? args.apart + ((size_t)(u.rt * sch.nsplit() + u.split) * 8 + q * 2 + h) * args.tp + colu
                               : nullptr;
       if (warp == 4 || warp == 12) T2_STAMP(10, u.k);
       // V one pass ahead (its L2 latency overlaps the O wait and the previous pass)
@@ -487,7 +501,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
     int b = 0;
     uint32_t ph_b = 0;
     int g = 0;
-    for (; c.valid(args); ++g) {
+    for (; c.valid(sch); ++g) {
       if ((g & 1) == grp) {
         mbar_wait(&bars->s_full[b][h], ph_b);
         if (warp == 4) T2_STAMP(4, g);
@@ -524,12 +538,12 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
         }
       }
       const int old_u = c.u, old_k = c.k;
-      c.advance(args, ntiles);
-      if (!c.valid(args) || c.k != old_k) { pu_u = old_u; pu_k = old_k; }
+      c.advance(sch, ntiles);
+      if (!c.valid(sch) || c.k != old_k) { pu_u = old_u; pu_k = old_k; }
       if (++b == NB2) { b = 0; ph_b ^= 1; }
     }
     // the CTA's last unit: one group (all of its TN columns) / every warp (its column half)
-    if (pu_u < args.nunits && grp == 0) readout(pu_u, pu_k);
+    if (pu_u < sch.nunits() && grp == 0) readout(pu_u, pu_k);
   }
   fence_before_sync();
   __syncthreads();
@@ -541,7 +555,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
     const int tp = args.tp;
     for (int col = threadIdx.x; col < tp; col += NT2) {
       double sum = 0.0;
-      for (int u = blockIdx.x; u < args.nunits; u += gridDim.x) {
+      for (int u = blockIdx.x; u < sch.nunits(); u += gridDim.x) {
         const int chunk = u % args.chunks;
         if (col / TN != chunk) continue;
         const size_t r0 = (size_t)(u / args.chunks) * 8;   // rows (rt * nsplit + split) * 8 + (q, h) slot
@@ -629,8 +643,8 @@ int tc2_units(int64_t rows, int nsplit, int chunks) { return (int)((rows + BM2 -
 // entries alone give ~1e-5 (scripts/diag_fp32_floor.py).  66 tiles keep C3 inside north_star's
 // 1e-4.  The per-split partial products are summed in fp32 (round to
 // nearest) by the consumer.
-int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm, int min_tiles) {
-  constexpr int64_t kMaxChain = 66;
+int tc2_choose_nsplit(int64_t rows, int64_t n, int chunks, int nsm, int min_tiles, int64_t max_chain) {
+  const int64_t kMaxChain = max_chain > 0 ? max_chain : kTc2MaxChain;
   const int64_t nrt = (rows + BM2 - 1) / BM2;
   const int64_t ntiles = (n + BN2 - 1) / BN2;
   const int smin = (int)((ntiles + kMaxChain - 1) / kMaxChain);

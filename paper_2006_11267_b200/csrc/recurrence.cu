@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? CIQ_UPD_MINB : 2) l
     Scal sc, const T* __restrict__ p, int nsplit, size_t split_stride, const T* __restrict__ wcur, const T* __restrict__ wprev,
     T* __restrict__ wnew, const T* __restrict__ d1base, T* __restrict__ d2base, int64_t qstride,
     T* __restrict__ y, int nq, int64_t rows, int tp, double* __restrict__ bpart, int final_only, PackOut pk,
-    float* __restrict__ xq, BasisOut bo) {
+    float* __restrict__ xq, BasisOut bo, int nsplit_relaxed) {
   constexpr int QB = CIQ_UPD_QB;
   constexpr bool kF32 = sizeof(T) == 4;
   const T* CA = coef_sel<T>(sc.ca, sc.da);
@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? CIQ_UPD_MINB : 2) l
   const Ctrl* ctrl = sc.ctrl;
   if (!final_only && ctrl->done) return;
   const int pending = ctrl->pending;
+  if (nsplit_relaxed > 0 && ctrl->relaxed) nsplit = nsplit_relaxed;   // the relaxed MVM's partial products
   // stored-basis variant: W_{j+1} also goes to basis slot j (= Givens steps done + 1; the Givens
   // pass of step j runs after this one), so no separate copy pass (store_basis) per iteration
   T* bslot = nullptr;
@@ -543,6 +544,8 @@ __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __re
       ctrl->max_relres = mx;
       ctrl->arrive = 0;
       if (!(mx <= 1e300)) ctrl->nonfinite = 1;   // stop: a NaN / inf never recovers
+      // relaxed inexact Krylov (params.mvm_relax): from here on the cheaper MVM variant runs
+      if (nq > 0 && ctrl->relax_thr > 0 && mx <= ctrl->relax_thr) ctrl->relaxed = 1;
       if (act == 0 || (ctrl->tol > 0 && mx <= ctrl->tol) || j >= ctrl->max_iters || ctrl->nonfinite) ctrl->done = 1;
     }
   }
@@ -797,14 +800,14 @@ cudaError_t launch_lanczos_update(const Scal& sc, const float* p, int nsplit, si
                                   float* wnew, float* const* d1, float* const* d2, float* y, int nq,
                                   int64_t rows, int tp, double* bpart, int final_only, cudaStream_t s,
                                   __half* planes, float* inv_scale, int64_t npad, int tn, int64_t n, float* xq,
-                                  int64_t plane_row0, float* basis, size_t basis_stride, int hlen) {
+                                  int64_t plane_row0, float* basis, size_t basis_stride, int hlen, int nsplit_relaxed) {
   const int64_t qstride = rows * tp;
   PackOut pk{planes, inv_scale, npad, tn, sqrt((double)n), plane_row0};
   dim3 grid = stream_grid(rows, tp);
   grid.x = (unsigned)update_blocks(rows);
   lanczos_update_kernel<float><<<grid, kThreads, 0, s>>>(sc, p, nsplit, split_stride, wcur, wprev, wnew, d1[0], d2[0],
                                                          qstride, y, nq, rows, tp, bpart, final_only, pk, xq,
-                                                         BasisOut{basis, basis_stride, nullptr, hlen});
+                                                         BasisOut{basis, basis_stride, nullptr, hlen}, nsplit_relaxed);
   return cudaGetLastError();
 }
 cudaError_t launch_lanczos_update64(const Scal& sc, const double* p, const double* wcur, const double* wprev,
@@ -816,7 +819,7 @@ cudaError_t launch_lanczos_update64(const Scal& sc, const double* p, const doubl
   grid.x = (unsigned)update_blocks64(rows);
   lanczos_update_kernel<double><<<grid, kThreads, 0, s>>>(sc, p, 1, 0, wcur, wprev, wnew, d1[0], d2[0], qstride, y, nq,
                                                           rows, tp, bpart, final_only, pk, nullptr,
-                                                          BasisOut{nullptr, 0, nullptr, 0});
+                                                          BasisOut{nullptr, 0, nullptr, 0}, 0);
   return cudaGetLastError();
 }
 cudaError_t launch_colsq_partials64(const double* v, int64_t rows, int tp, double* part, cudaStream_t s) {
