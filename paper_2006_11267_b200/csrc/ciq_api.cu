@@ -879,7 +879,8 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   }
 #endif
   if (nsplit > 1 && nsplit_out == nullptr)  // caller wants the complete product in p
-    LAUNCH(c, launch_sum_splits(c->psplit, nsplit, (size_t)rows * tp, rows * tp, p, c->stream));
+    LAUNCH(c, launch_sum_splits(c->psplit, nsplit, (size_t)rows * tp, rows * tp, p, c->stream,
+                                gated ? &done->relaxed : nullptr, gated ? c->mvm_gate.nsplit_alt : 0));
   if (nsplit_out) *nsplit_out = nsplit;
   if (apart_used) *apart_used = ap;
   if (apart_nblk) *apart_nblk = (int)nblk;
@@ -2268,7 +2269,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   int ns_acc = 0, ns_rel = 0;
   bool relax = false;
 #ifndef CIQ_NO_ALPHA_FUSE
-  if (p.mvm_relax && !P.on && !overlap && !c->sharded && !c->post.on && !c->deriv && use_tc(c, p.mvm_impl, tp) &&
+  if (p.mvm_relax && !P.on && !overlap && !c->sharded && !c->deriv && use_tc(c, p.mvm_impl, tp) &&
       is_kernel_op(c) && !use_mat(c, tp) && !use_sym(c, p.mvm_impl, tp) && !use_tc3(c, tp)) {
     int64_t nb = 0;
     mvm_geometry(c, tp, p.mvm_impl, &ns_acc, &nb);
@@ -2325,7 +2326,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
       nsplit = og.nsr + og.nsl;
       nbm = (int)(og.nbr + og.nbl);
       apart = c->apart_tc;
-    } else if (relax) {
+    } else if (relax && !c->post.on) {
       // relaxed schedule (params.mvm_relax): the kernel takes the accurate or the relaxed column
       // splits from ctrl->relaxed (set by the Givens pass once max relres <= relax_thr); alpha_j in
       // its tail either way (the consumer's split count follows the same flag)
@@ -2339,9 +2340,13 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
       c->alpha_fuse = nullptr;
     } else {
       c->alpha_fuse = P.on ? nullptr : &sc;   // the full-tile kernel computes alpha_j in its tail
+      // posterior operator (f2): the relaxed schedule applies to the K** MVM and its split sum; the
+      // downdate and alpha follow the posterior path
+      if (relax) c->mvm_gate = ciq_ctx::MvmGate{true, ns_acc, ns_rel};
       st2 = P.on ? apply_m(wcur, ws.p, &apart, &nbm)
                  : run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit,
                            &apart, &nbm, fuse_pack);
+      c->mvm_gate = ciq_ctx::MvmGate{};
       c->alpha_fuse = nullptr;
     }
     const bool alpha_done = !P.on && c->alpha_fused;
@@ -2366,7 +2371,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
                                     wnew + c->row0 * tp, &d1, &d2, ws.y, stored ? 0 : nqe, rows, tp, ws.bpart, 0, s,
                                     fuse_pack ? c->planes : nullptr, c->inv_scale, vrows(c), plane_cols(c, tp), c->op.n,
                                     xqk, c->row0, stored ? c->basis : nullptr, (size_t)rows * tp, hlen,
-                                    relax ? ns_rel : 0));
+                                    relax && !c->post.on ? ns_rel : 0));
     end_timed(c);
     // stored basis: the streaming pass wrote W_{j+1} to its basis slot, the Givens pass writes the
     // step's scalars (no separate copy pass)

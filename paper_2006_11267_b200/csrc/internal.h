@@ -153,8 +153,9 @@ cudaError_t launch_dot_rows(const float* a, int64_t lda, const float* b, int64_t
 int rowblocks(int64_t rows, int tp);   // number of CTAs of the row-streaming kernels
 int update_blocks(int64_t rows);       // CTAs (= beta^2 partial rows) of lanczos_update_kernel
 int update_blocks64(int64_t rows);     // ... of its fp64 instance (launch_lanczos_update64)
+// relaxed (may be null): nsplit_relaxed partial products once *relaxed (params.mvm_relax)
 cudaError_t launch_sum_splits(const float* parts, int nsplit, size_t stride, int64_t elems, float* out,
-                              cudaStream_t s);
+                              cudaStream_t s, const int* relaxed = nullptr, int nsplit_relaxed = 0);
 cudaError_t launch_load_block(const float* src, int64_t ld_src, int64_t rows, int cols, float* dst, int tp,
                               cudaStream_t s);
 cudaError_t launch_store_block(const float* src, int tp, int64_t rows, int cols, float* dst, int64_t ld_dst,

@@ -616,9 +616,10 @@ __global__ void lanczos_coeffs_kernel(const double* __restrict__ h1, const doubl
 
 // out = sum_s parts[s] (fixed order), float4 vectorised.
 __global__ void sum_splits_kernel(const float* __restrict__ parts, int nsplit, size_t stride, int64_t n4,
-                                  float* __restrict__ out) {
+                                  float* __restrict__ out, const int* __restrict__ relaxed, int nsplit_relaxed) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n4) return;
+  if (relaxed != nullptr && *relaxed) nsplit = nsplit_relaxed;   // the relaxed MVM schedule's split count
   float4 acc = reinterpret_cast<const float4*>(parts)[e];
   for (int s = 1; s < nsplit; s += 4) {   // split order; 4 loads in flight
     float4 q[4];
@@ -726,9 +727,9 @@ static dim3 stream_grid(int64_t rows, int tp) {
 }
 
 cudaError_t launch_sum_splits(const float* parts, int nsplit, size_t stride, int64_t elems, float* out,
-                              cudaStream_t s) {
+                              cudaStream_t s, const int* relaxed, int nsplit_relaxed) {
   const int64_t n4 = elems / 4;
-  sum_splits_kernel<<<nb_elem(n4, 256), 256, 0, s>>>(parts, nsplit, stride, n4, out);
+  sum_splits_kernel<<<nb_elem(n4, 256), 256, 0, s>>>(parts, nsplit, stride, n4, out, relaxed, nsplit_relaxed);
   return cudaGetLastError();
 }
 cudaError_t launch_load_block(const float* src, int64_t ld_src, int64_t rows, int cols, float* dst, int tp,
