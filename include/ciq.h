@@ -223,6 +223,8 @@ typedef struct {
   int32_t nested_iters;       /*   and the inner msMINRES iterations                             */
   int32_t overlap;            /* row-sharded: 1 if the Lanczos-block all-gather ran next to the
                                  local diagonal block's MVM */
+  int32_t relaxed_from;       /* params.mvm_relax: first msMINRES step run with the relaxed MVM  */
+                              /*   (longer accumulation chains); 0 if none                      */
 } ciq_info;
 
 typedef struct ciq_ctx ciq_ctx;

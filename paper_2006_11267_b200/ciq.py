@@ -74,7 +74,8 @@ class CiqInfo(ctypes.Structure):
                 ("ms_lambda", c_float), ("ms_loop", c_float), ("ms_final", c_float), ("kernel_launches", c_int64),
                 ("ms_mvm", c_float), ("mvm_timed", c_int32), ("ms_update", c_float), ("update_timed", c_int32),
                 ("mvm_impl_used", c_int32), ("mvm_splits", c_int32), ("fp64_route", c_int32),
-                ("nested_p_mvms", c_int32), ("nested_iters", c_int32), ("overlap", c_int32)]
+                ("nested_p_mvms", c_int32), ("nested_iters", c_int32), ("overlap", c_int32),
+                ("relaxed_from", c_int32)]
 
     def as_dict(self) -> dict:
         q = self.Q
@@ -88,7 +89,8 @@ class CiqInfo(ctypes.Structure):
                 "ms_update": self.ms_update, "update_timed": self.update_timed,
                 "mvm_impl_used": {1: "simt", 2: "tc", 3: "sym", 4: "fp64_tc"}.get(self.mvm_impl_used, "none"), "mvm_splits": self.mvm_splits,
                 "fp64_route": bool(self.fp64_route), "nested_p_mvms": self.nested_p_mvms,
-                "nested_iters": self.nested_iters, "overlap": bool(self.overlap)}
+                "nested_iters": self.nested_iters, "overlap": bool(self.overlap),
+                "relaxed_from": self.relaxed_from}
 
 
 def _load() -> ctypes.CDLL:

@@ -2279,9 +2279,9 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
 #endif
   {
     const double thr = relax ? kRelaxThr : 0.0;
-    const int zero = 0;
+    const int zero[2] = {0, 0};
     CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->relax_thr, &thr, sizeof(double), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->relaxed, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->relaxed, zero, 2 * sizeof(int), cudaMemcpyHostToDevice, s));   // + relaxed_from
   }
   const OverlapGeo og = overlap ? overlap_geometry(c, tp) : OverlapGeo{};
   auto enqueue_iter = [&](int j, int nqe) -> ciq_status {
@@ -2581,6 +2581,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     info->kernel_launches = c->launches;
     info->mvm_impl_used = loop_impl;
     info->overlap = overlap ? 1 : 0;
+    info->relaxed_from = hc.relaxed_from;
     info->mvm_splits = loop_nsplit;
     info->fp64_route = 0;
     for (auto& tm : c->timed) {

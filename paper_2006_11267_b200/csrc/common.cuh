@@ -60,6 +60,7 @@ struct Ctrl {
   double max_relres;
   int nonfinite;   // 1 once a residual or beta_{j+1} came out NaN / inf (the solve stops; CIQ_NOT_CONVERGED)
   int relaxed;     // 1 once max_relres <= relax_thr (params.mvm_relax): the cheap MVM variant runs
+  int relaxed_from;   // the first msMINRES step run with the relaxed MVM (0: none)
   double relax_thr;   // 0: never
 };
 
