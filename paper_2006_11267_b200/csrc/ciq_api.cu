@@ -2265,7 +2265,11 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   // error may grow as 1 / ||r_j|| without moving the result, so once the max relative residual is
   // <= kRelaxThr the full-tile kernel runs with 4x longer TMEM accumulation chains (kTc2RelaxedChain:
   // 4x the round-toward-zero bias, fewer column splits and partial products)
+#ifdef CIQ_EXPERIMENTS
+  static const double kRelaxThr = getenv("CIQ_RELAX_THR") ? atof(getenv("CIQ_RELAX_THR")) : 0.1;
+#else
   constexpr double kRelaxThr = 0.1;
+#endif
   int ns_acc = 0, ns_rel = 0;
   bool relax = false;
 #ifndef CIQ_NO_ALPHA_FUSE
