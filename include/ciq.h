@@ -225,6 +225,7 @@ typedef struct {
                                  local diagonal block's MVM */
   int32_t relaxed_from;       /* params.mvm_relax: first msMINRES step run with the relaxed MVM  */
                               /*   (longer accumulation chains); 0 if none                      */
+  int32_t relaxed2_from;      /*   ... and with kernel entries rounded to fp16 (second level)      */
 } ciq_info;
 
 typedef struct ciq_ctx ciq_ctx;

@@ -75,7 +75,7 @@ class CiqInfo(ctypes.Structure):
                 ("ms_mvm", c_float), ("mvm_timed", c_int32), ("ms_update", c_float), ("update_timed", c_int32),
                 ("mvm_impl_used", c_int32), ("mvm_splits", c_int32), ("fp64_route", c_int32),
                 ("nested_p_mvms", c_int32), ("nested_iters", c_int32), ("overlap", c_int32),
-                ("relaxed_from", c_int32)]
+                ("relaxed_from", c_int32), ("relaxed2_from", c_int32)]
 
     def as_dict(self) -> dict:
         q = self.Q
@@ -90,7 +90,7 @@ class CiqInfo(ctypes.Structure):
                 "mvm_impl_used": {1: "simt", 2: "tc", 3: "sym", 4: "fp64_tc"}.get(self.mvm_impl_used, "none"), "mvm_splits": self.mvm_splits,
                 "fp64_route": bool(self.fp64_route), "nested_p_mvms": self.nested_p_mvms,
                 "nested_iters": self.nested_iters, "overlap": bool(self.overlap),
-                "relaxed_from": self.relaxed_from}
+                "relaxed_from": self.relaxed_from, "relaxed2_from": self.relaxed2_from}
 
 
 def _load() -> ctypes.CDLL:

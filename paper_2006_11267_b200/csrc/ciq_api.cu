@@ -2265,10 +2265,15 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   // error may grow as 1 / ||r_j|| without moving the result, so once the max relative residual is
   // <= kRelaxThr the full-tile kernel runs with 4x longer TMEM accumulation chains (kTc2RelaxedChain:
   // 4x the round-toward-zero bias, fewer column splits and partial products)
+  // Second level: once <= kRelaxThr2 the kernel entries are rounded to fp16
+  // (k_hi only: the K_lo . V_hi product and the low split dropped, error ~2^-12 per entry, ~15-30x
+  // the accurate chains'): relaxation bound 1/30, kept with a 3x margin
 #ifdef CIQ_EXPERIMENTS
   static const double kRelaxThr = getenv("CIQ_RELAX_THR") ? atof(getenv("CIQ_RELAX_THR")) : 0.1;
+  static const double kRelaxThr2 = getenv("CIQ_RELAX_THR2") ? atof(getenv("CIQ_RELAX_THR2")) : 0.01;
 #else
   constexpr double kRelaxThr = 0.1;
+  constexpr double kRelaxThr2 = 0.01;
 #endif
   int ns_acc = 0, ns_rel = 0;
   bool relax = false;
@@ -2282,10 +2287,10 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   }
 #endif
   {
-    const double thr = relax ? kRelaxThr : 0.0;
-    const int zero[2] = {0, 0};
-    CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->relax_thr, &thr, sizeof(double), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->relaxed, zero, 2 * sizeof(int), cudaMemcpyHostToDevice, s));   // + relaxed_from
+    const double thr[2] = {relax ? kRelaxThr : 0.0, relax ? kRelaxThr2 : 0.0};
+    const int zero[3] = {0, 0, 0};
+    CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->relax_thr, thr, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->relaxed, zero, 3 * sizeof(int), cudaMemcpyHostToDevice, s));   // + the _from steps
   }
   const OverlapGeo og = overlap ? overlap_geometry(c, tp) : OverlapGeo{};
   auto enqueue_iter = [&](int j, int nqe) -> ciq_status {
@@ -2586,6 +2591,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     info->mvm_impl_used = loop_impl;
     info->overlap = overlap ? 1 : 0;
     info->relaxed_from = hc.relaxed_from;
+    info->relaxed2_from = hc.relaxed2_from;
     info->mvm_splits = loop_nsplit;
     info->fp64_route = 0;
     for (auto& tm : c->timed) {

@@ -59,9 +59,12 @@ struct Ctrl {
   double bd_tol;
   double max_relres;
   int nonfinite;   // 1 once a residual or beta_{j+1} came out NaN / inf (the solve stops; CIQ_NOT_CONVERGED)
-  int relaxed;     // 1 once max_relres <= relax_thr (params.mvm_relax): the cheap MVM variant runs
-  int relaxed_from;   // the first msMINRES step run with the relaxed MVM (0: none)
+  int relaxed;     // params.mvm_relax: 1 once max_relres <= relax_thr (long accumulation chains),
+                   // 2 once max_relres <= relax_thr2 (also k_hi only)
+  int relaxed_from;   // the first msMINRES step run at level 1 (0: none)
+  int relaxed2_from;  // ... at level 2
   double relax_thr;   // 0: never
+  double relax_thr2;
 };
 
 }  // namespace ciq

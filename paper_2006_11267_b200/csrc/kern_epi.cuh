@@ -132,6 +132,30 @@ CIQ_DEVICE void exp_split(const uint32_t (&sv)[32], uint32_t (&hi)[16], uint32_t
   }
 }
 
+// Second relaxation level (params.mvm_relax): k rounded to fp16 only (one
+// cvt.rn per pair, no low part) -- the late iterations' MVM uses K_hi . (V_hi + V_lo).
+template <int KIND, bool MASK>
+CIQ_DEVICE void exp_hi(const uint32_t (&sv)[32], uint32_t (&hi)[16], int jvalid) {
+#pragma unroll
+  for (int c = 0; c < 32; c += 2) {
+    float k0, k1;
+#ifndef CIQ_NO_PAIR_MATERN
+    if (KIND == 2 || KIND == 3) {
+      kern_pair<KIND>(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1]), k0, k1);
+    } else
+#endif
+    {
+      k0 = kern<KIND>(__uint_as_float(sv[c]));
+      k1 = kern<KIND>(__uint_as_float(sv[c + 1]));
+    }
+    if (MASK) {
+      k0 = (c < jvalid) ? k0 : 0.f;
+      k1 = (c + 1 < jvalid) ? k1 : 0.f;
+    }
+    hi[c / 2] = pack_half2(k0, k1);
+  }
+}
+
 // S(J) of one 128-row half: two SS MMAs (K-steps of 16 over the K = 32 feature contraction),
 // issued by one elected thread.  d: TMEM columns of the half; da: A descriptor of the half's rows;
 // db: column features of the tile.  K-step: +256 B = +16 in descriptor units.

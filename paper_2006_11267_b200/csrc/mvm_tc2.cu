@@ -88,6 +88,7 @@ struct Bars2 {
   uint64_t pro_full, o_full[NO2][2], o_empty[NO2][2];
   uint32_t tmem_base;
   int eff_nsplit, eff_nunits;   // this launch's unit grid (Sched)
+  int lowp;                     // second relaxation level: k_hi only (exp_hi, mma_kv8)
   uint32_t flags[8];   // per ring stage: the MMA issuers' schedule for that tile (written by the producer)
 };
 
@@ -183,6 +184,29 @@ CIQ_DEVICE void mma_kv12(uint32_t o, uint32_t kb, uint64_t dv, uint32_t idesc, u
       : "memory");
 }
 
+// KV(J) of one half with k_hi only (second relaxation level): k_hi.v_hi + k_hi.v_lo, 8 TS MMAs
+template <int TN>
+CIQ_DEVICE void mma_kv8(uint32_t o, uint32_t kb, uint64_t dv, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, t;\n\t.reg .b32 h<4>;\n\t.reg .b64 vh<4>, vl<4>;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, %4, %4;\n\t"
+      "add.u32 h0, %1, 0;\n\t add.u32 h1, %1, 8;\n\t add.u32 h2, %1, 32;\n\t add.u32 h3, %1, 40;\n\t"
+      "add.s64 vh0, %2, 0;\n\t add.s64 vh1, %2, %5;\n\t add.s64 vh2, %2, %6;\n\t add.s64 vh3, %2, %7;\n\t"
+      "add.s64 vl0, %2, %8;\n\t add.s64 vl1, %2, %9;\n\t add.s64 vl2, %2, %10;\n\t add.s64 vl3, %2, %11;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h0], vh0, %3, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h0], vl0, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], vh1, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], vl1, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], vh2, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], vl2, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], vh3, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], vl3, %3, t;\n\t}" ::"r"(o),
+      "r"(kb), "l"(dv), "r"(idesc), "r"(acc), "n"(2 * TN), "n"(4 * TN), "n"(6 * TN), "n"(8 * TN),
+      "n"(10 * TN), "n"(12 * TN), "n"(14 * TN)
+      : "memory");
+}
+
 // experiments only: per-tile clock64 stamps of CTA 0 (build with CIQ_TC_TRACE, run with
 // CIQ_TC_DEBUG=128; same slots as mvm_tc.cu)
 #ifdef CIQ_TC_TRACE
@@ -217,6 +241,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
     const bool alt = args.gate != nullptr && *args.gate != 0;   // relaxed schedule (params.mvm_relax)
     bars->eff_nsplit = alt ? args.nsplit_alt : args.nsplit;
     bars->eff_nunits = alt ? args.nunits_alt : args.nunits;
+    bars->lowp = (args.gate != nullptr && *args.gate >= 2) ? 1 : 0;
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 2); }
     for (int b = 0; b < NB2; ++b)
       for (int h = 0; h < 2; ++h) { mbar_init(&bars->s_full[b][h], 1); mbar_init(&bars->k_full[b][h], EPI_ARRIVALS); }
@@ -232,6 +257,7 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
   fence_after_sync();
   const uint32_t tbase = bars->tmem_base;
   const Sched sch{&bars->eff_nsplit, args.chunks};
+  const bool lowp = bars->lowp != 0;
   const size_t plane = (size_t)args.vrows * TN;   // one plane of one chunk
 
   if (warp == 0) {
@@ -349,7 +375,10 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
       const uint32_t kbu = __shfl_sync(0xffffffffu, tb_h + b * 128, 0);
       const uint64_t dvu = shfl64(dring_v + soff16);
       if (elect_one()) {
-        if (!(args.dbg & 1)) mma_kv12<TN>(to_h, kbu, dvu, idesc_o, fl & F_ACC);
+        if (!(args.dbg & 1)) {
+          if (lowp) mma_kv8<TN>(to_h, kbu, dvu, idesc_o, fl & F_ACC);
+          else mma_kv12<TN>(to_h, kbu, dvu, idesc_o, fl & F_ACC);
+        }
         if (fl & F_OLAST) commit_one(&bars->o_full[oslot][h]);
       }
       __syncwarp();
@@ -514,17 +543,24 @@ __global__ void __launch_bounds__(NT2, 1) mvm_tc2_kernel(TcArgs args) {
           uint32_t sv[32];
           tmem_ld32(tb, sv);
           tmem_ld_wait();
-          uint32_t hi[16], lo[16];
-          if (args.dbg & 2) {
-#pragma unroll
-            for (int m = 0; m < 16; ++m) { hi[m] = sv[m]; lo[m] = sv[m + 16]; }
-          } else if (jcol0 + 32 > n) {
-            exp_split<KIND, true>(sv, hi, lo, (int)(n - jcol0));
+          if (lowp) {   // second relaxation level: k_hi only
+            uint32_t hi[16];
+            if (jcol0 + 32 > n) exp_hi<KIND, true>(sv, hi, (int)(n - jcol0));
+            else exp_hi<KIND, false>(sv, hi, 32);
+            tmem_st16(tb, hi);
           } else {
-            exp_split<KIND, false>(sv, hi, lo, 32);
+            uint32_t hi[16], lo[16];
+            if (args.dbg & 2) {
+#pragma unroll
+              for (int m = 0; m < 16; ++m) { hi[m] = sv[m]; lo[m] = sv[m + 16]; }
+            } else if (jcol0 + 32 > n) {
+              exp_split<KIND, true>(sv, hi, lo, (int)(n - jcol0));
+            } else {
+              exp_split<KIND, false>(sv, hi, lo, 32);
+            }
+            tmem_st16(tb, hi);
+            tmem_st16(tb + 16, lo);
           }
-          tmem_st16(tb, hi);
-          tmem_st16(tb + 16, lo);
         }
         tmem_st_wait();
         fence_before_sync();

@@ -545,9 +545,13 @@ __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __re
       ctrl->arrive = 0;
       if (!(mx <= 1e300)) ctrl->nonfinite = 1;   // stop: a NaN / inf never recovers
       // relaxed inexact Krylov (params.mvm_relax): from here on the cheaper MVM variant runs
-      if (nq > 0 && ctrl->relax_thr > 0 && mx <= ctrl->relax_thr && !ctrl->relaxed) {
+      if (nq > 0 && ctrl->relax_thr > 0 && mx <= ctrl->relax_thr && ctrl->relaxed == 0) {
         ctrl->relaxed = 1;
         ctrl->relaxed_from = j + 1;
+      }
+      if (nq > 0 && ctrl->relax_thr2 > 0 && mx <= ctrl->relax_thr2 && ctrl->relaxed == 1) {
+        ctrl->relaxed = 2;
+        ctrl->relaxed2_from = j + 1;
       }
       if (act == 0 || (ctrl->tol > 0 && mx <= ctrl->tol) || j >= ctrl->max_iters || ctrl->nonfinite) ctrl->done = 1;
     }
