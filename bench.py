@@ -378,19 +378,24 @@ def run_ours(args, cfg):
                 "executed_frac_of_measured_peak": exec_flops / (mvm_ms * 1e-3) / 1e12 / peak}
         ncu = ncu_metrics().get(f"mvm_tc2_kernel/{cfg.name}")
         ncu_rel = ncu_metrics().get(f"mvm_tc2_kernel/{cfg.name}_relaxed")
+        ncu_rel2 = ncu_metrics().get(f"mvm_tc2_kernel/{cfg.name}_relaxed2")
         if ncu:
             roof["tensor_pipe_active_ncu"] = {"value": ncu["tensor_pipe_active"], "source": ncu["source"]}
-            rf = pinfo.get("relaxed_from", 0)
+            rf, rf2 = pinfo.get("relaxed_from", 0), pinfo.get("relaxed2_from", 0)
             if ncu_rel and rf > 0:
                 # relaxed schedule: MVMs of steps < relaxed_from (and the lambda
-                # warm-up / final MVM) on the accurate grid, the others on the relaxed one
-                n_rel = max(0, pinfo["iters"] - rf + 1)
-                n_acc = max(0, pinfo["mvms"] - n_rel)
+                # warm-up / final MVM) on the accurate grid, then level 1, then (relaxed2_from) level 2
+                n_rel2 = max(0, pinfo["iters"] - rf2 + 1) if (rf2 > 0 and ncu_rel2) else 0
+                n_rel = max(0, pinfo["iters"] - rf + 1) - n_rel2
+                n_acc = max(0, pinfo["mvms"] - n_rel - n_rel2)
+                tot = (n_acc * ncu["tensor_pipe_active"] + n_rel * ncu_rel["tensor_pipe_active"]
+                       + (n_rel2 * ncu_rel2["tensor_pipe_active"] if n_rel2 else 0.0))
                 roof["tensor_pipe_active_ncu"] = {
-                    "value": (n_acc * ncu["tensor_pipe_active"] + n_rel * ncu_rel["tensor_pipe_active"]) / max(1, n_acc + n_rel),
+                    "value": tot / max(1, n_acc + n_rel + n_rel2),
                     "accurate": ncu["tensor_pipe_active"], "relaxed": ncu_rel["tensor_pipe_active"],
-                    "mvms_accurate": n_acc, "mvms_relaxed": n_rel,
-                    "source": f"{ncu['source']}; {ncu_rel['source']} (MVM-count weighted)"}
+                    "relaxed2": ncu_rel2["tensor_pipe_active"] if ncu_rel2 else None,
+                    "mvms_accurate": n_acc, "mvms_relaxed": n_rel, "mvms_relaxed2": n_rel2,
+                    "source": "; ".join(x["source"] for x in (ncu, ncu_rel, ncu_rel2) if x) + " (MVM-count weighted)"}
         sm_count = torch.cuda.get_device_properties(local).multi_processor_count
         sfu_peak = sm_count * 16 * peaks.get("sm_max_mhz", 1965.0) * 1e6  # MUFU.EX2 per second
         roof["sfu"] = {"achieved_evals_per_s": rows_local * n / (mvm_ms * 1e-3), "peak_evals_per_s": sfu_peak,
@@ -432,8 +437,9 @@ def run_ours(args, cfg):
                     "mvms_per_step": infos[-1]["mvms"], "mvm_impl": impl_used,
                     "mvm_splits": infos[-1].get("mvm_splits"),
                     "relaxed_from_step": infos[-1].get("relaxed_from"),
-                    "mvm_schedule": "relaxed inexact Krylov: 66-tile chains until max relres <= 0.1, then 264 "
-                                    "(params.mvm_relax, DESIGN.md section 5)",
+                    "relaxed2_from_step": infos[-1].get("relaxed2_from"),
+                    "mvm_schedule": "relaxed inexact Krylov: 66-tile chains until max relres <= 0.1, then 264, "
+                                    "fp16 kernel entries from 0.01 (params.mvm_relax, DESIGN.md section 5)",
                     "parallelism": (f"rows{world}" if sharded else f"replicas{world}") if world > 1 else "single",
                     "recurrence": args.recurrence,
                     "converged": infos[-1]["converged"], "max_rel_residual": infos[-1]["max_rel_residual"],
