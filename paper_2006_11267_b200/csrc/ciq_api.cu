@@ -754,6 +754,7 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
     nblk = (rows + 255) / 256 * nsplit * 8;
   }
   const bool gated = c->mvm_gate.on && !dense && !sym && !win && !use_tc3(c, tp) && done != nullptr;
+  const bool gated_dense = c->mvm_gate.on && dense && done != nullptr;   // level 2 only (K_hi planes)
   if (gated) {   // the relaxed schedule's accurate grid (buffers sized for it; the alternative is smaller)
     nsplit = c->mvm_gate.nsplit;
     nblk = (rows + 255) / 256 * nsplit * 8;
@@ -811,6 +812,7 @@ ciq_status run_mvm(ciq_ctx* c, const float* v, int tp, float* p, double* apart, 
   a.kf = c->kf;
   a.nunits = dense ? (int)((rows + 127) / 128) * nsplit * chunks
                    : (pair ? tc3_units(rows, nsplit, chunks) : tc2_units(rows, nsplit, chunks));
+  if (gated_dense) a.gate = &done->relaxed;
   if (gated) {
     a.gate = &done->relaxed;
     a.nsplit_alt = c->mvm_gate.nsplit_alt;
@@ -2276,7 +2278,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   constexpr double kRelaxThr2 = 0.01;
 #endif
   int ns_acc = 0, ns_rel = 0;
-  bool relax = false;
+  bool relax = false, relax_dense = false;
 #ifndef CIQ_NO_ALPHA_FUSE
   if (p.mvm_relax && !P.on && !overlap && !c->sharded && !c->deriv && use_tc(c, p.mvm_impl, tp) &&
       is_kernel_op(c) && !use_mat(c, tp) && !use_sym(c, p.mvm_impl, tp) && !use_tc3(c, tp)) {
@@ -2285,9 +2287,14 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
     ns_rel = tc2_choose_nsplit(rows, c->op.n, tp / tc_chunk_cols(tp), sm_count(), 4, kTc2RelaxedChain);
     relax = ns_rel < ns_acc;
   }
+  // dense K (and the materialised kernel operator): level 2 only -- the HBM-bound dense kernel
+  // streams the K_hi planes alone (half the bytes); no long-chain level (its chains are short)
+  if (p.mvm_relax && !P.on && !overlap && !c->sharded && !c->post.on && !c->deriv && use_tc(c, p.mvm_impl, tp) &&
+      (c->op.kind == CIQ_OP_DENSE || use_mat(c, tp)))
+    relax_dense = true;
 #endif
   {
-    const double thr[2] = {relax ? kRelaxThr : 0.0, relax ? kRelaxThr2 : 0.0};
+    const double thr[2] = {relax ? kRelaxThr : 0.0, relax || relax_dense ? kRelaxThr2 : 0.0};
     const int zero[3] = {0, 0, 0};
     CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->relax_thr, thr, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
     CUDA_TRY(c, cudaMemcpyAsync(&sc.ctrl->relaxed, zero, 3 * sizeof(int), cudaMemcpyHostToDevice, s));   // + the _from steps
@@ -2351,7 +2358,7 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
       c->alpha_fuse = P.on ? nullptr : &sc;   // the full-tile kernel computes alpha_j in its tail
       // posterior operator (f2): the relaxed schedule applies to the K** MVM and its split sum; the
       // downdate and alpha follow the posterior path
-      if (relax) c->mvm_gate = ciq_ctx::MvmGate{true, ns_acc, ns_rel};
+      if (relax || relax_dense) c->mvm_gate = ciq_ctx::MvmGate{true, ns_acc, ns_rel};
       st2 = P.on ? apply_m(wcur, ws.p, &apart, &nbm)
                  : run_mvm(c, wcur, tp, ws.p, ws.apart, sc.ctrl, p.mvm_impl, sc.nrm_cur, true, &nsplit,
                            &apart, &nbm, fuse_pack);
@@ -2501,7 +2508,10 @@ ciq_status ciq_apply(ciq_ctx* c, const float* B, int64_t ldb, int64_t T, float* 
   st = prepare_mvm_buffers(c, tp, p.mvm_impl);   // every buffer the MVM may (re)allocate, before any capture
   if (st != CIQ_OK) return st;
   bool replayed = false;
-  st = run_iterations(c, p, j0, (uint64_t)p.mvm_impl ^ ((uint64_t)(uintptr_t)xqk << 1) ^ (stored ? 0x10000ull : 0ull),
+  // graph-cache key: every host-side decision that changes the captured kernels (the relaxed MVM
+  // schedule's gate and split counts included)
+  st = run_iterations(c, p, j0, (uint64_t)p.mvm_impl ^ ((uint64_t)(uintptr_t)xqk << 1) ^ (stored ? 0x10000ull : 0ull) ^
+                                    (relax ? 0x20000ull : 0ull) ^ (relax_dense ? 0x40000ull : 0ull),
                       enqueue_iter, &hc, &replayed);
   if (st != CIQ_OK) return st;
   if (replayed) {   // cached graph: the MVM kind / splits are those of the capture

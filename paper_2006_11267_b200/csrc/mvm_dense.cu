@@ -124,6 +124,28 @@ __device__ __forceinline__ void mma_dense12(uint32_t d, uint64_t ah, uint64_t al
       : "memory");
 }
 
+// 8 SS MMAs with K_hi only (relaxation level 2, params.mvm_relax): K_hi.V_hi, K_hi.V_lo
+template <int TN>
+__device__ __forceinline__ void mma_dense8(uint32_t d, uint64_t ah, uint64_t vh, uint64_t vl, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, t;\n\t.reg .b64 a<4>, c<4>, e<4>;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, %4, %4;\n\t"
+      "mov.b64 a0, %1;\n\t add.s64 a1, %1, 16;\n\t add.s64 a2, %1, 32;\n\t add.s64 a3, %1, 48;\n\t"
+      "mov.b64 c0, %2;\n\t add.s64 c1, %2, %5;\n\t add.s64 c2, %2, %6;\n\t add.s64 c3, %2, %7;\n\t"
+      "mov.b64 e0, %3;\n\t add.s64 e1, %3, %5;\n\t add.s64 e2, %3, %6;\n\t add.s64 e3, %3, %7;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a0, c0, %8, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a0, e0, %8, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, c1, %8, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, e1, %8, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, c2, %8, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, e2, %8, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, c3, %8, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, e3, %8, t;\n\t}" ::"r"(d),
+      "l"(ah), "l"(vh), "l"(vl), "r"(acc), "n"(2 * TN), "n"(4 * TN), "n"(6 * TN), "r"(idesc)
+      : "memory");
+}
+
 __device__ __forceinline__ bool elect_one_d() {
   uint32_t pred = 0;
   asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t@p mov.u32 %0, 1;\n\t}" : "+r"(pred));
@@ -160,6 +182,8 @@ __global__ void __launch_bounds__(D_THREADS, 1) mvm_dense2_kernel(TcArgs args) {
   __syncthreads();
   fence_after_sync();
   const uint32_t tbase = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
+  // relaxation level 2 (params.mvm_relax): K_hi only -- half the K bytes
+  const bool lowp = args.gate != nullptr && *args.gate >= 2;
   if (warp == 0) {
     if (lane == 0) {
       int g = 0;
@@ -175,9 +199,9 @@ __global__ void __launch_bounds__(D_THREADS, 1) mvm_dense2_kernel(TcArgs args) {
           mbar_wait_backoff(&bars->empty[st], ((g / C::STAGES) & 1) ^ 1);
           uint8_t* sb = ring + st * C::STAGE_BYTES;
           const int kt = kt0 + kk;
-          mbar_arrive_expect_tx(&bars->full[st], C::STAGE_BYTES);
+          mbar_arrive_expect_tx(&bars->full[st], lowp ? C::STAGE_BYTES - C::KT_BYTES : C::STAGE_BYTES);
           bulk_g2s(sb, kh + (size_t)kt * BM * DK, C::KT_BYTES, &bars->full[st]);
-          bulk_g2s(sb + C::KT_BYTES, kl + (size_t)kt * BM * DK, C::KT_BYTES, &bars->full[st]);
+          if (!lowp) bulk_g2s(sb + C::KT_BYTES, kl + (size_t)kt * BM * DK, C::KT_BYTES, &bars->full[st]);
           const size_t voff = (size_t)(kt / 2) * BN * TN + (size_t)(kt & 1) * DK * TN;
           bulk_g2s(sb + 2 * C::KT_BYTES, vh + voff, C::VT_BYTES, &bars->full[st]);
           bulk_g2s(sb + 2 * C::KT_BYTES + C::VT_BYTES, vl + voff, C::VT_BYTES, &bars->full[st]);
@@ -205,7 +229,8 @@ __global__ void __launch_bounds__(D_THREADS, 1) mvm_dense2_kernel(TcArgs args) {
         const uint64_t ah = shfl64_d(dah0 + so), vh = shfl64_d(dvh0 + so);
         const uint32_t acc = __shfl_sync(0xffffffffu, kk > 0 ? 1u : 0u, 0);
         if (elect_one_d()) {
-          mma_dense12<TN>(d, ah, ah + (C::KT_BYTES >> 4), vh, vh + (C::VT_BYTES >> 4), idesc_o, acc);
+          if (lowp) mma_dense8<TN>(d, ah, vh, vh + (C::VT_BYTES >> 4), idesc_o, acc);
+          else mma_dense12<TN>(d, ah, ah + (C::KT_BYTES >> 4), vh, vh + (C::VT_BYTES >> 4), idesc_o, acc);
           mma_commit(&bars->empty[st]);
           if (kk == nk - 1) mma_commit(&bars->o_full[ob]);
         }

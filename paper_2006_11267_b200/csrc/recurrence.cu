@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(256) givens_kernel(Scal sc, const double* __re
         ctrl->relaxed = 1;
         ctrl->relaxed_from = j + 1;
       }
-      if (nq > 0 && ctrl->relax_thr2 > 0 && mx <= ctrl->relax_thr2 && ctrl->relaxed == 1) {
+      if (nq > 0 && ctrl->relax_thr2 > 0 && mx <= ctrl->relax_thr2 && ctrl->relaxed < 2) {
         ctrl->relaxed = 2;
         ctrl->relaxed2_from = j + 1;
       }
