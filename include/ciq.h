@@ -191,12 +191,14 @@ typedef struct {
                               /*    Y = W_J z once at the end: ~5 vectors of HBM      */
                               /*    traffic per iteration instead of 3Q + 6.  Not  */
                               /*    with a preconditioner or keep_shift_solutions.  Default 0.     */
-  int32_t mvm_relax;          /* 1: relaxed inexact Krylov (Simoncini & Szyld): once the max       */
+  int32_t mvm_relax;          /* 1: relaxed inexact Krylov (Simoncini & Szyld): the MVM error may  */
+                              /*    grow as 1 / ||r_j|| without moving the result, so once the max */
                               /*    relative residual is <= 0.1 the full-tile tensor-core MVM runs */
-                              /*    with 4x longer TMEM accumulation chains (fewer column splits); */
-                              /*    the MVM error may grow as 1 / ||r_j|| without moving the       */
-                              /*    result.  Single GPU, no preconditioner.  */
-                              /*    Default 1; 0 = every MVM at the accurate chain length.         */
+                              /*    with 4x longer TMEM accumulation chains (fewer column splits), */
+                              /*    and from 0.01 with kernel entries rounded to fp16 (dense K: the */
+                              /*    K_hi planes only).  DESIGN.md section 5; ciq_info.relaxed_from / */
+                              /*    relaxed2_from report the switch steps.  Single GPU, no          */
+                              /*    preconditioner.  Default 1; 0 = every MVM accurate.            */
 } ciq_params;
 
 typedef struct {
